@@ -1,0 +1,231 @@
+/* rlhfspec_core — C ABI of the RLHFSpec verification hot path on B200 (sm_100a).
+ *
+ * Paper: RLHFSpec (arXiv 2512.04752), /root/reference/PAPER.md, cited P:<line>.
+ * Scope: DESIGN.md §1 / SURVEY.md §8. Readings Z1..Z20: DESIGN.md §2.
+ *
+ * Conventions (all entry points)
+ *  - Every call returns rs_status (RS_OK = 0). No exception crosses the ABI. On error,
+ *    rs_last_error() returns a thread-local, NUL-terminated message (valid until the next
+ *    call on the same thread).
+ *  - "device" pointers are caller-owned CUDA global-memory buffers on the current device;
+ *    "host" pointers are caller-owned CPU memory. The library never frees caller memory and
+ *    keeps no pointer past the call unless stated (rs_ctx registrations).
+ *  - Kernels are enqueued on `stream` (a cudaStream_t passed as void*; NULL = legacy default
+ *    stream) and are asynchronous: outputs are valid once the stream reaches that point.
+ *    Host-only calls are synchronous.
+ *  - No allocation happens on hot calls; workspace is caller-provided (size queries given).
+ *  - Data errors found on the device (malformed tree, non-finite logits) do not become a
+ *    return code: they set per-sample bits in `status_flags` (RS_FLAG_*).
+ *  - Tensor layouts are row-major, innermost index last. bf16 = IEEE bfloat16 bit pattern.
+ *  - Tree conventions (Z1): sample b owns flattened nodes tree_off[b] .. tree_off[b+1]-1
+ *    (T_b = tree_off[b+1]-tree_off[b], 1 <= T_b <= 64); parent[] and path[] hold LOCAL node
+ *    indices; node 0 is the root (the last committed token), parent[0] = -1, parent[i] < i.
+ *  - KV cache (one tensor per layer): [num_pages, Hkv, page_size, head_dim] bf16; logical slot
+ *    j of sample b is page block_table[b*max_pages + j/page_size], row j%page_size. Slots
+ *    0..P_b-1 hold the committed prefix, slot P_b+i holds tree node i (written upstream).
+ */
+#ifndef RLHFSPEC_CORE_H
+#define RLHFSPEC_CORE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    RS_OK = 0,
+    RS_ERR_INVALID_ARG = 1,        /* bad size / null pointer / out-of-range argument       */
+    RS_ERR_MALFORMED_TREE = 2,     /* host-checked tree is not a topological tree    */
+    RS_ERR_EMPTY_TREE = 3,         /* no candidate nodes                             */
+    RS_ERR_INSUFFICIENT_NODES = 4, /* fewer candidates than n_min                     */
+    RS_ERR_NONFINITE = 5,
+    RS_ERR_NO_MEMORY = 6,          /* page reservation refused (migration handshake) */
+    RS_ERR_LAYOUT_MISMATCH = 7,    /* migration header / buffer disagree            */
+    RS_ERR_UNSUPPORTED = 8,        /* shape outside what the kernels implement              */
+    RS_ERR_CUDA = 9,
+    RS_ERR_NCCL = 10,
+    RS_ERR_WORKSPACE = 11          /* workspace too small                                   */
+} rs_status;
+
+enum { RS_FLAG_MALFORMED = 1, RS_FLAG_NONFINITE = 2 };
+enum { RS_ACCEPT_GREEDY = 0, RS_ACCEPT_SAMPLE_DELTA = 1, RS_ACCEPT_SAMPLE_MSS = 2 };
+enum { RS_DTYPE_BF16 = 0, RS_DTYPE_F32 = 1 };
+#define RS_MAX_TREE 64
+
+const char* rs_last_error(void);
+const char* rs_version(void);
+
+/* ===================================================================================== a1
+ * rs_tree_build_mask — ancestor-or-self bitmask and depth per tree node ("each branch
+ * represents a token sequence awaiting verification"; Z3).
+ *   parent    device int32 [NT]   local parent index, -1 for the root
+ *   tree_off  device int32 [B+1]
+ *   tree_mask device uint64 [NT]  out: bit j set <=> local node j is on Path(root, i)
+ *   depth     device int32 [NT]   out: root depth 0
+ *   status_flags device int32 [B] out: RS_FLAG_MALFORMED if the tree is not topological or
+ *             T_b outside [1, 64] (that sample's mask/depth are then zero)
+ */
+rs_status rs_tree_build_mask(const int32_t* parent, const int32_t* tree_off, int32_t B,
+                             uint64_t* tree_mask, int32_t* depth, int32_t* status_flags,
+                             void* stream);
+
+/* ===================================================================================== a2
+ * Tree-verification attention (P:76-80 single-pass verification of all tree tokens; P:213
+ * "attention primarily incurs cost due to KVCache loading"). For sample b, q head h
+ * (kv head h/g), node i:  o = softmax_j(q.k_j * sm_scale) v_j over
+ *   j in {0..P_b-1} U {P_b + t : bit t of tree_mask[tree_off[b]+i]}.
+ * Implemented for head_dim in {64, 128}, page_size = 64, Hq % Hkv == 0, T_b*g <= 512.
+ *
+ * Plan/run split: the plan is host metadata built from HOST copies of prefix_len and tree_off
+ * (the lengths of this step; reused by every layer), uploaded once into device workspace.
+ */
+typedef struct rs_attn_plan rs_attn_plan;
+
+/* prefix_len_host int32 [B], tree_off_host int32 [B+1]; num_ctas: persistent grid size,
+ * 0 = number of SMs of the current device. */
+rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const int32_t* tree_off_host,
+                              int32_t B, int32_t Hq, int32_t Hkv, int32_t head_dim,
+                              int32_t page_size, int32_t num_ctas, rs_attn_plan** plan_out);
+/* Device workspace bytes the plan needs (schedule + split-KV partials). */
+size_t rs_attn_plan_workspace_bytes(const rs_attn_plan* plan);
+/* Copy the schedule into `ws` (device, >= rs_attn_plan_workspace_bytes, 256-byte aligned). */
+rs_status rs_attn_plan_upload(const rs_attn_plan* plan, void* ws, size_t ws_bytes, void* stream);
+/* Number of work items / split units (for reporting). */
+rs_status rs_attn_plan_info(const rs_attn_plan* plan, int32_t* num_ctas, int32_t* num_items,
+                            int32_t* num_split_units);
+void rs_attn_plan_destroy(rs_attn_plan* plan);
+
+/* q        device bf16 [NT, Hq, head_dim] (post-RoPE)
+ * k_pages, v_pages device bf16 [num_pages, Hkv, page_size, head_dim] (one layer)
+ * block_table device int32 [B, max_pages]; prefix_len device int32 [B]; tree_off device int32 [B+1]
+ * tree_mask device uint64 [NT] (rs_tree_build_mask)
+ * out      device bf16 [NT, Hq, head_dim]
+ * lse      device fp32 [NT, Hq] natural-log log-sum-exp, or NULL
+ * ws       the workspace the plan was uploaded into (the partials area is overwritten).
+ * The plan must have been created for the same B/Hq/Hkv/head_dim/page_size and lengths. */
+rs_status rs_tree_verify_attention(const rs_attn_plan* plan, const void* q, const void* k_pages,
+                                   const void* v_pages, int64_t num_pages,
+                                   const int32_t* block_table, int32_t max_pages,
+                                   const int32_t* prefix_len, const int32_t* tree_off,
+                                   const uint64_t* tree_mask, int32_t B, int32_t Hq, int32_t Hkv,
+                                   int32_t head_dim, int32_t page_size, float sm_scale, void* out,
+                                   float* lse, void* ws, size_t ws_bytes, void* stream);
+
+/* ===================================================================================== a3
+ * rs_tree_accept — walk each sample's tree from the root and return its longest accepted
+ * path and the bonus token (rule per mode in DESIGN.md §2 Z5-Z8, bit-exact
+ * arithmetic in "Bit-exact sampling").
+ *   mode        RS_ACCEPT_GREEDY | RS_ACCEPT_SAMPLE_DELTA | RS_ACCEPT_SAMPLE_MSS
+ *   logits      device [NT, V], RS_DTYPE_BF16 or RS_DTYPE_F32 (target LLM row per node)
+ *   draft_probs device fp32 [NT, V]: row c = the draft distribution the children of c were
+ *               drawn from (MSS only; must be NULL otherwise)
+ *   parent, token device int32 [NT]; tree_off device int32 [B+1]; gid device int64 [B]
+ *               (global sample ids; the RNG is keyed by gid, so results do not depend on
+ *               which GPU/slot holds the sample)
+ *   temperature > 0 (sampling modes; ignored by GREEDY); seed, step: RNG key / counter
+ *   accepted_len device int32 [B]  out: a_b (accepted drafts, bonus excluded)
+ *   path         device int32 [B, 64] out: path[b][0..a_b] local node ids (path[b][0]=0), -1 padded
+ *   bonus_token  device int32 [B]  out: the bonus token (-1 on a flagged sample)
+ *   status_flags device int32 [B]  out: RS_FLAG_* bits
+ *   ws: unused (pass NULL, 0); reserved. */
+rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t logits_dtype,
+                         const float* draft_probs, const int32_t* parent, const int32_t* token,
+                         const int32_t* tree_off, const int64_t* gid, int32_t B, int32_t V,
+                         float temperature, uint64_t seed, uint64_t step, int32_t* accepted_len,
+                         int32_t* path, int32_t* bonus_token, int32_t* status_flags, void* ws,
+                         size_t ws_bytes, void* stream);
+
+/* Device-side Philox4x32-10 and exp_spec over arrays (conformance hooks for the parity
+ * tests; the same device functions the acceptance kernel uses).
+ *   ctr device uint32 [n,4], key uint32 [2] (host), out device uint32 [n,4]
+ *   x device fp32 [n] (x <= 0), y device fp32 [n] */
+rs_status rs_philox4x32_10(const uint32_t* ctr, int64_t n, const uint32_t* key_host, uint32_t* out,
+                           void* stream);
+rs_status rs_exp_spec(const float* x, int64_t n, float* y, void* stream);
+
+/* ===================================================================================== a4
+ * rs_kv_compact — commit the accepted path's K/V (only this step's KVCache changes):
+ *   for k = 1..a_b:  K/V[b, slot P_b+k] <- K/V[b, slot P_b+path[b][k]]   (every layer, head)
+ *   new_len[b] = P_b + 1 + a_b
+ * with sequential ascending-k semantics (rows are gathered before any is written).
+ *   k_layers_host, v_layers_host  host arrays of L device pointers (one bf16 cache per layer)
+ *   accepted_len, path   device outputs of rs_tree_accept
+ *   new_len  device int32 [B] out; moves device int32 [B, 64, 2] out (src_slot, dst_slot per
+ *            k = 1..a_b, -1 padded) or NULL. Flagged samples (accepted_len 0) move nothing. */
+rs_status rs_kv_compact(void* const* k_layers_host, void* const* v_layers_host, int32_t L,
+                        int64_t num_pages, int32_t Hkv, int32_t head_dim, int32_t page_size,
+                        const int32_t* block_table, int32_t max_pages, const int32_t* prefix_len,
+                        const int32_t* accepted_len, const int32_t* path, int32_t B,
+                        int32_t* new_len, int32_t* moves, void* stream);
+
+/* ===================================================================================== a0
+ * Workload-aware drafting-strategy selection: n = argmax al(n)/t_sd(n) (Eq. 2)
+ * by layer-level priority-queue search with early stop (Eq. 3). Host only. */
+typedef struct {
+    double c_draft, b0, b1, b2, b3, k_sat;   /* t_sd = c_draft+b0+b1*Nseq+b2*Nd+b3*relu(Nd-k)*Nd */
+    int32_t seq_bucket, draft_bucket;        /* bucket widths of the prediction cache   */
+} rs_cost_model;
+
+typedef struct {
+    int32_t n, depth, width;     /* chosen draft-token num and the depth/width of T = n+1 trees */
+    int32_t n_stop;              /* n at which the early stop fired (or the last n searched)   */
+    int32_t cache_hit;           /* 1 if t_sd(n) of the chosen n came from the bucket cache     */
+    int32_t cache_entries;
+    double al, t_sd, objective;  /* predicted al(n) (sum of w over S(n), all samples), t_sd, ratio */
+} rs_strategy;
+
+typedef struct rs_selector rs_selector;
+/* knots_x/knots_y host double [n_knots]: the acceptance fit F (monotone piecewise linear,
+ * clamped to [0,1]). */
+rs_status rs_selector_create(const rs_cost_model* cost, const double* knots_x,
+                             const double* knots_y, int32_t n_knots, rs_selector** out);
+void rs_selector_destroy(rs_selector* sel);
+/* cand_parent host int32 [N] (per sample, -1 = child of the committed root, parent < index),
+ * cand_o host double [N] draft probabilities o(v) in (0,1], cand_off host int32 [B+1],
+ * prefix_len host int32 [B]. selected: host int32 [B, n_max] candidate ids in selection order
+ * (the first n of each row form S_b(n)), -1 padded, or NULL. */
+rs_status rs_select_strategy(rs_selector* sel, const int32_t* cand_parent, const double* cand_o,
+                             const int32_t* cand_off, const int32_t* prefix_len, int32_t B,
+                             int32_t n_min, int32_t n_max, int32_t patience, rs_strategy* out,
+                             int32_t* selected);
+/* Least-squares fit of the cost model's b0..b3 (c_draft kept) to measured step times. */
+rs_status rs_cost_model_fit(const double* n_seq, const double* n_draft, const double* t_sec,
+                            int32_t n, rs_cost_model* inout);
+
+/* ===================================================================================== a6
+ * Sample reallocation policy. Host only. */
+/* Knee of the throughput-vs-sample-count curve (Z13). counts strictly increasing. */
+rs_status rs_knee_threshold(const double* counts, const double* tput, int32_t n, double frac,
+                            int32_t* threshold);
+/* Greedy plan for Eq. 6: transfers (src[i], dst[i], count[i]), i < *n_transfers
+ * (arrays of capacity G). Every instance appears in at most one transfer. */
+rs_status rs_plan_reallocation(const int32_t* loads, int32_t G, int32_t threshold, int32_t* src,
+                               int32_t* dst, int32_t* count, int32_t* n_transfers);
+/* Samples to move: shortest sequence first, then lowest average accepted tokens, then gid. */
+rs_status rs_choose_samples(const int64_t* gid, const int32_t* seq_len, const double* avg_accepted,
+                            int32_t n, int32_t k, int64_t* chosen);
+
+/* ===================================================================================== a5
+ * KV migration: pack into one contiguous buffer ordered model -> layer -> sample
+ * (Z18: per segment K then V, each [Hkv][len][head_dim]), transfer, unpack. */
+/* Elements (bf16) of one model's part of the buffer: L * 2 * Hkv * head_dim * sum(lens). */
+int64_t rs_kv_pack_elems(int32_t L, int32_t Hkv, int32_t head_dim, const int32_t* lens_host,
+                         int32_t n);
+/* Gather n samples (rows sample_rows[i] of block_table, lens[i] tokens) of one model into
+ * buf + buf_offset_elems. sample_rows, lens: device int32 [n]. */
+rs_status rs_kv_pack(void* const* k_layers_host, void* const* v_layers_host, int32_t L, int32_t Hkv,
+                     int32_t head_dim, int32_t page_size, const int32_t* block_table,
+                     int32_t max_pages, const int32_t* sample_rows, const int32_t* lens, int32_t n,
+                     void* buf, int64_t buf_offset_elems, void* stream);
+/* Inverse: scatter from the buffer into the pages of block_table rows sample_rows[i]. */
+rs_status rs_kv_unpack(void* const* k_layers_host, void* const* v_layers_host, int32_t L,
+                       int32_t Hkv, int32_t head_dim, int32_t page_size, const int32_t* block_table,
+                       int32_t max_pages, const int32_t* sample_rows, const int32_t* lens,
+                       int32_t n, const void* buf, int64_t buf_offset_elems, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RLHFSPEC_CORE_H */

@@ -1,0 +1,99 @@
+"""One batched verification step through the C ABI (SURVEY.md §3 call stack (1)):
+
+    rs_tree_build_mask -> L x rs_tree_verify_attention -> rs_tree_accept -> rs_kv_compact
+
+Pure orchestration: buffers are torch tensors, every computation is a library call. The
+device part can be captured into a CUDA graph (one launch per step)."""
+from __future__ import annotations
+
+import torch
+
+from . import core
+
+
+class VerifyStep:
+    def __init__(self, batch: dict, mode: int = core.GREEDY, temperature: float = 1.0, num_ctas: int = 0,
+                 with_lse: bool = False, stream=None):
+        b = batch
+        dev = b["q"].device
+        self.b = b
+        self.mode = mode
+        self.temperature = temperature
+        self.B, self.Hq, self.Hkv, self.d, self.ps = b["B"], b["Hq"], b["Hkv"], b["d"], b["page_size"]
+        self.L = b["q"].shape[0]
+        self.sm_scale = b["sm_scale"]
+
+        def t32(x):
+            return torch.as_tensor(x, dtype=torch.int32).to(dev) if not isinstance(x, torch.Tensor) else x.to(dev)
+        self.parent = t32(b["parent"])
+        self.token = t32(b["token"])
+        self.tree_off = t32(b["tree_off"])
+        self.prefix_len = t32(b["prefix_len"])
+        self.block_table = t32(b["block_table"])
+        self.gid = torch.as_tensor(b["gid"], dtype=torch.int64).to(dev)
+        self.q = b["q"]
+        self.k_layers = [b["k_cache"][l] for l in range(self.L)]
+        self.v_layers = [b["v_cache"][l] for l in range(self.L)]
+        self.logits = b["logits"]
+        self.draft = b.get("draft_probs")
+        if mode != core.SAMPLE_MSS:
+            self.draft = None
+        # host-side plan from this step's lengths (shared by all layers)
+        self.plan = core.AttnPlan(b["prefix_len"], b["tree_off"], self.Hq, self.Hkv, self.d, self.ps,
+                                  num_ctas=num_ctas)
+        self.ws = core.alloc_workspace(self.plan.ws_bytes, dev)
+        self.plan.upload(self.ws)
+        NT = self.q.shape[1]
+        self.attn_out = torch.empty((self.L, NT, self.Hq, self.d), dtype=torch.bfloat16, device=dev)
+        self.lse = torch.empty((self.L, NT, self.Hq), dtype=torch.float32, device=dev) if with_lse else None
+        self.acc = torch.empty(self.B, dtype=torch.int32, device=dev)
+        self.path = torch.empty((self.B, core.MAX_TREE), dtype=torch.int32, device=dev)
+        self.bonus = torch.empty(self.B, dtype=torch.int32, device=dev)
+        self.flags = torch.empty(self.B, dtype=torch.int32, device=dev)
+        self.new_len = torch.empty(self.B, dtype=torch.int32, device=dev)
+        self.graph = None
+        self.seed, self.step_no = 0, 0
+
+    def device_step(self, seed=None, step=None, stream=None):
+        """Enqueue the whole step on `stream` (no host sync)."""
+        seed = self.seed if seed is None else seed
+        step = self.step_no if step is None else step
+        mask, _, flags = core.tree_build_mask(self.parent, self.tree_off, stream=stream)
+        self.mask = mask
+        for l in range(self.L):
+            core.tree_verify_attention(self.plan, self.q[l], self.k_layers[l], self.v_layers[l], self.block_table,
+                                       self.prefix_len, self.tree_off, mask, self.sm_scale, self.ws,
+                                       out=self.attn_out[l], lse=None if self.lse is None else self.lse[l],
+                                       stream=stream)
+        core.tree_accept(self.mode, self.logits, self.parent, self.token, self.tree_off, self.gid,
+                         draft_probs=self.draft, temperature=self.temperature, seed=seed, step=step,
+                         out=(self.acc, self.path, self.bonus, self.flags), stream=stream)
+        core.kv_compact(self.k_layers, self.v_layers, self.block_table, self.prefix_len, self.acc, self.path,
+                        self.ps, new_len=self.new_len, stream=stream)
+
+    def capture(self, seed=0, step=0):
+        """Capture the device step into a CUDA graph (seed/step are baked in)."""
+        self.seed, self.step_no = seed, step
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.device_step(seed, step, stream=s)   # warm-up (lazy init outside capture)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.device_step(seed, step, stream=torch.cuda.current_stream())
+        self.graph = g
+        return g
+
+    def replay(self):
+        self.graph.replay()
+
+    def results(self):
+        return dict(accepted_len=self.acc.cpu().numpy(), path=self.path.cpu().numpy(),
+                    bonus=self.bonus.cpu().numpy(), flags=self.flags.cpu().numpy(),
+                    new_len=self.new_len.cpu().numpy())
+
+    def run(self, seed=0, step=0):
+        self.device_step(seed, step)
+        return self.results()

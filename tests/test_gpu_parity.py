@@ -1,0 +1,281 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): attention max-abs <= 2e-2 and rel-L2 <= 5e-3 vs the fp64
+oracle (Z16); acceptance lengths/paths/bonus, compaction bytes/moves, masks, Philox and
+exp_spec bit-exact."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import accept as OAcc
+from oracle import attention as OA
+from oracle import compact as OC
+from oracle import tree as OT
+from synth import CONFIGS, VerifyConfig, make_verify_batch, random_tree_parents
+from tests.helpers import tensor_bf16_bits
+
+pytestmark = pytest.mark.gpu
+
+ATOL, RTOL_L2 = 2e-2, 5e-3
+
+
+def _dev(x, dtype=None):
+    t = torch.as_tensor(np.ascontiguousarray(x))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.cuda()
+
+
+# ------------------------------------------------------------------ a1 tree masks
+def test_tree_mask_matches_oracle(cuda_lib):
+    core = cuda_lib
+    rng = np.random.default_rng(0)
+    sizes = [1, 2, 8, 16, 33, 64] + list(rng.integers(1, 65, size=50))
+    parents = [random_tree_parents(rng, int(T)) for T in sizes]
+    parents[3] = parents[3].copy(); parents[3][5] = 7          # malformed (parent >= i)
+    parents[4] = parents[4].copy(); parents[4][0] = 0          # malformed root
+    tree_off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+    par = np.concatenate(parents).astype(np.int32)
+    mask, depth, flags = core.tree_build_mask(_dev(par), _dev(tree_off))
+    om, od, ok = OT.batch_masks(par, tree_off)
+    np.testing.assert_array_equal(mask.cpu().numpy().view(np.uint64), om)
+    np.testing.assert_array_equal(depth.cpu().numpy(), od)
+    np.testing.assert_array_equal(flags.cpu().numpy(), np.where(ok, 0, core.FLAG_MALFORMED))
+
+
+# ------------------------------------------------------------------ RNG / exp_spec
+def test_philox_device_bit_exact(cuda_lib):
+    core = cuda_lib
+    rng = np.random.default_rng(1)
+    ctr = rng.integers(0, 2**32, size=(4096, 4), dtype=np.uint64).astype(np.uint32)
+    ctr[0] = 0
+    ctr[1] = 0xFFFFFFFF
+    key = [0xA4093822, 0x299F31D0]
+    out = core.philox4x32_10(_dev(ctr.view(np.int32)), key).cpu().numpy().view(np.uint32)
+    for i in range(0, 4096, 97):
+        assert list(out[i]) == list(OAcc.philox4x32_10(ctr[i], key))
+
+
+def test_exp_spec_device_bit_exact(cuda_lib):
+    core = cuda_lib
+    # every 7th fp32 bit pattern in [-32, 0] (~1.6e8 values) plus all of [-2^-10, 0]
+    hi = np.float32(-32.0).view(np.uint32)
+    for start in range(0x80000000, int(hi) + 1, 1 << 26):
+        bits = np.arange(start, min(start + (1 << 26), int(hi) + 1), 7, dtype=np.uint64).astype(np.uint32)
+        x = bits.view(np.float32)
+        y = core.exp_spec(_dev(x)).cpu().numpy()
+        np.testing.assert_array_equal(y.view(np.uint32), OAcc.exp_spec_array(x).view(np.uint32))
+    x = -np.random.default_rng(2).random(1 << 20).astype(np.float32) * np.float32(2**-10)
+    y = core.exp_spec(_dev(x)).cpu().numpy()
+    np.testing.assert_array_equal(y.view(np.uint32), OAcc.exp_spec_array(x).view(np.uint32))
+
+
+# ------------------------------------------------------------------ a3 accept
+def _accept_case(cfg, with_bad=False):
+    b = make_verify_batch(cfg, device="cpu", layers=1)
+    logits = b["logits"]
+    if with_bad:
+        logits = logits.clone()
+        logits[b["tree_off"][1], 5] = float("nan")          # sample 1 root row non-finite
+    return b, logits
+
+
+def _run_accept_both(core, b, logits, mode, temperature=1.0, seed=11, step=3, parent=None):
+    parent = b["parent"] if parent is None else parent
+    dp = b["draft_probs"]
+    g = core.tree_accept(mode, logits.cuda(), _dev(parent), _dev(b["token"]), _dev(b["tree_off"]),
+                         _dev(b["gid"]), draft_probs=None if dp is None else dp.cuda(),
+                         temperature=temperature, seed=seed, step=step)
+    g = [x.cpu().numpy() for x in g]
+    lg = tensor_bf16_bits(logits) if logits.dtype == torch.bfloat16 else logits.numpy()
+    o = OAcc.tree_accept(mode, lg, parent, b["token"], b["tree_off"], b["gid"], b["V"],
+                         draft_probs=None if dp is None else dp.numpy(), temperature=temperature,
+                         seed=seed, step=step)
+    return g, o
+
+
+@pytest.mark.parametrize("cfgname", ["tiny", "greedy_ragged", "greedy_bigV"])
+def test_accept_greedy_bit_exact(cuda_lib, cfgname):
+    core = cuda_lib
+    if cfgname == "tiny":
+        cfg = CONFIGS["tiny"]
+    elif cfgname == "greedy_ragged":
+        cfg = VerifyConfig("g", B=40, Hq=4, Hkv=1, d=64, V=1000, L=1, prefix=("fixed", 5),
+                           tree=("range", 1, 64), mode="greedy", p_accept=0.85, seed=4)
+    else:
+        cfg = VerifyConfig("g2", B=6, Hq=4, Hkv=1, d=64, V=128256, L=1, prefix=("fixed", 5),
+                           tree=("range", 8, 32), mode="greedy", p_accept=0.9, seed=5)
+    b, logits = _accept_case(cfg, with_bad=(cfgname == "greedy_ragged"))
+    g, o = _run_accept_both(core, b, logits, core.GREEDY)
+    for x, y in zip(g, o):
+        np.testing.assert_array_equal(x, y)
+    # fp32 logits and a malformed tree
+    par = b["parent"].copy()
+    if b["B"] > 2:
+        par[b["tree_off"][2]] = 0
+    g, o = _run_accept_both(core, b, logits.float(), core.GREEDY, parent=par)
+    for x, y in zip(g, o):
+        np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("mode,V,temp", [("delta", 1000, 1.0), ("mss", 1000, 1.0), ("mss", 1000, 0.7),
+                                         ("delta", 128256, 1.0), ("mss", 128256, 1.3)])
+def test_accept_sampling_bit_exact(cuda_lib, mode, V, temp):
+    core = cuda_lib
+    B = 24 if V < 5000 else 4
+    cfg = VerifyConfig("s", B=B, Hq=4, Hkv=1, d=64, V=V, L=1, prefix=("fixed", 5), tree=("range", 2, 40),
+                       mode=mode, seed=7 + V % 13)
+    b, logits = _accept_case(cfg)
+    m = core.SAMPLE_DELTA if mode == "delta" else core.SAMPLE_MSS
+    for step in range(3):
+        g, o = _run_accept_both(core, b, logits, m, temperature=temp, seed=1234 + step, step=step)
+        for x, y in zip(g, o):
+            np.testing.assert_array_equal(x, y)
+
+
+def test_accept_sampling_distribution_gpu(cuda_lib):
+    """1e6 trials on the GPU: the first emitted token follows the target softmax."""
+    from tests.helpers import bits_to_f32, chi2_pvalue, softmax64
+    core = cuda_lib
+    rng = np.random.default_rng(3)
+    V, n = 8, 1_000_000
+    parent = np.array([-1, 0, 0, 1, 1, 2, 2], np.int32)
+    T = len(parent)
+    logits = torch.randn((T, V), generator=torch.Generator().manual_seed(1)) * 1.5
+    q = torch.softmax(torch.randn((T, V), generator=torch.Generator().manual_seed(2)), -1)
+    toks = np.zeros((n, T), np.int32)
+    for c in range(T):
+        kids = np.nonzero(parent == c)[0]
+        if len(kids):
+            toks[:, kids] = rng.choice(V, size=(n, len(kids)), p=q[c].double().numpy() / q[c].double().sum().item())
+    lg = logits.to(torch.bfloat16).repeat(n, 1).cuda()
+    dp = q.repeat(n, 1).cuda()
+    tree_off = torch.arange(n + 1, dtype=torch.int32, device="cuda") * T
+    acc, path, bonus, flags = core.tree_accept(core.SAMPLE_MSS, lg, _dev(np.tile(parent, n)), _dev(toks.reshape(-1)),
+                                               tree_off, torch.arange(n, device="cuda", dtype=torch.int64),
+                                               draft_probs=dp, seed=5, step=1)
+    acc, path, bonus = acc.cpu().numpy(), path.cpu().numpy(), bonus.cpu().numpy()
+    first = np.where(acc >= 1, toks[np.arange(n), np.maximum(path[:, 1], 0)], bonus)
+    p = softmax64(bits_to_f32(tensor_bf16_bits(logits.to(torch.bfloat16))))
+    pv, _ = chi2_pvalue(np.bincount(first, minlength=V), p[0])
+    assert pv > 1e-4, pv
+
+
+# ------------------------------------------------------------------ a4 compact
+def test_kv_compact_bit_exact(cuda_lib):
+    core = cuda_lib
+    cfg = VerifyConfig("c", B=12, Hq=8, Hkv=2, d=128, V=100, L=3, prefix=("lognormal", 100, 0.8, 0, 400),
+                       tree=("range", 1, 64), mode="greedy", seed=9)
+    b = make_verify_batch(cfg, device="cpu", with_logits=False)
+    rng = np.random.default_rng(9)
+    acc = np.zeros(b["B"], np.int32)
+    path = np.full((b["B"], 64), -1, np.int32)
+    for i in range(b["B"]):
+        s, e = b["tree_off"][i], b["tree_off"][i + 1]
+        node = int(rng.integers(0, e - s))
+        pth = OT.ancestors_or_self(list(b["parent"][s:e]), node)
+        acc[i] = len(pth) - 1
+        path[i, :len(pth)] = pth
+    kc = b["k_cache"].cuda()
+    vc = b["v_cache"].cuda()
+    ks = [kc[l] for l in range(cfg.L)]
+    vs = [vc[l] for l in range(cfg.L)]
+    moves = torch.empty((b["B"], 64, 2), dtype=torch.int32, device="cuda")
+    new_len, _ = core.kv_compact(ks, vs, _dev(b["block_table"]), _dev(b["prefix_len"]), _dev(acc), _dev(path),
+                                 moves=moves)
+    caches = [tensor_bf16_bits(b["k_cache"][l]).copy() for l in range(cfg.L)] + \
+             [tensor_bf16_bits(b["v_cache"][l]).copy() for l in range(cfg.L)]
+    onl, omv = OC.kv_compact(caches, b["block_table"], b["prefix_len"], acc, path, 64)
+    np.testing.assert_array_equal(new_len.cpu().numpy(), onl)
+    np.testing.assert_array_equal(moves.cpu().numpy(), omv)
+    for l in range(cfg.L):
+        np.testing.assert_array_equal(tensor_bf16_bits(kc[l]), caches[l])
+        np.testing.assert_array_equal(tensor_bf16_bits(vc[l]), caches[cfg.L + l])
+
+
+# ------------------------------------------------------------------ a2 attention
+def _attn_errors(o_gpu, o_ref):
+    diff = o_gpu - o_ref
+    return float(np.abs(diff).max()), float(np.linalg.norm(diff) / np.linalg.norm(o_ref))
+
+
+def _run_attention(core, b, num_ctas=0, samples=None, with_lse=True):
+    B, Hq, Hkv, d = b["B"], b["Hq"], b["Hkv"], b["d"]
+    q = b["q"][0].cuda()
+    kc = b["k_cache"][0].cuda()
+    vc = b["v_cache"][0].cuda()
+    par, to = _dev(b["parent"]), _dev(b["tree_off"])
+    mask, _, flags = core.tree_build_mask(par, to)
+    assert int(flags.abs().sum()) == 0
+    plan = core.AttnPlan(b["prefix_len"], b["tree_off"], Hq, Hkv, d, 64, num_ctas=num_ctas)
+    ws = core.alloc_workspace(plan.ws_bytes)
+    plan.upload(ws)
+    lse = torch.empty((b["NT"], Hq), dtype=torch.float32, device="cuda") if with_lse else None
+    out, _ = core.tree_verify_attention(plan, q, kc, vc, _dev(b["block_table"]), _dev(b["prefix_len"]), to, mask,
+                                        b["sm_scale"], ws, lse=lse)
+    torch.cuda.synchronize()
+    o_ref, lse_ref = OA.tree_verify_attention(
+        b["q"][0].double().numpy(), b["k_cache"][0].double().numpy(), b["v_cache"][0].double().numpy(),
+        b["block_table"], b["prefix_len"], b["tree_off"], mask.cpu().numpy().view(np.uint64), Hkv, 64,
+        b["sm_scale"], samples=samples)
+    og = out.float().cpu().numpy()
+    if samples is not None:
+        rows = np.concatenate([np.arange(b["tree_off"][s], b["tree_off"][s + 1]) for s in samples])
+        og, o_ref, lse_ref = og[rows], o_ref[rows], lse_ref[rows]
+        lg = lse.cpu().numpy()[rows] if with_lse else None
+    else:
+        lg = lse.cpu().numpy() if with_lse else None
+    return og, o_ref, lg, lse_ref, plan.info()
+
+
+ATTN_CASES = {
+    "tiny": CONFIGS["tiny"],
+    "c2_small": VerifyConfig("c2s", B=6, Hq=32, Hkv=8, d=128, V=10, L=1, prefix=("fixed", 1024),
+                             tree=("fixed", 16), seed=21),
+    "ragged_g4": VerifyConfig("rg4", B=20, Hq=32, Hkv=8, d=128, V=10, L=1,
+                              prefix=("lognormal", 150, 1.0, 0, 900), tree=("range", 1, 64), seed=22),
+    "g8_T64": VerifyConfig("g8", B=3, Hq=64, Hkv=8, d=128, V=10, L=1, prefix=("fixed", 700),
+                           tree=("fixed", 64), seed=23),
+    "d64_g2": VerifyConfig("d64", B=9, Hq=4, Hkv=2, d=64, V=10, L=1, prefix=("lognormal", 90, 1.2, 0, 500),
+                           tree=("range", 1, 64), seed=24),
+    "qscale8": VerifyConfig("q8", B=5, Hq=32, Hkv=8, d=128, V=10, L=1, prefix=("fixed", 333),
+                            tree=("range", 4, 40), q_scale=8.0, seed=25),
+}
+
+
+@pytest.mark.parametrize("case", list(ATTN_CASES))
+def test_attention_parity(cuda_lib, case):
+    b = make_verify_batch(ATTN_CASES[case], device="cpu", with_logits=False)
+    og, oref, lg, lref, info = _run_attention(cuda_lib, b)
+    mae, rel = _attn_errors(og, oref)
+    assert mae <= ATOL and rel <= RTOL_L2, (case, mae, rel, info)
+    np.testing.assert_allclose(lg, lref, atol=2e-2, rtol=1e-3)
+
+
+@pytest.mark.parametrize("num_ctas", [1, 3, 7, 29])
+def test_attention_split_kv_parity(cuda_lib, num_ctas):
+    """Few CTAs force split-KV cuts + the combine kernel (heavy-tailed prefixes)."""
+    cfg = VerifyConfig("split", B=7, Hq=32, Hkv=8, d=128, V=10, L=1, prefix=("lognormal", 600, 1.0, 0, 4000),
+                       tree=("range", 1, 64), seed=30 + num_ctas)
+    b = make_verify_batch(cfg, device="cpu", with_logits=False)
+    og, oref, lg, lref, info = _run_attention(cuda_lib, b, num_ctas=num_ctas)
+    mae, rel = _attn_errors(og, oref)
+    assert mae <= ATOL and rel <= RTOL_L2, (mae, rel, info)
+    np.testing.assert_allclose(lg, lref, atol=2e-2, rtol=1e-3)
+    if num_ctas > 1:
+        assert info["num_split_units"] > 0
+
+
+def test_attention_full_config2_sampled(cuda_lib):
+    """BASELINE configs[1] at full size (B=64, P=1K, T=16, 32/8 heads), in the launch
+    configuration bench.py times (plan over all SMs); oracle on 6 sampled samples."""
+    cfg = CONFIGS["c2"]
+    b = make_verify_batch(cfg, device="cuda", gen_device="cuda", layers=1, with_logits=False)
+    for k in ("q", "k_cache", "v_cache"):
+        b[k] = b[k].cpu()
+    samples = [0, 17, 31, 40, 58, 63]
+    og, oref, lg, lref, info = _run_attention(cuda_lib, b, samples=samples)
+    mae, rel = _attn_errors(og, oref)
+    assert mae <= ATOL and rel <= RTOL_L2, (mae, rel, info)
