@@ -1,0 +1,423 @@
+#!/usr/bin/env python
+"""Benchmark of the RLHFSpec verification hot path on B200 (contract: see DESIGN.md §6).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c5g8|tiny] [--impl ours|reference]
+
+A step = mask build + L x tree_verify_attention + tree_accept + kv_compact over one synthetic
+batch (all §8(a) rows of the verify path), through the C ABI. Metric: committed
+("verified-and-accepted") tokens per second, sum over ranks (weak scaling: every rank is an
+independent instance with its own samples). One JSON line is printed by rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+METRIC = "accepted tokens/sec per GPU (verify step) at 1/2/4/8 B200; % roofline"
+UNIT = "tokens/s"
+
+WORKLOAD_DESC = {
+    "c2": "BASELINE configs[1]: Llama-3-8B shapes (32 q / 8 kv heads, d=128, 32 layers, V=128256), "
+          "batch 64, prefix 1K, 16-node tree, greedy",
+    "c5g8": "BASELINE configs[4] per-GPU shard at 8 GPUs: Llama-3-70B shapes (64 q / 8 kv, d=128, 80 layers), "
+            "16 samples, prefix 8K, 64-node trees, greedy",
+    "tiny": "BASELINE configs[0]: 1 sample, prefix 32, 8-node tree, 1 head, d=64, V=1000, greedy",
+}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML during the timed region."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+        "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, device_index: int, period_s: float = 0.02):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period = period_s
+        self._stop = threading.Event()
+        self._ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception as e:  # pragma: no cover - only on boxes without NVML
+            self.err = str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, v in self.REASONS.items():
+                    if r & v and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._ok:
+            self.t.join()
+
+    def summary(self):
+        if not self._ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs"), d.get("bf16_tflops"), d.get("bf16_tflops_sustained"), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+def attention_algorithmic(b):
+    """per layer, bytes = sum_b 4*Hkv*d*(P+T) + 4*Hq*d*T + 8*T + 4*ceil((P+T)/64);
+    flops = 4*Hq*d*sum_i (P + |anc(i)|)."""
+    Hq, Hkv, d = b["Hq"], b["Hkv"], b["d"]
+    P = b["prefix_len"].astype(np.int64)
+    T = b["T"].astype(np.int64)
+    by = int(np.sum(4 * Hkv * d * (P + T) + 4 * Hq * d * T + 8 * T + 4 * ((P + T + 63) // 64)))
+    anc = np.zeros(len(b["parent"]), dtype=np.int64)     # |ancestors-or-self| = depth + 1
+    for i in range(b["B"]):
+        s, e = b["tree_off"][i], b["tree_off"][i + 1]
+        for x in range(s, e):
+            pa = b["parent"][x]
+            anc[x] = 1 if pa < 0 else anc[s + pa] + 1
+    fl = 0
+    for i in range(b["B"]):
+        s, e = b["tree_off"][i], b["tree_off"][i + 1]
+        fl += 4 * Hq * d * int(np.sum(P[i] + anc[s:e]))
+    return by, fl
+
+
+def cpu_baseline(host, cfg, budget_s=12.0):
+    """The oracle as it stands, on the host cores, on a bounded sample of the workload: whole
+    samples through all L layers of attention + acceptance + compaction."""
+    from oracle import accept as OAcc
+    from oracle import attention as OA
+    from oracle import compact as OC
+    from oracle import tree as OT
+    masks, _, _ = OT.batch_masks(host["parent"], host["tree_off"])
+    lg_bits = host["logits"].contiguous().view(torch.int16).numpy().view(np.uint16)
+    t0 = time.perf_counter()
+    tokens, done = 0, 0
+    L = host["q"].shape[0]
+    for s in range(host["B"]):
+        sl = slice(int(host["tree_off"][s]), int(host["tree_off"][s + 1]))
+        for l in range(L):
+            OA.tree_verify_attention(host["q"][l][sl].double().numpy(), host["kc_np"][l], host["vc_np"][l],
+                                     host["block_table"][s:s + 1], host["prefix_len"][s:s + 1],
+                                     np.array([0, sl.stop - sl.start]), masks[sl], cfg.Hkv, cfg.page_size,
+                                     host["sm_scale"])
+        acc, path, bonus, flags = OAcc.tree_accept(OAcc.GREEDY, lg_bits[sl], host["parent"][sl], host["token"][sl],
+                                                   np.array([0, sl.stop - sl.start]), host["gid"][s:s + 1], cfg.V)
+        OC.kv_compact([host["kc_np"][l] for l in range(L)] + [host["vc_np"][l] for l in range(L)],
+                      host["block_table"][s:s + 1], host["prefix_len"][s:s + 1], acc, path, cfg.page_size)
+        tokens += int(acc[0]) + 1
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return dict(value=tokens / dt, unit=UNIT, cores=1, kind="oracle",
+                sample=f"{done} of {host['B']} samples of the workload, all {L} layers + accept + compact, "
+                       f"numpy fp64 / C, single thread, {dt:.1f} s")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = _dist()
+    assert args.warmup >= 3, "W >= 3 warm-up steps"
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+    return run_ours(args, world, rank, local)
+
+
+def run_ours(args, world, rank, local):
+    from paper_2512_04752_b200 import core
+    from paper_2512_04752_b200.step import VerifyStep
+    from synth import CONFIGS, make_verify_batch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[args.config]
+    cfg = type(cfg)(**{**cfg.__dict__, "seed": cfg.seed + 1000 * rank})   # disjoint samples per rank
+    b = make_verify_batch(cfg, device=dev, gen_device=dev)
+    mode = {"greedy": core.GREEDY, "delta": core.SAMPLE_DELTA, "mss": core.SAMPLE_MSS}[cfg.mode]
+    step = VerifyStep(b, mode=mode, temperature=cfg.temperature)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for w in range(args.warmup):
+        step.device_step(seed=7, step=w)
+    barrier()
+    res = step.results()
+    tokens_per_step = int(np.sum(res["accepted_len"]) + b["B"])
+    accepted_drafts = int(np.sum(res["accepted_len"]))
+    info = step.plan.info()
+
+    # ---------------- device-timed region: exactly K steps ----------------
+    ev_a0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev_a1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches_per_step = 1 + step.L * (1 + (1 if info["num_split_units"] else 0)) + 1 + 1
+    sampler = ClockSampler(local)
+    barrier()
+    with sampler:
+        start.record(stream)
+        for k in range(args.steps):
+            mask, _, _ = core.tree_build_mask(step.parent, step.tree_off)
+            ev_a0[k].record(stream)
+            for l in range(step.L):
+                core.tree_verify_attention(step.plan, step.q[l], step.k_layers[l], step.v_layers[l],
+                                           step.block_table, step.prefix_len, step.tree_off, mask, step.sm_scale,
+                                           step.ws, out=step.attn_out[l])
+            ev_a1[k].record(stream)
+            core.tree_accept(step.mode, step.logits, step.parent, step.token, step.tree_off, step.gid,
+                             draft_probs=step.draft, temperature=step.temperature, seed=11, step=k,
+                             out=(step.acc, step.path, step.bonus, step.flags))
+            core.kv_compact(step.k_layers, step.v_layers, step.block_table, step.prefix_len, step.acc, step.path,
+                            step.ps, new_len=step.new_len)
+        end.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    elapsed_ms = start.elapsed_time(end)
+    attn_ms = sum(a.elapsed_time(c) for a, c in zip(ev_a0, ev_a1)) / args.steps
+    if world > 1:
+        t = torch.tensor([elapsed_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / args.steps
+    value = tokens_per_step * world * args.steps / (elapsed_ms / 1e3)
+
+    # ---------------- roofline of the dominant kernel (attention) ----------------
+    hbm, tc_burst, tc_sus, peak_src = _peaks()
+    host_meta = {k: b[k] for k in ("Hq", "Hkv", "d", "prefix_len", "T", "parent", "tree_off", "B")}
+    by, fl = attention_algorithmic(host_meta)
+    attn_launch_ms = attn_ms / step.L
+    achieved_gbs = by / (attn_launch_ms * 1e-3) / 1e9
+    achieved_tf = fl / (attn_launch_ms * 1e-3) / 1e12
+    t_hbm = by / (hbm * 1e9)
+    t_tc = fl / (tc_burst * 1e12)
+    bound = "hbm" if t_hbm >= t_tc else "tensor"
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    if bound == "hbm":
+        roof = {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved_gbs / hbm, 4), "traffic": traffic}
+    else:
+        roof = {"bound": "tensor", "achieved": round(achieved_tf, 1), "peak": tc_burst, "unit": "TFLOP/s",
+                "frac": round(achieved_tf / tc_burst, 4), "traffic": traffic}
+    roof.update({"kernel": "tree_attn_kernel (+combine)", "peak_source": peak_src,
+                 "algorithmic_bytes_per_launch": by, "algorithmic_flops_per_launch": fl,
+                 "launch_ms": round(attn_launch_ms, 5), "attention_share_of_step": round(attn_ms / ms_per_step, 4),
+                 "tensor_frac": round(achieved_tf / tc_burst, 4)})
+
+    # ---------------- end-to-end through the public API with host buffers ----------------
+    e2e = run_e2e(step, b, args.e2e_steps, tokens_per_step, world, dev, barrier)
+
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {WORKLOAD_DESC.get(args.config, args.config)}",
+                   "B": cfg.B, "Hq": cfg.Hq, "Hkv": cfg.Hkv, "d": cfg.d, "L": cfg.L, "V": cfg.V,
+                   "prefix": list(cfg.prefix), "tree": list(cfg.tree), "accept_mode": cfg.mode,
+                   "tokens_per_step": tokens_per_step, "accepted_drafts_per_step": accepted_drafts,
+                   "verified_tokens_per_step": int(b["NT"]),
+                   "l2": "inputs larger than L2: %.1f GB of distinct per-layer KV resident" %
+                         (2 * b["k_cache"].numel() * 2 / 1e9),
+                   "parallelism": f"dp{world} (independent sample-sharded instances, no collective)",
+                   "attn_plan": info},
+        "clocks": sampler.summary(),
+        "e2e": e2e,
+        "gpu_launches": launches_per_step * args.steps,
+        "roofline": roof,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = run_cpu_baseline(cfg, b)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def run_e2e(step, b, n_steps, tokens_per_step, world, dev, barrier):
+    """Same metric end to end: each step copies its inputs (Q of every layer, logits, tree
+    metadata) from pinned host memory, runs the step through the C ABI, and reads the results
+    (accepted_len, path, bonus, new_len) back to the host."""
+    from paper_2512_04752_b200 import core
+    stream = torch.cuda.current_stream()
+    h_q = torch.empty(step.q.shape, dtype=step.q.dtype, pin_memory=True)
+    h_q.copy_(step.q)
+    h_logits = torch.empty(step.logits.shape, dtype=step.logits.dtype, pin_memory=True)
+    h_logits.copy_(step.logits)
+    meta = [step.parent, step.token, step.tree_off, step.prefix_len, step.block_table, step.gid]
+    h_meta = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t) for t in meta]
+    h_draft = None
+    if step.draft is not None:
+        h_draft = torch.empty(step.draft.shape, dtype=step.draft.dtype, pin_memory=True).copy_(step.draft)
+    outs = [step.acc, step.path, step.bonus, step.new_len]
+    h_outs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in outs]
+    h2d = h_q.numel() * 2 + h_logits.numel() * 2 + sum(t.numel() * t.element_size() for t in h_meta)
+    if h_draft is not None:
+        h2d += h_draft.numel() * 4
+    d2h = sum(t.numel() * t.element_size() for t in h_outs)
+    barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for k in range(n_steps):
+        step.q.copy_(h_q, non_blocking=True)
+        step.logits.copy_(h_logits, non_blocking=True)
+        for t, h in zip(meta, h_meta):
+            t.copy_(h, non_blocking=True)
+        if h_draft is not None:
+            step.draft.copy_(h_draft, non_blocking=True)
+        step.device_step(seed=11, step=k)
+        for t, h in zip(outs, h_outs):
+            h.copy_(t, non_blocking=True)
+    e.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = s.elapsed_time(e)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"value": round(tokens_per_step * world * n_steps / (ms / 1e3), 1), "unit": UNIT,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": n_steps,
+            "ms_per_step": round(ms / n_steps, 3)}
+
+
+def run_cpu_baseline(cfg, b):
+    """Oracle on host cores over whole samples (bounded ~12 s)."""
+    L = b["q"].shape[0]
+    nsamp = min(b["B"], 8)
+    host = {k: b[k] for k in ("parent", "token", "tree_off", "prefix_len", "block_table", "gid", "sm_scale")}
+    ns = int(b["tree_off"][nsamp])
+    host["tree_off"] = b["tree_off"][:nsamp + 1]
+    host["parent"], host["token"] = b["parent"][:ns], b["token"][:ns]
+    host["prefix_len"], host["block_table"], host["gid"] = b["prefix_len"][:nsamp], b["block_table"][:nsamp], b["gid"][:nsamp]
+    host["B"] = nsamp
+    host["q"] = b["q"][:, :ns].cpu()
+    host["logits"] = b["logits"][:ns].cpu()
+    # only the pages of the sampled samples are copied (the cache itself stays on the GPU)
+    pages = np.unique(host["block_table"])
+    remap = {int(p): i for i, p in enumerate(pages)}
+    host["block_table"] = np.vectorize(lambda x: remap[int(x)])(host["block_table"]).astype(np.int32)
+    idx = torch.as_tensor(pages, device=b["k_cache"].device, dtype=torch.long)
+    host["kc_np"] = [b["k_cache"][l].index_select(0, idx).double().cpu().numpy() for l in range(L)]
+    host["vc_np"] = [b["v_cache"][l].index_select(0, idx).double().cpu().numpy() for l in range(L)]
+    return cpu_baseline(host, cfg)
+
+
+def run_reference(args, world, rank):
+    """Reference arm: the CPU oracle as it stands (no reference implementation exists for this
+    paper: /root/reference holds only the paper text). Rank 0 only."""
+    if rank != 0:
+        return
+    from synth import CONFIGS, make_verify_batch
+    cfg = CONFIGS[args.config]
+    # one whole sample per step (all L layers), drawn on the CPU with the same recipe
+    one = type(cfg)(**{**cfg.__dict__, "B": max(1, args.steps + args.warmup)})
+    b = make_verify_batch(one, device="cpu", spare_pages=0)
+    L = b["q"].shape[0]
+    from oracle import accept as OAcc
+    from oracle import attention as OA
+    from oracle import compact as OC
+    from oracle import tree as OT
+    masks, _, _ = OT.batch_masks(b["parent"], b["tree_off"])
+    lg_bits = b["logits"].contiguous().view(torch.int16).numpy().view(np.uint16)
+    kc = [b["k_cache"][l].double().numpy() for l in range(L)]
+    vc = [b["v_cache"][l].double().numpy() for l in range(L)]
+    tokens = 0
+    t_total = 0.0
+    budget_s = float(os.environ.get("RS_REF_BUDGET_S", "150"))
+    layers_run = L
+    for s in range(args.warmup + args.steps):
+        sl = slice(int(b["tree_off"][s]), int(b["tree_off"][s + 1]))
+        t0 = time.perf_counter()
+        ta = time.perf_counter()
+        for l in range(layers_run):
+            OA.tree_verify_attention(b["q"][l][sl].double().numpy(), kc[l], vc[l], b["block_table"][s:s + 1],
+                                     b["prefix_len"][s:s + 1], np.array([0, sl.stop - sl.start]), masks[sl], cfg.Hkv,
+                                     cfg.page_size, b["sm_scale"])
+        t_attn = (time.perf_counter() - ta) * L / layers_run        # layers not run: extrapolated
+        acc, path, _, _ = OAcc.tree_accept(OAcc.GREEDY, lg_bits[sl], b["parent"][sl], b["token"][sl],
+                                           np.array([0, sl.stop - sl.start]), b["gid"][s:s + 1], cfg.V)
+        OC.kv_compact(kc + vc, b["block_table"][s:s + 1], b["prefix_len"][s:s + 1], acc, path, cfg.page_size)
+        dt = (time.perf_counter() - t0) - (t_attn * layers_run / L) + t_attn
+        if s == 0 and dt * (args.warmup + args.steps) > budget_s:
+            layers_run = max(1, int(L * budget_s / (dt * (args.warmup + args.steps))))
+        if s >= args.warmup:
+            t_total += dt
+            tokens += int(acc[0]) + 1
+    value = tokens / t_total
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t_total / args.steps, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"{args.config}: {WORKLOAD_DESC.get(args.config, args.config)}",
+                       "step": "one whole sample of the workload through all layers (bounded sample)"},
+            "cpu_baseline": {"value": round(value, 2), "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{args.steps} whole samples; attention timed on {layers_run} of {L} layers "
+                                       f"per sample and scaled to {L}; accept + compact in full; numpy fp64 + C, "
+                                       f"single thread"},
+            "e2e": {"value": round(value, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

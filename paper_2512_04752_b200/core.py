@@ -43,6 +43,7 @@ _sig("rs_attn_plan_workspace_bytes", _sz, _P)
 _sig("rs_attn_plan_upload", _i32, _P, _P, _sz, _P)
 _sig("rs_attn_plan_info", _i32, _P, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32))
 _sig("rs_attn_plan_destroy", None, _P)
+_sig("rs_attn_plan_items", _i32, _P, _P, _P)
 _sig("rs_tree_verify_attention", _i32, _P, _P, _P, _P, _i64, _P, _i32, _P, _P, _P, _i32, _i32, _i32,
      _i32, _i32, _f32, _P, _P, _P, _sz, _P)
 _sig("rs_tree_accept", _i32, _i32, _P, _i32, _P, _P, _P, _P, _P, _i32, _i32, _f32, _u64, _u64, _P, _P,
@@ -113,6 +114,14 @@ class AttnPlan:
         _check(_lib.rs_attn_plan_info(self.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)),
                "rs_attn_plan_info")
         return dict(num_ctas=a.value, num_items=b.value, num_split_units=c.value)
+
+    def schedule(self):
+        """(cta_off [num_ctas+1], items [num_items, 6]) as numpy arrays."""
+        inf = self.info()
+        cta = np.zeros(inf["num_ctas"] + 1, dtype=np.int32)
+        items = np.zeros((inf["num_items"], 6), dtype=np.int32)
+        _check(_lib.rs_attn_plan_items(self.handle, _ptr(cta), _ptr(items)), "rs_attn_plan_items")
+        return cta, items
 
     def upload(self, ws: torch.Tensor, stream=None):
         _check(_lib.rs_attn_plan_upload(self.handle, _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)),

@@ -510,36 +510,47 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
     // Greedy contiguous fill: units are poured, in order, into CTAs of capacity `target`
     // (block units incl. a per-item overhead); a unit that overflows a CTA is cut (split-KV)
     // and continues on the next one. Parts are never smaller than kMinPart blocks.
-    const long long target = (W + n_ctas - 1) / n_ctas;
+    // CTA c owns the work interval [c*W/n, (c+1)*W/n) of the concatenated unit stream, so
+    // rounding never accumulates: a CTA that is left slightly under/over full is absorbed by
+    // the next boundary.
+    // (Each extra split part costs another kOvhBlocks, so the remaining work is re-divided over
+    // the remaining CTAs whenever a new CTA is entered.)
+    long long W_eff = W;
     std::vector<std::vector<WorkItem>> per_cta(n_ctas);
     int cta = 0;
-    long long load = 0;
+    long long pos = 0;
+    long long end = (W_eff + n_ctas - 1) / n_ctas;
+    auto next_cta = [&]() {
+        ++cta;
+        end = pos + (W_eff - pos + (n_ctas - cta) - 1) / (n_ctas - cta);
+    };
     int n_parts = 0;
     for (const U& u : units) {
         int rem = u.nblk, start = 0;
         std::vector<std::pair<int, int>> where;   // (cta, index) of this unit's parts
         while (rem > 0) {
-            const long long cap = target - load - kOvhBlocks;
+            if (cta < n_ctas - 1 && pos >= end) { next_cta(); continue; }
+            const long long room = (cta == n_ctas - 1) ? (1ll << 60) : end - pos - kOvhBlocks;
             int take;
-            if (cta == n_ctas - 1 || cap >= rem) {
+            if (room >= rem) {
                 take = rem;
-            } else if (cap < kMinPart && load > 0) {
-                ++cta;
-                load = 0;
-                continue;
+            } else if (room < kMinPart) {
+                if (per_cta[cta].empty()) {
+                    take = rem;               // never leave a CTA without work
+                } else {
+                    next_cta();               // too little room for a useful part: next CTA
+                    continue;
+                }
             } else {
-                take = (int)std::max<long long>(cap, kMinPart);
+                take = (int)room;
                 if (rem - take < kMinPart) take = (rem >= 2 * kMinPart) ? rem - kMinPart : rem;
             }
+            if (!where.empty()) W_eff += kOvhBlocks;   // an extra part of a split unit
             where.push_back({cta, (int)per_cta[cta].size()});
             per_cta[cta].push_back({u.b, u.kvh, u.mtile, start, start + take, -1});
-            load += take + kOvhBlocks;
+            pos += take + kOvhBlocks;
             start += take;
             rem -= take;
-            if (load >= target && cta < n_ctas - 1) {
-                ++cta;
-                load = 0;
-            }
         }
         if (where.size() > 1) {
             pl->units.push_back({u.b, u.kvh, u.mtile, (int)where.size(), n_parts, 0});
@@ -591,6 +602,13 @@ extern "C" rs_status rs_attn_plan_info(const rs_attn_plan* plan, int32_t* num_ct
     if (num_ctas) *num_ctas = plan->n_ctas;
     if (num_items) *num_items = (int32_t)plan->items.size();
     if (num_split_units) *num_split_units = (int32_t)plan->units.size();
+    return RS_OK;
+}
+
+extern "C" rs_status rs_attn_plan_items(const rs_attn_plan* plan, int32_t* cta_off, int32_t* items) {
+    RS_REQUIRE(plan, RS_ERR_INVALID_ARG, "rs_attn_plan_items: null plan");
+    if (cta_off) memcpy(cta_off, plan->cta_off.data(), sizeof(int32_t) * plan->cta_off.size());
+    if (items && !plan->items.empty()) memcpy(items, plan->items.data(), sizeof(WorkItem) * plan->items.size());
     return RS_OK;
 }
 

@@ -1,0 +1,90 @@
+"""Host-side library logic on CPU (no GPU): the C ABI loads and exports every declared symbol;
+the attention schedule covers every (sample, kv-head, m-tile, key block) exactly once and is
+balanced."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "rlhfspec_core.h")
+
+
+@pytest.fixture(scope="module")
+def core():
+    from paper_2512_04752_b200 import build
+    build.build(verbose=False)
+    from paper_2512_04752_b200 import core as c
+    return c
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rs_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol(core):
+    out = subprocess.run(["nm", "-D", "--defined-only", core.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(l.split()[-1] for l in out.splitlines() if " T " in l)
+    missing = [s for s in _declared() if s not in exported]
+    assert not missing, missing
+    assert core.version().startswith("rlhfspec_core")
+
+
+def _check_plan(core, P, T, Hq, Hkv, d=128, n=148):
+    to = np.concatenate([[0], np.cumsum(T)]).astype(np.int32)
+    pl = core.AttnPlan(P, to, Hq, Hkv, d, 64, num_ctas=n)
+    cta, items = pl.schedule()
+    info = pl.info()
+    assert cta[0] == 0 and cta[-1] == len(items) and np.all(np.diff(cta) >= 0)
+    g = Hq // Hkv
+    cover = {}
+    for b_, kvh, mt, b0, b1, part in items:
+        cover.setdefault((b_, kvh, mt), []).append((b0, b1, part))
+    nsplit = 0
+    for b in range(len(P)):
+        nblk = (P[b] + T[b] + 63) // 64
+        for kvh in range(Hkv):
+            for mt in range((T[b] * g + 127) // 128):
+                parts = sorted(cover.pop((b, kvh, mt)))
+                assert parts[0][0] == 0 and parts[-1][1] == nblk
+                assert all(x[1] == y[0] for x, y in zip(parts, parts[1:]))
+                if len(parts) > 1:
+                    nsplit += 1
+                    assert all(p[2] >= 0 for p in parts)
+                else:
+                    assert parts[0][2] == -1
+    assert not cover
+    assert nsplit == info["num_split_units"]
+    loads = [sum(items[i, 4] - items[i, 3] + 2 for i in range(cta[c], cta[c + 1])) for c in range(len(cta) - 1)]
+    return np.array(loads), info, pl
+
+
+def test_plan_covers_and_balances_config2(core):
+    loads, info, _ = _check_plan(core, np.full(64, 1024), np.full(64, 16), 32, 8)
+    assert loads.max() <= 1.2 * loads.mean()
+
+
+def test_plan_long_tail_and_gqa8(core):
+    from synth import CONFIGS, draw_prefix_lengths
+    rng = np.random.default_rng(0)
+    P = draw_prefix_lengths(rng, CONFIGS["c3"])
+    T = rng.integers(4, 65, size=len(P))
+    loads, _, _ = _check_plan(core, P, T, 32, 8)
+    assert loads.max() <= 1.05 * loads.mean()
+    loads, _, _ = _check_plan(core, np.full(16, 8192), np.full(16, 64), 64, 8)
+    assert loads.max() <= 1.05 * loads.mean()
+    for n in (1, 3, 7):
+        _check_plan(core, np.array([5000, 0, 20]), np.array([3, 37, 1]), 32, 8, n=n)
+
+
+def test_plan_rejects_bad_trees(core):
+    with pytest.raises(core.RSError):
+        core.AttnPlan([10], [0, 65], 32, 8, 128, 64, 4)
+    with pytest.raises(core.RSError):
+        core.AttnPlan([10], [0, 0], 32, 8, 128, 64, 4)
+    with pytest.raises(core.RSError):
+        core.AttnPlan([10], [0, 4], 32, 8, 96, 64, 4)
