@@ -96,10 +96,14 @@ rs_status rs_attn_plan_upload(const rs_attn_plan* plan, void* ws, size_t ws_byte
 rs_status rs_attn_plan_info(const rs_attn_plan* plan, int32_t* num_ctas, int32_t* num_items,
                             int32_t* num_split_units);
 /* Copy the schedule out (for inspection / tests): cta_off host int32 [num_ctas+1] (items of
- * CTA c are [cta_off[c], cta_off[c+1])), items host int32 [num_items, 6] =
- * (sample, kv_head, m_tile, first_block, end_block, partial_slot or -1). Either may be NULL. */
+ * CTA c are [cta_off[c], cta_off[c+1])), items host int32 [num_items, 8] =
+ * (sample, kv_head, m_tile, first_block, end_block, partial_slot or -1, rows per TMEM
+ * sub-partition R, split unit or -1). Either may be NULL. */
 rs_status rs_attn_plan_items(const rs_attn_plan* plan, int32_t* cta_off, int32_t* items);
 void rs_attn_plan_destroy(rs_attn_plan* plan);
+/* Profiling hook: when buf (device, >= num_ctas*256*8*8 bytes) is set, every attention launch
+ * records clock64() per (CTA, block, event) — see csrc/attention.cu. NULL disables. */
+rs_status rs_attn_set_trace(void* buf, size_t bytes);
 
 /* q        device bf16 [NT, Hq, head_dim] (post-RoPE)
  * k_pages, v_pages device bf16 [num_pages, Hkv, page_size, head_dim] (one layer)
@@ -116,6 +120,16 @@ rs_status rs_tree_verify_attention(const rs_attn_plan* plan, const void* q, cons
                                    const uint64_t* tree_mask, int32_t B, int32_t Hq, int32_t Hkv,
                                    int32_t head_dim, int32_t page_size, float sm_scale, void* out,
                                    float* lse, void* ws, size_t ws_bytes, void* stream);
+
+/* All L layers of one verify step in one call (same plan, tree mask and workspace; per-layer
+ * host arrays of device pointers q_layers/k_layers/v_layers/out_layers[L], lse_layers[L] or
+ * NULL). Launches L kernels back to back on `stream`. */
+rs_status rs_tree_verify_attention_layers(
+    const rs_attn_plan* plan, int32_t L, const void* const* q_layers, const void* const* k_layers,
+    const void* const* v_layers, int64_t num_pages, const int32_t* block_table, int32_t max_pages,
+    const int32_t* prefix_len, const int32_t* tree_off, const uint64_t* tree_mask, int32_t B, int32_t Hq,
+    int32_t Hkv, int32_t head_dim, int32_t page_size, float sm_scale, void* const* out_layers,
+    float* const* lse_layers, void* ws, size_t ws_bytes, void* stream);
 
 /* ===================================================================================== a3
  * rs_tree_accept — walk each sample's tree from the root and return its longest accepted

@@ -44,8 +44,11 @@ _sig("rs_attn_plan_upload", _i32, _P, _P, _sz, _P)
 _sig("rs_attn_plan_info", _i32, _P, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32))
 _sig("rs_attn_plan_destroy", None, _P)
 _sig("rs_attn_plan_items", _i32, _P, _P, _P)
+_sig("rs_attn_set_trace", _i32, _P, _sz)
 _sig("rs_tree_verify_attention", _i32, _P, _P, _P, _P, _i64, _P, _i32, _P, _P, _P, _i32, _i32, _i32,
      _i32, _i32, _f32, _P, _P, _P, _sz, _P)
+_sig("rs_tree_verify_attention_layers", _i32, _P, _i32, _P, _P, _P, _i64, _P, _i32, _P, _P, _P, _i32, _i32,
+     _i32, _i32, _i32, _f32, _P, _P, _P, _sz, _P)
 _sig("rs_tree_accept", _i32, _i32, _P, _i32, _P, _P, _P, _P, _P, _i32, _i32, _f32, _u64, _u64, _P, _P,
      _P, _P, _P, _sz, _P)
 _sig("rs_philox4x32_10", _i32, _P, _i64, _P, _P, _P)
@@ -84,12 +87,14 @@ def _host_i32(x):
 
 
 # ------------------------------------------------------------------ a1
-def tree_build_mask(parent: torch.Tensor, tree_off: torch.Tensor, stream=None):
+def tree_build_mask(parent: torch.Tensor, tree_off: torch.Tensor, stream=None, out=None):
     B = tree_off.numel() - 1
     NT = parent.numel()
-    mask = torch.empty(NT, dtype=torch.int64, device=parent.device)
-    depth = torch.empty(NT, dtype=torch.int32, device=parent.device)
-    flags = torch.empty(B, dtype=torch.int32, device=parent.device)
+    if out is None:
+        out = (torch.empty(NT, dtype=torch.int64, device=parent.device),
+               torch.empty(NT, dtype=torch.int32, device=parent.device),
+               torch.empty(B, dtype=torch.int32, device=parent.device))
+    mask, depth, flags = out
     _check(_lib.rs_tree_build_mask(_ptr(parent), _ptr(tree_off), B, _ptr(mask), _ptr(depth), _ptr(flags),
                                    _stream(stream)), "rs_tree_build_mask")
     return mask, depth, flags
@@ -116,10 +121,10 @@ class AttnPlan:
         return dict(num_ctas=a.value, num_items=b.value, num_split_units=c.value)
 
     def schedule(self):
-        """(cta_off [num_ctas+1], items [num_items, 6]) as numpy arrays."""
+        """(cta_off [num_ctas+1], items [num_items, 7]) as numpy arrays."""
         inf = self.info()
         cta = np.zeros(inf["num_ctas"] + 1, dtype=np.int32)
-        items = np.zeros((inf["num_items"], 6), dtype=np.int32)
+        items = np.zeros((inf["num_items"], 8), dtype=np.int32)
         _check(_lib.rs_attn_plan_items(self.handle, _ptr(cta), _ptr(items)), "rs_attn_plan_items")
         return cta, items
 
@@ -132,6 +137,12 @@ class AttnPlan:
         if h:
             _lib.rs_attn_plan_destroy(h)
             self.handle = None
+
+
+def attn_set_trace(buf):
+    """Profiling: per-(CTA, block, event) clock64 timestamps of every attention launch (None = off)."""
+    _check(_lib.rs_attn_set_trace(_ptr(buf), 0 if buf is None else buf.numel() * buf.element_size()),
+           "rs_attn_set_trace")
 
 
 def alloc_workspace(nbytes: int, device="cuda") -> torch.Tensor:
@@ -149,6 +160,33 @@ def tree_verify_attention(plan: AttnPlan, q, k_pages, v_pages, block_table, pref
         plan.page_size, float(sm_scale), _ptr(out), _ptr(lse), _ptr(ws), ws.numel() * ws.element_size(),
         _stream(stream)), "rs_tree_verify_attention")
     return out, lse
+
+
+def ptr_array(tensors):
+    """Host array of device pointers (for the *_layers entry points)."""
+    return (_P * len(tensors))(*[t.data_ptr() for t in tensors])
+
+
+class AttentionLayersCall:
+    """Pre-marshalled rs_tree_verify_attention_layers call for fixed buffers (one ctypes call
+    per step launches all L layers)."""
+
+    def __init__(self, plan: AttnPlan, q_layers, k_layers, v_layers, block_table, prefix_len, tree_off, tree_mask,
+                 sm_scale, ws, out_layers, lse_layers=None):
+        L = len(q_layers)
+        NT, Hq, d = q_layers[0].shape
+        self._keep = (q_layers, k_layers, v_layers, out_layers, lse_layers, ws, block_table, prefix_len, tree_off,
+                      tree_mask)
+        self._arrays = (ptr_array(q_layers), ptr_array(k_layers), ptr_array(v_layers), ptr_array(out_layers),
+                        ptr_array(lse_layers) if lse_layers is not None else None)
+        qa, ka, va, oa, la = self._arrays
+        self.args = [plan.handle, L, qa, ka, va, k_layers[0].shape[0], _ptr(block_table), block_table.shape[1],
+                     _ptr(prefix_len), _ptr(tree_off), _ptr(tree_mask), plan.B, Hq, plan.Hkv, d, plan.page_size,
+                     float(sm_scale), oa, la, _ptr(ws), ws.numel() * ws.element_size()]
+        self.plan = plan
+
+    def __call__(self, stream=None):
+        _check(_lib.rs_tree_verify_attention_layers(*self.args, _stream(stream)), "rs_tree_verify_attention_layers")
 
 
 # ------------------------------------------------------------------ a3

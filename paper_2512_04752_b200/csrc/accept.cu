@@ -1,24 +1,34 @@
 // a3: tree acceptance (readings Z5-Z8, Z15, "Bit-exact sampling").
 //
-// One CTA per sample walks its tree from the root. Only the rows of the nodes on the walk
-// are read (the algorithmic bytes are the visited rows): at node c the CTA
-// streams row c of the target logits (and, for MSS, the draft row) with 128-bit loads,
-// reduces with warp shuffles + shared memory, decides the child in one thread and moves on.
-//   GREEDY: block argmax (ties -> lowest id); accept the lowest-index child whose token
-//           equals it; bonus = argmax at the last node.
+// One thread-block CLUSTER per sample walks its tree from the root. The vocabulary is split
+// into contiguous slices, one per CTA of the cluster; only the rows of the nodes on the walk
+// are read (the algorithmic bytes are the visited rows), with 128-bit loads,
+// four in flight per thread. Every reduction (argmax, max, integer sums, 128-bit max) is done
+// per CTA with warp shuffles + shared memory and then all-reduced across the cluster through
+// distributed shared memory, so every CTA takes the same decision; the walk itself (child
+// tests, residual bookkeeping) is replicated.
+//   GREEDY: argmax (ties -> lowest id); accept the lowest-index child whose token equals it;
+//           bonus = argmax at the last node.
 //   DELTA / MSS: integer weights w_v (exp_spec), Philox uniforms, 128-bit exact tests; the
 //           residual after a rejection is kept implicitly (DELTA: excluded-token list; MSS:
-//           the chain of (Z, shift) scalars, re-applied per element when the row is re-read).
+//           the chain of (Z, shift) scalars, re-applied per element when the row is re-read);
+//           bonus by inverse CDF: cluster prefix over slice totals, then tile sums + a block
+//           scan inside the owning CTA.
 #include "common.cuh"
 #include "sampling.cuh"
+#include "sm100_ptx.cuh"
 
 namespace {
 
 using rs::u128;
-constexpr int kThreads = 512;
+using namespace rs::ptx;
+constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxTiles = 512;          // inverse-CDF tiles of kThreads*8 elements (V <= 2M)
-constexpr int kMaxChain = RS_MAX_TREE;  // residual steps per node (<= children)
+constexpr int kUnroll = 4;
+constexpr int kTileVecs = kThreads;        // 8-element vectors per inverse-CDF tile
+constexpr int kMaxTiles = 256;             // tiles per CTA slice
+constexpr int kMaxCluster = 8;
+constexpr int kMaxChain = RS_MAX_TREE;
 
 struct RowView {
     const void* base;
@@ -28,48 +38,82 @@ struct RowView {
     bool vec_ok;    // 16-byte aligned rows with V a multiple of the vector width
 };
 
-// Elements 8*i .. 8*i+7 of the row; n = number valid (elements past V are not touched).
-__device__ __forceinline__ int load8(const RowView& rv, int i, float (&x)[8]) {
-    int v0 = i * 8;
-    int n = min(8, rv.V - v0);
+struct Raw8 {       // one 8-element vector as loaded (bf16: 4 words; fp32: 8 words)
+    uint4 a, b;
+};
+
+__device__ __forceinline__ Raw8 load_raw(const RowView& rv, int i) {
+    Raw8 r;
+    const int v0 = i * 8;
     if (rv.dtype == RS_DTYPE_BF16) {
         const uint16_t* p = reinterpret_cast<const uint16_t*>(rv.base) + rv.row * (int64_t)rv.V + v0;
-        if (rv.vec_ok && n == 8) {
-            uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
-            uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                x[2 * j] = __uint_as_float(w[j] << 16);
-                x[2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
-            }
+        if (rv.vec_ok && v0 + 8 <= rv.V) {
+            r.a = __ldg(reinterpret_cast<const uint4*>(p));
         } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) x[j] = (j < n) ? rs::bf16_bits_to_f32(__ldg(p + j)) : 0.0f;
+            uint32_t w[4] = {0, 0, 0, 0};
+            for (int j = 0; j < 8 && v0 + j < rv.V; ++j) w[j >> 1] |= (uint32_t)__ldg(p + j) << (16 * (j & 1));
+            r.a = make_uint4(w[0], w[1], w[2], w[3]);
         }
+        r.b = make_uint4(0, 0, 0, 0);
     } else {
         const float* p = reinterpret_cast<const float*>(rv.base) + rv.row * (int64_t)rv.V + v0;
-        if (rv.vec_ok && n == 8) {
-            float4 a = __ldg(reinterpret_cast<const float4*>(p));
-            float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
-            x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
-            x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+        if (rv.vec_ok && v0 + 8 <= rv.V) {
+            r.a = __ldg(reinterpret_cast<const uint4*>(p));
+            r.b = __ldg(reinterpret_cast<const uint4*>(p) + 1);
         } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) x[j] = (j < n) ? __ldg(p + j) : 0.0f;
+            uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int j = 0; j < 8 && v0 + j < rv.V; ++j) w[j] = __float_as_uint(__ldg(p + j));
+            r.a = make_uint4(w[0], w[1], w[2], w[3]);
+            r.b = make_uint4(w[4], w[5], w[6], w[7]);
         }
     }
-    return n;
+    return r;
+}
+
+__device__ __forceinline__ float raw_elem(const Raw8& r, int dtype, int j) {
+    if (dtype == RS_DTYPE_BF16) {
+        const uint32_t w = j < 2 ? r.a.x : j < 4 ? r.a.y : j < 6 ? r.a.z : r.a.w;
+        return __uint_as_float((j & 1) ? (w & 0xFFFF0000u) : (w << 16));
+    }
+    const uint32_t w = j == 0 ? r.a.x : j == 1 ? r.a.y : j == 2 ? r.a.z : j == 3 ? r.a.w
+                     : j == 4 ? r.b.x : j == 5 ? r.b.y : j == 6 ? r.b.z : r.b.w;
+    return __uint_as_float(w);
+}
+
+// Visit every element of this CTA's slice [vbeg, vend) (in 8-vectors) of row lv (and, if
+// with_q, the same elements of row qv): fn(v, x, q). kUnroll loads in flight per thread.
+template <int kUnroll = 4, typename F>
+__device__ __forceinline__ void for_slice(const RowView& lv, const RowView& qv, bool with_q, int vbeg, int vend,
+                                          F fn) {
+    for (int i0 = vbeg + (int)threadIdx.x; i0 < vend; i0 += kUnroll * kThreads) {
+        Raw8 x[kUnroll], q[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const int i = i0 + u * kThreads;
+            if (i < vend) {
+                x[u] = load_raw(lv, i);
+                if (with_q) q[u] = load_raw(qv, i);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const int i = i0 + u * kThreads;
+            if (i < vend) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int v = i * 8 + j;
+                    if (v < lv.V) fn(v, raw_elem(x[u], lv.dtype, j), with_q ? raw_elem(q[u], RS_DTYPE_F32, j) : 0.0f);
+                }
+            }
+        }
+    }
 }
 
 struct Smem {
-    float f[kWarps];
-    int idx[kWarps];
-    unsigned long long u[kWarps];
-    unsigned long long uhi[kWarps];
-    int flag;
+    unsigned long long red[kWarps][2];
+    unsigned long long xch[2][kMaxCluster > 2 ? 4 : 4];   // cluster exchange slots (double-buffered)
     unsigned long long tile_sum[kMaxTiles];
     unsigned long long scan[kWarps];
-    // per-sample state
     int parent[RS_MAX_TREE];
     int token[RS_MAX_TREE];
     int excluded[RS_MAX_TREE];
@@ -77,65 +121,61 @@ struct Smem {
     unsigned long long chainZ[kMaxChain];
     int chainS[kMaxChain];
     int n_chain;
+    int flag;
     int bcast_i;
     unsigned long long bcast_u;
     int bonus_v;
 };
 
-__device__ __forceinline__ float block_max_f(float v, bool bad, Smem& sm, bool* any_bad) {
-    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    unsigned b = __ballot_sync(0xffffffffu, bad);
-    __syncthreads();
-    if (lane == 0) { sm.f[w] = v; sm.idx[w] = b ? 1 : 0; }
-    __syncthreads();
-    float r = sm.f[0];
-    int anyb = sm.idx[0];
-    for (int i = 1; i < kWarps; ++i) { r = fmaxf(r, sm.f[i]); anyb |= sm.idx[i]; }
-    *any_bad = anyb != 0;
-    return r;
+// Orderable 32-bit key of a float (larger float -> larger key).
+__device__ __forceinline__ uint32_t fkey(float f) {
+    const uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float fkey_inv(uint32_t k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
 }
 
-// (value, index) argmax with lowest index on ties.
-__device__ __forceinline__ void argmax_merge(float& v, int& i, float v2, int i2) {
-    if (v2 > v || (v2 == v && i2 < i)) { v = v2; i = i2; }
+enum Op { OP_MAX = 0, OP_SUM = 1, OP_OR = 2 };
+
+__device__ __forceinline__ unsigned long long op_apply(int op, unsigned long long a, unsigned long long b) {
+    return op == OP_MAX ? (a > b ? a : b) : op == OP_SUM ? a + b : (a | b);
 }
 
-__device__ __forceinline__ int block_argmax(float v, int i, bool bad, Smem& sm, bool* any_bad) {
-    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+// Block + cluster all-reduce of two u64 values (ops op0, op1); identical result in every thread
+// of every CTA of the cluster. `phase` alternates the exchange slot (see cluster_sync_all).
+__device__ __forceinline__ void allreduce2(unsigned long long& v0, int op0, unsigned long long& v1, int op1, Smem& sm,
+                                           int& phase) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
-        float v2 = __shfl_xor_sync(0xffffffffu, v, o);
-        int i2 = __shfl_xor_sync(0xffffffffu, i, o);
-        argmax_merge(v, i, v2, i2);
+        v0 = op_apply(op0, v0, __shfl_xor_sync(0xffffffffu, v0, o));
+        v1 = op_apply(op1, v1, __shfl_xor_sync(0xffffffffu, v1, o));
     }
-    unsigned b = __ballot_sync(0xffffffffu, bad);
     __syncthreads();
-    if (lane == 0) { sm.f[w] = v; sm.idx[w] = i; sm.u[w] = b ? 1ull : 0ull; }
+    if (lane == 0) { sm.red[w][0] = v0; sm.red[w][1] = v1; }
     __syncthreads();
-    float rv = sm.f[0];
-    int ri = sm.idx[0];
-    unsigned long long anyb = sm.u[0];
-    for (int k = 1; k < kWarps; ++k) { argmax_merge(rv, ri, sm.f[k], sm.idx[k]); anyb |= sm.u[k]; }
-    *any_bad = anyb != 0;
-    return ri;
+    unsigned long long a = sm.red[0][0], b = sm.red[0][1];
+    for (int k = 1; k < kWarps; ++k) { a = op_apply(op0, a, sm.red[k][0]); b = op_apply(op1, b, sm.red[k][1]); }
+    const uint32_t cs = cluster_size();
+    if (cs > 1) {
+        if (threadIdx.x == 0) { sm.xch[phase][0] = a; sm.xch[phase][1] = b; }
+        cluster_sync_all();
+        const uint32_t me = cluster_rank();
+        for (uint32_t c = 0; c < cs; ++c) {
+            if (c == me) continue;
+            a = op_apply(op0, a, ld_dsmem_u64(&sm.xch[phase][0], c));
+            b = op_apply(op1, b, ld_dsmem_u64(&sm.xch[phase][1], c));
+        }
+        phase ^= 1;
+    }
+    v0 = a;
+    v1 = b;
 }
 
-__device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long v, Smem& sm) {
-    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    __syncthreads();
-    if (lane == 0) sm.u[w] = v;
-    __syncthreads();
-    unsigned long long r = 0;
-    for (int k = 0; k < kWarps; ++k) r += sm.u[k];
-    return r;
-}
-
-__device__ __forceinline__ u128 block_max_u128(u128 v, Smem& sm) {
-    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+// 128-bit max all-reduce (hi/lo lexicographic).
+__device__ __forceinline__ u128 allreduce_max128(u128 v, Smem& sm, int& phase) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         unsigned long long hi = __shfl_xor_sync(0xffffffffu, (unsigned long long)(v >> 64), o);
@@ -144,20 +184,32 @@ __device__ __forceinline__ u128 block_max_u128(u128 v, Smem& sm) {
         if (v2 > v) v = v2;
     }
     __syncthreads();
-    if (lane == 0) { sm.uhi[w] = (unsigned long long)(v >> 64); sm.u[w] = (unsigned long long)v; }
+    if (lane == 0) { sm.red[w][0] = (unsigned long long)(v >> 64); sm.red[w][1] = (unsigned long long)v; }
     __syncthreads();
     u128 r = 0;
     for (int k = 0; k < kWarps; ++k) {
-        u128 x = ((u128)sm.uhi[k] << 64) | sm.u[k];
+        u128 x = ((u128)sm.red[k][0] << 64) | sm.red[k][1];
         if (x > r) r = x;
+    }
+    const uint32_t cs = cluster_size();
+    if (cs > 1) {
+        if (threadIdx.x == 0) { sm.xch[phase][0] = (unsigned long long)(r >> 64); sm.xch[phase][1] = (unsigned long long)r; }
+        cluster_sync_all();
+        const uint32_t me = cluster_rank();
+        for (uint32_t c = 0; c < cs; ++c) {
+            if (c == me) continue;
+            u128 x = ((u128)ld_dsmem_u64(&sm.xch[phase][0], c) << 64) | ld_dsmem_u64(&sm.xch[phase][1], c);
+            if (x > r) r = x;
+        }
+        phase ^= 1;
     }
     return r;
 }
 
 // Current residual weight of a token from its base weight: DELTA zeroes excluded tokens;
 // MSS re-applies the recorded residual steps w <- max(w*Zq - qw*Z_j, 0) >> s_j.
-__device__ __forceinline__ uint64_t residual_weight(int mode, uint64_t w, uint64_t qw, int tok,
-                                                    uint64_t Zq, const Smem& sm) {
+__device__ __forceinline__ uint64_t residual_weight(int mode, uint64_t w, uint64_t qw, int tok, uint64_t Zq,
+                                                    const Smem& sm) {
     if (mode == RS_ACCEPT_SAMPLE_DELTA) {
         for (int e = 0; e < sm.n_excluded; ++e)
             if (sm.excluded[e] == tok) return 0;
@@ -171,100 +223,93 @@ __device__ __forceinline__ uint64_t residual_weight(int mode, uint64_t w, uint64
     return w;
 }
 
-__global__ void __launch_bounds__(kThreads)
-tree_accept_kernel(int mode, const void* __restrict__ logits, int dtype,
-                   const float* __restrict__ draft, const int32_t* __restrict__ parent,
-                   const int32_t* __restrict__ token, const int32_t* __restrict__ tree_off,
-                   const int64_t* __restrict__ gid, int V, float inv_tau, uint64_t seed,
-                   uint64_t step, int32_t* __restrict__ acc_out, int32_t* __restrict__ path_out,
-                   int32_t* __restrict__ bonus_out, int32_t* __restrict__ flags_out,
-                   bool logits_vec_ok, bool draft_vec_ok) {
+// MODE is a template parameter so the greedy walk compiles without the 128-bit sampling
+// machinery (register budget: 4 CTAs/SM greedy, 2 CTAs/SM sampling).
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, MODE == RS_ACCEPT_GREEDY ? 4 : 2)
+tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype, const float* __restrict__ draft,
+                   const int32_t* __restrict__ parent, const int32_t* __restrict__ token,
+                   const int32_t* __restrict__ tree_off, const int64_t* __restrict__ gid, int V, float inv_tau,
+                   uint64_t seed, uint64_t step, int32_t* __restrict__ acc_out, int32_t* __restrict__ path_out,
+                   int32_t* __restrict__ bonus_out, int32_t* __restrict__ flags_out, bool logits_vec_ok,
+                   bool draft_vec_ok) {
+    (void)mode_rt;
+    constexpr int mode = MODE;
     __shared__ Smem sm;
-    const int b = blockIdx.x;
+    const uint32_t cs = cluster_size();
+    const uint32_t crank = cluster_rank();
+    const int b = blockIdx.x / cs;
     const int tid = threadIdx.x;
+    const bool leader = crank == 0;
     const int off = tree_off[b];
     const int T = tree_off[b + 1] - off;
     int32_t* pth = path_out + (int64_t)b * RS_MAX_TREE;
-    if (tid < RS_MAX_TREE) pth[tid] = -1;
+    int phase = 0;
+    if (leader && tid < RS_MAX_TREE) pth[tid] = -1;
     if (tid == 0) {
         bool ok = (T >= 1 && T <= RS_MAX_TREE);
         if (ok) ok = parent[off] == -1;
         for (int i = 1; ok && i < T; ++i) {
-            int p = parent[off + i];
-            ok = (p >= 0 && p < i);
+            const int pp = parent[off + i];
+            ok = (pp >= 0 && pp < i);
         }
         sm.flag = ok ? 0 : RS_FLAG_MALFORMED;
     }
     __syncthreads();
     if (sm.flag) {
-        if (tid == 0) { acc_out[b] = 0; bonus_out[b] = -1; flags_out[b] = RS_FLAG_MALFORMED; }
-        return;
+        if (leader && tid == 0) { acc_out[b] = 0; bonus_out[b] = -1; flags_out[b] = RS_FLAG_MALFORMED; }
+        return;   // uniform across the cluster: no cluster barrier is reached
     }
     if (tid < T) { sm.parent[tid] = parent[off + tid]; sm.token[tid] = token[off + tid]; }
     const int64_t g = gid[b];
     const int nvec = (V + 7) / 8;
+    const int per = (nvec + (int)cs - 1) / (int)cs;
+    const int vbeg = min(nvec, (int)crank * per), vend = min(nvec, vbeg + per);
     int c = 0, a = 0, bonus = -1, flags = 0;
-    if (tid == 0) pth[0] = 0;
+    bool bonus_mine = leader;   // which CTA writes the bonus
+    if (leader && tid == 0) pth[0] = 0;
     __syncthreads();
 
     for (;;) {
-        RowView lv{logits, (int64_t)(off + c), V, dtype, logits_vec_ok};
+        const RowView lv{logits, (int64_t)(off + c), V, dtype, logits_vec_ok};
+        const RowView qv{draft, (int64_t)(off + c), V, RS_DTYPE_F32, draft_vec_ok};
         int next = -1;
         bool stop = false;
         if (mode == RS_ACCEPT_GREEDY) {
-            float best = -INFINITY;
-            int bi = 0x7fffffff;
-            bool bad = false;
-            for (int i = tid; i < nvec; i += kThreads) {
-                float x[8];
-                int n = load8(lv, i, x);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    if (j < n) {
-                        bad |= !isfinite(x[j]);
-                        argmax_merge(best, bi, x[j], i * 8 + j);
-                    }
-                }
-            }
-            bool any_bad;
-            int am = block_argmax(best, bi, bad, sm, &any_bad);
-            if (any_bad) { flags |= RS_FLAG_NONFINITE; break; }
+            // key = (orderable value << 32) | ~index: max key = max value, lowest index on ties
+            unsigned long long best = 0, bad = 0;
+            for_slice(lv, qv, false, vbeg, vend, [&](int v, float x, float) {
+                bad |= isfinite(x) ? 0ull : 1ull;
+                const unsigned long long k = ((unsigned long long)fkey(x) << 32) | (uint32_t)(~(uint32_t)v);
+                best = best > k ? best : k;
+            });
+            allreduce2(best, OP_MAX, bad, OP_OR, sm, phase);
+            if (bad) { flags |= RS_FLAG_NONFINITE; break; }
+            const int am = (int)(~(uint32_t)best);
             for (int x = c + 1; x < T; ++x)
                 if (sm.parent[x] == c && sm.token[x] == am) { next = x; break; }
             if (next < 0) { bonus = am; stop = true; }
         } else {
             // pass 1: row max (+ non-finite check)
-            float mx = -INFINITY;
-            bool bad = false;
-            for (int i = tid; i < nvec; i += kThreads) {
-                float x[8];
-                int n = load8(lv, i, x);
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    if (j < n) { bad |= !isfinite(x[j]); mx = fmaxf(mx, x[j]); }
-            }
-            bool any_bad;
-            const float m = block_max_f(mx, bad, sm, &any_bad);
-            if (any_bad) { flags |= RS_FLAG_NONFINITE; break; }
+            unsigned long long mk = 0, bad = 0;
+            for_slice(lv, qv, false, vbeg, vend, [&](int, float x, float) {
+                bad |= isfinite(x) ? 0ull : 1ull;
+                const unsigned long long k = fkey(x);
+                mk = mk > k ? mk : k;
+            });
+            allreduce2(mk, OP_MAX, bad, OP_OR, sm, phase);
+            if (bad) { flags |= RS_FLAG_NONFINITE; break; }
+            const float m = fkey_inv((uint32_t)mk);
             // pass 2: Z = sum w, Zq = sum qw
-            RowView qv{draft, (int64_t)(off + c), V, RS_DTYPE_F32, draft_vec_ok};
+            constexpr bool mss = mode == RS_ACCEPT_SAMPLE_MSS;
             unsigned long long zs = 0, zq = 0;
-            for (int i = tid; i < nvec; i += kThreads) {
-                float x[8];
-                int n = load8(lv, i, x);
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    if (j < n) zs += rs::target_weight(x[j], m, inv_tau);
-                if (mode == RS_ACCEPT_SAMPLE_MSS) {
-                    float q[8];
-                    load8(qv, i, q);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        if (j < n) zq += rs::draft_weight(q[j]);
-                }
-            }
-            uint64_t Z = block_sum_u64(zs, sm);
-            const uint64_t Zq = (mode == RS_ACCEPT_SAMPLE_MSS) ? block_sum_u64(zq, sm) : 0ull;
+            for_slice<mss ? 2 : 4>(lv, qv, mss, vbeg, vend, [&](int, float x, float q) {
+                zs += rs::target_weight(x, m, inv_tau);
+                if (mss) zq += rs::draft_weight(q);
+            });
+            allreduce2(zs, OP_SUM, zq, OP_SUM, sm, phase);
+            uint64_t Z = zs;
+            const uint64_t Zq = mss ? zq : 0ull;
             if (tid == 0) { sm.n_excluded = 0; sm.n_chain = 0; }
             __syncthreads();
             int rank = 0;
@@ -273,12 +318,12 @@ tree_accept_kernel(int mode, const void* __restrict__ logits, int dtype,
                 const int tk = sm.token[x];
                 if (tid == 0) {
                     const int64_t ro = (int64_t)(off + c) * V + tk;
-                    float l = (dtype == RS_DTYPE_BF16)
-                                  ? rs::bf16_bits_to_f32(reinterpret_cast<const uint16_t*>(logits)[ro])
-                                  : reinterpret_cast<const float*>(logits)[ro];
-                    uint64_t qw = (mode == RS_ACCEPT_SAMPLE_MSS) ? rs::draft_weight(draft[ro]) : 0ull;
-                    uint64_t wt = residual_weight(mode, rs::target_weight(l, m, inv_tau), qw, tk, Zq, sm);
-                    uint32_t U = rs::uniform_word(seed, step, g, (uint32_t)rank, (uint32_t)c);
+                    const float l = (dtype == RS_DTYPE_BF16)
+                                        ? rs::bf16_bits_to_f32(reinterpret_cast<const uint16_t*>(logits)[ro])
+                                        : reinterpret_cast<const float*>(logits)[ro];
+                    const uint64_t qw = mss ? rs::draft_weight(draft[ro]) : 0ull;
+                    const uint64_t wt = residual_weight(mode, rs::target_weight(l, m, inv_tau), qw, tk, Zq, sm);
+                    const uint32_t U = rs::uniform_word(seed, step, g, (uint32_t)rank, (uint32_t)c);
                     bool acc;
                     if (mode == RS_ACCEPT_SAMPLE_DELTA)
                         acc = ((u128)U * Z) < ((u128)wt << 32);
@@ -300,79 +345,61 @@ tree_accept_kernel(int mode, const void* __restrict__ logits, int dtype,
                     if (tid == 0) sm.excluded[sm.n_excluded++] = tk;
                     __syncthreads();
                 } else {
-                    // residual r_v = max(w_v*Zq - qw_v*Z, 0): max, then shifted sum
+                    // residual r_v = max(w_v*Zq - qw_v*Z, 0): cluster max, then shifted sum
                     u128 rmax = 0;
-                    for (int i = tid; i < nvec; i += kThreads) {
-                        float x8[8], q8[8];
-                        int n = load8(lv, i, x8);
-                        load8(qv, i, q8);
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            if (j < n) {
-                                uint64_t qw = rs::draft_weight(q8[j]);
-                                uint64_t w = residual_weight(mode, rs::target_weight(x8[j], m, inv_tau),
-                                                             qw, 0, Zq, sm);
-                                u128 lhs = (u128)w * Zq, rhs = (u128)qw * Z;
-                                u128 r = lhs > rhs ? lhs - rhs : 0;
-                                if (r > rmax) rmax = r;
-                            }
-                        }
-                    }
-                    u128 mxr = block_max_u128(rmax, sm);
+                    for_slice<2>(lv, qv, true, vbeg, vend, [&](int, float xv, float q) {
+                        const uint64_t qw = rs::draft_weight(q);
+                        const uint64_t w = residual_weight(mode, rs::target_weight(xv, m, inv_tau), qw, 0, Zq, sm);
+                        const u128 lhs = (u128)w * Zq, rhs = (u128)qw * Z;
+                        const u128 r = lhs > rhs ? lhs - rhs : 0;
+                        if (r > rmax) rmax = r;
+                    });
+                    const u128 mxr = allreduce_max128(rmax, sm, phase);
                     int s = rs::bitlen128(mxr) - 32;
                     if (s < 0) s = 0;
-                    unsigned long long zn = 0;
-                    for (int i = tid; i < nvec; i += kThreads) {
-                        float x8[8], q8[8];
-                        int n = load8(lv, i, x8);
-                        load8(qv, i, q8);
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            if (j < n) {
-                                uint64_t qw = rs::draft_weight(q8[j]);
-                                uint64_t w = residual_weight(mode, rs::target_weight(x8[j], m, inv_tau),
-                                                             qw, 0, Zq, sm);
-                                u128 lhs = (u128)w * Zq, rhs = (u128)qw * Z;
-                                u128 r = lhs > rhs ? lhs - rhs : 0;
-                                zn += (unsigned long long)(r >> s);
-                            }
-                        }
-                    }
-                    uint64_t Znew = block_sum_u64(zn, sm);
-                    __syncthreads();
-                    if (Znew != 0) {      // an all-zero residual keeps the pre-rejection weights
+                    unsigned long long zn = 0, dummy = 0;
+                    for_slice<2>(lv, qv, true, vbeg, vend, [&](int, float xv, float q) {
+                        const uint64_t qw = rs::draft_weight(q);
+                        const uint64_t w = residual_weight(mode, rs::target_weight(xv, m, inv_tau), qw, 0, Zq, sm);
+                        const u128 lhs = (u128)w * Zq, rhs = (u128)qw * Z;
+                        const u128 r = lhs > rhs ? lhs - rhs : 0;
+                        zn += (unsigned long long)(r >> s);
+                    });
+                    allreduce2(zn, OP_SUM, dummy, OP_OR, sm, phase);
+                    if (zn != 0) {      // an all-zero residual keeps the pre-rejection weights
                         if (tid == 0) {
                             sm.chainZ[sm.n_chain] = Z;
                             sm.chainS[sm.n_chain] = s;
                             sm.n_chain++;
                         }
-                        Z = Znew;
+                        Z = zn;
                     }
                     __syncthreads();
                 }
             }
             if (next < 0) {
-                // bonus ~ current residual: t = (U' * Z) >> 32, smallest v with cumsum > t
-                uint32_t U2 = rs::uniform_word(seed, step, g, 0xFFFFFFFFu, (uint32_t)c);
+                // bonus ~ current residual: t = (U' * Z) >> 32, smallest v with cumsum > t.
+                // (1) per-tile sums of this CTA's slice; (2) cluster prefix of slice totals finds
+                // the owning CTA; (3) it locates the tile, then the element by a block scan.
+                const uint32_t U2 = rs::uniform_word(seed, step, g, 0xFFFFFFFFu, (uint32_t)c);
                 const uint64_t t = (uint64_t)(((u128)U2 * Z) >> 32);
-                const int tile_elems = kThreads * 8;
-                const int ntiles = (V + tile_elems - 1) / tile_elems;
-                for (int k = tid; k < ntiles; k += kThreads) sm.tile_sum[k] = 0ull;
+                const int ntiles = (vend - vbeg + kTileVecs - 1) / kTileVecs;
+                for (int k = tid; k < kMaxTiles; k += kThreads) sm.tile_sum[k] = 0ull;
                 __syncthreads();
-                // thread tid owns elements tile*tile_elems + tid*8 .. +7 (contiguous within a tile)
                 for (int tile = 0; tile < ntiles; ++tile) {
-                    int i = tile * kThreads + tid;
+                    const int i = vbeg + tile * kTileVecs + tid;
                     unsigned long long s8 = 0;
-                    if (i < nvec) {
-                        float x8[8], q8[8];
-                        int n = load8(lv, i, x8);
-                        if (mode == RS_ACCEPT_SAMPLE_MSS) load8(qv, i, q8);
+                    if (i < vend) {
+                        const Raw8 xr = load_raw(lv, i);
+                        Raw8 qr;
+                        if (mss) qr = load_raw(qv, i);
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
-                            if (j < n) {
-                                uint64_t qw = (mode == RS_ACCEPT_SAMPLE_MSS) ? rs::draft_weight(q8[j]) : 0ull;
-                                s8 += residual_weight(mode, rs::target_weight(x8[j], m, inv_tau), qw,
-                                                      i * 8 + j, Zq, sm);
+                            const int v = i * 8 + j;
+                            if (v < V) {
+                                const uint64_t qw = mss ? rs::draft_weight(raw_elem(qr, RS_DTYPE_F32, j)) : 0ull;
+                                s8 += residual_weight(mode, rs::target_weight(raw_elem(xr, dtype, j), m, inv_tau), qw,
+                                                      v, Zq, sm);
                             }
                         }
                     }
@@ -381,75 +408,101 @@ tree_accept_kernel(int mode, const void* __restrict__ logits, int dtype,
                     if ((tid & 31) == 0 && s8) atomicAdd(&sm.tile_sum[tile], s8);
                 }
                 __syncthreads();
-                if (tid == 0) {
-                    unsigned long long run = 0;
-                    int tile = ntiles - 1;
-                    for (int k = 0; k < ntiles; ++k) {
-                        if (run + sm.tile_sum[k] > t) { tile = k; break; }
-                        run += sm.tile_sum[k];
-                    }
-                    sm.bcast_i = tile;
-                    sm.bcast_u = run;
+                unsigned long long slice_total = 0;
+                for (int k = 0; k < ntiles; ++k) slice_total += sm.tile_sum[k];
+                // exclusive prefix of slice totals over the cluster (every CTA computes all)
+                unsigned long long before = 0;
+                if (cs > 1) {
+                    if (tid == 0) sm.xch[phase][0] = slice_total;
+                    cluster_sync_all();
+                    for (uint32_t r = 0; r < crank; ++r) before += ld_dsmem_u64(&sm.xch[phase][0], r);
+                    phase ^= 1;
                 }
-                __syncthreads();
-                const int tile = sm.bcast_i;
-                const unsigned long long base = sm.bcast_u;
-                // exclusive scan of per-thread 8-element sums inside the tile
-                int i = tile * kThreads + tid;
-                uint64_t w8[8];
-                unsigned long long s8 = 0;
-                int n = 0;
-                if (i < nvec) {
-                    float x8[8], q8[8];
-                    n = load8(lv, i, x8);
-                    if (mode == RS_ACCEPT_SAMPLE_MSS) load8(qv, i, q8);
+                const bool owner = slice_total > 0 && before <= t && t < before + slice_total;
+                bonus_mine = owner;
+                if (owner) {
+                    if (tid == 0) {
+                        unsigned long long run = before;
+                        int tile = ntiles - 1;
+                        for (int k = 0; k < ntiles; ++k) {
+                            if (run + sm.tile_sum[k] > t) { tile = k; break; }
+                            run += sm.tile_sum[k];
+                        }
+                        sm.bcast_i = tile;
+                        sm.bcast_u = run;
+                        sm.bonus_v = V - 1;
+                    }
+                    __syncthreads();
+                    const int tile = sm.bcast_i;
+                    const unsigned long long base = sm.bcast_u;
+                    const int i = vbeg + tile * kTileVecs + tid;
+                    uint64_t w8[8];
+                    unsigned long long s8 = 0;
+                    if (i < vend) {
+                        const Raw8 xr = load_raw(lv, i);
+                        Raw8 qr;
+                        if (mss) qr = load_raw(qv, i);
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        w8[j] = 0;
-                        if (j < n) {
-                            uint64_t qw = (mode == RS_ACCEPT_SAMPLE_MSS) ? rs::draft_weight(q8[j]) : 0ull;
-                            w8[j] = residual_weight(mode, rs::target_weight(x8[j], m, inv_tau), qw,
-                                                    i * 8 + j, Zq, sm);
-                            s8 += w8[j];
+                        for (int j = 0; j < 8; ++j) {
+                            w8[j] = 0;
+                            const int v = i * 8 + j;
+                            if (v < V) {
+                                const uint64_t qw = mss ? rs::draft_weight(raw_elem(qr, RS_DTYPE_F32, j)) : 0ull;
+                                w8[j] = residual_weight(mode, rs::target_weight(raw_elem(xr, dtype, j), m, inv_tau),
+                                                        qw, v, Zq, sm);
+                                s8 += w8[j];
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) w8[j] = 0;
+                    }
+                    unsigned long long incl = s8;
+                    const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    if (lane == 31) sm.scan[wid] = incl;
+                    __syncthreads();
+                    unsigned long long wbase = base;
+                    for (int k = 0; k < wid; ++k) wbase += sm.scan[k];
+                    const unsigned long long excl = wbase + incl - s8;
+                    if (s8 && excl <= t && t < excl + s8) {
+                        unsigned long long accum = excl;
+                        for (int j = 0; j < 8; ++j) {
+                            accum += w8[j];
+                            if (accum > t) { sm.bonus_v = i * 8 + j; break; }
                         }
                     }
+                    __syncthreads();
+                    bonus = sm.bonus_v;
                 }
-                unsigned long long incl = s8;
-                const int lane = tid & 31, wid = tid >> 5;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += y;
-                }
-                if (lane == 31) sm.scan[wid] = incl;
-                if (tid == 0) sm.bonus_v = V - 1;
-                __syncthreads();
-                unsigned long long wbase = base;
-                for (int k = 0; k < wid; ++k) wbase += sm.scan[k];
-                unsigned long long excl = wbase + incl - s8;
-                if (s8 && excl <= t && t < excl + s8) {
-                    unsigned long long accum = excl;
-                    for (int j = 0; j < 8; ++j) {
-                        accum += w8[j];
-                        if (accum > t) { sm.bonus_v = i * 8 + j; break; }
-                    }
-                }
-                __syncthreads();
-                bonus = sm.bonus_v;
                 stop = true;
             }
         }
         if (stop) break;
         c = next;
         ++a;
-        if (tid == 0) pth[a] = c;
+        if (leader && tid == 0) pth[a] = c;
         __syncthreads();
     }
     if (tid == 0) {
-        acc_out[b] = a;
-        bonus_out[b] = (flags & RS_FLAG_NONFINITE) ? -1 : bonus;
-        flags_out[b] = flags;
+        if (leader) {
+            acc_out[b] = a;
+            flags_out[b] = flags;
+        }
+        if (flags & RS_FLAG_NONFINITE) {
+            if (leader) bonus_out[b] = -1;
+        } else if (bonus_mine && mode != RS_ACCEPT_GREEDY) {
+            bonus_out[b] = bonus;
+        } else if (leader && mode == RS_ACCEPT_GREEDY) {
+            bonus_out[b] = bonus;
+        }
     }
+    // keep every CTA's shared memory alive until all remote reads of the cluster are done
+    if (cs > 1) cluster_sync_all();
 }
 
 __global__ void philox_kernel(const uint4* ctr, int64_t n, uint2 key, uint4* out) {
@@ -483,20 +536,38 @@ extern "C" rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t lo
                "rs_tree_accept: draft_probs must be given for MSS only");
     RS_REQUIRE(mode == RS_ACCEPT_GREEDY || temperature > 0.0f, RS_ERR_INVALID_ARG,
                "rs_tree_accept: temperature must be > 0");
-    RS_REQUIRE((V + kThreads * 8 - 1) / (kThreads * 8) <= kMaxTiles, RS_ERR_UNSUPPORTED,
-               "rs_tree_accept: V=%d too large", V);
     if (B == 0) return RS_OK;
     RS_REQUIRE(logits && parent && token && tree_off && gid && accepted_len && path && bonus_token &&
                    status_flags,
                RS_ERR_INVALID_ARG, "rs_tree_accept: null pointer");
+    // cluster size: enough CTAs per sample that one row streams in ~a microsecond, without
+    // exceeding ~2 waves of the GPU when B is large
+    const int nvec = (V + 7) / 8;
+    int cs = 1;
+    while (cs < kMaxCluster && nvec / (cs * 2) >= kThreads * 2 && (int64_t)B * cs * 2 <= 148 * 4) cs *= 2;
+    const int per = (nvec + cs - 1) / cs;
+    RS_REQUIRE((per + kTileVecs - 1) / kTileVecs <= kMaxTiles, RS_ERR_UNSUPPORTED, "rs_tree_accept: V=%d too large", V);
     const float inv_tau = (mode == RS_ACCEPT_GREEDY) ? 1.0f : 1.0f / temperature;
     const int esz = logits_dtype == RS_DTYPE_BF16 ? 2 : 4;
-    bool lvec = ((reinterpret_cast<uintptr_t>(logits) & 15) == 0) && ((int64_t)V * esz % 16 == 0);
-    bool dvec = draft_probs && ((reinterpret_cast<uintptr_t>(draft_probs) & 15) == 0) && (V % 4 == 0);
-    tree_accept_kernel<<<B, kThreads, 0, rs::as_stream(stream)>>>(
-        mode, logits, logits_dtype, draft_probs, parent, token, tree_off, gid, V, inv_tau, seed,
-        step, accepted_len, path, bonus_token, status_flags, lvec, dvec);
-    RS_LAUNCH_CHECK();
+    const bool lvec = ((reinterpret_cast<uintptr_t>(logits) & 15) == 0) && ((int64_t)V * esz % 16 == 0);
+    const bool dvec = draft_probs && ((reinterpret_cast<uintptr_t>(draft_probs) & 15) == 0) && (V % 4 == 0);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(B * cs));
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = rs::as_stream(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    auto kern = mode == RS_ACCEPT_GREEDY        ? tree_accept_kernel<RS_ACCEPT_GREEDY>
+                : mode == RS_ACCEPT_SAMPLE_DELTA ? tree_accept_kernel<RS_ACCEPT_SAMPLE_DELTA>
+                                                 : tree_accept_kernel<RS_ACCEPT_SAMPLE_MSS>;
+    RS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, (int)mode, logits, (int)logits_dtype, draft_probs, parent, token,
+                                     tree_off, gid, (int)V, inv_tau, seed, step, accepted_len, path, bonus_token,
+                                     status_flags, lvec, dvec));
     return RS_OK;
 }
 

@@ -1,0 +1,575 @@
+// a2 device code: tree-verification attention on sm_100a (tcgen05 / TMEM / TMA).
+// P:76-80 (single-pass verification of the whole draft tree), P:213 (attention cost is
+// "KVCache loading"); readings Z1-Z4. Host side (plan, launch): attention.cu.
+//
+// Work item = (sample b, kv head, M tile of 128 query rows, key-block range). Rows of a tile are
+// the T_b*g (node, head-in-group) pairs, node-major, padded to 128 (UMMA M = 128); keys are the
+// sample's logical slots in 64-key blocks = one KV page each.
+//
+// Persistent kernel, one CTA per SM, 12 warps, warp-specialised:
+//   warp 0        TMA producer for Q (3-D map, 2 buffers) and K pages (4-slot ring)
+//   warp 3        TMA producer for V pages (6-slot ring; V lives longer than K)
+//   warp 1        MMA issuer, one thread, non-blocking: S_J = Q K_J^T (SS, M=128, N=64, K=D)
+//                 into S[J&1]; O[J&1] += P_J V_J (TS: P from TMEM, V MN-major, N=D)
+//   warp 2        TMEM allocator (512 columns)
+//   warps 4..7    softmax warpgroup 0: blocks with even J      (one query row per thread)
+//   warps 8..11   softmax warpgroup 1: blocks with odd J
+// Each softmax warpgroup keeps its own running max/sum and its own O accumulator in TMEM, so
+// the two run concurrently on alternate key blocks with no per-block synchronisation; the two
+// partial states are merged in the epilogue (exchange of (m, l) through TMEM columns).
+// Online softmax in the exp2 domain with lazy rescaling (threshold 2^8) of O in TMEM.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "sm100_ptx.cuh"
+
+namespace attn {
+
+using namespace rs::ptx;
+
+constexpr int kBlockN = 64;      // keys per KV block (= page_size)
+constexpr int kM = 128;          // query rows per work item (UMMA M)
+constexpr int kKSlots = 4;
+constexpr int kVSlots = 6;
+constexpr int kQBufs = 2;
+constexpr int kThreads = 384;    // 12 warps
+constexpr int kTraceJ = 256;
+
+// Row layout of a tile: logical query row r (node-major (node, head-in-group) pairs of the unit)
+// lives in TMEM lane / UMMA row m = (r / R) * 32 + r % R, R = rstride in {16, 32}: each of the
+// four TMEM sub-partitions (= softmax warps) holds R consecutive rows, so a short tile
+// (T*g <= 64, R = 16) still spreads its work over all four SM sub-partitions.
+struct WorkItem {
+    int32_t b, kvh, mtile, blk_begin, blk_end, part;  // part: -1 = direct, else partial slot
+    int32_t rstride;                                  // R (tile covers 4*R logical rows)
+    int32_t unit;                                     // split-unit index, -1 if direct
+};
+struct SplitUnit {
+    int32_t b, kvh, mtile, n_parts, part_base, rstride;
+};
+
+template <int D>
+struct Cfg {
+    static constexpr int kBoxes = D / 64;                    // 64-element (128 B) SW128 boxes
+    static constexpr int kQBytes = kM * D * 2;
+    static constexpr int kKVBytes = kBlockN * D * 2;         // one K or V page tile
+    static constexpr int kOffQ = 0;
+    static constexpr int kOffK = kOffQ + kQBufs * kQBytes;
+    static constexpr int kOffV = kOffK + kKSlots * kKVBytes;
+    static constexpr int kOffBar = kOffV + kVSlots * kKVBytes;
+    static constexpr int kSmemBytes = kOffBar + 256 + 1024;  // + barriers + alignment slack
+    // TMEM columns: O0 [0,D) O1 [D,2D) | S0 S1 (64 fp32 each) | P0 P1 (32 bf16x2 each) | m,l x2
+    static constexpr int kTmemCols = 512;
+    static constexpr int kColS = 2 * D;
+    static constexpr int kColP = 2 * D + 2 * kBlockN;
+    static constexpr int kColML = 2 * D + 3 * kBlockN;
+    static_assert(kColML + 8 <= kTmemCols, "TMEM budget");
+};
+
+struct Bars {
+    uint64_t q_full[kQBufs], q_empty[kQBufs];
+    uint64_t k_full[kKSlots], k_empty[kKSlots];
+    uint64_t v_full[kVSlots], v_empty[kVSlots];
+    uint64_t s_full[2], s_free[2];
+    uint64_t p_full[2], pv_done[2];
+    uint64_t o_free;
+    uint32_t tmem_base;
+    int merge_flag;
+};
+
+struct Params {
+    const int32_t* cta_off;
+    const WorkItem* items;
+    float* part_o;      // [n_parts][kM][D] fp32, normalised
+    float* part_lse;    // [n_parts][kM] fp32 (log2 domain)
+    const SplitUnit* units;
+    int* unit_counter;  // [n_units], zero between launches (reset by the merging CTA)
+    const int32_t* prefix_len;
+    const int32_t* tree_off;
+    const uint64_t* tree_mask;
+    const int32_t* block_table;
+    int max_pages;
+    int Hq, Hkv, g;
+    float scale_log2;   // sm_scale * log2(e)
+    __nv_bfloat16* out;
+    float* lse;
+    unsigned long long* trace;   // optional per-block event timestamps (profiling)
+};
+
+// Profiling events (clock64 per CTA / block J): 0 K issued, 1 V issued, 2 S issued,
+// 3 S ready (softmax), 4 P written, 5 PV issued, 6 epilogue start, 7 epilogue end.
+#define TRACE(J, ev)                                                                          \
+    do {                                                                                      \
+        if (p.trace && (J) < (uint32_t)kTraceJ)                                               \
+            p.trace[((size_t)blockIdx.x * kTraceJ + (J)) * 16 + (ev)] = clock64();             \
+    } while (0)
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                 const __grid_constant__ CUtensorMap tmV, const Params p) {
+    using C = Cfg<D>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    Bars* bars = reinterpret_cast<Bars*>(smem + C::kOffBar);
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int item_begin = p.cta_off[blockIdx.x];
+    const int item_end = p.cta_off[blockIdx.x + 1];
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kQBufs; ++i) { mbar_init(&bars->q_full[i], 1); mbar_init(&bars->q_empty[i], 1); }
+        for (int i = 0; i < kKSlots; ++i) { mbar_init(&bars->k_full[i], 1); mbar_init(&bars->k_empty[i], 1); }
+        for (int i = 0; i < kVSlots; ++i) { mbar_init(&bars->v_full[i], 1); mbar_init(&bars->v_empty[i], 1); }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bars->s_full[i], 1);
+            mbar_init(&bars->s_free[i], 4);
+            mbar_init(&bars->p_full[i], 4);
+            mbar_init(&bars->pv_done[i], 1);
+        }
+        mbar_init(&bars->o_free, 8);
+        fence_mbar_init();
+        prefetch_tmap(&tmQ);
+        prefetch_tmap(&tmK);
+        prefetch_tmap(&tmV);
+    }
+    if (warp == 2) tmem_alloc<C::kTmemCols>(&bars->tmem_base);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = bars->tmem_base;
+    if (warp == 0) {
+        // ============================ TMA producer: Q + K ============================
+        // (whole warp runs the loop; one elected lane issues)
+        uint32_t J = 0;
+        int it = 0;
+        for (int w = item_begin; w < item_end; ++w, ++it) {
+            const WorkItem wi = p.items[w];
+            const int qb = it % kQBufs;
+            mbar_wait(&bars->q_empty[qb], ((it / kQBufs) & 1) ^ 1);
+            const int R = wi.rstride;
+            const int row0 = wi.mtile * 4 * R;              // first logical row of the tile
+            uint8_t* qs = smem + C::kOffQ + qb * C::kQBytes;
+            const int nodeb = p.tree_off[wi.b];
+            if (elect_one()) {
+                mbar_arrive_expect_tx(&bars->q_full[qb], 4 * R * 128 * C::kBoxes);
+                // boxes of 16 rows (16/g nodes x g heads x 64 d): logical rows q*R + 16*s of
+                // quarter q go to UMMA rows 32*q + 16*s
+                for (int q = 0; q < 4; ++q)
+                    for (int s = 0; s < R; s += 16) {
+                        const int node = nodeb + (row0 + q * R + s) / p.g;
+#pragma unroll
+                        for (int bx = 0; bx < C::kBoxes; ++bx)
+                            tma_load_3d(qs + bx * (kM * 128) + (32 * q + s) * 128, &tmQ, &bars->q_full[qb],
+                                        bx * 64, wi.kvh * p.g, node);
+                    }
+            }
+            __syncwarp();
+            const int32_t* bt = p.block_table + (int64_t)wi.b * p.max_pages;
+            for (int blk = wi.blk_begin; blk < wi.blk_end; ++blk, ++J) {
+                const int s = J % kKSlots;
+                mbar_wait(&bars->k_empty[s], ((J / kKSlots) & 1) ^ 1);
+                const int row = (bt[blk] * p.Hkv + wi.kvh) * kBlockN;
+                uint8_t* ks = smem + C::kOffK + s * C::kKVBytes;
+                if (elect_one()) {
+                    TRACE(J, 0);
+                    mbar_arrive_expect_tx(&bars->k_full[s], C::kKVBytes);
+#pragma unroll
+                    for (int bx = 0; bx < C::kBoxes; ++bx)
+                        tma_load_2d(ks + bx * (kBlockN * 128), &tmK, &bars->k_full[s], bx * 64, row);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp == 3) {
+        // ============================ TMA producer: V ============================
+        uint32_t J = 0;
+        for (int w = item_begin; w < item_end; ++w) {
+            const WorkItem wi = p.items[w];
+            const int32_t* bt = p.block_table + (int64_t)wi.b * p.max_pages;
+            for (int blk = wi.blk_begin; blk < wi.blk_end; ++blk, ++J) {
+                const int s = J % kVSlots;
+                mbar_wait(&bars->v_empty[s], ((J / kVSlots) & 1) ^ 1);
+                const int row = (bt[blk] * p.Hkv + wi.kvh) * kBlockN;
+                uint8_t* vs = smem + C::kOffV + s * C::kKVBytes;
+                if (elect_one()) {
+                    TRACE(J, 1);
+                    mbar_arrive_expect_tx(&bars->v_full[s], C::kKVBytes);
+#pragma unroll
+                    for (int bx = 0; bx < C::kBoxes; ++bx)
+                        tma_load_2d(vs + bx * (kBlockN * 128), &tmV, &bars->v_full[s], bx * 64, row);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp == 2) {
+        // profiling only: observe when each K / V tile lands (events 8 / 9)
+        if (p.trace && lane < 2) {
+            uint32_t J = 0;
+            for (int w = item_begin; w < item_end; ++w)
+                for (int blk = p.items[w].blk_begin; blk < p.items[w].blk_end; ++blk, ++J) {
+                    if (J >= (uint32_t)kTraceJ) break;
+                    if (lane == 0) mbar_wait(&bars->k_full[J % kKSlots], (J / kKSlots) & 1);
+                    else mbar_wait(&bars->v_full[J % kVSlots], (J / kVSlots) & 1);
+                    TRACE(J, 8 + lane);
+                }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ============================ MMA issuer ============================
+        // Blocking, in the order S_0, S_1, S_2, PV_0, S_3, PV_1, ...: S runs two blocks ahead
+        // of PV, so each softmax warpgroup finds its next S already computed when it finishes
+        // a block (S_{J+2} only needs S_J consumed, long before P_J is ready).
+        constexpr uint32_t idS = idesc_bf16_f32(kM, kBlockN, 0);
+        constexpr uint32_t idPV = idesc_bf16_f32(kM, D, 1);
+        const uint32_t sbase = smem_u32(smem);
+        int s_item = item_begin, s_j = 0, s_it = 0, s_nblk = 0;   // S cursor
+        uint32_t sJ = 0;
+        if (s_item < item_end) s_nblk = p.items[s_item].blk_end - p.items[s_item].blk_begin;
+        int p_item = item_begin, p_j = 0, p_it = 0, p_nblk = s_nblk;  // PV cursor
+        uint32_t pJ = 0;
+        while (p_item < item_end) {
+            while (s_item < item_end && sJ < pJ + 3) {
+                const int qb = s_it % kQBufs;
+                if (s_j == 0) mbar_wait(&bars->q_full[qb], (s_it / kQBufs) & 1);
+                if (lane == 0) TRACE(sJ, 10);
+                mbar_wait(&bars->k_full[sJ % kKSlots], (sJ / kKSlots) & 1);
+                if (lane == 0) TRACE(sJ, 11);
+                mbar_wait(&bars->s_free[sJ & 1], ((sJ >> 1) & 1) ^ 1);
+                if (lane == 0) TRACE(sJ, 12);
+                tc_fence_after();
+                const uint32_t qa = sbase + C::kOffQ + qb * C::kQBytes;
+                const uint32_t ka = sbase + C::kOffK + (sJ % kKSlots) * C::kKVBytes;
+                const uint32_t sd = tmem + C::kColS + (sJ & 1) * kBlockN;
+                if (elect_one()) {
+#pragma unroll
+                    for (int k = 0; k < D / 16; ++k) {
+                        const int bx = k >> 2, within = (k & 3) * 32;
+                        uint64_t ad = smem_desc_sw128(qa + bx * (kM * 128) + within, 16, 1024);
+                        uint64_t bd = smem_desc_sw128(ka + bx * (kBlockN * 128) + within, 16, 1024);
+                        umma_f16(sd, ad, bd, idS, k > 0 ? 1u : 0u);
+                    }
+                    TRACE(sJ, 2);
+                    umma_commit(&bars->s_full[sJ & 1]);
+                    umma_commit(&bars->k_empty[sJ % kKSlots]);
+                }
+                __syncwarp();
+                ++sJ;
+                if (++s_j == s_nblk) {
+                    if (elect_one()) umma_commit(&bars->q_empty[qb]);
+                    __syncwarp();
+                    s_j = 0;
+                    ++s_it;
+                    ++s_item;
+                    if (s_item < item_end) s_nblk = p.items[s_item].blk_end - p.items[s_item].blk_begin;
+                }
+            }
+            const bool first = p_j < 2;   // first block of its warpgroup in this item
+            if (lane == 0) TRACE(pJ, 13);
+            mbar_wait(&bars->p_full[pJ & 1], (pJ >> 1) & 1);
+            if (lane == 0) TRACE(pJ, 14);
+            mbar_wait(&bars->v_full[pJ % kVSlots], (pJ / kVSlots) & 1);
+            if (p_j == 0) mbar_wait(&bars->o_free, (p_it & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t pa = tmem + C::kColP + (pJ & 1) * (kBlockN / 2);
+            const uint32_t va = sbase + C::kOffV + (pJ % kVSlots) * C::kKVBytes;
+            const uint32_t od = tmem + (pJ & 1) * D;
+            if (elect_one()) {
+                TRACE(pJ, 5);
+#pragma unroll
+                for (int kk = 0; kk < kBlockN / 16; ++kk) {
+                    uint64_t bd = smem_desc_sw128(va + kk * 2048, kBlockN * 128, 1024);
+                    umma_f16_ts(od, pa + kk * 8, bd, idPV, (first && kk == 0) ? 0u : 1u);
+                }
+                umma_commit(&bars->pv_done[pJ & 1]);
+                umma_commit(&bars->v_empty[pJ % kVSlots]);
+                TRACE(pJ, 15);
+            }
+            __syncwarp();
+            ++pJ;
+            if (++p_j == p_nblk) {
+                p_j = 0;
+                ++p_it;
+                ++p_item;
+                if (p_item < item_end) p_nblk = p.items[p_item].blk_end - p.items[p_item].blk_begin;
+            }
+        }
+    } else if (warp >= 4) {
+        // ============================ softmax + epilogue ============================
+        const int grp = (warp - 4) >> 2;         // warpgroup: handles blocks with (J & 1) == grp
+        const int wq = warp & 3;                 // TMEM sub-partition of this warp
+        const int r = wq * 32 + lane;            // UMMA row / TMEM lane of this thread
+        const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+        const uint32_t o_mine = tmem + lane_base + grp * D;
+        uint32_t J = 0;
+        int it = 0;
+        for (int w = item_begin; w < item_end; ++w, ++it) {
+            const WorkItem wi = p.items[w];
+            const int b = wi.b;
+            const int P = p.prefix_len[b];
+            const int off = p.tree_off[b];
+            const int T = p.tree_off[b + 1] - off;
+            const int R = wi.rstride;
+            const int rl = wq * R + lane;                // logical row within the tile
+            const int rows = min(4 * R, T * p.g - wi.mtile * 4 * R);
+            const bool warp_active = wq * R < rows;
+            const bool row_valid = lane < R && rl < rows;
+            const int grow = wi.mtile * 4 * R + rl;      // row within the unit
+            const int node = grow / p.g;
+            const uint64_t mask = row_valid ? p.tree_mask[off + node] : 0ull;
+            const int key_end = P + T;                   // keys >= key_end do not exist
+            const int nblk = wi.blk_end - wi.blk_begin;
+            float m_run = -INFINITY, l_run = 0.0f;
+            bool had = false;
+            uint32_t Jlast = 0;
+            for (int j = (int)((J & 1) != (uint32_t)grp); j < nblk; j += 2) {
+                const uint32_t Jj = J + j;
+                const int kbase = (wi.blk_begin + j) * kBlockN;
+                mbar_wait(&bars->s_full[grp], (Jj >> 1) & 1);
+                tc_fence_after();
+                if (wq == 0 && lane == 0) TRACE(Jj, 3);
+                // sr: raw S bits -> masked S -> packed bf16 P in sr[0..31]
+                uint32_t sr[64];
+                if (warp_active) {
+                    const uint32_t sa = tmem + lane_base + C::kColS + grp * kBlockN;
+                    tmem_ld32(sa, reinterpret_cast<uint32_t(&)[32]>(sr[0]));
+                    tmem_ld32(sa + 32, reinterpret_cast<uint32_t(&)[32]>(sr[32]));
+                    tmem_wait_ld();
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->s_free[grp]);
+                // P buffer / O of this warpgroup were last used by its previous block (Jj - 2)
+                if (Jj >= 2) mbar_wait(&bars->pv_done[grp], ((Jj - 2) >> 1) & 1);
+                tc_fence_after();
+                if (warp_active) {
+                    float mx = -INFINITY;
+                    if (kbase + kBlockN <= P) {
+#pragma unroll
+                        for (int c = 0; c < 64; ++c) mx = fmaxf(mx, __uint_as_float(sr[c]));
+                    } else {
+                        // visible-column bitmap of this block: prefix columns c < P - kbase,
+                        // tree column c <-> node c - (P - kbase) (its ancestor bit)
+                        const int dlt = P - kbase;
+                        uint64_t vb = dlt >= 64 ? ~0ull : (dlt <= 0 ? 0ull : ((1ull << dlt) - 1ull));
+                        if (dlt >= 0 && dlt < 64) vb |= mask << dlt;
+                        else if (dlt < 0 && dlt > -64) vb |= mask >> (-dlt);
+                        const uint32_t vlo = (uint32_t)vb, vhi = (uint32_t)(vb >> 32);
+#pragma unroll
+                        for (int c = 0; c < 64; ++c) {
+                            const bool ok = ((c < 32 ? vlo >> c : vhi >> (c - 32)) & 1u) != 0u;
+                            sr[c] = ok ? sr[c] : 0xFF800000u;   // -inf
+                            mx = fmaxf(mx, __uint_as_float(sr[c]));
+                        }
+                    }
+                    const float m_blk = mx * p.scale_log2;
+                    bool need_o = false;
+                    float alpha = 1.0f;
+                    if (m_blk > m_run + 8.0f) {          // lazy rescale (values stay <= 2^8)
+                        alpha = ex2(m_run - m_blk);      // m_run = -inf -> 0
+                        need_o = had && row_valid && (m_run != -INFINITY);
+                        l_run *= alpha;
+                        m_run = m_blk;
+                    }
+                    if (__any_sync(0xffffffffu, need_o)) {
+                        const float f = need_o ? alpha : 1.0f;
+#pragma unroll 1
+                        for (int c0 = 0; c0 < D; c0 += 32) {
+                            uint32_t o[32];
+                            tmem_ld32(o_mine + c0, o);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
+                            tmem_st32(o_mine + c0, o);
+                        }
+                    }
+                    const float mo = (m_run == -INFINITY) ? 0.0f : m_run;
+                    float ls = 0.0f;
+#pragma unroll
+                    for (int c = 0; c < 64; c += 2) {
+                        const float e0 = ex2(fmaf(__uint_as_float(sr[c]), p.scale_log2, -mo));
+                        const float e1 = ex2(fmaf(__uint_as_float(sr[c + 1]), p.scale_log2, -mo));
+                        const uint32_t pk = pack_bf16(e0, e1);
+                        sr[c >> 1] = pk;
+                        ls += __uint_as_float(pk << 16) + __uint_as_float(pk & 0xFFFF0000u);
+                    }
+                    l_run += ls;
+                    tmem_st32(tmem + lane_base + C::kColP + grp * (kBlockN / 2),
+                              reinterpret_cast<const uint32_t(&)[32]>(sr[0]));
+                    tmem_wait_st();
+                }
+                // keys past the end of the sample in its last page: zero those V rows so that
+                // garbage (possibly NaN) bytes never meet a zero probability in the MMA
+                const int nvalid = key_end - kbase;
+                if (nvalid < kBlockN) {
+                    const uint32_t s = Jj % kVSlots;
+                    mbar_wait(&bars->v_full[s], (Jj / kVSlots) & 1);
+                    if (r < kBlockN && r >= nvalid) {
+                        uint8_t* vs = smem + C::kOffV + s * C::kKVBytes;
+#pragma unroll
+                        for (int bx = 0; bx < C::kBoxes; ++bx) {
+                            uint4* row = reinterpret_cast<uint4*>(vs + bx * (kBlockN * 128) + r * 128);
+#pragma unroll
+                            for (int c = 0; c < 8; ++c) row[c] = make_uint4(0, 0, 0, 0);
+                        }
+                    }
+                    fence_proxy_async_smem();
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (wq == 0 && lane == 0) TRACE(Jj, 4);
+                if (lane == 0) mbar_arrive(&bars->p_full[grp]);
+                had = true;
+                Jlast = Jj;
+            }
+            // ---------------- epilogue: merge the two warpgroups' states ----------------
+            if (wq == 0 && lane == 0) TRACE(J + nblk - 1, 6);
+            const bool had0 = nblk >= 2 || (J & 1) == 0;
+            const bool had1 = nblk >= 2 || (J & 1) == 1;
+            if (had) {
+                mbar_wait(&bars->pv_done[grp], (Jlast >> 1) & 1);
+                tc_fence_after();
+            }
+            // (m, l) exchange columns are double-buffered by item parity: a warpgroup can be at
+            // most one epilogue ahead of the other (the named barrier needs both).
+            const uint32_t ml_col = C::kColML + 4 * (it & 1);
+            if (warp_active) {
+                tmem_st2(tmem + lane_base + ml_col + 2 * grp, __float_as_uint(m_run), __float_as_uint(l_run));
+                tmem_wait_st();
+            }
+            tc_fence_before();
+            named_bar_sync(2, 256);
+            tc_fence_after();
+            if (warp_active) {
+                uint32_t mo_u, lo_u;
+                tmem_ld2(tmem + lane_base + ml_col + 2 * (grp ^ 1), mo_u, lo_u);
+                tmem_wait_ld();
+                const float m0 = grp == 0 ? m_run : __uint_as_float(mo_u);
+                const float l0 = grp == 0 ? l_run : __uint_as_float(lo_u);
+                const float m1 = grp == 1 ? m_run : __uint_as_float(mo_u);
+                const float l1 = grp == 1 ? l_run : __uint_as_float(lo_u);
+                const float M = fmaxf(had0 ? m0 : -INFINITY, had1 ? m1 : -INFINITY);
+                const float w0 = (had0 && l0 > 0.0f) ? ex2(m0 - M) : 0.0f;
+                const float w1 = (had1 && l1 > 0.0f) ? ex2(m1 - M) : 0.0f;
+                const float L = l0 * w0 + l1 * w1;
+                const float invL = L > 0.0f ? 1.0f / L : 0.0f;
+                const float f0 = w0 * invL, f1 = w1 * invL;
+                const int h = wi.kvh * p.g + (grow % p.g);
+                const bool direct = wi.part < 0;
+                __nv_bfloat16* orow = p.out + ((int64_t)(off + node) * p.Hq + h) * D;
+                float* prow = direct ? nullptr : p.part_o + ((int64_t)wi.part * kM + r) * D;
+                const uint32_t rowbase = tmem + lane_base;
+#pragma unroll 1
+                for (int c0 = grp * (D / 2); c0 < (grp + 1) * (D / 2); c0 += 16) {
+                    uint32_t a[16], bb[16];
+                    if (had0) tmem_ld16(rowbase + c0, a);
+                    if (had1) tmem_ld16(rowbase + D + c0, bb);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < 16; ++c)
+                        a[c] = __float_as_uint((had0 ? __uint_as_float(a[c]) * f0 : 0.0f) +
+                                               (had1 ? __uint_as_float(bb[c]) * f1 : 0.0f));
+                    if (row_valid) {
+                        if (direct) {
+#pragma unroll
+                            for (int c = 0; c < 16; c += 8) {
+                                uint4 u;
+                                u.x = pack_bf16(__uint_as_float(a[c]), __uint_as_float(a[c + 1]));
+                                u.y = pack_bf16(__uint_as_float(a[c + 2]), __uint_as_float(a[c + 3]));
+                                u.z = pack_bf16(__uint_as_float(a[c + 4]), __uint_as_float(a[c + 5]));
+                                u.w = pack_bf16(__uint_as_float(a[c + 6]), __uint_as_float(a[c + 7]));
+                                *reinterpret_cast<uint4*>(orow + c0 + c) = u;
+                            }
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < 16; c += 4)
+                                *reinterpret_cast<uint4*>(prow + c0 + c) = make_uint4(a[c], a[c + 1], a[c + 2], a[c + 3]);
+                        }
+                    }
+                }
+                if (row_valid && grp == 0) {
+                    const float lse2 = L > 0.0f ? M + __log2f(L) : -INFINITY;
+                    if (direct) {
+                        if (p.lse) p.lse[(int64_t)(off + node) * p.Hq + h] = lse2 * 0.6931471805599453f;
+                    } else {
+                        p.part_lse[(int64_t)wi.part * kM + r] = lse2;
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (wq == 0 && lane == 0 && grp == 0) TRACE(J + nblk - 1, 7);
+            if (lane == 0) mbar_arrive(&bars->o_free);
+            if (wi.part >= 0) {
+                // split-KV unit: the CTA that completes its last part merges all parts
+                // o = sum_q 2^(lse_q - M) o_q / sum_q 2^(lse_q - M)  (threadfence-reduction pattern)
+                __threadfence();
+                named_bar_sync(3, 256);
+                if (threadIdx.x == 128) {
+                    const int old = atomicAdd(&p.unit_counter[wi.unit], 1);
+                    const int last = (old == p.units[wi.unit].n_parts - 1) ? 1 : 0;
+                    if (last) p.unit_counter[wi.unit] = 0;          // ready for the next launch
+                    bars->merge_flag = last;
+                }
+                named_bar_sync(3, 256);
+                if (bars->merge_flag && row_valid) {
+                    __threadfence();
+                    const SplitUnit u = p.units[wi.unit];
+                    float M = -INFINITY;
+                    for (int q = 0; q < u.n_parts; ++q)
+                        M = fmaxf(M, __ldcg(p.part_lse + (int64_t)(u.part_base + q) * kM + r));
+                    float wsum = 0.0f;
+                    for (int q = 0; q < u.n_parts; ++q) {
+                        const float lq = __ldcg(p.part_lse + (int64_t)(u.part_base + q) * kM + r);
+                        wsum += (lq == -INFINITY) ? 0.0f : ex2(lq - M);
+                    }
+                    const float inv = wsum > 0.0f ? 1.0f / wsum : 0.0f;
+                    const int h = wi.kvh * p.g + (grow % p.g);
+                    __nv_bfloat16* orow = p.out + ((int64_t)(off + node) * p.Hq + h) * D;
+#pragma unroll 1
+                    for (int c0 = grp * (D / 2); c0 < (grp + 1) * (D / 2); c0 += 8) {
+                        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                        for (int q = 0; q < u.n_parts; ++q) {
+                            const float lq = __ldcg(p.part_lse + (int64_t)(u.part_base + q) * kM + r);
+                            const float wq = (lq == -INFINITY) ? 0.0f : ex2(lq - M) * inv;
+                            const float4* src = reinterpret_cast<const float4*>(
+                                p.part_o + ((int64_t)(u.part_base + q) * kM + r) * D + c0);
+                            const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
+                            acc[0] += wq * x0.x; acc[1] += wq * x0.y; acc[2] += wq * x0.z; acc[3] += wq * x0.w;
+                            acc[4] += wq * x1.x; acc[5] += wq * x1.y; acc[6] += wq * x1.z; acc[7] += wq * x1.w;
+                        }
+                        uint4 o;
+                        o.x = pack_bf16(acc[0], acc[1]);
+                        o.y = pack_bf16(acc[2], acc[3]);
+                        o.z = pack_bf16(acc[4], acc[5]);
+                        o.w = pack_bf16(acc[6], acc[7]);
+                        *reinterpret_cast<uint4*>(orow + c0) = o;
+                    }
+                    if (grp == 0 && p.lse)
+                        p.lse[(int64_t)(off + node) * p.Hq + h] = (M + __log2f(wsum)) * 0.6931471805599453f;
+                }
+            }
+            J += nblk;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 2) tmem_dealloc<C::kTmemCols>(tmem);
+}
+
+}  // namespace attn

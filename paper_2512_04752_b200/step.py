@@ -1,9 +1,10 @@
 """One batched verification step through the C ABI (SURVEY.md §3 call stack (1)):
 
-    rs_tree_build_mask -> L x rs_tree_verify_attention -> rs_tree_accept -> rs_kv_compact
+    rs_tree_build_mask -> rs_tree_verify_attention_layers (L layers) -> rs_tree_accept -> rs_kv_compact
 
-Pure orchestration: buffers are torch tensors, every computation is a library call. The
-device part can be captured into a CUDA graph (one launch per step)."""
+Pure orchestration: buffers are torch tensors, every computation is a library call; arguments
+are marshalled once so a step costs four ctypes calls. The device part can be captured into a
+CUDA graph (one launch per step)."""
 from __future__ import annotations
 
 import torch
@@ -13,7 +14,7 @@ from . import core
 
 class VerifyStep:
     def __init__(self, batch: dict, mode: int = core.GREEDY, temperature: float = 1.0, num_ctas: int = 0,
-                 with_lse: bool = False, stream=None):
+                 with_lse: bool = False):
         b = batch
         dev = b["q"].device
         self.b = b
@@ -35,15 +36,16 @@ class VerifyStep:
         self.k_layers = [b["k_cache"][l] for l in range(self.L)]
         self.v_layers = [b["v_cache"][l] for l in range(self.L)]
         self.logits = b["logits"]
-        self.draft = b.get("draft_probs")
-        if mode != core.SAMPLE_MSS:
-            self.draft = None
+        self.draft = b.get("draft_probs") if mode == core.SAMPLE_MSS else None
+        NT = self.q.shape[1]
+        self.mask = torch.empty(NT, dtype=torch.int64, device=dev)
+        self.depth = torch.empty(NT, dtype=torch.int32, device=dev)
+        self.tflags = torch.empty(self.B, dtype=torch.int32, device=dev)
         # host-side plan from this step's lengths (shared by all layers)
         self.plan = core.AttnPlan(b["prefix_len"], b["tree_off"], self.Hq, self.Hkv, self.d, self.ps,
                                   num_ctas=num_ctas)
         self.ws = core.alloc_workspace(self.plan.ws_bytes, dev)
         self.plan.upload(self.ws)
-        NT = self.q.shape[1]
         self.attn_out = torch.empty((self.L, NT, self.Hq, self.d), dtype=torch.bfloat16, device=dev)
         self.lse = torch.empty((self.L, NT, self.Hq), dtype=torch.float32, device=dev) if with_lse else None
         self.acc = torch.empty(self.B, dtype=torch.int32, device=dev)
@@ -51,29 +53,34 @@ class VerifyStep:
         self.bonus = torch.empty(self.B, dtype=torch.int32, device=dev)
         self.flags = torch.empty(self.B, dtype=torch.int32, device=dev)
         self.new_len = torch.empty(self.B, dtype=torch.int32, device=dev)
+        self.attn_call = core.AttentionLayersCall(
+            self.plan, [self.q[l] for l in range(self.L)], self.k_layers, self.v_layers, self.block_table,
+            self.prefix_len, self.tree_off, self.mask, self.sm_scale, self.ws,
+            [self.attn_out[l] for l in range(self.L)], None if self.lse is None else [self.lse[l] for l in range(self.L)])
         self.graph = None
-        self.seed, self.step_no = 0, 0
 
-    def device_step(self, seed=None, step=None, stream=None):
-        """Enqueue the whole step on `stream` (no host sync)."""
-        seed = self.seed if seed is None else seed
-        step = self.step_no if step is None else step
-        mask, _, flags = core.tree_build_mask(self.parent, self.tree_off, stream=stream)
-        self.mask = mask
-        for l in range(self.L):
-            core.tree_verify_attention(self.plan, self.q[l], self.k_layers[l], self.v_layers[l], self.block_table,
-                                       self.prefix_len, self.tree_off, mask, self.sm_scale, self.ws,
-                                       out=self.attn_out[l], lse=None if self.lse is None else self.lse[l],
-                                       stream=stream)
+    def mask_step(self, stream=None):
+        core.tree_build_mask(self.parent, self.tree_off, stream=stream, out=(self.mask, self.depth, self.tflags))
+
+    def attention_step(self, stream=None):
+        self.attn_call(stream)
+
+    def accept_compact_step(self, seed, step, stream=None):
         core.tree_accept(self.mode, self.logits, self.parent, self.token, self.tree_off, self.gid,
                          draft_probs=self.draft, temperature=self.temperature, seed=seed, step=step,
                          out=(self.acc, self.path, self.bonus, self.flags), stream=stream)
         core.kv_compact(self.k_layers, self.v_layers, self.block_table, self.prefix_len, self.acc, self.path,
                         self.ps, new_len=self.new_len, stream=stream)
 
-    def capture(self, seed=0, step=0):
-        """Capture the device step into a CUDA graph (seed/step are baked in)."""
-        self.seed, self.step_no = seed, step
+    def device_step(self, seed=0, step=0, stream=None):
+        """Enqueue the whole step on `stream` (no host sync)."""
+        self.mask_step(stream)
+        self.attention_step(stream)
+        self.accept_compact_step(seed, step, stream)
+
+    def capture(self, seed=0, step=0, events=None):
+        """Capture the device step into a CUDA graph (seed/step are baked in). `events`: optional
+        (before_attention, after_attention) torch events recorded inside the graph."""
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
@@ -82,12 +89,38 @@ class VerifyStep:
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            self.device_step(seed, step, stream=torch.cuda.current_stream())
+            cs = torch.cuda.current_stream()
+            self.mask_step(cs)
+            if events is not None:
+                events[0].record(cs)
+            self.attention_step(cs)
+            if events is not None:
+                events[1].record(cs)
+            self.accept_compact_step(seed, step, cs)
         self.graph = g
         return g
 
     def replay(self):
         self.graph.replay()
+
+    def capture_parts(self, seed=0, step=0):
+        """Three CUDA graphs (mask | L x attention | accept + compact) so a caller can time the
+        attention part with events between replays."""
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.device_step(seed, step, stream=s)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        parts = []
+        for fn in (lambda st: self.mask_step(st), lambda st: self.attention_step(st),
+                   lambda st: self.accept_compact_step(seed, step, st)):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn(torch.cuda.current_stream())
+            parts.append(g)
+        self.parts = parts
+        return parts
 
     def results(self):
         return dict(accepted_len=self.acc.cpu().numpy(), path=self.path.cpu().numpy(),

@@ -42,13 +42,15 @@ def _check_plan(core, P, T, Hq, Hkv, d=128, n=148):
     assert cta[0] == 0 and cta[-1] == len(items) and np.all(np.diff(cta) >= 0)
     g = Hq // Hkv
     cover = {}
-    for b_, kvh, mt, b0, b1, part in items:
+    for b_, kvh, mt, b0, b1, part, R, unit in items:
+        assert (part < 0) == (unit < 0)
         cover.setdefault((b_, kvh, mt), []).append((b0, b1, part))
     nsplit = 0
     for b in range(len(P)):
         nblk = (P[b] + T[b] + 63) // 64
         for kvh in range(Hkv):
-            for mt in range((T[b] * g + 127) // 128):
+            R = 16 if T[b] * g <= 64 else 32
+            for mt in range((T[b] * g + 4 * R - 1) // (4 * R)):
                 parts = sorted(cover.pop((b, kvh, mt)))
                 assert parts[0][0] == 0 and parts[-1][1] == nblk
                 assert all(x[1] == y[0] for x, y in zip(parts, parts[1:]))
