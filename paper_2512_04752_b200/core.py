@@ -124,7 +124,7 @@ class AttnPlan:
         """(cta_off [num_ctas+1], items [num_items, 7]) as numpy arrays."""
         inf = self.info()
         cta = np.zeros(inf["num_ctas"] + 1, dtype=np.int32)
-        items = np.zeros((inf["num_items"], 8), dtype=np.int32)
+        items = np.zeros((inf["num_items"], 10), dtype=np.int32)
         _check(_lib.rs_attn_plan_items(self.handle, _ptr(cta), _ptr(items)), "rs_attn_plan_items")
         return cta, items
 

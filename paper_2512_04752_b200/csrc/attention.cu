@@ -159,7 +159,7 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
             }
             if (!where.empty()) W_eff += kOvhBlocks;   // an extra part of a split unit
             where.push_back({cta, (int)per_cta[cta].size()});
-            per_cta[cta].push_back({u.b, u.kvh, u.mtile, start, start + take, -1, u.R, -1});
+            per_cta[cta].push_back({u.b, u.kvh, u.mtile, start, start + take, -1, u.R, -1, 0, 0});
             pos += take + kOvhBlocks;
             start += take;
             rem -= take;
@@ -171,6 +171,15 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
                 per_cta[wc.first][wc.second].part = n_parts++;
                 per_cta[wc.first][wc.second].unit = uid;
             }
+        }
+    }
+    // two softmax streams per CTA: each item goes to the stream with less work so far
+    const bool one_stream = getenv("RS_ATTN_ONE_STREAM") != nullptr;   // debugging aid
+    for (auto& list : per_cta) {
+        long long ld[2] = {0, 0};
+        for (auto& w : list) {
+            w.stream = (!one_stream && ld[1] < ld[0]) ? 1 : 0;
+            ld[w.stream] += (w.blk_end - w.blk_begin) + kOvhBlocks;
         }
     }
     pl->cta_off.assign(n_ctas + 1, 0);
@@ -245,16 +254,19 @@ static rs_status launch_attn(const rs_attn_plan* pl, const void* q, const void* 
     using C = Cfg<D>;
     PFN_encodeTiled enc = get_encode();
     RS_REQUIRE(enc, RS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    CUtensorMap tmQ, tmK, tmV;
-    {
+    CUtensorMap tmQ, tmK, tmV, tmO;
+    // Q (load) and O (store) share the geometry [NT][Hq][D]; box = 16 rows (16/g nodes x g heads) x 64 d
+    const void* qo[2] = {q, out};
+    CUtensorMap* tqo[2] = {&tmQ, &tmO};
+    for (int i = 0; i < 2; ++i) {
         cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)pl->Hq, (cuuint64_t)std::max(pl->NT, 1)};
         cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)pl->Hq * D * 2};
         cuuint32_t box[3] = {64, (cuuint32_t)pl->g, (cuuint32_t)(16 / pl->g)};
         cuuint32_t es[3] = {1, 1, 1};
-        CUresult r = enc(&tmQ, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(q), dims, strides, box, es,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+        CUresult r = enc(tqo[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(qo[i]), dims, strides, box,
+                         es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        RS_REQUIRE(r == CUDA_SUCCESS, RS_ERR_CUDA, "tensor map Q failed (%d)", (int)r);
+        RS_REQUIRE(r == CUDA_SUCCESS, RS_ERR_CUDA, "tensor map Q/O failed (%d)", (int)r);
     }
     const void* kv[2] = {k_pages, v_pages};
     CUtensorMap* tm[2] = {&tmK, &tmV};
@@ -295,7 +307,7 @@ static rs_status launch_attn(const rs_attn_plan* pl, const void* q, const void* 
                                            C::kSmemBytes));
         attr_set[D == 128] = true;
     }
-    tree_attn_kernel<D><<<pl->n_ctas, kThreads, C::kSmemBytes, st>>>(tmQ, tmK, tmV, prm);
+    tree_attn_kernel<D><<<pl->n_ctas, kThreads, C::kSmemBytes, st>>>(tmQ, tmK, tmV, tmO, prm);
     RS_LAUNCH_CHECK();
     return RS_OK;
 }

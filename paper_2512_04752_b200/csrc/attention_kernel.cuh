@@ -32,7 +32,7 @@ using namespace rs::ptx;
 constexpr int kBlockN = 64;      // keys per KV block (= page_size)
 constexpr int kM = 128;          // query rows per work item (UMMA M)
 constexpr int kKSlots = 4;
-constexpr int kVSlots = 6;
+constexpr int kVSlots = 4;
 constexpr int kQBufs = 2;
 constexpr int kThreads = 384;    // 12 warps
 constexpr int kTraceJ = 256;
@@ -45,6 +45,8 @@ struct WorkItem {
     int32_t b, kvh, mtile, blk_begin, blk_end, part;  // part: -1 = direct, else partial slot
     int32_t rstride;                                  // R (tile covers 4*R logical rows)
     int32_t unit;                                     // split-unit index, -1 if direct
+    int32_t stream;                                   // (two-stream variant; unused here)
+    int32_t pad;
 };
 struct SplitUnit {
     int32_t b, kvh, mtile, n_parts, part_base, rstride;
@@ -58,7 +60,8 @@ struct Cfg {
     static constexpr int kOffQ = 0;
     static constexpr int kOffK = kOffQ + kQBufs * kQBytes;
     static constexpr int kOffV = kOffK + kKSlots * kKVBytes;
-    static constexpr int kOffBar = kOffV + kVSlots * kKVBytes;
+    static constexpr int kOffStage = kOffV + kVSlots * kKVBytes;   // epilogue staging [2][128 rows][128 B]
+    static constexpr int kOffBar = kOffStage + 2 * kM * 128;
     static constexpr int kSmemBytes = kOffBar + 256 + 1024;  // + barriers + alignment slack
     // TMEM columns: O0 [0,D) O1 [D,2D) | S0 S1 (64 fp32 each) | P0 P1 (32 bf16x2 each) | m,l x2
     static constexpr int kTmemCols = 512;
@@ -106,6 +109,12 @@ struct Params {
             p.trace[((size_t)blockIdx.x * kTraceJ + (J)) * 16 + (ev)] = clock64();             \
     } while (0)
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -121,7 +130,8 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
 tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                 const __grid_constant__ CUtensorMap tmV, const Params p) {
+                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                 const Params p) {
     using C = Cfg<D>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -130,6 +140,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     const int lane = threadIdx.x & 31;
     const int item_begin = p.cta_off[blockIdx.x];
     const int item_end = p.cta_off[blockIdx.x + 1];
+    if (p.trace && threadIdx.x == 0) p.trace[(size_t)blockIdx.x * kTraceJ * 16 + 8] = globaltimer_ns();
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kQBufs; ++i) { mbar_init(&bars->q_full[i], 1); mbar_init(&bars->q_empty[i], 1); }
@@ -216,43 +227,22 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 __syncwarp();
             }
         }
-    } else if (warp == 2) {
-        // profiling only: observe when each K / V tile lands (events 8 / 9)
-        if (p.trace && lane < 2) {
-            uint32_t J = 0;
-            for (int w = item_begin; w < item_end; ++w)
-                for (int blk = p.items[w].blk_begin; blk < p.items[w].blk_end; ++blk, ++J) {
-                    if (J >= (uint32_t)kTraceJ) break;
-                    if (lane == 0) mbar_wait(&bars->k_full[J % kKSlots], (J / kKSlots) & 1);
-                    else mbar_wait(&bars->v_full[J % kVSlots], (J / kVSlots) & 1);
-                    TRACE(J, 8 + lane);
-                }
-        }
-        __syncwarp();
     } else if (warp == 1) {
-        // ============================ MMA issuer ============================
-        // Blocking, in the order S_0, S_1, S_2, PV_0, S_3, PV_1, ...: S runs two blocks ahead
-        // of PV, so each softmax warpgroup finds its next S already computed when it finishes
-        // a block (S_{J+2} only needs S_J consumed, long before P_J is ready).
+        // ============================ MMA issuer: S = Q K^T ============================
+        // Runs ahead as far as the S double buffer allows (S_J needs S_{J-2} consumed).
         constexpr uint32_t idS = idesc_bf16_f32(kM, kBlockN, 0);
-        constexpr uint32_t idPV = idesc_bf16_f32(kM, D, 1);
         const uint32_t sbase = smem_u32(smem);
-        int s_item = item_begin, s_j = 0, s_it = 0, s_nblk = 0;   // S cursor
         uint32_t sJ = 0;
-        if (s_item < item_end) s_nblk = p.items[s_item].blk_end - p.items[s_item].blk_begin;
-        int p_item = item_begin, p_j = 0, p_it = 0, p_nblk = s_nblk;  // PV cursor
-        uint32_t pJ = 0;
-        while (p_item < item_end) {
-            while (s_item < item_end && sJ < pJ + 3) {
-                const int qb = s_it % kQBufs;
-                if (s_j == 0) mbar_wait(&bars->q_full[qb], (s_it / kQBufs) & 1);
-                if (lane == 0) TRACE(sJ, 10);
+        int it = 0;
+        for (int w = item_begin; w < item_end; ++w, ++it) {
+            const int nblk = p.items[w].blk_end - p.items[w].blk_begin;
+            const int qb = it % kQBufs;
+            mbar_wait(&bars->q_full[qb], (it / kQBufs) & 1);
+            const uint32_t qa = sbase + C::kOffQ + qb * C::kQBytes;
+            for (int j = 0; j < nblk; ++j, ++sJ) {
                 mbar_wait(&bars->k_full[sJ % kKSlots], (sJ / kKSlots) & 1);
-                if (lane == 0) TRACE(sJ, 11);
                 mbar_wait(&bars->s_free[sJ & 1], ((sJ >> 1) & 1) ^ 1);
-                if (lane == 0) TRACE(sJ, 12);
                 tc_fence_after();
-                const uint32_t qa = sbase + C::kOffQ + qb * C::kQBytes;
                 const uint32_t ka = sbase + C::kOffK + (sJ % kKSlots) * C::kKVBytes;
                 const uint32_t sd = tmem + C::kColS + (sJ & 1) * kBlockN;
                 if (elect_one()) {
@@ -266,46 +256,39 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                     TRACE(sJ, 2);
                     umma_commit(&bars->s_full[sJ & 1]);
                     umma_commit(&bars->k_empty[sJ % kKSlots]);
+                    if (j == nblk - 1) umma_commit(&bars->q_empty[qb]);
                 }
                 __syncwarp();
-                ++sJ;
-                if (++s_j == s_nblk) {
-                    if (elect_one()) umma_commit(&bars->q_empty[qb]);
-                    __syncwarp();
-                    s_j = 0;
-                    ++s_it;
-                    ++s_item;
-                    if (s_item < item_end) s_nblk = p.items[s_item].blk_end - p.items[s_item].blk_begin;
-                }
             }
-            const bool first = p_j < 2;   // first block of its warpgroup in this item
-            if (lane == 0) TRACE(pJ, 13);
-            mbar_wait(&bars->p_full[pJ & 1], (pJ >> 1) & 1);
-            if (lane == 0) TRACE(pJ, 14);
-            mbar_wait(&bars->v_full[pJ % kVSlots], (pJ / kVSlots) & 1);
-            if (p_j == 0) mbar_wait(&bars->o_free, (p_it & 1) ^ 1);
-            tc_fence_after();
-            const uint32_t pa = tmem + C::kColP + (pJ & 1) * (kBlockN / 2);
-            const uint32_t va = sbase + C::kOffV + (pJ % kVSlots) * C::kKVBytes;
-            const uint32_t od = tmem + (pJ & 1) * D;
-            if (elect_one()) {
-                TRACE(pJ, 5);
+        }
+    } else if (warp == 2) {
+        // ============================ MMA issuer: O += P V ============================
+        constexpr uint32_t idPV = idesc_bf16_f32(kM, D, 1);
+        const uint32_t sbase = smem_u32(smem);
+        uint32_t pJ = 0;
+        int it = 0;
+        for (int w = item_begin; w < item_end; ++w, ++it) {
+            const int nblk = p.items[w].blk_end - p.items[w].blk_begin;
+            for (int j = 0; j < nblk; ++j, ++pJ) {
+                const bool first = j < 2;   // first block of its warpgroup in this item
+                mbar_wait(&bars->p_full[pJ & 1], (pJ >> 1) & 1);
+                mbar_wait(&bars->v_full[pJ % kVSlots], (pJ / kVSlots) & 1);
+                if (j == 0) mbar_wait(&bars->o_free, (it & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t pa = tmem + C::kColP + (pJ & 1) * (kBlockN / 2);
+                const uint32_t va = sbase + C::kOffV + (pJ % kVSlots) * C::kKVBytes;
+                const uint32_t od = tmem + (pJ & 1) * D;
+                if (elect_one()) {
+                    TRACE(pJ, 5);
 #pragma unroll
-                for (int kk = 0; kk < kBlockN / 16; ++kk) {
-                    uint64_t bd = smem_desc_sw128(va + kk * 2048, kBlockN * 128, 1024);
-                    umma_f16_ts(od, pa + kk * 8, bd, idPV, (first && kk == 0) ? 0u : 1u);
+                    for (int kk = 0; kk < kBlockN / 16; ++kk) {
+                        uint64_t bd = smem_desc_sw128(va + kk * 2048, kBlockN * 128, 1024);
+                        umma_f16_ts(od, pa + kk * 8, bd, idPV, (first && kk == 0) ? 0u : 1u);
+                    }
+                    umma_commit(&bars->pv_done[pJ & 1]);
+                    umma_commit(&bars->v_empty[pJ % kVSlots]);
                 }
-                umma_commit(&bars->pv_done[pJ & 1]);
-                umma_commit(&bars->v_empty[pJ % kVSlots]);
-                TRACE(pJ, 15);
-            }
-            __syncwarp();
-            ++pJ;
-            if (++p_j == p_nblk) {
-                p_j = 0;
-                ++p_it;
-                ++p_item;
-                if (p_item < item_end) p_nblk = p.items[p_item].blk_end - p.items[p_item].blk_begin;
+                __syncwarp();
             }
         }
     } else if (warp >= 4) {
@@ -353,14 +336,24 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->s_free[grp]);
-                // P buffer / O of this warpgroup were last used by its previous block (Jj - 2)
-                if (Jj >= 2) mbar_wait(&bars->pv_done[grp], ((Jj - 2) >> 1) & 1);
-                tc_fence_after();
+                // P buffer / O of this warpgroup were last used by its previous block (Jj - 2);
+                // waited for only right before they are touched (rescale / P store)
+                bool pv_waited = Jj < 2;
+                auto wait_prev_pv = [&]() {
+                    if (!pv_waited) {
+                        mbar_wait(&bars->pv_done[grp], ((Jj - 2) >> 1) & 1);
+                        tc_fence_after();
+                        pv_waited = true;
+                    }
+                };
                 if (warp_active) {
-                    float mx = -INFINITY;
+                    // row max over the block: 8 independent partial maxima (short dependency chains)
+                    float mx8[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) mx8[k] = -INFINITY;
                     if (kbase + kBlockN <= P) {
 #pragma unroll
-                        for (int c = 0; c < 64; ++c) mx = fmaxf(mx, __uint_as_float(sr[c]));
+                        for (int c = 0; c < 64; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sr[c]));
                     } else {
                         // visible-column bitmap of this block: prefix columns c < P - kbase,
                         // tree column c <-> node c - (P - kbase) (its ancestor bit)
@@ -373,9 +366,11 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                         for (int c = 0; c < 64; ++c) {
                             const bool ok = ((c < 32 ? vlo >> c : vhi >> (c - 32)) & 1u) != 0u;
                             sr[c] = ok ? sr[c] : 0xFF800000u;   // -inf
-                            mx = fmaxf(mx, __uint_as_float(sr[c]));
+                            mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sr[c]));
                         }
                     }
+                    const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                           fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
                     const float m_blk = mx * p.scale_log2;
                     bool need_o = false;
                     float alpha = 1.0f;
@@ -386,6 +381,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                         m_run = m_blk;
                     }
                     if (__any_sync(0xffffffffu, need_o)) {
+                        wait_prev_pv();
                         const float f = need_o ? alpha : 1.0f;
 #pragma unroll 1
                         for (int c0 = 0; c0 < D; c0 += 32) {
@@ -398,19 +394,25 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                         }
                     }
                     const float mo = (m_run == -INFINITY) ? 0.0f : m_run;
-                    float ls = 0.0f;
+                    float ls8[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) ls8[k] = 0.0f;
 #pragma unroll
                     for (int c = 0; c < 64; c += 2) {
                         const float e0 = ex2(fmaf(__uint_as_float(sr[c]), p.scale_log2, -mo));
                         const float e1 = ex2(fmaf(__uint_as_float(sr[c + 1]), p.scale_log2, -mo));
                         const uint32_t pk = pack_bf16(e0, e1);
                         sr[c >> 1] = pk;
-                        ls += __uint_as_float(pk << 16) + __uint_as_float(pk & 0xFFFF0000u);
+                        // the normaliser sums the bf16-rounded probabilities the PV MMA uses
+                        ls8[(c >> 1) & 7] += __uint_as_float(pk << 16) + __uint_as_float(pk & 0xFFFF0000u);
                     }
-                    l_run += ls;
+                    l_run += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
+                    wait_prev_pv();
                     tmem_st32(tmem + lane_base + C::kColP + grp * (kBlockN / 2),
                               reinterpret_cast<const uint32_t(&)[32]>(sr[0]));
                     tmem_wait_st();
+                } else {
+                    wait_prev_pv();
                 }
                 // keys past the end of the sample in its last page: zero those V rows so that
                 // garbage (possibly NaN) bytes never meet a zero probability in the MMA
@@ -444,6 +446,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 mbar_wait(&bars->pv_done[grp], (Jlast >> 1) & 1);
                 tc_fence_after();
             }
+            if (grp == 0 && wq == 0 && lane == 0) TRACE(J + nblk - 1, 10);
             // (m, l) exchange columns are double-buffered by item parity: a warpgroup can be at
             // most one epilogue ahead of the other (the named barrier needs both).
             const uint32_t ml_col = C::kColML + 4 * (it & 1);
@@ -453,7 +456,23 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             }
             tc_fence_before();
             named_bar_sync(2, 256);
+            if (grp == 0 && wq == 0 && lane == 0) TRACE(J + nblk - 1, 11);
             tc_fence_after();
+            const bool direct = wi.part < 0;
+            const int R_ = wi.rstride;
+            // Direct items (D = 128): each warpgroup stages its 64-column half of the tile (bf16,
+            // SW128 swizzle) and one thread stores every fully valid 16-row group with a TMA
+            // store; rows of a partially valid group are stored by their threads.
+            constexpr bool kStage = (D == 128);
+            const bool staged = kStage && direct;
+            uint8_t* stage = smem + C::kOffStage + grp * (kM * 128);
+            const bool issuer = wq == 0 && lane == 0;
+            if (staged) {
+                if (issuer) bulk_wait_read_all();            // previous store done reading staging
+                named_bar_sync(5 + grp, 128);
+            }
+            const int qgrp = lane < R_ ? (wq * R_ + (lane & ~15)) : 0;   // first logical row of my 16-row group
+            const bool grp_full = staged && (qgrp + 16) <= rows;
             if (warp_active) {
                 uint32_t mo_u, lo_u;
                 tmem_ld2(tmem + lane_base + ml_col + 2 * (grp ^ 1), mo_u, lo_u);
@@ -469,10 +488,10 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 const float invL = L > 0.0f ? 1.0f / L : 0.0f;
                 const float f0 = w0 * invL, f1 = w1 * invL;
                 const int h = wi.kvh * p.g + (grow % p.g);
-                const bool direct = wi.part < 0;
                 __nv_bfloat16* orow = p.out + ((int64_t)(off + node) * p.Hq + h) * D;
                 float* prow = direct ? nullptr : p.part_o + ((int64_t)wi.part * kM + r) * D;
                 const uint32_t rowbase = tmem + lane_base;
+                if (grp == 0 && wq == 0 && lane == 0) TRACE(J + nblk - 1, 14);
 #pragma unroll 1
                 for (int c0 = grp * (D / 2); c0 < (grp + 1) * (D / 2); c0 += 16) {
                     uint32_t a[16], bb[16];
@@ -483,6 +502,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                     for (int c = 0; c < 16; ++c)
                         a[c] = __float_as_uint((had0 ? __uint_as_float(a[c]) * f0 : 0.0f) +
                                                (had1 ? __uint_as_float(bb[c]) * f1 : 0.0f));
+                    if (grp == 0 && wq == 0 && lane == 0 && c0 == 0) TRACE(J + nblk - 1, 15);
                     if (row_valid) {
                         if (direct) {
 #pragma unroll
@@ -492,7 +512,12 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                                 u.y = pack_bf16(__uint_as_float(a[c + 2]), __uint_as_float(a[c + 3]));
                                 u.z = pack_bf16(__uint_as_float(a[c + 4]), __uint_as_float(a[c + 5]));
                                 u.w = pack_bf16(__uint_as_float(a[c + 6]), __uint_as_float(a[c + 7]));
-                                *reinterpret_cast<uint4*>(orow + c0 + c) = u;
+                                if (grp_full) {
+                                    const int chunk = ((c0 + c) - grp * (D / 2)) >> 3;   // 16-byte chunk in the 128-byte row
+                                    *reinterpret_cast<uint4*>(stage + r * 128 + ((chunk ^ (r & 7)) << 4)) = u;
+                                } else {
+                                    *reinterpret_cast<uint4*>(orow + c0 + c) = u;
+                                }
                             }
                         } else {
 #pragma unroll
@@ -511,6 +536,22 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 }
             }
             tc_fence_before();
+            if (grp == 0 && wq == 0 && lane == 0) TRACE(J + nblk - 1, 12);
+            if (staged) {
+                fence_proxy_async_smem();
+                named_bar_sync(5 + grp, 128);
+                if (issuer) {
+                    const int row0 = wi.mtile * 4 * R_;
+                    const int nodeb = off;
+                    for (int q = 0; q < 4; ++q)
+                        for (int t = 0; t < R_; t += 16)
+                            if (q * R_ + t + 16 <= rows)
+                                tma_store_3d(&tmO, stage + (32 * q + t) * 128, grp * (D / 2), wi.kvh * p.g,
+                                             nodeb + (row0 + q * R_ + t) / p.g);
+                    bulk_commit_group();
+                    if (grp == 0) TRACE(J + nblk - 1, 13);
+                }
+            }
             __syncwarp();
             if (wq == 0 && lane == 0 && grp == 0) TRACE(J + nblk - 1, 7);
             if (lane == 0) mbar_arrive(&bars->o_free);
@@ -565,11 +606,13 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             }
             J += nblk;
         }
+        if (wq == 0 && lane == 0) bulk_wait_all();   // output TMA stores complete before exit
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     if (warp == 2) tmem_dealloc<C::kTmemCols>(tmem);
+    if (p.trace && threadIdx.x == 0) p.trace[(size_t)blockIdx.x * kTraceJ * 16 + 9] = globaltimer_ns();
 }
 
 }  // namespace attn

@@ -75,6 +75,15 @@ def main():
     base = c0[0, 0]
     res["cta0_timeline"] = [[int(x - base) if x > 0 else -1 for x in row] for row in c0]
     res["cta0_items"] = items[cta[0]:cta[1]].tolist()
+    g0 = t[:, 0, 8]
+    g1 = t[:, 0, 9]
+    ok = (g0 > 0) & (g1 > 0)
+    res["globaltimer_us"] = {"kernel_span": float((g1[ok].max() - g0[ok].min()) / 1e3),
+                             "start_skew": float((g0[ok].max() - g0[ok].min()) / 1e3),
+                             "cta_median": float(np.median(g1[ok] - g0[ok]) / 1e3),
+                             "cta_max": float(np.max(g1[ok] - g0[ok]) / 1e3)}
+    t[:, 0, 8] = 0
+    t[:, 0, 9] = 0
     spans = []
     for c in range(n):
         v = t[c][t[c] > 0]
