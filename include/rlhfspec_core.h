@@ -243,6 +243,53 @@ rs_status rs_kv_unpack(void* const* k_layers_host, void* const* v_layers_host, i
                        int32_t max_pages, const int32_t* sample_rows, const int32_t* lens,
                        int32_t n, const void* buf, int64_t buf_offset_elems, void* stream);
 
+/* Host page allocator of one instance's paged KV store (same page ids in every layer/model).
+ * Allocation is all-or-nothing: RS_ERR_NO_MEMORY and nothing reserved if too few pages are
+ * free. Freeing a page that is not allocated is RS_ERR_INVALID_ARG. */
+typedef struct rs_page_pool rs_page_pool;
+rs_status rs_page_pool_create(int32_t num_pages, rs_page_pool** out);
+void rs_page_pool_destroy(rs_page_pool* pool);
+int32_t rs_page_pool_free_count(const rs_page_pool* pool);
+rs_status rs_page_pool_alloc(rs_page_pool* pool, int32_t n, int32_t* pages_out);
+rs_status rs_page_pool_free(rs_page_pool* pool, const int32_t* pages, int32_t n);
+/* Destination side of the handshake: reserve ceil(lens[i]/page_size) pages per sample
+ * (all-or-nothing) and write host block-table rows [n, max_pages] (tail padded with the last
+ * page). */
+rs_status rs_migrate_reserve(rs_page_pool* pool, const int32_t* lens_host, int32_t n,
+                             int32_t page_size, int32_t max_pages, int32_t* block_table_rows_out);
+
+/* NCCL communicator between generation instances (one process per GPU). The unique id is
+ * made on one rank and distributed by the caller (e.g. torch.distributed broadcast). */
+typedef struct rs_comm rs_comm;
+rs_status rs_comm_unique_id(uint8_t* id_out_128);
+rs_status rs_comm_create(const uint8_t* id_128, int32_t rank, int32_t world, rs_comm** out);
+rs_status rs_comm_destroy(rs_comm* comm);
+
+/* One instance's KV store: per model (SSM then LLM; L_ssm may be 0) host arrays of per-layer
+ * device page pools [pages, Hkv, page_size, head_dim] bf16. */
+typedef struct {
+    void* const* k_ssm;
+    void* const* v_ssm;
+    int32_t L_ssm, Hkv_ssm, d_ssm;
+    void* const* k_llm;
+    void* const* v_llm;
+    int32_t L_llm, Hkv_llm, d_llm;
+    int32_t page_size;
+} rs_kv_desc;
+
+/* Move n samples from src_rank to dst_rank, called collectively by both ranks
+ * (other ranks return at once). src: gids_host/lens_host [n], src_block_table device int32
+ * [n, max_pages] (row i = sample i). dst: pool reserves the pages; dst_block_table_host
+ * [n, max_pages] receives the new rows. Both: staging device buffer >= 2*(elems SSM + LLM)
+ * bytes; device_scratch device int32 >= 2n + n*max_pages. Blocking (returns after the
+ * stream is synchronised). On refusal both ranks return RS_ERR_NO_MEMORY and the source
+ * keeps its samples (nothing was sent). */
+rs_status rs_migrate_samples(rs_comm* comm, int32_t src_rank, int32_t dst_rank,
+                             const rs_kv_desc* kv, rs_page_pool* pool, const int64_t* gids_host,
+                             const int32_t* lens_host, int32_t n, const int32_t* src_block_table,
+                             int32_t max_pages, int32_t* dst_block_table_host, void* staging,
+                             size_t staging_bytes, int32_t* device_scratch, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -237,3 +237,240 @@ def kv_compact(k_layers, v_layers, block_table, prefix_len, accepted_len, path, 
                               _ptr(prefix_len), _ptr(accepted_len), _ptr(path), B, _ptr(new_len), _ptr(moves),
                               _stream(stream)), "rs_kv_compact")
     return new_len, moves
+
+
+# ------------------------------------------------------------------ a0 (host C++)
+class CostModelC(ctypes.Structure):
+    _fields_ = [("c_draft", _f64), ("b0", _f64), ("b1", _f64), ("b2", _f64), ("b3", _f64), ("k_sat", _f64),
+                ("seq_bucket", _i32), ("draft_bucket", _i32)]
+
+
+class StrategyC(ctypes.Structure):
+    _fields_ = [("n", _i32), ("depth", _i32), ("width", _i32), ("n_stop", _i32), ("cache_hit", _i32),
+                ("cache_entries", _i32), ("al", _f64), ("t_sd", _f64), ("objective", _f64)]
+
+
+_sig("rs_selector_create", _i32, ctypes.POINTER(CostModelC), _P, _P, _i32, ctypes.POINTER(_P))
+_sig("rs_selector_destroy", None, _P)
+_sig("rs_select_strategy", _i32, _P, _P, _P, _P, _P, _i32, _i32, _i32, _i32, ctypes.POINTER(StrategyC), _P)
+_sig("rs_cost_model_fit", _i32, _P, _P, _P, _i32, ctypes.POINTER(CostModelC))
+
+
+def _cost_c(cost) -> CostModelC:
+    """cost: any object with c_draft, b0..b3, k_sat, seq_bucket, draft_bucket attributes."""
+    return CostModelC(float(cost.c_draft), float(cost.b0), float(cost.b1), float(cost.b2), float(cost.b3),
+                      float(cost.k_sat), int(cost.seq_bucket), int(cost.draft_bucket))
+
+
+class Selector:
+    """Drafting-strategy selector with its bucket cache of t_sd predictions."""
+
+    def __init__(self, cost, knots_x, knots_y):
+        self._kx = np.ascontiguousarray(knots_x, dtype=np.float64)
+        self._ky = np.ascontiguousarray(knots_y, dtype=np.float64)
+        self._h = _P()
+        _check(_lib.rs_selector_create(ctypes.byref(_cost_c(cost)), _ptr(self._kx), _ptr(self._ky), len(self._kx),
+                                       ctypes.byref(self._h)), "rs_selector_create")
+
+    def select(self, trees, prefix_len, n_min=2, n_max=48, patience=2, return_selected=False):
+        """trees: per sample (parent int array, o float array) of the candidate tree."""
+        B = len(trees)
+        off = np.zeros(B + 1, dtype=np.int32)
+        for b, (p, _) in enumerate(trees):
+            off[b + 1] = off[b] + len(p)
+        parent = np.ascontiguousarray(np.concatenate([np.asarray(p, np.int32) for p, _ in trees]) if B else
+                                      np.zeros(0, np.int32), dtype=np.int32)
+        o = np.ascontiguousarray(np.concatenate([np.asarray(q, np.float64) for _, q in trees]) if B else
+                                 np.zeros(0), dtype=np.float64)
+        pl = _host_i32(prefix_len)
+        sel = np.full((max(B, 1), n_max), -1, dtype=np.int32)
+        out = StrategyC()
+        _check(_lib.rs_select_strategy(self._h, _ptr(parent), _ptr(o), _ptr(off), _ptr(pl), B, n_min, n_max,
+                                       patience, ctypes.byref(out), _ptr(sel)), "rs_select_strategy")
+        res = {k: getattr(out, k) for k, _ in StrategyC._fields_}
+        if return_selected:
+            res["selected"] = sel[:B]
+        return res
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.rs_selector_destroy(self._h)
+            self._h = None
+
+
+def cost_model_fit(n_seq, n_draft, t_sec, cost):
+    """Least-squares b0..b3 (c_draft and k_sat kept); returns a CostModelC."""
+    a = [np.ascontiguousarray(x, dtype=np.float64) for x in (n_seq, n_draft, t_sec)]
+    c = _cost_c(cost)
+    _check(_lib.rs_cost_model_fit(_ptr(a[0]), _ptr(a[1]), _ptr(a[2]), len(a[0]), ctypes.byref(c)),
+           "rs_cost_model_fit")
+    return c
+
+
+# ------------------------------------------------------------------ a6 (host C++)
+_sig("rs_knee_threshold", _i32, _P, _P, _i32, _f64, ctypes.POINTER(_i32))
+_sig("rs_plan_reallocation", _i32, _P, _i32, _i32, _P, _P, _P, ctypes.POINTER(_i32))
+_sig("rs_choose_samples", _i32, _P, _P, _P, _i32, _i32, _P)
+
+
+def knee_threshold(counts, tput, frac=0.1) -> int:
+    c = np.ascontiguousarray(counts, dtype=np.float64)
+    t = np.ascontiguousarray(tput, dtype=np.float64)
+    thr = _i32()
+    _check(_lib.rs_knee_threshold(_ptr(c), _ptr(t), len(c), float(frac), ctypes.byref(thr)), "rs_knee_threshold")
+    return thr.value
+
+
+def plan_reallocation(loads, threshold):
+    ld = _host_i32(loads)
+    G = len(ld)
+    s, d, c = (np.zeros(max(G, 1), np.int32) for _ in range(3))
+    m = _i32()
+    _check(_lib.rs_plan_reallocation(_ptr(ld), G, int(threshold), _ptr(s), _ptr(d), _ptr(c), ctypes.byref(m)),
+           "rs_plan_reallocation")
+    return [(int(s[i]), int(d[i]), int(c[i])) for i in range(m.value)]
+
+
+def choose_samples(gid, seq_len, avg_accepted, k):
+    g = np.ascontiguousarray(gid, dtype=np.int64)
+    sl = _host_i32(seq_len)
+    aa = np.ascontiguousarray(avg_accepted, dtype=np.float64)
+    out = np.zeros(max(k, 1), np.int64)
+    _check(_lib.rs_choose_samples(_ptr(g), _ptr(sl), _ptr(aa), len(g), int(k), _ptr(out)), "rs_choose_samples")
+    return [int(x) for x in out[:k]]
+
+
+# ------------------------------------------------------------------ a5
+_lib.rs_kv_pack_elems.restype = _i64
+_lib.rs_kv_pack_elems.argtypes = [_i32, _i32, _i32, _P, _i32]
+_sig("rs_kv_pack", _i32, _P, _P, _i32, _i32, _i32, _i32, _P, _i32, _P, _P, _i32, _P, _i64, _P)
+_sig("rs_kv_unpack", _i32, _P, _P, _i32, _i32, _i32, _i32, _P, _i32, _P, _P, _i32, _P, _i64, _P)
+_sig("rs_page_pool_create", _i32, _i32, ctypes.POINTER(_P))
+_sig("rs_page_pool_destroy", None, _P)
+_sig("rs_page_pool_free_count", _i32, _P)
+_sig("rs_page_pool_alloc", _i32, _P, _i32, _P)
+_sig("rs_page_pool_free", _i32, _P, _P, _i32)
+_sig("rs_migrate_reserve", _i32, _P, _P, _i32, _i32, _i32, _P)
+_sig("rs_comm_unique_id", _i32, _P)
+_sig("rs_comm_create", _i32, _P, _i32, _i32, ctypes.POINTER(_P))
+_sig("rs_comm_destroy", _i32, _P)
+
+
+class KVDescC(ctypes.Structure):
+    _fields_ = [("k_ssm", _P), ("v_ssm", _P), ("L_ssm", _i32), ("Hkv_ssm", _i32), ("d_ssm", _i32),
+                ("k_llm", _P), ("v_llm", _P), ("L_llm", _i32), ("Hkv_llm", _i32), ("d_llm", _i32),
+                ("page_size", _i32)]
+
+
+_sig("rs_migrate_samples", _i32, _P, _i32, _i32, ctypes.POINTER(KVDescC), _P, _P, _P, _i32, _P, _i32, _P, _P, _sz,
+     _P, _P)
+
+
+def kv_pack_elems(L, Hkv, head_dim, lens) -> int:
+    ln = _host_i32(lens)
+    return int(_lib.rs_kv_pack_elems(L, Hkv, head_dim, _ptr(ln), len(ln)))
+
+
+def kv_pack(k_layers, v_layers, block_table, sample_rows, lens, buf, offset_elems=0, stream=None):
+    """Gather the samples' K/V of one model (per-layer page pools [pages, Hkv, ps, d]) into buf."""
+    _, Hkv, ps, d = k_layers[0].shape
+    _check(_lib.rs_kv_pack(_layer_ptrs(k_layers), _layer_ptrs(v_layers), len(k_layers), Hkv, d, ps,
+                           _ptr(block_table), block_table.shape[1], _ptr(sample_rows), _ptr(lens), lens.numel(),
+                           _ptr(buf), int(offset_elems), _stream(stream)), "rs_kv_pack")
+    return buf
+
+
+def kv_unpack(k_layers, v_layers, block_table, sample_rows, lens, buf, offset_elems=0, stream=None):
+    _, Hkv, ps, d = k_layers[0].shape
+    _check(_lib.rs_kv_unpack(_layer_ptrs(k_layers), _layer_ptrs(v_layers), len(k_layers), Hkv, d, ps,
+                             _ptr(block_table), block_table.shape[1], _ptr(sample_rows), _ptr(lens), lens.numel(),
+                             _ptr(buf), int(offset_elems), _stream(stream)), "rs_kv_unpack")
+
+
+class PagePool:
+    """Host page allocator of one instance's KV store (all-or-nothing reservations)."""
+
+    def __init__(self, num_pages: int):
+        self._h = _P()
+        _check(_lib.rs_page_pool_create(int(num_pages), ctypes.byref(self._h)), "rs_page_pool_create")
+
+    @property
+    def handle(self):
+        return self._h
+
+    def free_count(self) -> int:
+        return int(_lib.rs_page_pool_free_count(self._h))
+
+    def alloc(self, n: int):
+        out = np.zeros(max(n, 1), np.int32)
+        st = _lib.rs_page_pool_alloc(self._h, int(n), _ptr(out))
+        if st == 6:   # RS_ERR_NO_MEMORY
+            return None
+        _check(st, "rs_page_pool_alloc")
+        return out[:n]
+
+    def free(self, pages):
+        p = _host_i32(pages)
+        _check(_lib.rs_page_pool_free(self._h, _ptr(p), len(p)), "rs_page_pool_free")
+
+    def reserve(self, lens, page_size, max_pages):
+        ln = _host_i32(lens)
+        rows = np.zeros((max(len(ln), 1), max_pages), np.int32)
+        st = _lib.rs_migrate_reserve(self._h, _ptr(ln), len(ln), int(page_size), int(max_pages), _ptr(rows))
+        if st == 6:
+            return None
+        _check(st, "rs_migrate_reserve")
+        return rows[:len(ln)]
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.rs_page_pool_destroy(self._h)
+            self._h = None
+
+
+class Comm:
+    """NCCL communicator between generation instances; the unique id travels over the
+    torch.distributed group `pg` (any backend) from rank 0."""
+
+    def __init__(self, rank: int, world: int, pg=None):
+        import torch.distributed as dist
+        uid = np.zeros(128, np.uint8)
+        if rank == 0:
+            _check(_lib.rs_comm_unique_id(_ptr(uid)), "rs_comm_unique_id")
+        if world > 1:
+            t = torch.from_numpy(uid.astype(np.int64))
+            dist.broadcast(t, 0, group=pg)
+            uid = np.ascontiguousarray(t.numpy().astype(np.uint8))
+        self._h = _P()
+        _check(_lib.rs_comm_create(_ptr(uid), int(rank), int(world), ctypes.byref(self._h)), "rs_comm_create")
+        self.rank, self.world = rank, world
+
+    def destroy(self):
+        if getattr(self, "_h", None):
+            _lib.rs_comm_destroy(self._h)
+            self._h = None
+
+
+def migrate_samples(comm: Comm, src_rank, dst_rank, llm_layers, ssm_layers, page_size, pool: PagePool | None,
+                    gids, lens, src_block_table, max_pages, staging, scratch, stream=None):
+    """Collective over (src, dst). llm_layers/ssm_layers: (k_layers, v_layers) lists or None.
+    Returns the destination block-table rows (dst) or None (src); raises RSError on refusal."""
+    def _model(m):
+        if not m:
+            return None, None, 0, 1, 8
+        k, v = m
+        return _layer_ptrs(k), _layer_ptrs(v), len(k), k[0].shape[1], k[0].shape[3]
+    ks, vs, Ls, Hs, ds = _model(ssm_layers)
+    kl, vl, Ll, Hl, dl = _model(llm_layers)
+    desc = KVDescC(ctypes.cast(ks, _P) if ks else None, ctypes.cast(vs, _P) if vs else None, Ls, Hs, ds,
+                   ctypes.cast(kl, _P), ctypes.cast(vl, _P), Ll, Hl, dl, int(page_size))
+    n = len(lens)
+    g = np.ascontiguousarray(gids, dtype=np.int64)
+    ln = _host_i32(lens)
+    rows = np.zeros((max(n, 1), max_pages), np.int32)
+    _check(_lib.rs_migrate_samples(comm._h, int(src_rank), int(dst_rank), ctypes.byref(desc),
+                                   pool.handle if pool is not None else None, _ptr(g), _ptr(ln), n,
+                                   _ptr(src_block_table), int(max_pages), _ptr(rows), _ptr(staging),
+                                   staging.numel() * staging.element_size(), _ptr(scratch), _stream(stream)),
+           "rs_migrate_samples")
+    return rows[:n] if comm.rank == dst_rank else None
