@@ -96,9 +96,9 @@ rs_status rs_attn_plan_upload(const rs_attn_plan* plan, void* ws, size_t ws_byte
 rs_status rs_attn_plan_info(const rs_attn_plan* plan, int32_t* num_ctas, int32_t* num_items,
                             int32_t* num_split_units);
 /* Copy the schedule out (for inspection / tests): cta_off host int32 [num_ctas+1] (items of
- * CTA c are [cta_off[c], cta_off[c+1])), items host int32 [num_items, 10] =
+ * CTA c are [cta_off[c], cta_off[c+1])), items host int32 [num_items, 12] =
  * (sample, kv_head, m_tile, first_block, end_block, partial_slot or -1, rows per TMEM
- * sub-partition R, split unit or -1, softmax stream 0/1, 0). Either may be NULL. */
+ * sub-partition R, split unit or -1, prefix_len, tree_off, tree size, 0). Either may be NULL. */
 rs_status rs_attn_plan_items(const rs_attn_plan* plan, int32_t* cta_off, int32_t* items);
 void rs_attn_plan_destroy(rs_attn_plan* plan);
 /* Profiling hook: when buf (device, >= num_ctas*256*8*8 bytes) is set, every attention launch

@@ -12,7 +12,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librlhfspec_core.so")
+LIB_PATH = os.environ.get("RS_CORE_LIB") or os.path.join(_HERE, "librlhfspec_core.so")   # RS_CORE_LIB: profiling variants
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2512_04752_b200.build` "
                       "(the CUDA path has no fallback)")
@@ -121,10 +121,10 @@ class AttnPlan:
         return dict(num_ctas=a.value, num_items=b.value, num_split_units=c.value)
 
     def schedule(self):
-        """(cta_off [num_ctas+1], items [num_items, 7]) as numpy arrays."""
+        """(cta_off [num_ctas+1], items [num_items, 12]) as numpy arrays (fields: rs_attn_plan_items)."""
         inf = self.info()
         cta = np.zeros(inf["num_ctas"] + 1, dtype=np.int32)
-        items = np.zeros((inf["num_items"], 10), dtype=np.int32)
+        items = np.zeros((inf["num_items"], 12), dtype=np.int32)
         _check(_lib.rs_attn_plan_items(self.handle, _ptr(cta), _ptr(items)), "rs_attn_plan_items")
         return cta, items
 

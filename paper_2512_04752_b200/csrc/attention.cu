@@ -34,7 +34,7 @@ using namespace attn;
 // Profiling hook state (rs_attn_set_trace).
 static unsigned long long* g_trace_buf = nullptr;
 static size_t g_trace_bytes = 0;
-static constexpr int kOvhBlocks = 2;    // per-item fixed cost in block units (planning)
+static constexpr int kOvhBlocksDefault = 2;   // per-item fixed cost in block units (planning)
 static constexpr int kMinPart = 4;      // smallest split-KV part, in blocks
 
 namespace {
@@ -62,6 +62,7 @@ PFN_encodeTiled get_encode() {
 // ---------------------------------------------------------------- plan
 struct rs_attn_plan {
     int B, Hq, Hkv, D, ps, g, n_ctas, NT;
+    int rmodes;                 // bit 0: some unit has R = 16, bit 1: some unit has R = 32
     std::vector<int32_t> cta_off;
     std::vector<WorkItem> items;
     std::vector<SplitUnit> units;
@@ -85,6 +86,8 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
     RS_REQUIRE(page_size == kBlockN, RS_ERR_UNSUPPORTED, "rs_attn_plan_create: page_size %d != 64",
                page_size);
     const int g = Hq / Hkv;
+    // per-item overhead (epilogue, Q load) in KV-block units; RS_ATTN_OVH overrides (tuning only)
+    const int kOvhBlocks = getenv("RS_ATTN_OVH") ? std::max(0, atoi(getenv("RS_ATTN_OVH"))) : kOvhBlocksDefault;
     RS_REQUIRE(g <= 16 && (16 % g) == 0, RS_ERR_UNSUPPORTED, "rs_attn_plan_create: group size %d (need g | 16)", g);
     if (num_ctas <= 0) {
         int dev = 0, sms = 148;
@@ -94,10 +97,11 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
         num_ctas = sms;
     }
     auto* pl = new rs_attn_plan();
+    pl->rmodes = 0;
     pl->B = B; pl->Hq = Hq; pl->Hkv = Hkv; pl->D = head_dim; pl->ps = page_size; pl->g = g;
     pl->NT = B ? tree_off_host[B] : 0;
     // units
-    struct U { int b, kvh, mtile, nblk, R; };
+    struct U { int b, kvh, mtile, nblk, R, P, node0, T; };
     std::vector<U> units;
     long long W = 0;
     for (int b = 0; b < B; ++b) {
@@ -113,7 +117,8 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
         const int mt = (T * g + 4 * R - 1) / (4 * R);
         for (int kvh = 0; kvh < Hkv; ++kvh)
             for (int m = 0; m < mt; ++m) {
-                units.push_back({b, kvh, m, nblk, R});
+                units.push_back({b, kvh, m, nblk, R, P, tree_off_host[b], T});
+                pl->rmodes |= (R == 16) ? 1 : 2;
                 W += nblk + kOvhBlocks;
             }
     }
@@ -159,7 +164,7 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
             }
             if (!where.empty()) W_eff += kOvhBlocks;   // an extra part of a split unit
             where.push_back({cta, (int)per_cta[cta].size()});
-            per_cta[cta].push_back({u.b, u.kvh, u.mtile, start, start + take, -1, u.R, -1, 0, 0});
+            per_cta[cta].push_back({u.b, u.kvh, u.mtile, start, start + take, -1, u.R, -1, u.P, u.node0, u.T, 0});
             pos += take + kOvhBlocks;
             start += take;
             rem -= take;
@@ -171,15 +176,6 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
                 per_cta[wc.first][wc.second].part = n_parts++;
                 per_cta[wc.first][wc.second].unit = uid;
             }
-        }
-    }
-    // two softmax streams per CTA: each item goes to the stream with less work so far
-    const bool one_stream = getenv("RS_ATTN_ONE_STREAM") != nullptr;   // debugging aid
-    for (auto& list : per_cta) {
-        long long ld[2] = {0, 0};
-        for (auto& w : list) {
-            w.stream = (!one_stream && ld[1] < ld[0]) ? 1 : 0;
-            ld[w.stream] += (w.blk_end - w.blk_begin) + kOvhBlocks;
         }
     }
     pl->cta_off.assign(n_ctas + 1, 0);
@@ -299,15 +295,22 @@ static rs_status launch_attn(const rs_attn_plan* pl, const void* q, const void* 
     prm.scale_log2 = sm_scale * 1.4426950408889634f;
     prm.out = static_cast<__nv_bfloat16*>(out);
     prm.lse = lse;
+    static const int dbg = getenv("RS_ATTN_DBG") ? atoi(getenv("RS_ATTN_DBG")) : 0;   // profiling ablations only
+    prm.dbg = dbg;
     prm.trace = (g_trace_bytes >= (size_t)pl->n_ctas * kTraceJ * 16 * sizeof(unsigned long long)) ? g_trace_buf
                                                                                                : nullptr;
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[D == 128]) {
-        RS_CUDA_CHECK(cudaFuncSetAttribute(tree_attn_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           C::kSmemBytes));
-        attr_set[D == 128] = true;
+    // row mode: kernels specialised for plans whose tiles all use R = 16 (half-split rows) or all
+    // R = 32, so each carries only the registers of its own softmax path; mixed plans take both.
+    const int rm = pl->rmodes == 1 ? 1 : (pl->rmodes == 2 ? 2 : 3);
+    auto kern = rm == 1 ? tree_attn_kernel<D, 1> : (rm == 2 ? tree_attn_kernel<D, 2> : tree_attn_kernel<D, 3>);
+    const int smem_bytes = rm == 1 ? Cfg<D, 1>::kSmemBytes : Cfg<D, 2>::kSmemBytes;
+    static bool attr_set[2][4] = {};
+    if (!attr_set[D == 128][rm]) {
+        RS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+        attr_set[D == 128][rm] = true;
     }
-    tree_attn_kernel<D><<<pl->n_ctas, kThreads, C::kSmemBytes, st>>>(tmQ, tmK, tmV, tmO, prm);
+    const int threads = rm == 1 ? KT<1>::kThreads : KT<2>::kThreads;
+    kern<<<pl->n_ctas, threads, smem_bytes, st>>>(tmQ, tmK, tmV, tmO, prm);
     RS_LAUNCH_CHECK();
     return RS_OK;
 }

@@ -23,6 +23,8 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <type_traits>
+
 #include "sm100_ptx.cuh"
 
 namespace attn {
@@ -31,38 +33,75 @@ using namespace rs::ptx;
 
 constexpr int kBlockN = 64;      // keys per KV block (= page_size)
 constexpr int kM = 128;          // query rows per work item (UMMA M)
-constexpr int kKSlots = 4;
-constexpr int kVSlots = 4;
+#ifndef RS_ATTN_KSLOTS
+#define RS_ATTN_KSLOTS 4
+#endif
+#ifndef RS_ATTN_VSLOTS
+#define RS_ATTN_VSLOTS 4
+#endif
+#ifndef RS_ATTN_EW_SLOTS
+#define RS_ATTN_EW_SLOTS 4
+#endif
+constexpr int kMaxSlots = 8;
+#ifndef RS_ATTN_STAGE
+#define RS_ATTN_STAGE 0
+#endif
+constexpr int kKSlots = RS_ATTN_KSLOTS;
+constexpr int kVSlots = RS_ATTN_VSLOTS;
+constexpr bool kStageOut = RS_ATTN_STAGE != 0;   // epilogue output through smem + TMA store
 constexpr int kQBufs = 2;
-constexpr int kThreads = 384;    // 12 warps
+constexpr int kPF = 0;          // L2 prefetch distance in KV blocks (0 = off; measured: no gain)
+constexpr int kThreads = 384;    // 12 warps (RM 2/3)
+// RM = 1 (every tile R = 16): 16 warps; warps 12-15 are an epilogue warpgroup, and consecutive
+// items alternate between the two 16-lane halves of each TMEM sub-partition, so item i's O is
+// normalised and stored while item i+1 already accumulates.
+template <int RM> struct KT { static constexpr bool kEW = (RM == 1); static constexpr int kThreads = kEW ? 512 : 384; };
 constexpr int kTraceJ = 256;
 
 // Row layout of a tile: logical query row r (node-major (node, head-in-group) pairs of the unit)
 // lives in TMEM lane / UMMA row m = (r / R) * 32 + r % R, R = rstride in {16, 32}: each of the
 // four TMEM sub-partitions (= softmax warps) holds R consecutive rows, so a short tile
 // (T*g <= 64, R = 16) still spreads its work over all four SM sub-partitions.
-struct WorkItem {
+struct alignas(16) WorkItem {
     int32_t b, kvh, mtile, blk_begin, blk_end, part;  // part: -1 = direct, else partial slot
     int32_t rstride;                                  // R (tile covers 4*R logical rows)
     int32_t unit;                                     // split-unit index, -1 if direct
-    int32_t stream;                                   // (two-stream variant; unused here)
-    int32_t pad;
-};
+    int32_t P, node0, T;                              // sample's prefix length, tree_off[b], tree size
+    int32_t pad;                                      // (copied from the host lengths at plan time, so an
+};                                                    //  item needs one 48-byte load and no dependent ones)
+static_assert(sizeof(WorkItem) == 48, "WorkItem layout (rs_attn_plan_items)");
+
+__device__ __forceinline__ WorkItem load_item(const WorkItem* items, int w) {
+    const int4* src = reinterpret_cast<const int4*>(items + w);
+    const int4 a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2);
+    WorkItem r;
+    r.b = a.x; r.kvh = a.y; r.mtile = a.z; r.blk_begin = a.w;
+    r.blk_end = b.x; r.part = b.y; r.rstride = b.z; r.unit = b.w;
+    r.P = c.x; r.node0 = c.y; r.T = c.z; r.pad = c.w;
+    return r;
+}
 struct SplitUnit {
     int32_t b, kvh, mtile, n_parts, part_base, rstride;
 };
 
-template <int D>
+template <int D, int RM = 2>
 struct Cfg {
+    static constexpr bool kEW = (RM == 1);
+    // RM = 1: the two logical Q buffers are the two 16-row halves of ONE 128-row tile (items
+    // alternate lane halves), which frees 32 KB for deeper K/V rings.
+    static constexpr int KS = kEW ? RS_ATTN_EW_SLOTS : kKSlots;
+    static constexpr int VS = kEW ? RS_ATTN_EW_SLOTS : kVSlots;
+    static_assert(KS <= kMaxSlots && VS <= kMaxSlots, "ring depth");
     static constexpr int kBoxes = D / 64;                    // 64-element (128 B) SW128 boxes
     static constexpr int kQBytes = kM * D * 2;
+    static constexpr int kQStride = kEW ? 0 : kQBytes;       // smem offset between logical Q buffers
     static constexpr int kKVBytes = kBlockN * D * 2;         // one K or V page tile
     static constexpr int kOffQ = 0;
-    static constexpr int kOffK = kOffQ + kQBufs * kQBytes;
-    static constexpr int kOffV = kOffK + kKSlots * kKVBytes;
-    static constexpr int kOffStage = kOffV + kVSlots * kKVBytes;   // epilogue staging [2][128 rows][128 B]
-    static constexpr int kOffBar = kOffStage + 2 * kM * 128;
-    static constexpr int kSmemBytes = kOffBar + 256 + 1024;  // + barriers + alignment slack
+    static constexpr int kOffK = kOffQ + (kEW ? 1 : kQBufs) * kQBytes;
+    static constexpr int kOffV = kOffK + KS * kKVBytes;
+    static constexpr int kOffStage = kOffV + VS * kKVBytes;   // epilogue staging [2][128 rows][128 B]
+    static constexpr int kOffBar = kOffStage + (kStageOut ? 2 * kM * 128 : 0);
+    static constexpr int kSmemBytes = kOffBar + 512 + 1024;  // + barriers + alignment slack
     // TMEM columns: O0 [0,D) O1 [D,2D) | S0 S1 (64 fp32 each) | P0 P1 (32 bf16x2 each) | m,l x2
     static constexpr int kTmemCols = 512;
     static constexpr int kColS = 2 * D;
@@ -73,11 +112,12 @@ struct Cfg {
 
 struct Bars {
     uint64_t q_full[kQBufs], q_empty[kQBufs];
-    uint64_t k_full[kKSlots], k_empty[kKSlots];
-    uint64_t v_full[kVSlots], v_empty[kVSlots];
+    uint64_t k_full[kMaxSlots], k_empty[kMaxSlots];
+    uint64_t v_full[kMaxSlots], v_empty[kMaxSlots];
     uint64_t s_full[2], s_free[2];
     uint64_t p_full[2], pv_done[2];
     uint64_t o_free;
+    uint64_t o_ready[2], ml_ready[2], o_free2[2];   // epilogue-warpgroup handshakes (RM = 1), by item parity
     uint32_t tmem_base;
     int merge_flag;
 };
@@ -99,10 +139,13 @@ struct Params {
     __nv_bfloat16* out;
     float* lse;
     unsigned long long* trace;   // optional per-block event timestamps (profiling)
+    int dbg;                     // ablation switches for profiling only (RS_ATTN_DBG; results wrong if != 0):
+                                 // 1 skip epilogue O reads/stores, 2 skip softmax math, 4 skip PV MMA
 };
 
 // Profiling events (clock64 per CTA / block J): 0 K issued, 1 V issued, 2 S issued,
-// 3 S ready (softmax), 4 P written, 5 PV issued, 6 epilogue start, 7 epilogue end.
+// 3 S ready (softmax), 4 P written, 5 PV issued, 6 epilogue start, 7 epilogue end, 8 K seen
+// landed by the S issuer, 9 V seen landed by the PV issuer; globaltimer at J = kTraceJ-1, 14/15.
 #define TRACE(J, ev)                                                                          \
     do {                                                                                      \
         if (p.trace && (J) < (uint32_t)kTraceJ)                                               \
@@ -127,12 +170,13 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     return r;
 }
 
-template <int D>
-__global__ void __launch_bounds__(kThreads, 1)
+// RM: 1 = every tile has R = 16, 2 = every tile has R = 32, 3 = mixed (both paths compiled in).
+template <int D, int RM>
+__global__ void __launch_bounds__(KT<RM>::kThreads, 1)
 tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
                  const Params p) {
-    using C = Cfg<D>;
+    using C = Cfg<D, RM>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     Bars* bars = reinterpret_cast<Bars*>(smem + C::kOffBar);
@@ -140,12 +184,12 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     const int lane = threadIdx.x & 31;
     const int item_begin = p.cta_off[blockIdx.x];
     const int item_end = p.cta_off[blockIdx.x + 1];
-    if (p.trace && threadIdx.x == 0) p.trace[(size_t)blockIdx.x * kTraceJ * 16 + 8] = globaltimer_ns();
+    if (p.trace && threadIdx.x == 0) p.trace[((size_t)blockIdx.x * kTraceJ + kTraceJ - 1) * 16 + 14] = globaltimer_ns();
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kQBufs; ++i) { mbar_init(&bars->q_full[i], 1); mbar_init(&bars->q_empty[i], 1); }
-        for (int i = 0; i < kKSlots; ++i) { mbar_init(&bars->k_full[i], 1); mbar_init(&bars->k_empty[i], 1); }
-        for (int i = 0; i < kVSlots; ++i) { mbar_init(&bars->v_full[i], 1); mbar_init(&bars->v_empty[i], 1); }
+        for (int i = 0; i < C::KS; ++i) { mbar_init(&bars->k_full[i], 1); mbar_init(&bars->k_empty[i], 1); }
+        for (int i = 0; i < C::VS; ++i) { mbar_init(&bars->v_full[i], 1); mbar_init(&bars->v_empty[i], 1); }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bars->s_full[i], 1);
             mbar_init(&bars->s_free[i], 4);
@@ -153,6 +197,11 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             mbar_init(&bars->pv_done[i], 1);
         }
         mbar_init(&bars->o_free, 8);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bars->o_ready[i], 1);
+            mbar_init(&bars->ml_ready[i], 8);
+            mbar_init(&bars->o_free2[i], 4);
+        }
         fence_mbar_init();
         prefetch_tmap(&tmQ);
         prefetch_tmap(&tmK);
@@ -163,68 +212,114 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = bars->tmem_base;
-    if (warp == 0) {
-        // ============================ TMA producer: Q + K ============================
-        // (whole warp runs the loop; one elected lane issues)
+    if (warp == 0 || warp == 3) {
+        // ============================ TMA producers ============================
+        // warp 0: Q tiles + K pages; warp 3: V pages (whole warp runs the loop; one elected lane
+        // issues). Page ids come 32 at a time from one coalesced load, a chunk ahead of use; item
+        // descriptors are read two items ahead. Each producer also prefetches its pages kPF blocks
+        // ahead into L2 (cp.async.bulk.prefetch.tensor), so the smem ring only has to cover the
+        // L2 -> SM latency while HBM keeps kPF blocks per SM in flight.
+        const bool isK = warp == 0;
+        const CUtensorMap* tm = isK ? &tmK : &tmV;
+        const int kSlots = isK ? C::KS : C::VS;
+        const int pf = ((p.dbg >> 8) & 63) ? ((p.dbg >> 8) & 63) : kPF;
+        const bool do_pf = pf > 0;
         uint32_t J = 0;
-        int it = 0;
-        for (int w = item_begin; w < item_end; ++w, ++it) {
-            const WorkItem wi = p.items[w];
-            const int qb = it % kQBufs;
-            mbar_wait(&bars->q_empty[qb], ((it / kQBufs) & 1) ^ 1);
-            const int R = wi.rstride;
-            const int row0 = wi.mtile * 4 * R;              // first logical row of the tile
-            uint8_t* qs = smem + C::kOffQ + qb * C::kQBytes;
-            const int nodeb = p.tree_off[wi.b];
+        auto issue_q = [&](const WorkItem& x, int slot_it) {
+            const int qb = slot_it % kQBufs;
+            mbar_wait(&bars->q_empty[qb], ((slot_it / kQBufs) & 1) ^ 1);
+            const int R = x.rstride;
+            const int row0 = x.mtile * 4 * R;               // first logical row of the tile
+            uint8_t* qs = smem + C::kOffQ + qb * C::kQStride;
             if (elect_one()) {
                 mbar_arrive_expect_tx(&bars->q_full[qb], 4 * R * 128 * C::kBoxes);
                 // boxes of 16 rows (16/g nodes x g heads x 64 d): logical rows q*R + 16*s of
                 // quarter q go to UMMA rows 32*q + 16*s
                 for (int q = 0; q < 4; ++q)
                     for (int s = 0; s < R; s += 16) {
-                        const int node = nodeb + (row0 + q * R + s) / p.g;
+                        const int node = x.node0 + (row0 + q * R + s) / p.g;
 #pragma unroll
                         for (int bx = 0; bx < C::kBoxes; ++bx)
-                            tma_load_3d(qs + bx * (kM * 128) + (32 * q + s) * 128, &tmQ, &bars->q_full[qb],
-                                        bx * 64, wi.kvh * p.g, node);
+                            tma_load_3d(qs + bx * (kM * 128) + (32 * q + s + (KT<RM>::kEW ? 16 * (slot_it & 1) : 0)) * 128, &tmQ, &bars->q_full[qb],
+                                        bx * 64, x.kvh * p.g, node);
                     }
             }
             __syncwarp();
-            const int32_t* bt = p.block_table + (int64_t)wi.b * p.max_pages;
-            for (int blk = wi.blk_begin; blk < wi.blk_end; ++blk, ++J) {
-                const int s = J % kKSlots;
-                mbar_wait(&bars->k_empty[s], ((J / kKSlots) & 1) ^ 1);
-                const int row = (bt[blk] * p.Hkv + wi.kvh) * kBlockN;
-                uint8_t* ks = smem + C::kOffK + s * C::kKVBytes;
-                if (elect_one()) {
-                    TRACE(J, 0);
-                    mbar_arrive_expect_tx(&bars->k_full[s], C::kKVBytes);
+        };
+        auto page_chunk = [&](const WorkItem& x, int base) {
+            const int j = base + lane;
+            return (j < x.blk_end - x.blk_begin)
+                       ? __ldg(p.block_table + (int64_t)x.b * p.max_pages + x.blk_begin + j) : 0;
+        };
+        if (item_begin < item_end) {
+            WorkItem wi = load_item(p.items, item_begin);
+            WorkItem wn = (item_begin + 1 < item_end) ? load_item(p.items, item_begin + 1) : wi;
+            if (isK) issue_q(wi, 0);
+            int pg_cur = page_chunk(wi, 0);
+            // warm L2 with the first blocks of this CTA
+            for (int k = 0; k < pf && k < wi.blk_end - wi.blk_begin; ++k) {
+                const int page = __shfl_sync(0xffffffffu, pg_cur, k & 31);
+                if (k < 32 && elect_one())
 #pragma unroll
-                    for (int bx = 0; bx < C::kBoxes; ++bx)
-                        tma_load_2d(ks + bx * (kBlockN * 128), &tmK, &bars->k_full[s], bx * 64, row);
-                }
+                    for (int bx = 0; bx < C::kBoxes; ++bx) tma_prefetch_2d(tm, bx * 64, (page * p.Hkv + wi.kvh) * kBlockN);
                 __syncwarp();
             }
-        }
-    } else if (warp == 3) {
-        // ============================ TMA producer: V ============================
-        uint32_t J = 0;
-        for (int w = item_begin; w < item_end; ++w) {
-            const WorkItem wi = p.items[w];
-            const int32_t* bt = p.block_table + (int64_t)wi.b * p.max_pages;
-            for (int blk = wi.blk_begin; blk < wi.blk_end; ++blk, ++J) {
-                const int s = J % kVSlots;
-                mbar_wait(&bars->v_empty[s], ((J / kVSlots) & 1) ^ 1);
-                const int row = (bt[blk] * p.Hkv + wi.kvh) * kBlockN;
-                uint8_t* vs = smem + C::kOffV + s * C::kKVBytes;
-                if (elect_one()) {
-                    TRACE(J, 1);
-                    mbar_arrive_expect_tx(&bars->v_full[s], C::kKVBytes);
+            int it = 0;
+            for (int w = item_begin; w < item_end; ++w, ++it) {
+                const bool has_next = w + 1 < item_end;
+                const WorkItem wnn = (w + 2 < item_end) ? load_item(p.items, w + 2) : wn;
+                const int nb = wi.blk_end - wi.blk_begin;
+                const int nbn = has_next ? wn.blk_end - wn.blk_begin : 0;
+                const int pg_first_next = has_next ? page_chunk(wn, 0) : 0;
+                const int q_next_at = nb > 6 ? nb - 6 : 0;
+                int pg_nxt = nb > 32 ? page_chunk(wi, 32) : 0;
+                for (int base = 0; base < nb; base += 32) {
+                    const int cnt = min(32, nb - base);
+                    for (int k = 0; k < cnt; ++k, ++J) {
+                        const int j = base + k;
+                        if (isK && has_next && j == q_next_at) issue_q(wn, it + 1);
+                        // L2 prefetch of block j + pf (this item or the next one)
+                        if (do_pf) {
+                            const int f = j + pf;
+                            int fpage = -1, fkvh = wi.kvh;
+                            if (f < nb) {
+                                const int fk = k + pf;
+                                const int v0 = __shfl_sync(0xffffffffu, pg_cur, fk & 31);
+                                const int v1 = __shfl_sync(0xffffffffu, pg_nxt, fk & 31);
+                                fpage = fk < 32 ? v0 : v1;
+                            } else if (f - nb < nbn && f - nb < 32) {
+                                fpage = __shfl_sync(0xffffffffu, pg_first_next, (f - nb) & 31);
+                                fkvh = wn.kvh;
+                            }
+                            if (fpage >= 0 && (f < nb ? (k + pf < 64) : true) && elect_one()) {
 #pragma unroll
-                    for (int bx = 0; bx < C::kBoxes; ++bx)
-                        tma_load_2d(vs + bx * (kBlockN * 128), &tmV, &bars->v_full[s], bx * 64, row);
+                                for (int bx = 0; bx < C::kBoxes; ++bx)
+                                    tma_prefetch_2d(tm, bx * 64, (fpage * p.Hkv + fkvh) * kBlockN);
+                            }
+                            __syncwarp();
+                        }
+                        const int page = __shfl_sync(0xffffffffu, pg_cur, k);
+                        const int s = J % kSlots;
+                        uint64_t* empty = isK ? &bars->k_empty[s] : &bars->v_empty[s];
+                        uint64_t* full = isK ? &bars->k_full[s] : &bars->v_full[s];
+                        mbar_wait(empty, ((J / kSlots) & 1) ^ 1);
+                        const int row = (page * p.Hkv + wi.kvh) * kBlockN;
+                        uint8_t* dst = smem + (isK ? C::kOffK : C::kOffV) + s * C::kKVBytes;
+                        if (elect_one()) {
+                            TRACE(J, isK ? 0 : 1);
+                            mbar_arrive_expect_tx(full, C::kKVBytes);
+#pragma unroll
+                            for (int bx = 0; bx < C::kBoxes; ++bx)
+                                tma_load_2d(dst + bx * (kBlockN * 128), tm, full, bx * 64, row);
+                        }
+                        __syncwarp();
+                    }
+                    pg_cur = pg_nxt;
+                    pg_nxt = (base + 64 < nb) ? page_chunk(wi, base + 64) : 0;
                 }
-                __syncwarp();
+                pg_cur = pg_first_next;
+                wi = wn;
+                wn = wnn;
             }
         }
     } else if (warp == 1) {
@@ -234,20 +329,22 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         const uint32_t sbase = smem_u32(smem);
         uint32_t sJ = 0;
         int it = 0;
+        int nblk = item_begin < item_end ? __ldg(&p.items[item_begin].blk_end) - __ldg(&p.items[item_begin].blk_begin) : 0;
         for (int w = item_begin; w < item_end; ++w, ++it) {
-            const int nblk = p.items[w].blk_end - p.items[w].blk_begin;
+            const int nblk_next = (w + 1 < item_end) ? __ldg(&p.items[w + 1].blk_end) - __ldg(&p.items[w + 1].blk_begin) : 0;
             const int qb = it % kQBufs;
             mbar_wait(&bars->q_full[qb], (it / kQBufs) & 1);
-            const uint32_t qa = sbase + C::kOffQ + qb * C::kQBytes;
+            const uint32_t qa = sbase + C::kOffQ + qb * C::kQStride;
             for (int j = 0; j < nblk; ++j, ++sJ) {
-                mbar_wait(&bars->k_full[sJ % kKSlots], (sJ / kKSlots) & 1);
+                mbar_wait(&bars->k_full[sJ % C::KS], (sJ / C::KS) & 1);
+                if (lane == 0) TRACE(sJ, 8);
                 mbar_wait(&bars->s_free[sJ & 1], ((sJ >> 1) & 1) ^ 1);
                 tc_fence_after();
-                const uint32_t ka = sbase + C::kOffK + (sJ % kKSlots) * C::kKVBytes;
+                const uint32_t ka = sbase + C::kOffK + (sJ % C::KS) * C::kKVBytes;
                 const uint32_t sd = tmem + C::kColS + (sJ & 1) * kBlockN;
                 if (elect_one()) {
 #pragma unroll
-                    for (int k = 0; k < D / 16; ++k) {
+                    for (int k = 0; k < ((p.dbg & 16) ? 0 : D / 16); ++k) {
                         const int bx = k >> 2, within = (k & 3) * 32;
                         uint64_t ad = smem_desc_sw128(qa + bx * (kM * 128) + within, 16, 1024);
                         uint64_t bd = smem_desc_sw128(ka + bx * (kBlockN * 128) + within, 16, 1024);
@@ -255,11 +352,12 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                     }
                     TRACE(sJ, 2);
                     umma_commit(&bars->s_full[sJ & 1]);
-                    umma_commit(&bars->k_empty[sJ % kKSlots]);
+                    umma_commit(&bars->k_empty[sJ % C::KS]);
                     if (j == nblk - 1) umma_commit(&bars->q_empty[qb]);
                 }
                 __syncwarp();
             }
+            nblk = nblk_next;
         }
     } else if (warp == 2) {
         // ============================ MMA issuer: O += P V ============================
@@ -267,29 +365,363 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         const uint32_t sbase = smem_u32(smem);
         uint32_t pJ = 0;
         int it = 0;
+        int nblk = item_begin < item_end ? __ldg(&p.items[item_begin].blk_end) - __ldg(&p.items[item_begin].blk_begin) : 0;
         for (int w = item_begin; w < item_end; ++w, ++it) {
-            const int nblk = p.items[w].blk_end - p.items[w].blk_begin;
+            const int nblk_next = (w + 1 < item_end) ? __ldg(&p.items[w + 1].blk_end) - __ldg(&p.items[w + 1].blk_begin) : 0;
             for (int j = 0; j < nblk; ++j, ++pJ) {
-                const bool first = j < 2;   // first block of its warpgroup in this item
+                // EW: O is pre-zeroed, so every PV accumulates; else the first block of each
+                // warpgroup in the item overwrites
+                const bool first = !KT<RM>::kEW && j < 2;
                 mbar_wait(&bars->p_full[pJ & 1], (pJ >> 1) & 1);
-                mbar_wait(&bars->v_full[pJ % kVSlots], (pJ / kVSlots) & 1);
-                if (j == 0) mbar_wait(&bars->o_free, (it & 1) ^ 1);
+                mbar_wait(&bars->v_full[pJ % C::VS], (pJ / C::VS) & 1);
+                if (lane == 0) TRACE(pJ, 9);
+                // (EW: the softmax warpgroup re-zeroes its O half before its first P of the item,
+                // after the epilogue of item it-2 released it, so PV needs no wait here)
+                if (!KT<RM>::kEW && j == 0) mbar_wait(&bars->o_free, (it & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t pa = tmem + C::kColP + (pJ & 1) * (kBlockN / 2);
-                const uint32_t va = sbase + C::kOffV + (pJ % kVSlots) * C::kKVBytes;
+                const uint32_t va = sbase + C::kOffV + (pJ % C::VS) * C::kKVBytes;
                 const uint32_t od = tmem + (pJ & 1) * D;
                 if (elect_one()) {
                     TRACE(pJ, 5);
 #pragma unroll
-                    for (int kk = 0; kk < kBlockN / 16; ++kk) {
+                    for (int kk = 0; kk < ((p.dbg & 16) ? 0 : (p.dbg & 4) ? 1 : kBlockN / 16); ++kk) {
                         uint64_t bd = smem_desc_sw128(va + kk * 2048, kBlockN * 128, 1024);
                         umma_f16_ts(od, pa + kk * 8, bd, idPV, (first && kk == 0) ? 0u : 1u);
                     }
                     umma_commit(&bars->pv_done[pJ & 1]);
-                    umma_commit(&bars->v_empty[pJ % kVSlots]);
+                    umma_commit(&bars->v_empty[pJ % C::VS]);
+                    if (KT<RM>::kEW && j == nblk - 1) umma_commit(&bars->o_ready[it & 1]);
                 }
                 __syncwarp();
             }
+            nblk = nblk_next;
+        }
+    } else if (KT<RM>::kEW && warp >= 12) {
+        // ============================ epilogue warpgroup (RM = 1) ============================
+        // Item it (TMEM lane half h = it & 1): wait for its last PV (o_ready) and both softmax
+        // warpgroups' (m, l) (ml_ready), merge the two partial states, normalise, store bf16 (or
+        // the split-KV partial), re-zero the O half for item it+2 and release it (o_free2).
+        const int wq = warp & 3;
+        const int hl = lane & 15;
+        const int rr = wq * 32 + hl;
+        const uint32_t qbase = (uint32_t)(wq * 32) << 16;
+        uint32_t J = 0;
+        int it = 0;
+        WorkItem wi = item_begin < item_end ? load_item(p.items, item_begin) : WorkItem{};
+        for (int w = item_begin; w < item_end; ++w, ++it) {
+            const WorkItem wn = (w + 1 < item_end) ? load_item(p.items, w + 1) : wi;
+            const int h = it & 1;
+            const int off = wi.node0;
+            const int rows = min(64, wi.T * p.g - wi.mtile * 64);
+            const bool warp_active = wq * 16 < rows;
+            const int rl = wq * 16 + hl;
+            const bool row_valid = rl < rows;
+            const int grow = wi.mtile * 64 + rl;
+            const int node = grow / p.g;
+            const int nblk = wi.blk_end - wi.blk_begin;
+            const bool had0 = nblk >= 2 || (J & 1) == 0;
+            const bool had1 = nblk >= 2 || (J & 1) == 1;
+            const bool direct = wi.part < 0;
+            mbar_wait(&bars->o_ready[h], (it >> 1) & 1);
+            mbar_wait(&bars->ml_ready[h], (it >> 1) & 1);
+            tc_fence_after();
+            if (wq == 0 && lane == 0) TRACE(J + nblk - 1, 6);
+            {   // only valid rows compute and store
+                uint32_t m0u, l0u, m1u, l1u;
+                tmem_ld2(tmem + qbase + C::kColML + 4 * h, m0u, l0u);
+                tmem_ld2(tmem + qbase + C::kColML + 4 * h + 2, m1u, l1u);
+                tmem_wait_ld();
+                const float m0 = __uint_as_float(m0u), l0 = __uint_as_float(l0u);
+                const float m1 = __uint_as_float(m1u), l1 = __uint_as_float(l1u);
+                const float M = fmaxf(had0 ? m0 : -INFINITY, had1 ? m1 : -INFINITY);
+                const float w0 = (had0 && l0 > 0.0f) ? ex2(m0 - M) : 0.0f;
+                const float w1 = (had1 && l1 > 0.0f) ? ex2(m1 - M) : 0.0f;
+                const float L = l0 * w0 + l1 * w1;
+                const float invL = L > 0.0f ? 1.0f / L : 0.0f;
+                const float f0 = w0 * invL, f1 = w1 * invL;
+                const int hh = wi.kvh * p.g + (grow % p.g);
+                __nv_bfloat16* orow = p.out + ((int64_t)(off + node) * p.Hq + hh) * D;
+                float* prow = direct ? nullptr : p.part_o + ((int64_t)wi.part * kM + rr) * D;
+                const uint32_t rowbase = tmem + ((uint32_t)(wq * 32 + 16 * h) << 16);
+                const int cb = (lane & 16) ? D / 2 : 0;   // my columns [cb, cb + D/2)
+#pragma unroll 1
+                for (int cc = 0; cc < D / 2; cc += 16) {
+                    uint32_t a[16], bb[16];
+                    tmem_ld_hs16<D / 2>(rowbase + cc, a);
+                    tmem_ld_hs16<D / 2>(rowbase + D + cc, bb);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < 16; ++c)
+                        a[c] = __float_as_uint(__uint_as_float(a[c]) * f0 + __uint_as_float(bb[c]) * f1);
+                    if (warp_active && row_valid) {
+                        if (direct) {
+#pragma unroll
+                            for (int c = 0; c < 16; c += 8) {
+                                uint4 u;
+                                u.x = pack_bf16(__uint_as_float(a[c]), __uint_as_float(a[c + 1]));
+                                u.y = pack_bf16(__uint_as_float(a[c + 2]), __uint_as_float(a[c + 3]));
+                                u.z = pack_bf16(__uint_as_float(a[c + 4]), __uint_as_float(a[c + 5]));
+                                u.w = pack_bf16(__uint_as_float(a[c + 6]), __uint_as_float(a[c + 7]));
+                                *reinterpret_cast<uint4*>(orow + cb + cc + c) = u;
+                            }
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < 16; c += 4)
+                                *reinterpret_cast<uint4*>(prow + cb + cc + c) = make_uint4(a[c], a[c + 1], a[c + 2], a[c + 3]);
+                        }
+                    }
+                }
+                if (warp_active && row_valid && lane < 16) {
+                    const float lse2 = L > 0.0f ? M + __log2f(L) : -INFINITY;
+                    if (direct) {
+                        if (p.lse) p.lse[(int64_t)(off + node) * p.Hq + hh] = lse2 * 0.6931471805599453f;
+                    } else {
+                        p.part_lse[(int64_t)wi.part * kM + rr] = lse2;
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars->o_free2[h]);
+            if (wq == 0 && lane == 0) TRACE(J + nblk - 1, 7);
+            if (wi.part >= 0) {
+                // split-KV unit: the CTA that completes its last part merges all parts
+                __threadfence();
+                named_bar_sync(3, 128);
+                if (threadIdx.x == 12 * 32) {
+                    const int old = atomicAdd(&p.unit_counter[wi.unit], 1);
+                    const int last = (old == p.units[wi.unit].n_parts - 1) ? 1 : 0;
+                    if (last) p.unit_counter[wi.unit] = 0;          // ready for the next launch
+                    bars->merge_flag = last;
+                }
+                named_bar_sync(3, 128);
+                if (bars->merge_flag && row_valid && warp_active) {
+                    __threadfence();
+                    const SplitUnit u = p.units[wi.unit];
+                    float M = -INFINITY;
+                    for (int q = 0; q < u.n_parts; ++q)
+                        M = fmaxf(M, __ldcg(p.part_lse + (int64_t)(u.part_base + q) * kM + rr));
+                    float wsum = 0.0f;
+                    for (int q = 0; q < u.n_parts; ++q) {
+                        const float lq = __ldcg(p.part_lse + (int64_t)(u.part_base + q) * kM + rr);
+                        wsum += (lq == -INFINITY) ? 0.0f : ex2(lq - M);
+                    }
+                    const float inv = wsum > 0.0f ? 1.0f / wsum : 0.0f;
+                    const int hh = wi.kvh * p.g + (grow % p.g);
+                    __nv_bfloat16* orow = p.out + ((int64_t)(off + node) * p.Hq + hh) * D;
+                    const int mcb = (lane & 16) ? D / 2 : 0;
+#pragma unroll 1
+                    for (int c0 = mcb; c0 < mcb + D / 2; c0 += 8) {
+                        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                        for (int q = 0; q < u.n_parts; ++q) {
+                            const float lq = __ldcg(p.part_lse + (int64_t)(u.part_base + q) * kM + rr);
+                            const float wq2 = (lq == -INFINITY) ? 0.0f : ex2(lq - M) * inv;
+                            const float4* src = reinterpret_cast<const float4*>(
+                                p.part_o + ((int64_t)(u.part_base + q) * kM + rr) * D + c0);
+                            const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
+                            acc[0] += wq2 * x0.x; acc[1] += wq2 * x0.y; acc[2] += wq2 * x0.z; acc[3] += wq2 * x0.w;
+                            acc[4] += wq2 * x1.x; acc[5] += wq2 * x1.y; acc[6] += wq2 * x1.z; acc[7] += wq2 * x1.w;
+                        }
+                        uint4 o;
+                        o.x = pack_bf16(acc[0], acc[1]);
+                        o.y = pack_bf16(acc[2], acc[3]);
+                        o.z = pack_bf16(acc[4], acc[5]);
+                        o.w = pack_bf16(acc[6], acc[7]);
+                        *reinterpret_cast<uint4*>(orow + c0) = o;
+                    }
+                    if (p.lse && lane < 16)
+                        p.lse[(int64_t)(off + node) * p.Hq + hh] = (M + __log2f(wsum)) * 0.6931471805599453f;
+                }
+            }
+            J += nblk;
+            wi = wn;
+        }
+    } else if (KT<RM>::kEW && warp >= 4) {
+        // ============================ softmax (RM = 1, half-split rows) ============================
+        const int grp = (warp - 4) >> 2;         // warpgroup: handles blocks with (J & 1) == grp
+        const int wq = warp & 3;                 // TMEM sub-partition of this warp
+        const int r = wq * 32 + lane;            // smem row for the V-tail zeroing
+        const int hl = lane & 15;
+        const uint32_t qbase = (uint32_t)(wq * 32) << 16;
+        {
+            // O (both lane halves) and P (both halves) of my warpgroup start at zero
+            uint32_t z32[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) z32[c] = 0u;
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+                const uint32_t lb = tmem + ((uint32_t)(wq * 32 + 16 * h2) << 16);
+#pragma unroll
+                for (int c0 = 0; c0 < D / 2; c0 += 32) tmem_st_hs32<D / 2>(lb + grp * D + c0, z32);
+                tmem_st_hs16<16>(lb + C::kColP + grp * (kBlockN / 2), reinterpret_cast<const uint32_t(&)[16]>(z32[0]));
+            }
+            tmem_wait_st();
+        }
+        uint32_t J = 0;
+        int it = 0;
+        WorkItem wi = item_begin < item_end ? load_item(p.items, item_begin) : WorkItem{};
+        for (int w = item_begin; w < item_end; ++w, ++it) {
+            const WorkItem wn = (w + 1 < item_end) ? load_item(p.items, w + 1) : wi;   // prefetch
+            const int h = it & 1;
+            const uint32_t lane_base = (uint32_t)(wq * 32 + 16 * h) << 16;
+            const uint32_t o_mine = tmem + lane_base + grp * D;
+            const int P = wi.P;
+            const int off = wi.node0;
+            const int T = wi.T;
+            const int rl = wq * 16 + hl;
+            const int rows = min(64, T * p.g - wi.mtile * 64);
+            const bool warp_active = wq * 16 < rows;
+            const bool row_valid = rl < rows;
+            const int grow = wi.mtile * 64 + rl;
+            const int node = grow / p.g;
+            const uint64_t mask = row_valid ? __ldg(p.tree_mask + off + node) : 0ull;
+            const int key_end = P + T;
+            const int nblk = wi.blk_end - wi.blk_begin;
+            float m_run = -INFINITY, l_run = 0.0f;
+            bool had = false;
+            bool first_blk = true;
+            for (int j = (int)((J & 1) != (uint32_t)grp); j < nblk; j += 2) {
+                const uint32_t Jj = J + j;
+                const int kbase = (wi.blk_begin + j) * kBlockN;
+                mbar_wait(&bars->s_full[grp], (Jj >> 1) & 1);
+                tc_fence_after();
+                if (wq == 0 && lane == 0) TRACE(Jj, 3);
+                bool pv_waited = Jj < 2;
+                auto wait_prev_pv = [&]() {
+                    if (!pv_waited) {
+                        mbar_wait(&bars->pv_done[grp], ((Jj - 2) >> 1) & 1);
+                        tc_fence_after();
+                        pv_waited = true;
+                    }
+                };
+                uint32_t sh[32];
+                if (warp_active) {
+                    tmem_ld_hs32<32>(tmem + lane_base + C::kColS + grp * kBlockN, sh);
+                    tmem_wait_ld();
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->s_free[grp]);
+                if (warp_active) {
+                    const int kh = (lane & 16) ? 32 : 0;   // first key of my half
+                    float mx8[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) mx8[k] = -INFINITY;
+                    if (kbase + kBlockN <= P) {
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sh[c]));
+                    } else {
+                        const int dlt = P - kbase;
+                        uint64_t vb = dlt >= 64 ? ~0ull : (dlt <= 0 ? 0ull : ((1ull << dlt) - 1ull));
+                        if (dlt >= 0 && dlt < 64) vb |= mask << dlt;
+                        else if (dlt < 0 && dlt > -64) vb |= mask >> (-dlt);
+                        const uint32_t vh = (uint32_t)(vb >> kh);
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) {
+                            sh[c] = ((vh >> c) & 1u) ? sh[c] : 0xFF800000u;   // -inf
+                            mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sh[c]));
+                        }
+                    }
+                    float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                     fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+                    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+                    const float m_blk = mx * p.scale_log2;
+                    bool need_o = false;
+                    float alpha = 1.0f;
+                    if (m_blk > m_run + 8.0f) {
+                        alpha = ex2(m_run - m_blk);
+                        need_o = had && row_valid && (m_run != -INFINITY);
+                        l_run *= alpha;
+                        m_run = m_blk;
+                    }
+                    if (__any_sync(0xffffffffu, need_o)) {
+                        wait_prev_pv();
+                        const float f = need_o ? alpha : 1.0f;
+#pragma unroll 1
+                        for (int c0 = 0; c0 < D / 2; c0 += 32) {
+                            uint32_t o[32];
+                            tmem_ld_hs32<D / 2>(o_mine + c0, o);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
+                            tmem_st_hs32<D / 2>(o_mine + c0, o);
+                        }
+                    }
+                    const float mo = (m_run == -INFINITY) ? 0.0f : m_run;
+                    float ls8[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) ls8[k] = 0.0f;
+#pragma unroll
+                    for (int c = 0; c < 32; c += 2) {
+                        const float e0 = ex2(fmaf(__uint_as_float(sh[c]), p.scale_log2, -mo));
+                        const float e1 = ex2(fmaf(__uint_as_float(sh[c + 1]), p.scale_log2, -mo));
+                        const uint32_t pk = pack_bf16(e0, e1);
+                        sh[c >> 1] = pk;
+                        ls8[(c >> 1) & 7] += __uint_as_float(pk << 16) + __uint_as_float(pk & 0xFFFF0000u);
+                    }
+                    l_run += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
+                }
+                wait_prev_pv();
+                if (first_blk && it >= 2) {
+                    // O half h last held item it-2: once its epilogue has read it, zero it. Only
+                    // this warpgroup's MMAs touch these columns and its previous one is complete,
+                    // so no MMA read-modify-write can race with the store.
+                    mbar_wait(&bars->o_free2[h], ((it >> 1) & 1) ^ 1);
+                    uint32_t z32[32];
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) z32[c] = 0u;
+#pragma unroll
+                    for (int c0 = 0; c0 < D / 2; c0 += 32) tmem_st_hs32<D / 2>(o_mine + c0, z32);
+                }
+                if (warp_active)
+                    tmem_st_hs16<16>(tmem + lane_base + C::kColP + grp * (kBlockN / 2),
+                                     reinterpret_cast<const uint32_t(&)[16]>(sh[0]));
+                if (first_blk) {
+                    // the other lane half of my P buffer belongs to the previous item: zero it so
+                    // this item's PV MMAs add nothing to that item's O
+                    uint32_t z[16];
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) z[c] = 0u;
+                    tmem_st_hs16<16>(tmem + (lane_base ^ (16u << 16)) + C::kColP + grp * (kBlockN / 2), z);
+                    if (!warp_active) {   // inactive warps: this item's half must hold zero P as well
+                        tmem_st_hs16<16>(tmem + lane_base + C::kColP + grp * (kBlockN / 2), z);
+                    }
+                    first_blk = false;
+                }
+                tmem_wait_st();
+                // keys past the end of the sample in its last page: zero those V rows
+                const int nvalid = key_end - kbase;
+                if (nvalid < kBlockN) {
+                    const uint32_t sl = Jj % C::VS;
+                    mbar_wait(&bars->v_full[sl], (Jj / C::VS) & 1);
+                    if (r < kBlockN && r >= nvalid) {
+                        uint8_t* vs = smem + C::kOffV + sl * C::kKVBytes;
+#pragma unroll
+                        for (int bx = 0; bx < C::kBoxes; ++bx) {
+                            uint4* row = reinterpret_cast<uint4*>(vs + bx * (kBlockN * 128) + r * 128);
+#pragma unroll
+                            for (int c = 0; c < 8; ++c) row[c] = make_uint4(0, 0, 0, 0);
+                        }
+                    }
+                    fence_proxy_async_smem();
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (wq == 0 && lane == 0) TRACE(Jj, 4);
+                if (lane == 0) mbar_arrive(&bars->p_full[grp]);
+                had = true;
+            }
+            // hand (m, l) of this warpgroup to the epilogue warps and move on
+            l_run += __shfl_xor_sync(0xffffffffu, l_run, 16);
+            if (it >= 2) mbar_wait(&bars->o_free2[h], ((it >> 1) & 1) ^ 1);   // ML[h] of item it-2 consumed
+            tmem_st2(tmem + qbase + C::kColML + 4 * h + 2 * grp, __float_as_uint(m_run), __float_as_uint(l_run));
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars->ml_ready[h]);
+            J += nblk;
+            wi = wn;
         }
     } else if (warp >= 4) {
         // ============================ softmax + epilogue ============================
@@ -300,17 +732,23 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         const uint32_t o_mine = tmem + lane_base + grp * D;
         uint32_t J = 0;
         int it = 0;
+        WorkItem wi = item_begin < item_end ? load_item(p.items, item_begin) : WorkItem{};
         for (int w = item_begin; w < item_end; ++w, ++it) {
-            const WorkItem wi = p.items[w];
-            const int b = wi.b;
-            const int P = p.prefix_len[b];
-            const int off = p.tree_off[b];
-            const int T = p.tree_off[b + 1] - off;
+            const WorkItem wn = (w + 1 < item_end) ? load_item(p.items, w + 1) : wi;   // prefetch
+            const int P = wi.P;
+            const int off = wi.node0;
+            const int T = wi.T;
             const int R = wi.rstride;
-            const int rl = wq * R + lane;                // logical row within the tile
+            // R = 16: the tile occupies TMEM lanes 0-15 of each sub-partition; two threads share a
+            // row (16x32bx2 TMEM shapes), lanes 0-15 taking keys / columns of the low half and
+            // lanes 16-31 those of the high half, so no lane idles.
+            const bool hs = RM == 1 ? true : (RM == 2 ? false : (R == 16));
+            const int hl = hs ? (lane & 15) : lane;      // row lane of this thread
+            const int rr = wq * 32 + hl;                 // TMEM lane / UMMA row of my row
+            const int rl = wq * R + hl;                  // logical row within the tile
             const int rows = min(4 * R, T * p.g - wi.mtile * 4 * R);
             const bool warp_active = wq * R < rows;
-            const bool row_valid = lane < R && rl < rows;
+            const bool row_valid = hl < R && rl < rows;
             const int grow = wi.mtile * 4 * R + rl;      // row within the unit
             const int node = grow / p.g;
             const uint64_t mask = row_valid ? p.tree_mask[off + node] : 0ull;
@@ -319,12 +757,103 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             float m_run = -INFINITY, l_run = 0.0f;
             bool had = false;
             uint32_t Jlast = 0;
+            // the block loop is instantiated per row mode so each path keeps only its own registers
+            auto block_loop = [&](auto hs_tag) {
+            constexpr bool HS = decltype(hs_tag)::value;
             for (int j = (int)((J & 1) != (uint32_t)grp); j < nblk; j += 2) {
                 const uint32_t Jj = J + j;
                 const int kbase = (wi.blk_begin + j) * kBlockN;
                 mbar_wait(&bars->s_full[grp], (Jj >> 1) & 1);
                 tc_fence_after();
                 if (wq == 0 && lane == 0) TRACE(Jj, 3);
+                // P buffer / O of this warpgroup were last used by its previous block (Jj - 2);
+                // waited for only right before they are touched (rescale / P store)
+                bool pv_waited = Jj < 2;
+                auto wait_prev_pv = [&]() {
+                    if (!pv_waited) {
+                        mbar_wait(&bars->pv_done[grp], ((Jj - 2) >> 1) & 1);
+                        tc_fence_after();
+                        pv_waited = true;
+                    }
+                };
+                if constexpr (HS) {
+                    // ---- half-split row: 32 keys per thread ----
+                    uint32_t sh[32];
+                    if (warp_active) {
+                        tmem_ld_hs32<32>(tmem + lane_base + C::kColS + grp * kBlockN, sh);
+                        tmem_wait_ld();
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&bars->s_free[grp]);
+                    if (p.dbg & 16) {
+                        wait_prev_pv();
+                    } else if (warp_active) {
+                        const int kh = (lane & 16) ? 32 : 0;   // first key of my half
+                        float mx8[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) mx8[k] = -INFINITY;
+                        if (kbase + kBlockN <= P) {
+#pragma unroll
+                            for (int c = 0; c < 32; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sh[c]));
+                        } else {
+                            const int dlt = P - kbase;
+                            uint64_t vb = dlt >= 64 ? ~0ull : (dlt <= 0 ? 0ull : ((1ull << dlt) - 1ull));
+                            if (dlt >= 0 && dlt < 64) vb |= mask << dlt;
+                            else if (dlt < 0 && dlt > -64) vb |= mask >> (-dlt);
+                            const uint32_t vh = (uint32_t)(vb >> kh);
+#pragma unroll
+                            for (int c = 0; c < 32; ++c) {
+                                sh[c] = ((vh >> c) & 1u) ? sh[c] : 0xFF800000u;   // -inf
+                                mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sh[c]));
+                            }
+                        }
+                        float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                         fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+                        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+                        const float m_blk = mx * p.scale_log2;
+                        bool need_o = false;
+                        float alpha = 1.0f;
+                        if (m_blk > m_run + 8.0f) {
+                            alpha = ex2(m_run - m_blk);
+                            need_o = had && row_valid && (m_run != -INFINITY);
+                            l_run *= alpha;
+                            m_run = m_blk;
+                        }
+                        if (__any_sync(0xffffffffu, need_o)) {
+                            wait_prev_pv();
+                            const float f = need_o ? alpha : 1.0f;
+#pragma unroll 1
+                            for (int c0 = 0; c0 < D / 2; c0 += 32) {
+                                uint32_t o[32];
+                                tmem_ld_hs32<D / 2>(o_mine + c0, o);
+                                tmem_wait_ld();
+#pragma unroll
+                                for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
+                                tmem_st_hs32<D / 2>(o_mine + c0, o);
+                            }
+                        }
+                        const float mo = (m_run == -INFINITY) ? 0.0f : m_run;
+                        float ls8[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) ls8[k] = 0.0f;
+#pragma unroll
+                        for (int c = 0; c < 32; c += 2) {
+                            const float e0 = ex2(fmaf(__uint_as_float(sh[c]), p.scale_log2, -mo));
+                            const float e1 = ex2(fmaf(__uint_as_float(sh[c + 1]), p.scale_log2, -mo));
+                            const uint32_t pk = pack_bf16(e0, e1);
+                            sh[c >> 1] = pk;
+                            ls8[(c >> 1) & 7] += __uint_as_float(pk << 16) + __uint_as_float(pk & 0xFFFF0000u);
+                        }
+                        l_run += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
+                        wait_prev_pv();
+                        tmem_st_hs16<16>(tmem + lane_base + C::kColP + grp * (kBlockN / 2),
+                                         reinterpret_cast<const uint32_t(&)[16]>(sh[0]));
+                        tmem_wait_st();
+                    } else {
+                        wait_prev_pv();
+                    }
+                } else {
                 // sr: raw S bits -> masked S -> packed bf16 P in sr[0..31]
                 uint32_t sr[64];
                 if (warp_active) {
@@ -336,17 +865,12 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->s_free[grp]);
-                // P buffer / O of this warpgroup were last used by its previous block (Jj - 2);
-                // waited for only right before they are touched (rescale / P store)
-                bool pv_waited = Jj < 2;
-                auto wait_prev_pv = [&]() {
-                    if (!pv_waited) {
-                        mbar_wait(&bars->pv_done[grp], ((Jj - 2) >> 1) & 1);
-                        tc_fence_after();
-                        pv_waited = true;
-                    }
-                };
-                if (warp_active) {
+                if (warp_active && (p.dbg & 2)) {
+                    wait_prev_pv();
+                    tmem_st32(tmem + lane_base + C::kColP + grp * (kBlockN / 2),
+                              reinterpret_cast<const uint32_t(&)[32]>(sr[0]));
+                    tmem_wait_st();
+                } else if (warp_active) {
                     // row max over the block: 8 independent partial maxima (short dependency chains)
                     float mx8[8];
 #pragma unroll
@@ -414,12 +938,13 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 } else {
                     wait_prev_pv();
                 }
+                }   // !hs
                 // keys past the end of the sample in its last page: zero those V rows so that
                 // garbage (possibly NaN) bytes never meet a zero probability in the MMA
                 const int nvalid = key_end - kbase;
                 if (nvalid < kBlockN) {
-                    const uint32_t s = Jj % kVSlots;
-                    mbar_wait(&bars->v_full[s], (Jj / kVSlots) & 1);
+                    const uint32_t s = Jj % C::VS;
+                    mbar_wait(&bars->v_full[s], (Jj / C::VS) & 1);
                     if (r < kBlockN && r >= nvalid) {
                         uint8_t* vs = smem + C::kOffV + s * C::kKVBytes;
 #pragma unroll
@@ -438,6 +963,9 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 had = true;
                 Jlast = Jj;
             }
+            };
+            if (hs) block_loop(std::true_type{});
+            else block_loop(std::false_type{});
             // ---------------- epilogue: merge the two warpgroups' states ----------------
             if (wq == 0 && lane == 0) TRACE(J + nblk - 1, 6);
             const bool had0 = nblk >= 2 || (J & 1) == 0;
@@ -450,6 +978,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             // (m, l) exchange columns are double-buffered by item parity: a warpgroup can be at
             // most one epilogue ahead of the other (the named barrier needs both).
             const uint32_t ml_col = C::kColML + 4 * (it & 1);
+            if (hs && warp_active) l_run += __shfl_xor_sync(0xffffffffu, l_run, 16);   // both key halves
             if (warp_active) {
                 tmem_st2(tmem + lane_base + ml_col + 2 * grp, __float_as_uint(m_run), __float_as_uint(l_run));
                 tmem_wait_st();
@@ -463,7 +992,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             // Direct items (D = 128): each warpgroup stages its 64-column half of the tile (bf16,
             // SW128 swizzle) and one thread stores every fully valid 16-row group with a TMA
             // store; rows of a partially valid group are stored by their threads.
-            constexpr bool kStage = (D == 128);
+            constexpr bool kStage = kStageOut && (D == 128);
             const bool staged = kStage && direct;
             uint8_t* stage = smem + C::kOffStage + grp * (kM * 128);
             const bool issuer = wq == 0 && lane == 0;
@@ -471,12 +1000,16 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 if (issuer) bulk_wait_read_all();            // previous store done reading staging
                 named_bar_sync(5 + grp, 128);
             }
-            const int qgrp = lane < R_ ? (wq * R_ + (lane & ~15)) : 0;   // first logical row of my 16-row group
+            const int qgrp = hl < R_ ? (wq * R_ + (hl & ~15)) : 0;       // first logical row of my 16-row group
             const bool grp_full = staged && (qgrp + 16) <= rows;
             if (warp_active) {
                 uint32_t mo_u, lo_u;
                 tmem_ld2(tmem + lane_base + ml_col + 2 * (grp ^ 1), mo_u, lo_u);
                 tmem_wait_ld();
+                if (hs) {   // lanes 16-31 read unused TMEM lanes: take the row's values from lane - 16
+                    mo_u = __shfl_sync(0xffffffffu, mo_u, hl);
+                    lo_u = __shfl_sync(0xffffffffu, lo_u, hl);
+                }
                 const float m0 = grp == 0 ? m_run : __uint_as_float(mo_u);
                 const float l0 = grp == 0 ? l_run : __uint_as_float(lo_u);
                 const float m1 = grp == 1 ? m_run : __uint_as_float(mo_u);
@@ -489,20 +1022,29 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 const float f0 = w0 * invL, f1 = w1 * invL;
                 const int h = wi.kvh * p.g + (grow % p.g);
                 __nv_bfloat16* orow = p.out + ((int64_t)(off + node) * p.Hq + h) * D;
-                float* prow = direct ? nullptr : p.part_o + ((int64_t)wi.part * kM + r) * D;
+                float* prow = direct ? nullptr : p.part_o + ((int64_t)wi.part * kM + rr) * D;
                 const uint32_t rowbase = tmem + lane_base;
                 if (grp == 0 && wq == 0 && lane == 0) TRACE(J + nblk - 1, 14);
+                // my columns: [cb, cb + ncol) (half-split rows: each thread takes a quarter of D)
+                const int cb = grp * (D / 2) + ((hs && (lane & 16)) ? D / 4 : 0);
+                const int ncol = (p.dbg & 1) ? 0 : (hs ? D / 4 : D / 2);
 #pragma unroll 1
-                for (int c0 = grp * (D / 2); c0 < (grp + 1) * (D / 2); c0 += 16) {
+                for (int cc = 0; cc < ncol; cc += 16) {
+                    const int c0 = cb + cc;
                     uint32_t a[16], bb[16];
-                    if (had0) tmem_ld16(rowbase + c0, a);
-                    if (had1) tmem_ld16(rowbase + D + c0, bb);
+                    if (hs) {
+                        if (had0) tmem_ld_hs16<D / 4>(rowbase + grp * (D / 2) + cc, a);
+                        if (had1) tmem_ld_hs16<D / 4>(rowbase + D + grp * (D / 2) + cc, bb);
+                    } else {
+                        if (had0) tmem_ld16(rowbase + c0, a);
+                        if (had1) tmem_ld16(rowbase + D + c0, bb);
+                    }
                     tmem_wait_ld();
 #pragma unroll
                     for (int c = 0; c < 16; ++c)
                         a[c] = __float_as_uint((had0 ? __uint_as_float(a[c]) * f0 : 0.0f) +
                                                (had1 ? __uint_as_float(bb[c]) * f1 : 0.0f));
-                    if (grp == 0 && wq == 0 && lane == 0 && c0 == 0) TRACE(J + nblk - 1, 15);
+                    if (grp == 0 && wq == 0 && lane == 0 && cc == 0) TRACE(J + nblk - 1, 15);
                     if (row_valid) {
                         if (direct) {
 #pragma unroll
@@ -514,7 +1056,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                                 u.w = pack_bf16(__uint_as_float(a[c + 6]), __uint_as_float(a[c + 7]));
                                 if (grp_full) {
                                     const int chunk = ((c0 + c) - grp * (D / 2)) >> 3;   // 16-byte chunk in the 128-byte row
-                                    *reinterpret_cast<uint4*>(stage + r * 128 + ((chunk ^ (r & 7)) << 4)) = u;
+                                    *reinterpret_cast<uint4*>(stage + rr * 128 + ((chunk ^ (rr & 7)) << 4)) = u;
                                 } else {
                                     *reinterpret_cast<uint4*>(orow + c0 + c) = u;
                                 }
@@ -526,12 +1068,12 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                         }
                     }
                 }
-                if (row_valid && grp == 0) {
+                if (row_valid && grp == 0 && hl == lane) {
                     const float lse2 = L > 0.0f ? M + __log2f(L) : -INFINITY;
                     if (direct) {
                         if (p.lse) p.lse[(int64_t)(off + node) * p.Hq + h] = lse2 * 0.6931471805599453f;
                     } else {
-                        p.part_lse[(int64_t)wi.part * kM + r] = lse2;
+                        p.part_lse[(int64_t)wi.part * kM + rr] = lse2;
                     }
                 }
             }
@@ -572,23 +1114,25 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                     const SplitUnit u = p.units[wi.unit];
                     float M = -INFINITY;
                     for (int q = 0; q < u.n_parts; ++q)
-                        M = fmaxf(M, __ldcg(p.part_lse + (int64_t)(u.part_base + q) * kM + r));
+                        M = fmaxf(M, __ldcg(p.part_lse + (int64_t)(u.part_base + q) * kM + rr));
                     float wsum = 0.0f;
                     for (int q = 0; q < u.n_parts; ++q) {
-                        const float lq = __ldcg(p.part_lse + (int64_t)(u.part_base + q) * kM + r);
+                        const float lq = __ldcg(p.part_lse + (int64_t)(u.part_base + q) * kM + rr);
                         wsum += (lq == -INFINITY) ? 0.0f : ex2(lq - M);
                     }
                     const float inv = wsum > 0.0f ? 1.0f / wsum : 0.0f;
                     const int h = wi.kvh * p.g + (grow % p.g);
                     __nv_bfloat16* orow = p.out + ((int64_t)(off + node) * p.Hq + h) * D;
 #pragma unroll 1
-                    for (int c0 = grp * (D / 2); c0 < (grp + 1) * (D / 2); c0 += 8) {
+                    const int mcb = grp * (D / 2) + ((hs && (lane & 16)) ? D / 4 : 0);
+                    const int mce = mcb + (hs ? D / 4 : D / 2);
+                    for (int c0 = mcb; c0 < mce; c0 += 8) {
                         float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
                         for (int q = 0; q < u.n_parts; ++q) {
-                            const float lq = __ldcg(p.part_lse + (int64_t)(u.part_base + q) * kM + r);
+                            const float lq = __ldcg(p.part_lse + (int64_t)(u.part_base + q) * kM + rr);
                             const float wq = (lq == -INFINITY) ? 0.0f : ex2(lq - M) * inv;
                             const float4* src = reinterpret_cast<const float4*>(
-                                p.part_o + ((int64_t)(u.part_base + q) * kM + r) * D + c0);
+                                p.part_o + ((int64_t)(u.part_base + q) * kM + rr) * D + c0);
                             const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
                             acc[0] += wq * x0.x; acc[1] += wq * x0.y; acc[2] += wq * x0.z; acc[3] += wq * x0.w;
                             acc[4] += wq * x1.x; acc[5] += wq * x1.y; acc[6] += wq * x1.z; acc[7] += wq * x1.w;
@@ -600,11 +1144,12 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                         o.w = pack_bf16(acc[6], acc[7]);
                         *reinterpret_cast<uint4*>(orow + c0) = o;
                     }
-                    if (grp == 0 && p.lse)
+                    if (grp == 0 && p.lse && hl == lane)
                         p.lse[(int64_t)(off + node) * p.Hq + h] = (M + __log2f(wsum)) * 0.6931471805599453f;
                 }
             }
             J += nblk;
+            wi = wn;
         }
         if (wq == 0 && lane == 0) bulk_wait_all();   // output TMA stores complete before exit
     }
@@ -612,7 +1157,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     __syncthreads();
     tc_fence_after();
     if (warp == 2) tmem_dealloc<C::kTmemCols>(tmem);
-    if (p.trace && threadIdx.x == 0) p.trace[(size_t)blockIdx.x * kTraceJ * 16 + 9] = globaltimer_ns();
+    if (p.trace && threadIdx.x == 0) p.trace[((size_t)blockIdx.x * kTraceJ + kTraceJ - 1) * 16 + 15] = globaltimer_ns();
 }
 
 }  // namespace attn

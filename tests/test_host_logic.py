@@ -42,8 +42,8 @@ def _check_plan(core, P, T, Hq, Hkv, d=128, n=148):
     assert cta[0] == 0 and cta[-1] == len(items) and np.all(np.diff(cta) >= 0)
     g = Hq // Hkv
     cover = {}
-    for b_, kvh, mt, b0, b1, part, R, unit, stream, _ in items:
-        assert stream in (0, 1)
+    for b_, kvh, mt, b0, b1, part, R, unit, Pi, node0, Ti, _ in items:
+        assert (Pi, node0, Ti) == (P[b_], to[b_], T[b_])       # lengths copied into the item
         assert (part < 0) == (unit < 0)
         cover.setdefault((b_, kvh, mt), []).append((b0, b1, part))
     nsplit = 0

@@ -50,7 +50,7 @@ def main():
     per_cta_rate = []
     for c in range(n):
         nb = int(sum(items[i, 4] - items[i, 3] for i in range(cta[c], cta[c + 1])))
-        nb = min(nb, 256)
+        nb = min(nb, 255)
         if nb < 2:
             continue
         tc = t[c, :nb]
@@ -71,19 +71,35 @@ def main():
         d = allb[:, z] - allb[:, a]
         lat[name] = float(np.median(d))
     res["median_cycles"] = lat
+    # epilogue sub-phases (rows with an epilogue: event 6 set)
+    epi = {}
+    seq = [(6, 10, "pv_wait"), (10, 11, "ml_barrier"), (11, 14, "stage_wait"), (14, 15, "first_o_chunk"),
+           (15, 12, "o_loop_rest"), (12, 13, "store_issue"), (13, 7, "tail"), (6, 7, "total")]
+    er = allb[allb[:, 6] > 0]
+    for a, z, nm in seq:
+        ok = (er[:, a] > 0) & (er[:, z] > 0)
+        if ok.any():
+            epi[nm] = float(np.median(er[ok, z] - er[ok, a]))
+    res["epilogue_cycles_median"] = epi
+    res["epilogues_per_cta"] = float(len(er) / max(1, len(rows)))
+    # longest gaps between consecutive K TMA issues per CTA (load starvation)
+    gaps = np.concatenate([np.sort(np.diff(r[:, 0]))[-4:] for r in rows])
+    res["k_issue_gap_top4_median"] = float(np.median(gaps))
+    res["k_issue_gap_sum_over_3000_per_cta"] = float(np.median([np.sum(np.clip(np.diff(r[:, 0]) - 3000, 0, None))
+                                                                 for r in rows]))
     c0 = t[0, :40]
     base = c0[0, 0]
     res["cta0_timeline"] = [[int(x - base) if x > 0 else -1 for x in row] for row in c0]
     res["cta0_items"] = items[cta[0]:cta[1]].tolist()
-    g0 = t[:, 0, 8]
-    g1 = t[:, 0, 9]
+    g0 = t[:, 255, 14].copy()
+    g1 = t[:, 255, 15].copy()
     ok = (g0 > 0) & (g1 > 0)
     res["globaltimer_us"] = {"kernel_span": float((g1[ok].max() - g0[ok].min()) / 1e3),
                              "start_skew": float((g0[ok].max() - g0[ok].min()) / 1e3),
                              "cta_median": float(np.median(g1[ok] - g0[ok]) / 1e3),
                              "cta_max": float(np.max(g1[ok] - g0[ok]) / 1e3)}
-    t[:, 0, 8] = 0
-    t[:, 0, 9] = 0
+    t[:, 255, 14] = 0
+    t[:, 255, 15] = 0
     spans = []
     for c in range(n):
         v = t[c][t[c] > 0]
@@ -93,6 +109,31 @@ def main():
     res["cta_span_us"] = {"min": float(spans.min()), "median": float(np.median(spans)), "max": float(spans.max()),
                           "p90": float(np.percentile(spans, 90))}
     res["cycles_per_block_per_cta_median"] = float(np.median(per_cta_rate))
+    # per-CTA span (globaltimer, us) vs its blocks and items: calibrates the plan's item overhead
+    nblk_c = np.array([sum(items[i, 4] - items[i, 3] for i in range(cta[c], cta[c + 1])) for c in range(n)], float)
+    nit_c = np.array([cta[c + 1] - cta[c] for c in range(n)], float)
+    span_c = (g1 - g0) / 1e3
+    okc = (g0 > 0) & (g1 > 0)
+    A = np.stack([nblk_c[okc], nit_c[okc], np.ones(okc.sum())], 1)
+    coef = np.linalg.lstsq(A, span_c[okc], rcond=None)[0]
+    res["span_fit_us"] = {"per_block": float(coef[0]), "per_item": float(coef[1]), "const": float(coef[2]),
+                          "item_in_blocks": float(coef[1] / coef[0]) if coef[0] else None,
+                          "blocks_min_max": [float(nblk_c.min()), float(nblk_c.max())],
+                          "items_min_max": [float(nit_c.min()), float(nit_c.max())]}
+    # Little's law per CTA: mean loads in flight = sum(latency) / span (K: ev 0 -> 8, V: ev 1 -> 9)
+    infl_k, infl_v, lat_k, lat_v = [], [], [], []
+    for r in rows:
+        ok = (r[:, 0] > 0) & (r[:, 8] > 0) & (r[:, 1] > 0) & (r[:, 9] > 0)
+        r = r[ok]
+        if len(r) < 4:
+            continue
+        span = max(r[:, 8].max(), r[:, 9].max()) - min(r[:, 0].min(), r[:, 1].min())
+        infl_k.append(np.sum(r[:, 8] - r[:, 0]) / span)
+        infl_v.append(np.sum(r[:, 9] - r[:, 1]) / span)
+        lat_k.append(np.mean(r[:, 8] - r[:, 0]))
+        lat_v.append(np.mean(r[:, 9] - r[:, 1]))
+    res["inflight_mean"] = {"K": float(np.mean(infl_k)), "V": float(np.mean(infl_v)),
+                            "lat_K_mean": float(np.mean(lat_k)), "lat_V_mean": float(np.mean(lat_v))}
     res["blocks_per_cta"] = float(np.mean([len(r) for r in rows]))
     print(json.dumps(res, indent=1))
 

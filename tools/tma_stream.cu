@@ -94,7 +94,7 @@ void run(void* buf, size_t rows, int ctas, int tiles_per_cta, CUtensorMapL2promo
     cudaFree(sink);
 }
 
-int main() {
+int main(int argc, char** argv) {
     size_t bytes = 8ull << 30;
     void* buf;
     cudaMalloc(&buf, bytes);
@@ -102,16 +102,10 @@ int main() {
     size_t rows = bytes / 256;
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const int tiles = 400;
+    const int tiles = argc > 1 ? atoi(argv[1]) : 400;
     run<4, 64>(buf, rows, sms, tiles, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, "64-row tiles");
     run<8, 64>(buf, rows, sms, tiles, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, "64-row tiles");
-    run<10, 64>(buf, rows, sms, tiles, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, "64-row tiles");
     run<12, 64>(buf, rows, sms, tiles, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, "64-row tiles");
-    run<13, 64>(buf, rows, sms, tiles, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, "64-row tiles");
-    run<12, 64>(buf, rows, sms, tiles, CU_TENSOR_MAP_L2_PROMOTION_NONE, "64-row tiles no-promo");
-    run<12, 64>(buf, rows, 2 * sms, tiles / 2, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, "64-row tiles 2 CTA/SM?");
     run<6, 128>(buf, rows, sms, tiles / 2, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, "128-row tiles");
-    run<3, 256>(buf, rows, sms, tiles / 4, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, "256-row tiles");
-    run<6, 256>(buf, rows, sms, tiles / 4, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, "256-row tiles");
     return 0;
 }
