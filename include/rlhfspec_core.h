@@ -147,7 +147,10 @@ rs_status rs_tree_verify_attention_layers(
  *   path         device int32 [B, 64] out: path[b][0..a_b] local node ids (path[b][0]=0), -1 padded
  *   bonus_token  device int32 [B]  out: the bonus token (-1 on a flagged sample)
  *   status_flags device int32 [B]  out: RS_FLAG_* bits
- *   ws: unused (pass NULL, 0); reserved. */
+ *   ws, ws_bytes: device workspace >= rs_tree_accept_workspace_bytes(mode, B, V) bytes, 16-byte
+ *               aligned (MSS keeps each sample's residual weights there; 0 bytes otherwise:
+ *               NULL allowed); too small -> RS_ERR_WORKSPACE. */
+size_t rs_tree_accept_workspace_bytes(int32_t mode, int32_t B, int32_t V);
 rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t logits_dtype,
                          const float* draft_probs, const int32_t* parent, const int32_t* token,
                          const int32_t* tree_off, const int64_t* gid, int32_t B, int32_t V,

@@ -51,6 +51,7 @@ _sig("rs_tree_verify_attention_layers", _i32, _P, _i32, _P, _P, _P, _i64, _P, _i
      _i32, _i32, _i32, _f32, _P, _P, _P, _sz, _P)
 _sig("rs_tree_accept", _i32, _i32, _P, _i32, _P, _P, _P, _P, _P, _i32, _i32, _f32, _u64, _u64, _P, _P,
      _P, _P, _P, _sz, _P)
+_sig("rs_tree_accept_workspace_bytes", _sz, _i32, _i32, _i32)
 _sig("rs_philox4x32_10", _i32, _P, _i64, _P, _P, _P)
 _sig("rs_exp_spec", _i32, _P, _i64, _P, _P)
 _sig("rs_kv_compact", _i32, _P, _P, _i32, _i64, _i32, _i32, _i32, _P, _i32, _P, _P, _P, _i32, _P, _P, _P)
@@ -190,10 +191,18 @@ class AttentionLayersCall:
 
 
 # ------------------------------------------------------------------ a3
+def accept_workspace_bytes(mode, B, V) -> int:
+    return int(_lib.rs_tree_accept_workspace_bytes(int(mode), int(B), int(V)))
+
+
 def tree_accept(mode, logits, parent, token, tree_off, gid, draft_probs=None, temperature=1.0, seed=0, step=0,
-                out=None, stream=None):
+                out=None, stream=None, ws=None):
+    """ws: device workspace of >= accept_workspace_bytes(mode, B, V) bytes (allocated here if None)."""
     NT, V = logits.shape
     B = tree_off.numel() - 1
+    need = accept_workspace_bytes(mode, B, V)
+    if ws is None and need:
+        ws = torch.empty(need, dtype=torch.uint8, device=logits.device)
     dt = DTYPE_BF16 if logits.dtype == torch.bfloat16 else DTYPE_F32
     dev = logits.device
     if out is None:
@@ -202,7 +211,8 @@ def tree_accept(mode, logits, parent, token, tree_off, gid, draft_probs=None, te
     acc, path, bonus, flags = out
     _check(_lib.rs_tree_accept(int(mode), _ptr(logits), dt, _ptr(draft_probs), _ptr(parent), _ptr(token),
                                _ptr(tree_off), _ptr(gid), B, V, float(temperature), int(seed), int(step), _ptr(acc),
-                               _ptr(path), _ptr(bonus), _ptr(flags), None, 0, _stream(stream)), "rs_tree_accept")
+                               _ptr(path), _ptr(bonus), _ptr(flags), _ptr(ws) if need else None,
+                               ws.numel() if need else 0, _stream(stream)), "rs_tree_accept")
     return acc, path, bonus, flags
 
 

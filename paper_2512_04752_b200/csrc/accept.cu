@@ -10,8 +10,8 @@
 //   GREEDY: argmax (ties -> lowest id); accept the lowest-index child whose token equals it;
 //           bonus = argmax at the last node.
 //   DELTA / MSS: integer weights w_v (exp_spec), Philox uniforms, 128-bit exact tests; the
-//           residual after a rejection is kept implicitly (DELTA: excluded-token list; MSS:
-//           the chain of (Z, shift) scalars, re-applied per element when the row is re-read);
+//           residual after a rejection is kept implicitly for DELTA (excluded-token list) and
+//           materialised for MSS (u64 weights per token in the workspace, updated in place);
 //           bonus by inverse CDF: cluster prefix over slice totals, then tile sums + a block
 //           scan inside the owning CTA.
 #include "common.cuh"
@@ -24,11 +24,9 @@ using rs::u128;
 using namespace rs::ptx;
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kUnroll = 4;
 constexpr int kTileVecs = kThreads;        // 8-element vectors per inverse-CDF tile
 constexpr int kMaxTiles = 256;             // tiles per CTA slice
 constexpr int kMaxCluster = 8;
-constexpr int kMaxChain = RS_MAX_TREE;
 
 struct RowView {
     const void* base;
@@ -118,9 +116,6 @@ struct Smem {
     int token[RS_MAX_TREE];
     int excluded[RS_MAX_TREE];
     int n_excluded;
-    unsigned long long chainZ[kMaxChain];
-    int chainS[kMaxChain];
-    int n_chain;
     int flag;
     int bcast_i;
     unsigned long long bcast_u;
@@ -206,20 +201,10 @@ __device__ __forceinline__ u128 allreduce_max128(u128 v, Smem& sm, int& phase) {
     return r;
 }
 
-// Current residual weight of a token from its base weight: DELTA zeroes excluded tokens;
-// MSS re-applies the recorded residual steps w <- max(w*Zq - qw*Z_j, 0) >> s_j.
-__device__ __forceinline__ uint64_t residual_weight(int mode, uint64_t w, uint64_t qw, int tok, uint64_t Zq,
-                                                    const Smem& sm) {
-    if (mode == RS_ACCEPT_SAMPLE_DELTA) {
-        for (int e = 0; e < sm.n_excluded; ++e)
-            if (sm.excluded[e] == tok) return 0;
-        return w;
-    }
-    for (int j = 0; j < sm.n_chain; ++j) {
-        u128 lhs = (u128)w * Zq, rhs = (u128)qw * sm.chainZ[j];
-        u128 r = lhs > rhs ? lhs - rhs : 0;
-        w = (uint64_t)(r >> sm.chainS[j]);
-    }
+// DELTA residual: rejected tokens are excluded (weight 0); other weights are unchanged.
+__device__ __forceinline__ uint64_t delta_weight(uint64_t w, int tok, const Smem& sm) {
+    for (int e = 0; e < sm.n_excluded; ++e)
+        if (sm.excluded[e] == tok) return 0;
     return w;
 }
 
@@ -232,7 +217,7 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype, cons
                    const int32_t* __restrict__ tree_off, const int64_t* __restrict__ gid, int V, float inv_tau,
                    uint64_t seed, uint64_t step, int32_t* __restrict__ acc_out, int32_t* __restrict__ path_out,
                    int32_t* __restrict__ bonus_out, int32_t* __restrict__ flags_out, bool logits_vec_ok,
-                   bool draft_vec_ok) {
+                   bool draft_vec_ok, uint64_t* __restrict__ wbuf) {
     (void)mode_rt;
     constexpr int mode = MODE;
     __shared__ Smem sm;
@@ -303,14 +288,21 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype, cons
             // pass 2: Z = sum w, Zq = sum qw
             constexpr bool mss = mode == RS_ACCEPT_SAMPLE_MSS;
             unsigned long long zs = 0, zq = 0;
-            for_slice<mss ? 2 : 4>(lv, qv, mss, vbeg, vend, [&](int, float x, float q) {
-                zs += rs::target_weight(x, m, inv_tau);
-                if (mss) zq += rs::draft_weight(q);
+            // MSS: the current (residual) weights live in wbuf[b][V] (workspace), so residual
+            // passes read one u64 per token instead of re-deriving it from the logits
+            uint64_t* wrow = mss ? wbuf + (int64_t)b * V : nullptr;
+            for_slice<mss ? 2 : 4>(lv, qv, mss, vbeg, vend, [&](int v, float x, float q) {
+                const uint64_t w = rs::target_weight(x, m, inv_tau);
+                zs += w;
+                if (mss) {
+                    zq += rs::draft_weight(q);
+                    wrow[v] = w;
+                }
             });
             allreduce2(zs, OP_SUM, zq, OP_SUM, sm, phase);
             uint64_t Z = zs;
             const uint64_t Zq = mss ? zq : 0ull;
-            if (tid == 0) { sm.n_excluded = 0; sm.n_chain = 0; }
+            if (tid == 0) sm.n_excluded = 0;
             __syncthreads();
             int rank = 0;
             for (int x = c + 1; x < T && next < 0; ++x) {
@@ -322,7 +314,8 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype, cons
                                         ? rs::bf16_bits_to_f32(reinterpret_cast<const uint16_t*>(logits)[ro])
                                         : reinterpret_cast<const float*>(logits)[ro];
                     const uint64_t qw = mss ? rs::draft_weight(draft[ro]) : 0ull;
-                    const uint64_t wt = residual_weight(mode, rs::target_weight(l, m, inv_tau), qw, tk, Zq, sm);
+                    const uint64_t wt = mss ? __ldcg(wrow + tk)
+                                            : delta_weight(rs::target_weight(l, m, inv_tau), tk, sm);
                     const uint32_t U = rs::uniform_word(seed, step, g, (uint32_t)rank, (uint32_t)c);
                     bool acc;
                     if (mode == RS_ACCEPT_SAMPLE_DELTA)
@@ -345,34 +338,32 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype, cons
                     if (tid == 0) sm.excluded[sm.n_excluded++] = tk;
                     __syncthreads();
                 } else {
-                    // residual r_v = max(w_v*Zq - qw_v*Z, 0): cluster max, then shifted sum
+                    // residual r_v = max(w_v*Zq - qw_v*Z, 0): cluster max, then shifted sum,
+                    // written back in place. zn = 0 <=> max r = 0 (the shift keeps the max
+                    // >= 2^31), so an all-zero residual is known after the first pass and the
+                    // pre-rejection weights are simply kept.
                     u128 rmax = 0;
-                    for_slice<2>(lv, qv, true, vbeg, vend, [&](int, float xv, float q) {
-                        const uint64_t qw = rs::draft_weight(q);
-                        const uint64_t w = residual_weight(mode, rs::target_weight(xv, m, inv_tau), qw, 0, Zq, sm);
-                        const u128 lhs = (u128)w * Zq, rhs = (u128)qw * Z;
+                    for (int i = vbeg * 8 + tid; i < min(V, vend * 8); i += kThreads) {
+                        const uint64_t qw = rs::draft_weight(__ldg(draft + (int64_t)(off + c) * V + i));
+                        const u128 lhs = (u128)__ldcg(wrow + i) * Zq, rhs = (u128)qw * Z;
                         const u128 r = lhs > rhs ? lhs - rhs : 0;
                         if (r > rmax) rmax = r;
-                    });
+                    }
                     const u128 mxr = allreduce_max128(rmax, sm, phase);
-                    int s = rs::bitlen128(mxr) - 32;
-                    if (s < 0) s = 0;
-                    unsigned long long zn = 0, dummy = 0;
-                    for_slice<2>(lv, qv, true, vbeg, vend, [&](int, float xv, float q) {
-                        const uint64_t qw = rs::draft_weight(q);
-                        const uint64_t w = residual_weight(mode, rs::target_weight(xv, m, inv_tau), qw, 0, Zq, sm);
-                        const u128 lhs = (u128)w * Zq, rhs = (u128)qw * Z;
-                        const u128 r = lhs > rhs ? lhs - rhs : 0;
-                        zn += (unsigned long long)(r >> s);
-                    });
-                    allreduce2(zn, OP_SUM, dummy, OP_OR, sm, phase);
-                    if (zn != 0) {      // an all-zero residual keeps the pre-rejection weights
-                        if (tid == 0) {
-                            sm.chainZ[sm.n_chain] = Z;
-                            sm.chainS[sm.n_chain] = s;
-                            sm.n_chain++;
+                    if (mxr != 0) {
+                        int s = rs::bitlen128(mxr) - 32;
+                        if (s < 0) s = 0;
+                        unsigned long long zn = 0, dummy = 0;
+                        for (int i = vbeg * 8 + tid; i < min(V, vend * 8); i += kThreads) {
+                            const uint64_t qw = rs::draft_weight(__ldg(draft + (int64_t)(off + c) * V + i));
+                            const u128 lhs = (u128)__ldcg(wrow + i) * Zq, rhs = (u128)qw * Z;
+                            const u128 r = lhs > rhs ? lhs - rhs : 0;
+                            const uint64_t wn = (uint64_t)(r >> s);
+                            wrow[i] = wn;
+                            zn += wn;
                         }
-                        Z = zn;
+                        allreduce2(zn, OP_SUM, dummy, OP_OR, sm, phase);   // (cluster barrier: the
+                        Z = zn;                                             //  new weights are visible)
                     }
                     __syncthreads();
                 }
@@ -390,16 +381,19 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype, cons
                     const int i = vbeg + tile * kTileVecs + tid;
                     unsigned long long s8 = 0;
                     if (i < vend) {
-                        const Raw8 xr = load_raw(lv, i);
-                        Raw8 qr;
-                        if (mss) qr = load_raw(qv, i);
+                        if (mss) {
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const int v = i * 8 + j;
-                            if (v < V) {
-                                const uint64_t qw = mss ? rs::draft_weight(raw_elem(qr, RS_DTYPE_F32, j)) : 0ull;
-                                s8 += residual_weight(mode, rs::target_weight(raw_elem(xr, dtype, j), m, inv_tau), qw,
-                                                      v, Zq, sm);
+                            for (int j = 0; j < 8; ++j) {
+                                const int v = i * 8 + j;
+                                if (v < V) s8 += __ldcg(wrow + v);
+                            }
+                        } else {
+                            const Raw8 xr = load_raw(lv, i);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                const int v = i * 8 + j;
+                                if (v < V)
+                                    s8 += delta_weight(rs::target_weight(raw_elem(xr, dtype, j), m, inv_tau), v, sm);
                             }
                         }
                     }
@@ -439,17 +433,15 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype, cons
                     uint64_t w8[8];
                     unsigned long long s8 = 0;
                     if (i < vend) {
-                        const Raw8 xr = load_raw(lv, i);
-                        Raw8 qr;
-                        if (mss) qr = load_raw(qv, i);
+                        Raw8 xr;
+                        if (!mss) xr = load_raw(lv, i);
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
                             w8[j] = 0;
                             const int v = i * 8 + j;
                             if (v < V) {
-                                const uint64_t qw = mss ? rs::draft_weight(raw_elem(qr, RS_DTYPE_F32, j)) : 0ull;
-                                w8[j] = residual_weight(mode, rs::target_weight(raw_elem(xr, dtype, j), m, inv_tau),
-                                                        qw, v, Zq, sm);
+                                w8[j] = mss ? __ldcg(wrow + v)
+                                            : delta_weight(rs::target_weight(raw_elem(xr, dtype, j), m, inv_tau), v, sm);
                                 s8 += w8[j];
                             }
                         }
@@ -517,6 +509,10 @@ __global__ void exp_spec_kernel(const float* x, int64_t n, float* y) {
 
 }  // namespace
 
+extern "C" size_t rs_tree_accept_workspace_bytes(int32_t mode, int32_t B, int32_t V) {
+    return mode == RS_ACCEPT_SAMPLE_MSS && B > 0 && V > 0 ? (size_t)B * (size_t)V * sizeof(uint64_t) : 0;
+}
+
 extern "C" rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t logits_dtype,
                                     const float* draft_probs, const int32_t* parent,
                                     const int32_t* token, const int32_t* tree_off,
@@ -524,8 +520,6 @@ extern "C" rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t lo
                                     uint64_t seed, uint64_t step, int32_t* accepted_len,
                                     int32_t* path, int32_t* bonus_token, int32_t* status_flags,
                                     void* ws, size_t ws_bytes, void* stream) {
-    (void)ws;
-    (void)ws_bytes;
     RS_REQUIRE(mode == RS_ACCEPT_GREEDY || mode == RS_ACCEPT_SAMPLE_DELTA ||
                    mode == RS_ACCEPT_SAMPLE_MSS,
                RS_ERR_INVALID_ARG, "rs_tree_accept: bad mode %d", mode);
@@ -540,6 +534,9 @@ extern "C" rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t lo
     RS_REQUIRE(logits && parent && token && tree_off && gid && accepted_len && path && bonus_token &&
                    status_flags,
                RS_ERR_INVALID_ARG, "rs_tree_accept: null pointer");
+    const size_t need = rs_tree_accept_workspace_bytes(mode, B, V);
+    RS_REQUIRE(ws_bytes >= need && (need == 0 || (ws && (reinterpret_cast<uintptr_t>(ws) & 15) == 0)), RS_ERR_WORKSPACE,
+               "rs_tree_accept: workspace %zu < %zu bytes (16-byte aligned)", ws_bytes, need);
     // cluster size: enough CTAs per sample that one row streams in ~a microsecond, without
     // exceeding ~2 waves of the GPU when B is large
     const int nvec = (V + 7) / 8;
@@ -567,7 +564,7 @@ extern "C" rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t lo
                                                  : tree_accept_kernel<RS_ACCEPT_SAMPLE_MSS>;
     RS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, (int)mode, logits, (int)logits_dtype, draft_probs, parent, token,
                                      tree_off, gid, (int)V, inv_tau, seed, step, accepted_len, path, bonus_token,
-                                     status_flags, lvec, dvec));
+                                     status_flags, lvec, dvec, static_cast<uint64_t*>(need ? ws : nullptr)));
     return RS_OK;
 }
 

@@ -53,6 +53,8 @@ class VerifyStep:
         self.bonus = torch.empty(self.B, dtype=torch.int32, device=dev)
         self.flags = torch.empty(self.B, dtype=torch.int32, device=dev)
         self.new_len = torch.empty(self.B, dtype=torch.int32, device=dev)
+        nws = core.accept_workspace_bytes(mode, self.B, self.logits.shape[1])
+        self.accept_ws = torch.empty(max(nws, 16), dtype=torch.uint8, device=dev)   # MSS residual weights
         self.attn_call = core.AttentionLayersCall(
             self.plan, [self.q[l] for l in range(self.L)], self.k_layers, self.v_layers, self.block_table,
             self.prefix_len, self.tree_off, self.mask, self.sm_scale, self.ws,
@@ -68,7 +70,7 @@ class VerifyStep:
     def accept_compact_step(self, seed, step, stream=None):
         core.tree_accept(self.mode, self.logits, self.parent, self.token, self.tree_off, self.gid,
                          draft_probs=self.draft, temperature=self.temperature, seed=seed, step=step,
-                         out=(self.acc, self.path, self.bonus, self.flags), stream=stream)
+                         out=(self.acc, self.path, self.bonus, self.flags), stream=stream, ws=self.accept_ws)
         core.kv_compact(self.k_layers, self.v_layers, self.block_table, self.prefix_len, self.acc, self.path,
                         self.ps, new_len=self.new_len, stream=stream)
 
