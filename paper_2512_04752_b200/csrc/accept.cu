@@ -27,6 +27,10 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kTileVecs = kThreads;        // 8-element vectors per inverse-CDF tile
 constexpr int kMaxTiles = 256;             // tiles per CTA slice
 constexpr int kMaxCluster = 8;
+#ifndef RS_ACC_INFLIGHT
+#define RS_ACC_INFLIGHT 4
+#endif
+constexpr int kGreedyInflight = RS_ACC_INFLIGHT;   // 16-byte loads in flight per thread (greedy, bf16)
 
 struct RowView {
     const void* base;
@@ -156,12 +160,22 @@ __device__ __forceinline__ void allreduce2(unsigned long long& v0, int op0, unsi
     if (cs > 1) {
         if (threadIdx.x == 0) { sm.xch[phase][0] = a; sm.xch[phase][1] = b; }
         cluster_sync_all();
-        const uint32_t me = cluster_rank();
-        for (uint32_t c = 0; c < cs; ++c) {
-            if (c == me) continue;
-            a = op_apply(op0, a, ld_dsmem_u64(&sm.xch[phase][0], c));
-            b = op_apply(op1, b, ld_dsmem_u64(&sm.xch[phase][1], c));
+        // lane c of warp 0 fetches CTA c's pair (all remote loads in flight at once), then a
+        // shuffle reduction; the result is broadcast through shared memory
+        if (w == 0) {
+            const uint32_t c = (uint32_t)lane;
+            unsigned long long ra = 0, rb = 0;   // identity of MAX (unsigned), SUM and OR
+            if (c < cs) { ra = ld_dsmem_u64(&sm.xch[phase][0], c); rb = ld_dsmem_u64(&sm.xch[phase][1], c); }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                ra = op_apply(op0, ra, __shfl_xor_sync(0xffffffffu, ra, o));
+                rb = op_apply(op1, rb, __shfl_xor_sync(0xffffffffu, rb, o));
+            }
+            if (lane == 0) { sm.red[0][0] = ra; sm.red[0][1] = rb; }
         }
+        __syncthreads();
+        a = sm.red[0][0];
+        b = sm.red[0][1];
         phase ^= 1;
     }
     v0 = a;
@@ -263,11 +277,39 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype, cons
         if (mode == RS_ACCEPT_GREEDY) {
             // key = (orderable value << 32) | ~index: max key = max value, lowest index on ties
             unsigned long long best = 0, bad = 0;
-            for_slice(lv, qv, false, vbeg, vend, [&](int v, float x, float) {
+            auto upd = [&](int v, float x) {
                 bad |= isfinite(x) ? 0ull : 1ull;
                 const unsigned long long k = ((unsigned long long)fkey(x) << 32) | (uint32_t)(~(uint32_t)v);
                 best = best > k ? best : k;
-            });
+            };
+            if (dtype == RS_DTYPE_BF16 && logits_vec_ok) {
+                // bf16 rows: 8 x 16-byte loads in flight per thread (one memory round trip per
+                // node at the usual slice size)
+                const uint4* row = reinterpret_cast<const uint4*>(
+                    reinterpret_cast<const uint16_t*>(logits) + (int64_t)(off + c) * V);
+                for (int i0 = vbeg + tid; i0 < vend; i0 += kGreedyInflight * kThreads) {
+                    uint4 x[kGreedyInflight];
+#pragma unroll
+                    for (int u = 0; u < kGreedyInflight; ++u) {
+                        const int i = i0 + u * kThreads;
+                        if (i < vend) x[u] = __ldg(row + i);
+                    }
+#pragma unroll
+                    for (int u = 0; u < kGreedyInflight; ++u) {
+                        const int i = i0 + u * kThreads;
+                        if (i < vend) {
+                            const uint32_t w[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                const uint32_t h = (j & 1) ? (w[j >> 1] & 0xFFFF0000u) : (w[j >> 1] << 16);
+                                upd(i * 8 + j, __uint_as_float(h));
+                            }
+                        }
+                    }
+                }
+            } else {
+                for_slice<2>(lv, qv, false, vbeg, vend, [&](int v, float x, float) { upd(v, x); });
+            }
             allreduce2(best, OP_MAX, bad, OP_OR, sm, phase);
             if (bad) { flags |= RS_FLAG_NONFINITE; break; }
             const int am = (int)(~(uint32_t)best);

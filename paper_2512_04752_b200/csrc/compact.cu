@@ -4,27 +4,33 @@
 // node at depth k has index >= k), copy k never reads a slot written by an earlier copy; only a
 // LATER copy can overwrite a slot an earlier one reads. So the rows are processed in chunks of
 // ascending k, each chunk gathered into registers (all loads in flight) before it is scattered.
-// One CTA per (sample, group of layers): the flattened row index runs k-major over
-// (layer, K|V, head, 16-byte column), so one CTA moves every layer of its group at once with
-// coalesced 128-bit loads/stores. Identity moves (path[k] == k) are skipped.
+// One CTA per (sample, pair of layers); consecutive threads own consecutive 16-byte columns,
+// so every gather/scatter is a coalesced 128-bit access. Identity moves (path[k] == k) are skipped.
 #include "common.cuh"
 
 namespace {
 
 constexpr int kMaxLayers = 256;
-constexpr int kLayersPerCta = 8;
+constexpr int kLayersPerCta = 2;
 constexpr int kThreads = 256;
-constexpr int kPerThread = 16;   // 16-byte registers per thread per chunk
+constexpr int kLanesPerThread = 2;   // (layer, K|V, head, 16-byte column) lanes owned by a thread
+constexpr int kChunk = 4;            // accepted tokens gathered per round
 
 struct LayerPtrs {
     void* k[kMaxLayers];
     void* v[kMaxLayers];
 };
 
+// A "lane" = one 16-byte column of one (layer, K|V, kv head) row. Every copy of a lane is done
+// by the thread that owns it, in ascending-k chunks, each chunk gathered into registers before it
+// is scattered: that reproduces the sequential semantics without any block barrier (copies of
+// different lanes never touch the same bytes).
 __global__ void __launch_bounds__(kThreads)
 kv_compact_kernel(LayerPtrs layers, int nl, int Hkv, int d, int ps, const int32_t* __restrict__ block_table,
                   int max_pages, const int32_t* __restrict__ prefix_len, const int32_t* __restrict__ accepted_len,
                   const int32_t* __restrict__ path, int32_t* __restrict__ new_len, int32_t* __restrict__ moves) {
+    __shared__ int64_t s_src[RS_MAX_TREE], s_dst[RS_MAX_TREE];   // token row offsets (16-byte units, head 0)
+    __shared__ int s_n;
     const int b = blockIdx.x;
     const int l0 = blockIdx.y * kLayersPerCta;
     const int a = accepted_len[b];
@@ -41,41 +47,55 @@ kv_compact_kernel(LayerPtrs layers, int nl, int Hkv, int d, int ps, const int32_
     }
     const int nlay = min(kLayersPerCta, nl - l0);
     if (a <= 0 || nlay <= 0) return;
-    const int vec_per_row = d / 8;                        // 16-byte vectors per (token, head) row
-    const int per_layer_kv = Hkv * vec_per_row;           // one token, one layer, one of K/V
-    const int per_k = nlay * 2 * per_layer_kv;            // one accepted token, all layers of the group
+    const int vpr = d / 8;                                  // 16-byte vectors per (token, head) row
     const int32_t* bt = block_table + (int64_t)b * max_pages;
-    const int total = a * per_k;
-    for (int e0 = 0; e0 < total; e0 += kThreads * kPerThread) {
-        uint4 buf[kPerThread];
-        uint4* dst[kPerThread];
+    if (threadIdx.x == 0) {
+        int n = 0;
+        for (int k = 1; k <= a; ++k) {
+            const int src = P + pth[k], dst = P + k;
+            if (src == dst) continue;                       // identity moves are skipped
+            s_src[n] = ((int64_t)bt[src / ps] * Hkv * ps + (src % ps)) * vpr;
+            s_dst[n] = ((int64_t)bt[dst / ps] * Hkv * ps + (dst % ps)) * vpr;
+            ++n;
+        }
+        s_n = n;
+    }
+    __syncthreads();
+    const int n = s_n;
+    if (n == 0) return;
+    const int lanes_per_layer = 2 * Hkv * vpr;
+    const int lanes = nlay * lanes_per_layer;
+    for (int lb = 0; lb < lanes; lb += kThreads * kLanesPerThread) {
+        uint4* base[kLanesPerThread];
+        int64_t loff[kLanesPerThread];
 #pragma unroll
-        for (int r = 0; r < kPerThread; ++r) {
-            const int e = e0 + threadIdx.x + r * kThreads;
-            dst[r] = nullptr;
-            if (e < total) {
-                const int k = 1 + e / per_k;
-                int rem = e % per_k;
-                const int lay = rem / (2 * per_layer_kv);
-                rem %= 2 * per_layer_kv;
-                const int kv = rem / per_layer_kv;
-                rem %= per_layer_kv;
-                const int h = rem / vec_per_row, c = rem % vec_per_row;
-                const int src = P + pth[k], dsts = P + k;
-                if (src != dsts) {
-                    uint4* cache = reinterpret_cast<uint4*>(kv ? layers.v[l0 + lay] : layers.k[l0 + lay]);
-                    const int64_t so = (((int64_t)bt[src / ps] * Hkv + h) * ps + (src % ps)) * vec_per_row + c;
-                    const int64_t dof = (((int64_t)bt[dsts / ps] * Hkv + h) * ps + (dsts % ps)) * vec_per_row + c;
-                    buf[r] = cache[so];
-                    dst[r] = cache + dof;
-                }
+        for (int i = 0; i < kLanesPerThread; ++i) {
+            const int q = lb + threadIdx.x + i * kThreads;
+            base[i] = nullptr;
+            loff[i] = 0;
+            if (q < lanes) {
+                const int lay = q / lanes_per_layer;
+                int rem = q - lay * lanes_per_layer;
+                const int kv = rem / (Hkv * vpr);
+                rem -= kv * (Hkv * vpr);
+                const int h = rem / vpr, c = rem - h * vpr;
+                base[i] = reinterpret_cast<uint4*>(kv ? layers.v[l0 + lay] : layers.k[l0 + lay]);
+                loff[i] = (int64_t)h * ps * vpr + c;
             }
         }
-        __syncthreads();
+        for (int k0 = 0; k0 < n; k0 += kChunk) {
+            uint4 buf[kLanesPerThread][kChunk];
 #pragma unroll
-        for (int r = 0; r < kPerThread; ++r)
-            if (dst[r]) *dst[r] = buf[r];
-        __syncthreads();
+            for (int i = 0; i < kLanesPerThread; ++i)
+#pragma unroll
+                for (int j = 0; j < kChunk; ++j)
+                    if (base[i] && k0 + j < n) buf[i][j] = base[i][s_src[k0 + j] + loff[i]];
+#pragma unroll
+            for (int i = 0; i < kLanesPerThread; ++i)
+#pragma unroll
+                for (int j = 0; j < kChunk; ++j)
+                    if (base[i] && k0 + j < n) base[i][s_dst[k0 + j] + loff[i]] = buf[i][j];
+        }
     }
 }
 
