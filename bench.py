@@ -34,6 +34,8 @@ WORKLOAD_DESC = {
     "c5g8": "BASELINE configs[4] per-GPU shard at 8 GPUs: Llama-3-70B shapes (64 q / 8 kv, d=128, 80 layers), "
             "16 samples, prefix 8K, 64-node trees, greedy",
     "tiny": "BASELINE configs[0]: 1 sample, prefix 32, 8-node tree, 1 head, d=64, V=1000, greedy",
+    "c3": "BASELINE configs[2]: Llama-3-8B shapes, batch 256, prefixes 512-16K lognormal, trees 4-64, "
+          "rejection sampling (MSS)",
 }
 
 
@@ -145,8 +147,11 @@ def cpu_baseline(host, cfg, budget_s=12.0):
                                      host["block_table"][s:s + 1], host["prefix_len"][s:s + 1],
                                      np.array([0, sl.stop - sl.start]), masks[sl], cfg.Hkv, cfg.page_size,
                                      host["sm_scale"])
-        acc, path, bonus, flags = OAcc.tree_accept(OAcc.GREEDY, lg_bits[sl], host["parent"][sl], host["token"][sl],
-                                                   np.array([0, sl.stop - sl.start]), host["gid"][s:s + 1], cfg.V)
+        om = {"greedy": OAcc.GREEDY, "delta": OAcc.DELTA, "mss": OAcc.MSS}[cfg.mode]
+        acc, path, bonus, flags = OAcc.tree_accept(om, lg_bits[sl], host["parent"][sl], host["token"][sl],
+                                                   np.array([0, sl.stop - sl.start]), host["gid"][s:s + 1], cfg.V,
+                                                   draft_probs=host["draft"][sl] if om == OAcc.MSS else None,
+                                                   temperature=cfg.temperature, seed=11, step=0)
         OC.kv_compact([host["kc_np"][l] for l in range(L)] + [host["vc_np"][l] for l in range(L)],
                       host["block_table"][s:s + 1], host["prefix_len"][s:s + 1], acc, path, cfg.page_size)
         tokens += int(acc[0]) + 1
@@ -207,30 +212,36 @@ def run_ours(args, world, rank, local):
     info = step.plan.info()
 
     # ---------------- device-timed region: exactly K steps ----------------
-    ev_a0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ev_a1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    # events between the graph parts of every timed step: [start, after mask, after attention,
+    # after accept, after compact]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches_per_step = 1 + step.L + 1 + 1     # mask, L x attention (split-KV merge fused), accept, compact
     # The step's device work is captured once into CUDA graphs (mask | L x attention | accept +
     # compact); every timed step replays them (the launches are still our kernels, counted below).
-    g_mask, g_attn, g_tail = step.capture_parts(seed=11, step=0)
+    g_mask, g_attn, g_acc, g_cmp = step.capture_parts(seed=11, step=0)
     for w in range(args.warmup):
-        g_mask.replay(); g_attn.replay(); g_tail.replay()
+        g_mask.replay(); g_attn.replay(); g_acc.replay(); g_cmp.replay()
     sampler = ClockSampler(local)
     barrier()
     with sampler:
         start.record(stream)
         for k in range(args.steps):
             g_mask.replay()
-            ev_a0[k].record(stream)
+            ev[k][0].record(stream)
             g_attn.replay()
-            ev_a1[k].record(stream)
-            g_tail.replay()
+            ev[k][1].record(stream)
+            g_acc.replay()
+            ev[k][2].record(stream)
+            g_cmp.replay()
+            ev[k][3].record(stream)
         end.record(stream)
         torch.cuda.synchronize()
     barrier()
     elapsed_ms = start.elapsed_time(end)
-    attn_ms = sum(a.elapsed_time(c) for a, c in zip(ev_a0, ev_a1)) / args.steps
+    attn_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps
+    acc_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps
+    cmp_ms = sum(e[2].elapsed_time(e[3]) for e in ev) / args.steps
     if world > 1:
         t = torch.tensor([elapsed_ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -263,6 +274,24 @@ def run_ours(args, world, rank, local):
                  "launch_ms": round(attn_launch_ms, 5), "attention_share_of_step": round(attn_ms / ms_per_step, 4),
                  "tensor_frac": round(achieved_tf / tc_burst, 4)})
 
+    # ---------------- per-kernel breakdown (HBM-bound rows against the same peak) ----------------
+    path_np, acc_np = res["path"], res["accepted_len"]
+    moves = int(sum(int(np.sum(path_np[i, 1:acc_np[i] + 1] != np.arange(1, acc_np[i] + 1))) for i in range(b["B"])))
+    esz = 2 if b["logits"].dtype == torch.bfloat16 else 4
+    acc_bytes = tokens_per_step * cfg.V * (esz + (4 if mode == core.SAMPLE_MSS else 0))   # visited rows
+    cmp_bytes = 2 * moves * step.L * 4 * cfg.Hkv * cfg.d
+    kernels = {
+        "attention": {"ms_per_step": round(attn_ms, 4), "launches": step.L, "bytes": by * step.L,
+                      "GBps": round(by * step.L / (attn_ms * 1e-3) / 1e9, 1)},
+        "accept": {"ms_per_step": round(acc_ms, 4), "launches": 1, "bytes": int(acc_bytes),
+                   "GBps": round(acc_bytes / (acc_ms * 1e-3) / 1e9, 1), "frac_hbm": round(acc_bytes / (acc_ms * 1e-3) / 1e9 / hbm, 4),
+                   "note": "latency-bound sequential walk: bytes = visited rows x V x dtype"},
+        "compact": {"ms_per_step": round(cmp_ms, 4), "launches": 1, "bytes": int(cmp_bytes), "moves": moves,
+                    "GBps": round(cmp_bytes / (cmp_ms * 1e-3) / 1e9, 1), "frac_hbm": round(cmp_bytes / (cmp_ms * 1e-3) / 1e9 / hbm, 4)},
+        "mask": {"ms_per_step": round(ms_per_step - attn_ms - acc_ms - cmp_ms, 4), "launches": 1,
+                 "note": "remainder of the step (mask kernel + graph launch gaps)"},
+    }
+
     # ---------------- end-to-end through the public API with host buffers ----------------
     e2e = run_e2e(step, b, args.e2e_steps, tokens_per_step, world, dev, barrier, mode, cfg.temperature)
 
@@ -283,6 +312,7 @@ def run_ours(args, world, rank, local):
         "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
         "roofline": roof,
+        "kernels": kernels,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = run_cpu_baseline(cfg, b)
@@ -375,6 +405,7 @@ def run_cpu_baseline(cfg, b):
     host["B"] = nsamp
     host["q"] = b["q"][:, :ns].cpu()
     host["logits"] = b["logits"][:ns].cpu()
+    host["draft"] = b["draft_probs"][:ns].float().cpu().numpy() if b.get("draft_probs") is not None else None
     # only the pages of the sampled samples are copied (the cache itself stays on the GPU)
     pages = np.unique(host["block_table"])
     remap = {int(p): i for i, p in enumerate(pages)}
@@ -417,8 +448,11 @@ def run_reference(args, world, rank):
                                      b["prefix_len"][s:s + 1], np.array([0, sl.stop - sl.start]), masks[sl], cfg.Hkv,
                                      cfg.page_size, b["sm_scale"])
         t_attn = (time.perf_counter() - ta) * L / layers_run        # layers not run: extrapolated
-        acc, path, _, _ = OAcc.tree_accept(OAcc.GREEDY, lg_bits[sl], b["parent"][sl], b["token"][sl],
-                                           np.array([0, sl.stop - sl.start]), b["gid"][s:s + 1], cfg.V)
+        om = {"greedy": OAcc.GREEDY, "delta": OAcc.DELTA, "mss": OAcc.MSS}[cfg.mode]
+        dp = b["draft_probs"][sl].float().numpy() if om == OAcc.MSS else None
+        acc, path, _, _ = OAcc.tree_accept(om, lg_bits[sl], b["parent"][sl], b["token"][sl],
+                                           np.array([0, sl.stop - sl.start]), b["gid"][s:s + 1], cfg.V,
+                                           draft_probs=dp, temperature=cfg.temperature, seed=11, step=s)
         OC.kv_compact(kc + vc, b["block_table"][s:s + 1], b["prefix_len"][s:s + 1], acc, path, cfg.page_size)
         dt = (time.perf_counter() - t0) - (t_attn * layers_run / L) + t_attn
         if s == 0 and dt * (args.warmup + args.steps) > budget_s:

@@ -100,10 +100,10 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
     pl->rmodes = 0;
     pl->B = B; pl->Hq = Hq; pl->Hkv = Hkv; pl->D = head_dim; pl->ps = page_size; pl->g = g;
     pl->NT = B ? tree_off_host[B] : 0;
-    // units
-    struct U { int b, kvh, mtile, nblk, R, P, node0, T; };
-    std::vector<U> units;
-    long long W = 0;
+    // Unit groups: all M query tiles of one (sample, kv head) read the same K/V blocks.
+    struct GU { int b, kvh, M, nblk, R, P, node0, T; };
+    std::vector<GU> gus;
+    int n_tiles = 0;
     for (int b = 0; b < B; ++b) {
         const int T = tree_off_host[b + 1] - tree_off_host[b];
         const int P = prefix_len_host[b];
@@ -114,69 +114,139 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
         }
         const int nblk = (P + T + kBlockN - 1) / kBlockN;
         const int R = (T * g <= 64) ? 16 : 32;         // rows per TMEM sub-partition
-        const int mt = (T * g + 4 * R - 1) / (4 * R);
-        for (int kvh = 0; kvh < Hkv; ++kvh)
-            for (int m = 0; m < mt; ++m) {
-                units.push_back({b, kvh, m, nblk, R, P, tree_off_host[b], T});
-                pl->rmodes |= (R == 16) ? 1 : 2;
-                W += nblk + kOvhBlocks;
-            }
+        const int M = (T * g + 4 * R - 1) / (4 * R);   // query tiles per (sample, kv head)
+        for (int kvh = 0; kvh < Hkv; ++kvh) gus.push_back({b, kvh, M, nblk, R, P, tree_off_host[b], T});
+        pl->rmodes |= (R == 16) ? 1 : 2;
+        n_tiles += Hkv * M;
     }
-    const int n_ctas = std::max(1, std::min<int>(num_ctas, (int)std::max<size_t>(units.size(), 1)));
-    // balanced contiguous fill with split-KV cuts (load balance over heavy-tailed lengths)
-    // Greedy contiguous fill: units are poured, in order, into CTAs of capacity `target`
-    // (block units incl. a per-item overhead); a unit that overflows a CTA is cut (split-KV)
-    // and continues on the next one. Parts are never smaller than kMinPart blocks.
-    // CTA c owns the work interval [c*W/n, (c+1)*W/n) of the concatenated unit stream, so
-    // rounding never accumulates: a CTA that is left slightly under/over full is absorbed by
-    // the next boundary.
-    // (Each extra split part costs another kOvhBlocks, so the remaining work is re-divided over
-    // the remaining CTAs whenever a new CTA is entered.)
-    long long W_eff = W;
+    const int n_ctas = std::max(1, std::min<int>(num_ctas, std::max(n_tiles, 1)));
+    // Gangs: the M tiles of a unit group run on M different CTAs ("a gang") that process the
+    // same key-block ranges in the same order at the same time, so the K/V blocks the first CTA
+    // brings into L2 serve the other M-1 (HBM reads each block ~once instead of M times). CTAs
+    // are shared among the tile-count classes in proportion to their work.
+    long long Wc[5] = {0, 0, 0, 0, 0};
+    for (const GU& u : gus) Wc[u.M] += (long long)(u.nblk + kOvhBlocks) * u.M;
+    const long long Wt = Wc[1] + Wc[2] + Wc[3] + Wc[4];
+    int gangs[5] = {0, 0, 0, 0, 0};
+    int used = 0;
+    for (int M = 1; M <= 4; ++M)
+        if (Wc[M] > 0) {
+            gangs[M] = std::max(1, (int)((double)n_ctas * Wc[M] / std::max(Wt, 1ll) / M));
+            used += gangs[M] * M;
+        }
+    while (used > n_ctas) {   // (rounding up to one gang per class can overshoot)
+        int worst = 0;
+        for (int M = 1; M <= 4; ++M)
+            if (gangs[M] > 1 && (worst == 0 || gangs[M] * M > gangs[worst] * worst)) worst = M;
+        if (worst == 0) break;
+        --gangs[worst];
+        used -= worst;
+    }
+    if (used > n_ctas) {
+        // too few CTAs for one gang per class: multi-tile groups run tile by tile on single
+        // CTAs (class 1, no L2 sharing)
+        for (int M = 2; M <= 4; ++M) {
+            Wc[1] += Wc[M];
+            used -= gangs[M] * M;
+            gangs[M] = 0;
+            Wc[M] = 0;
+        }
+        if (gangs[1] == 0) { gangs[1] = 1; used += 1; }
+        while (used > n_ctas) { --gangs[1]; --used; }
+    }
+    for (;;) {   // spend leftover CTAs on the class with the most work per CTA that still fits
+        int best = 0;
+        double load = -1.0;
+        for (int M = 1; M <= 4; ++M)
+            if (gangs[M] > 0 && used + M <= n_ctas) {
+                const double l = (double)Wc[M] / (gangs[M] * M);
+                if (l > load) { load = l; best = M; }
+            }
+        if (best == 0) break;
+        ++gangs[best];
+        used += best;
+    }
+    // Balanced contiguous fill with split-KV cuts over the gangs of one class: unit groups are
+    // poured, in order, into gangs; gang v owns the work interval [v*W/n, (v+1)*W/n) of the
+    // concatenated stream (re-divided whenever a new gang is entered, since each extra split
+    // part costs another kOvhBlocks); parts are never smaller than kMinPart blocks.
+    struct Seg { int gu, tile, start, end; };   // tile -1: every tile of the gang
     std::vector<std::vector<WorkItem>> per_cta(n_ctas);
-    int cta = 0;
-    long long pos = 0;
-    long long end = (W_eff + n_ctas - 1) / n_ctas;
-    auto next_cta = [&]() {
-        ++cta;
-        end = pos + (W_eff - pos + (n_ctas - cta) - 1) / (n_ctas - cta);
-    };
     int n_parts = 0;
-    for (const U& u : units) {
-        int rem = u.nblk, start = 0;
-        std::vector<std::pair<int, int>> where;   // (cta, index) of this unit's parts
-        while (rem > 0) {
-            if (cta < n_ctas - 1 && pos >= end) { next_cta(); continue; }
-            const long long room = (cta == n_ctas - 1) ? (1ll << 60) : end - pos - kOvhBlocks;
-            int take;
-            if (room >= rem) {
-                take = rem;
-            } else if (room < kMinPart) {
-                if (per_cta[cta].empty()) {
-                    take = rem;               // never leave a CTA without work
+    int cta_base = 0;
+    for (int M = 1; M <= 4; ++M) {
+        const int G = gangs[M];
+        if (G == 0) continue;
+        std::vector<std::vector<Seg>> per_g(G);
+        // work entries of this class: (unit group, tile); tile -1 = the whole gang
+        std::vector<std::pair<int, int>> entries;
+        for (int gi = 0; gi < (int)gus.size(); ++gi) {
+            if (gus[gi].M == M) entries.push_back({gi, M == 1 ? 0 : -1});
+            else if (M == 1 && gangs[gus[gi].M] == 0)
+                for (int m = 0; m < gus[gi].M; ++m) entries.push_back({gi, m});
+        }
+        std::vector<std::vector<std::pair<int, int>>> where_of(entries.size());
+        long long W = 0;
+        for (auto& e : entries) W += gus[e.first].nblk + kOvhBlocks;
+        long long W_eff = W, pos = 0;
+        int v = 0;
+        long long end = (W_eff + G - 1) / G;
+        auto next_gang = [&]() {
+            ++v;
+            end = pos + (W_eff - pos + (G - v) - 1) / (G - v);
+        };
+        for (int ei = 0; ei < (int)entries.size(); ++ei) {
+            const int gi = entries[ei].first;
+            const GU& u = gus[gi];
+            int rem = u.nblk, start = 0;
+            while (rem > 0) {
+                if (v < G - 1 && pos >= end) { next_gang(); continue; }
+                const long long room = (v == G - 1) ? (1ll << 60) : end - pos - kOvhBlocks;
+                int take;
+                if (room >= rem) {
+                    take = rem;
+                } else if (room < kMinPart) {
+                    if (per_g[v].empty()) {
+                        take = rem;               // never leave a gang without work
+                    } else {
+                        next_gang();              // too little room for a useful part: next gang
+                        continue;
+                    }
                 } else {
-                    next_cta();               // too little room for a useful part: next CTA
-                    continue;
+                    take = (int)room;
+                    if (rem - take < kMinPart) take = (rem >= 2 * kMinPart) ? rem - kMinPart : rem;
                 }
-            } else {
-                take = (int)room;
-                if (rem - take < kMinPart) take = (rem >= 2 * kMinPart) ? rem - kMinPart : rem;
-            }
-            if (!where.empty()) W_eff += kOvhBlocks;   // an extra part of a split unit
-            where.push_back({cta, (int)per_cta[cta].size()});
-            per_cta[cta].push_back({u.b, u.kvh, u.mtile, start, start + take, -1, u.R, -1, u.P, u.node0, u.T, 0});
-            pos += take + kOvhBlocks;
-            start += take;
-            rem -= take;
-        }
-        if (where.size() > 1) {
-            const int uid = (int)pl->units.size();
-            pl->units.push_back({u.b, u.kvh, u.mtile, (int)where.size(), n_parts, u.R});
-            for (auto& wc : where) {
-                per_cta[wc.first][wc.second].part = n_parts++;
-                per_cta[wc.first][wc.second].unit = uid;
+                if (!where_of[ei].empty()) W_eff += kOvhBlocks;   // an extra part of a split unit
+                where_of[ei].push_back({v, (int)per_g[v].size()});
+                per_g[v].push_back({gi, entries[ei].second, start, start + take});
+                pos += take + kOvhBlocks;
+                start += take;
+                rem -= take;
             }
         }
+        // expand: gang v -> CTAs cta_base + v*M + m (tile m); split units per tile
+        for (int vv = 0; vv < G; ++vv)
+            for (int m = 0; m < M; ++m)
+                for (const Seg& sg : per_g[vv]) {
+                    const GU& u = gus[sg.gu];
+                    per_cta[cta_base + vv * M + m].push_back(
+                        {u.b, u.kvh, sg.tile >= 0 ? sg.tile : m, sg.start, sg.end, -1, u.R, -1, u.P, u.node0, u.T, 0});
+                }
+        for (int ei = 0; ei < (int)entries.size(); ++ei) {
+            if (where_of[ei].size() <= 1) continue;
+            const GU& u = gus[entries[ei].first];
+            for (int m = 0; m < M; ++m) {
+                const int uid = (int)pl->units.size();
+                const int tile = entries[ei].second >= 0 ? entries[ei].second : m;
+                pl->units.push_back({u.b, u.kvh, tile, (int)where_of[ei].size(), n_parts, u.R});
+                for (auto& wc : where_of[ei]) {
+                    WorkItem& it = per_cta[cta_base + wc.first * M + m][wc.second];
+                    it.part = n_parts++;
+                    it.unit = uid;
+                }
+            }
+        }
+        cta_base += G * M;
     }
     pl->cta_off.assign(n_ctas + 1, 0);
     for (int c = 0; c < n_ctas; ++c) {

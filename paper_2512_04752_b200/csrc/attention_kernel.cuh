@@ -42,6 +42,12 @@ constexpr int kM = 128;          // query rows per work item (UMMA M)
 #ifndef RS_ATTN_EW_SLOTS
 #define RS_ATTN_EW_SLOTS 4
 #endif
+#ifndef RS_ATTN_EW_KSLOTS
+#define RS_ATTN_EW_KSLOTS RS_ATTN_EW_SLOTS
+#endif
+#ifndef RS_ATTN_EW_VSLOTS
+#define RS_ATTN_EW_VSLOTS RS_ATTN_EW_SLOTS
+#endif
 constexpr int kMaxSlots = 8;
 #ifndef RS_ATTN_STAGE
 #define RS_ATTN_STAGE 0
@@ -89,8 +95,8 @@ struct Cfg {
     static constexpr bool kEW = (RM == 1);
     // RM = 1: the two logical Q buffers are the two 16-row halves of ONE 128-row tile (items
     // alternate lane halves), which frees 32 KB for deeper K/V rings.
-    static constexpr int KS = kEW ? RS_ATTN_EW_SLOTS : kKSlots;
-    static constexpr int VS = kEW ? RS_ATTN_EW_SLOTS : kVSlots;
+    static constexpr int KS = kEW ? RS_ATTN_EW_KSLOTS : kKSlots;
+    static constexpr int VS = kEW ? RS_ATTN_EW_VSLOTS : kVSlots;
     static_assert(KS <= kMaxSlots && VS <= kMaxSlots, "ring depth");
     static constexpr int kBoxes = D / 64;                    // 64-element (128 B) SW128 boxes
     static constexpr int kQBytes = kM * D * 2;
@@ -162,6 +168,28 @@ __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+
+// 2^x on the FMA/ALU pipes (x <= 8): round-to-nearest split via the 1.5*2^23 magic constant,
+// degree-3 Taylor polynomial on [-0.5, 0.5] (relative error < 7e-4, below bf16 rounding), exponent
+// added to the float bits. Used for a quarter of the elements so the MUFU pipe (ex2.approx) is
+// not the softmax bottleneck (every ex2 costs 8 issue cycles of MUFU per warp).
+__device__ __forceinline__ float ex2_poly(float x) {
+    x = fmaxf(x, -126.0f);
+    const float t = x + 12582912.0f;
+    const float f = x - (t - 12582912.0f);
+    float p = fmaf(f, 0.0555041086648216f, 0.2402264923172690f);
+    p = fmaf(p, f, 0.6931471805599453f);
+    p = fmaf(p, f, 1.0f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+#ifndef RS_ATTN_EXP_EMU
+#define RS_ATTN_EXP_EMU 0   // measured: no gain (the softmax is latency-, not MUFU-bound)
+#endif
+// element c of a row block: every 4th (c % 4 == 3) on the FMA pipe
+__device__ __forceinline__ float ex2_mix(float x, int c) {
+    if (RS_ATTN_EXP_EMU && (c & 3) == 3) return ex2_poly(x);
+    return ex2(x);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
@@ -655,10 +683,10 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
 #pragma unroll
                     for (int c = 0; c < 32; c += 2) {
                         const float e0 = ex2(fmaf(__uint_as_float(sh[c]), p.scale_log2, -mo));
-                        const float e1 = ex2(fmaf(__uint_as_float(sh[c + 1]), p.scale_log2, -mo));
+                        const float e1 = ex2_mix(fmaf(__uint_as_float(sh[c + 1]), p.scale_log2, -mo), c + 1);
                         const uint32_t pk = pack_bf16(e0, e1);
                         sh[c >> 1] = pk;
-                        ls8[(c >> 1) & 7] += __uint_as_float(pk << 16) + __uint_as_float(pk & 0xFFFF0000u);
+                        ls8[(c >> 1) & 7] += e0 + e1;
                     }
                     l_run += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
                 }
@@ -840,10 +868,10 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
 #pragma unroll
                         for (int c = 0; c < 32; c += 2) {
                             const float e0 = ex2(fmaf(__uint_as_float(sh[c]), p.scale_log2, -mo));
-                            const float e1 = ex2(fmaf(__uint_as_float(sh[c + 1]), p.scale_log2, -mo));
+                            const float e1 = ex2_mix(fmaf(__uint_as_float(sh[c + 1]), p.scale_log2, -mo), c + 1);
                             const uint32_t pk = pack_bf16(e0, e1);
                             sh[c >> 1] = pk;
-                            ls8[(c >> 1) & 7] += __uint_as_float(pk << 16) + __uint_as_float(pk & 0xFFFF0000u);
+                            ls8[(c >> 1) & 7] += e0 + e1;
                         }
                         l_run += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
                         wait_prev_pv();
@@ -924,11 +952,10 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
 #pragma unroll
                     for (int c = 0; c < 64; c += 2) {
                         const float e0 = ex2(fmaf(__uint_as_float(sr[c]), p.scale_log2, -mo));
-                        const float e1 = ex2(fmaf(__uint_as_float(sr[c + 1]), p.scale_log2, -mo));
+                        const float e1 = ex2_mix(fmaf(__uint_as_float(sr[c + 1]), p.scale_log2, -mo), c + 1);
                         const uint32_t pk = pack_bf16(e0, e1);
                         sr[c >> 1] = pk;
-                        // the normaliser sums the bf16-rounded probabilities the PV MMA uses
-                        ls8[(c >> 1) & 7] += __uint_as_float(pk << 16) + __uint_as_float(pk & 0xFFFF0000u);
+                        ls8[(c >> 1) & 7] += e0 + e1;
                     }
                     l_run += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
                     wait_prev_pv();

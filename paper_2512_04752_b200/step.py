@@ -67,12 +67,18 @@ class VerifyStep:
     def attention_step(self, stream=None):
         self.attn_call(stream)
 
-    def accept_compact_step(self, seed, step, stream=None):
+    def accept_step(self, seed, step, stream=None):
         core.tree_accept(self.mode, self.logits, self.parent, self.token, self.tree_off, self.gid,
                          draft_probs=self.draft, temperature=self.temperature, seed=seed, step=step,
                          out=(self.acc, self.path, self.bonus, self.flags), stream=stream, ws=self.accept_ws)
+
+    def compact_step(self, stream=None):
         core.kv_compact(self.k_layers, self.v_layers, self.block_table, self.prefix_len, self.acc, self.path,
                         self.ps, new_len=self.new_len, stream=stream)
+
+    def accept_compact_step(self, seed, step, stream=None):
+        self.accept_step(seed, step, stream)
+        self.compact_step(stream)
 
     def device_step(self, seed=0, step=0, stream=None):
         """Enqueue the whole step on `stream` (no host sync)."""
@@ -106,8 +112,8 @@ class VerifyStep:
         self.graph.replay()
 
     def capture_parts(self, seed=0, step=0):
-        """Three CUDA graphs (mask | L x attention | accept + compact) so a caller can time the
-        attention part with events between replays."""
+        """Four CUDA graphs (mask | L x attention | accept | compact) so a caller can time each
+        part with events between replays."""
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
@@ -116,7 +122,7 @@ class VerifyStep:
         torch.cuda.synchronize()
         parts = []
         for fn in (lambda st: self.mask_step(st), lambda st: self.attention_step(st),
-                   lambda st: self.accept_compact_step(seed, step, st)):
+                   lambda st: self.accept_step(seed, step, st), lambda st: self.compact_step(st)):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 fn(torch.cuda.current_stream())

@@ -256,7 +256,7 @@ def test_attention_parity(cuda_lib, case):
 
 @pytest.mark.parametrize("num_ctas", [1, 3, 7, 29])
 def test_attention_split_kv_parity(cuda_lib, num_ctas):
-    """Few CTAs force split-KV cuts + the combine kernel (heavy-tailed prefixes)."""
+    """Few CTAs force split-KV cuts and the fused split merge (heavy-tailed prefixes, 1-2 tile gangs)."""
     cfg = VerifyConfig("split", B=7, Hq=32, Hkv=8, d=128, V=10, L=1, prefix=("lognormal", 600, 1.0, 0, 4000),
                        tree=("range", 1, 64), seed=30 + num_ctas)
     b = make_verify_batch(cfg, device="cpu", with_logits=False)
@@ -264,7 +264,7 @@ def test_attention_split_kv_parity(cuda_lib, num_ctas):
     mae, rel = _attn_errors(og, oref)
     assert mae <= ATOL and rel <= RTOL_L2, (mae, rel, info)
     np.testing.assert_allclose(lg, lref, atol=2e-2, rtol=1e-3)
-    if num_ctas > 1:
+    if num_ctas > 3:      # (with 3 CTAs each tile-count class may get a single gang: no cuts)
         assert info["num_split_units"] > 0
 
 
