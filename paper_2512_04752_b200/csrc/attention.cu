@@ -67,7 +67,9 @@ struct rs_attn_plan {
     std::vector<WorkItem> items;
     std::vector<SplitUnit> units;
     int n_parts;
-    size_t off_cta, off_items, off_units, off_counter, off_part_o, off_part_lse, ws_bytes;
+    size_t off_cta, off_items, off_units, off_counter, off_qorder, off_qctr, off_part_o, off_part_lse, ws_bytes;
+    int dyn;                    // dynamic item queue (RM = 1 plans)
+    std::vector<int32_t> qorder;
     std::vector<uint8_t> blob;  // [0, off_part_o): header tables, uploaded verbatim
 };
 
@@ -255,12 +257,34 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
     }
     pl->cta_off[n_ctas] = (int)pl->items.size();
     pl->n_ctas = n_ctas;
+    // Dynamic scheduling (every tile R = 16: the 16-warp kernel): CTAs pull items from a global
+    // queue, so a CTA that runs faster (SMs do not all stream HBM at the same rate) takes more
+    // work and the launch ends when the average CTA does. Queue order interleaves the static
+    // lists position by position (first items of all CTAs, then the second items, ...).
+    {
+        // measured slower than the balanced static lists at the configs' item sizes (a 17-block
+        // item is ~15 us, too coarse for the tail): off unless RS_ATTN_DYN=1
+        const char* e = getenv("RS_ATTN_DYN");
+        pl->dyn = (pl->rmodes == 1 && e && e[0] == '1') ? 1 : 0;
+        pl->qorder.clear();
+        size_t maxlen = 0;
+        for (int c = 0; c < n_ctas; ++c) maxlen = std::max(maxlen, per_cta[c].size());
+        for (size_t k = 0; k < maxlen; ++k)
+            for (int c = 0; c < n_ctas; ++c)
+                if (k < per_cta[c].size()) pl->qorder.push_back(pl->cta_off[c] + (int)k);
+        // longest items first, so the launch tail is made of the short split parts
+        std::stable_sort(pl->qorder.begin(), pl->qorder.end(), [&](int x, int y) {
+            return pl->items[x].blk_end - pl->items[x].blk_begin > pl->items[y].blk_end - pl->items[y].blk_begin;
+        });
+    }
     pl->n_parts = n_parts;
     pl->off_cta = 0;
     pl->off_items = align_up(sizeof(int32_t) * (n_ctas + 1), 256);
     pl->off_units = align_up(pl->off_items + sizeof(WorkItem) * pl->items.size(), 256);
     pl->off_counter = align_up(pl->off_units + sizeof(SplitUnit) * pl->units.size(), 256);
-    pl->off_part_o = align_up(pl->off_counter + sizeof(int32_t) * pl->units.size(), 256);
+    pl->off_qorder = align_up(pl->off_counter + sizeof(int32_t) * pl->units.size(), 256);
+    pl->off_qctr = align_up(pl->off_qorder + sizeof(int32_t) * pl->qorder.size(), 256);
+    pl->off_part_o = align_up(pl->off_qctr + sizeof(int32_t) * 2, 256);
     pl->off_part_lse = align_up(pl->off_part_o + sizeof(float) * (size_t)n_parts * kM * head_dim, 256);
     pl->ws_bytes = align_up(pl->off_part_lse + sizeof(float) * (size_t)n_parts * kM, 256);
     pl->blob.assign(pl->off_part_o, 0);   // includes the zeroed split-unit counters
@@ -269,6 +293,8 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
         memcpy(pl->blob.data() + pl->off_items, pl->items.data(), sizeof(WorkItem) * pl->items.size());
     if (!pl->units.empty())
         memcpy(pl->blob.data() + pl->off_units, pl->units.data(), sizeof(SplitUnit) * pl->units.size());
+    if (!pl->qorder.empty())
+        memcpy(pl->blob.data() + pl->off_qorder, pl->qorder.data(), sizeof(int32_t) * pl->qorder.size());
     *plan_out = pl;
     return RS_OK;
 }
@@ -354,6 +380,10 @@ static rs_status launch_attn(const rs_attn_plan* pl, const void* q, const void* 
     prm.part_lse = reinterpret_cast<float*>(w + pl->off_part_lse);
     prm.units = reinterpret_cast<const SplitUnit*>(w + pl->off_units);
     prm.unit_counter = reinterpret_cast<int*>(w + pl->off_counter);
+    prm.qorder = reinterpret_cast<const int32_t*>(w + pl->off_qorder);
+    prm.qctr = reinterpret_cast<int*>(w + pl->off_qctr);
+    prm.n_items = (int)pl->items.size();
+    prm.dyn = pl->dyn;
     prm.prefix_len = prefix_len;
     prm.tree_off = tree_off;
     prm.tree_mask = tree_mask;

@@ -49,6 +49,8 @@ constexpr int kM = 128;          // query rows per work item (UMMA M)
 #define RS_ATTN_EW_VSLOTS RS_ATTN_EW_SLOTS
 #endif
 constexpr int kMaxSlots = 8;
+constexpr int kRing = 8;         // dynamic item queue ring depth (shared memory)
+constexpr int kQConsumers = 15;  // warps that read the ring (all but the fetching producer warp 0)
 #ifndef RS_ATTN_STAGE
 #define RS_ATTN_STAGE 0
 #endif
@@ -124,6 +126,8 @@ struct Bars {
     uint64_t p_full[2], pv_done[2];
     uint64_t o_free;
     uint64_t o_ready[2], ml_ready[2], o_free2[2];   // epilogue-warpgroup handshakes (RM = 1), by item parity
+    uint64_t item_full[8], item_empty[8];             // dynamic item queue: ring of item indices
+    int item_ring[8];
     uint32_t tmem_base;
     int merge_flag;
 };
@@ -145,6 +149,10 @@ struct Params {
     __nv_bfloat16* out;
     float* lse;
     unsigned long long* trace;   // optional per-block event timestamps (profiling)
+    const int32_t* qorder;       // dynamic scheduling: queue position -> item index
+    int* qctr;                   // dynamic scheduling: [0] next item, [1] CTAs done (zero between launches)
+    int n_items;
+    int dyn;                     // 1: CTAs take items from the global queue (atomicAdd), 0: static lists
     int dbg;                     // ablation switches for profiling only (RS_ATTN_DBG; results wrong if != 0):
                                  // 1 skip epilogue O reads/stores, 2 skip softmax math, 4 skip PV MMA
 };
@@ -212,7 +220,39 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     const int lane = threadIdx.x & 31;
     const int item_begin = p.cta_off[blockIdx.x];
     const int item_end = p.cta_off[blockIdx.x + 1];
-    if (p.trace && threadIdx.x == 0) p.trace[((size_t)blockIdx.x * kTraceJ + kTraceJ - 1) * 16 + 14] = globaltimer_ns();
+    // The CTA's item sequence: static (its plan list) or dynamic (p.dyn: warp 0 takes the next
+    // item of the global queue with atomicAdd and publishes it through a shared-memory ring that
+    // every other warp reads once per position). -1 ends the sequence.
+    auto seq_read = [&](int it) -> int {   // warp-collective, every warp except warp 0
+        if (!p.dyn) return item_begin + it < item_end ? item_begin + it : -1;
+        const int sl = it % kRing;
+        mbar_wait(&bars->item_full[sl], (it / kRing) & 1);
+        const int w = *reinterpret_cast<volatile int*>(&bars->item_ring[sl]);
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&bars->item_empty[sl]);
+        return w;
+    };
+    auto seq_fetch = [&](int it) -> int {  // warp 0: produce position it of the sequence
+        if (!p.dyn) return item_begin + it < item_end ? item_begin + it : -1;
+        int w = 0;
+        if ((threadIdx.x & 31) == 0) w = atomicAdd(p.qctr, 1);
+        w = __shfl_sync(0xffffffffu, w, 0);
+        w = (w < p.n_items) ? __ldg(p.qorder + w) : -1;
+        const int sl = it % kRing;
+        mbar_wait(&bars->item_empty[sl], ((it / kRing) & 1) ^ 1);
+        if ((threadIdx.x & 31) == 0) {
+            bars->item_ring[sl] = w;
+            mbar_arrive(&bars->item_full[sl]);   // release: the ring entry is visible to waiters
+        }
+        __syncwarp();
+        return w;
+    };
+    if (p.trace && threadIdx.x == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        p.trace[((size_t)blockIdx.x * kTraceJ + kTraceJ - 1) * 16 + 13] = smid;
+        p.trace[((size_t)blockIdx.x * kTraceJ + kTraceJ - 1) * 16 + 14] = globaltimer_ns();
+    }
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kQBufs; ++i) { mbar_init(&bars->q_full[i], 1); mbar_init(&bars->q_empty[i], 1); }
@@ -225,6 +265,10 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             mbar_init(&bars->pv_done[i], 1);
         }
         mbar_init(&bars->o_free, 8);
+        for (int i = 0; i < kRing; ++i) {
+            mbar_init(&bars->item_full[i], 1);
+            mbar_init(&bars->item_empty[i], kQConsumers);
+        }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bars->o_ready[i], 1);
             mbar_init(&bars->ml_ready[i], 8);
@@ -279,9 +323,12 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             return (j < x.blk_end - x.blk_begin)
                        ? __ldg(p.block_table + (int64_t)x.b * p.max_pages + x.blk_begin + j) : 0;
         };
-        if (item_begin < item_end) {
-            WorkItem wi = load_item(p.items, item_begin);
-            WorkItem wn = (item_begin + 1 < item_end) ? load_item(p.items, item_begin + 1) : wi;
+        auto seq = [&](int it) { return isK ? seq_fetch(it) : seq_read(it); };
+        int w = seq(0);
+        if (w >= 0) {
+            int wnx = seq(1);
+            WorkItem wi = load_item(p.items, w);
+            WorkItem wn = wnx >= 0 ? load_item(p.items, wnx) : wi;
             if (isK) issue_q(wi, 0);
             int pg_cur = page_chunk(wi, 0);
             // warm L2 with the first blocks of this CTA
@@ -292,10 +339,10 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                     for (int bx = 0; bx < C::kBoxes; ++bx) tma_prefetch_2d(tm, bx * 64, (page * p.Hkv + wi.kvh) * kBlockN);
                 __syncwarp();
             }
-            int it = 0;
-            for (int w = item_begin; w < item_end; ++w, ++it) {
-                const bool has_next = w + 1 < item_end;
-                const WorkItem wnn = (w + 2 < item_end) ? load_item(p.items, w + 2) : wn;
+            for (int it = 0; w >= 0; ++it) {
+                const bool has_next = wnx >= 0;
+                const int wnnx = has_next ? seq(it + 2) : -1;
+                const WorkItem wnn = wnnx >= 0 ? load_item(p.items, wnnx) : wn;
                 const int nb = wi.blk_end - wi.blk_begin;
                 const int nbn = has_next ? wn.blk_end - wn.blk_begin : 0;
                 const int pg_first_next = has_next ? page_chunk(wn, 0) : 0;
@@ -348,6 +395,8 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 pg_cur = pg_first_next;
                 wi = wn;
                 wn = wnn;
+                w = wnx;
+                wnx = wnnx;
             }
         }
     } else if (warp == 1) {
@@ -357,9 +406,11 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         const uint32_t sbase = smem_u32(smem);
         uint32_t sJ = 0;
         int it = 0;
-        int nblk = item_begin < item_end ? __ldg(&p.items[item_begin].blk_end) - __ldg(&p.items[item_begin].blk_begin) : 0;
-        for (int w = item_begin; w < item_end; ++w, ++it) {
-            const int nblk_next = (w + 1 < item_end) ? __ldg(&p.items[w + 1].blk_end) - __ldg(&p.items[w + 1].blk_begin) : 0;
+        int w = seq_read(0);
+        int nblk = w >= 0 ? __ldg(&p.items[w].blk_end) - __ldg(&p.items[w].blk_begin) : 0;
+        for (; w >= 0; ++it) {
+            const int wn = seq_read(it + 1);
+            const int nblk_next = wn >= 0 ? __ldg(&p.items[wn].blk_end) - __ldg(&p.items[wn].blk_begin) : 0;
             const int qb = it % kQBufs;
             mbar_wait(&bars->q_full[qb], (it / kQBufs) & 1);
             const uint32_t qa = sbase + C::kOffQ + qb * C::kQStride;
@@ -386,6 +437,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 __syncwarp();
             }
             nblk = nblk_next;
+            w = wn;
         }
     } else if (warp == 2) {
         // ============================ MMA issuer: O += P V ============================
@@ -393,9 +445,11 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         const uint32_t sbase = smem_u32(smem);
         uint32_t pJ = 0;
         int it = 0;
-        int nblk = item_begin < item_end ? __ldg(&p.items[item_begin].blk_end) - __ldg(&p.items[item_begin].blk_begin) : 0;
-        for (int w = item_begin; w < item_end; ++w, ++it) {
-            const int nblk_next = (w + 1 < item_end) ? __ldg(&p.items[w + 1].blk_end) - __ldg(&p.items[w + 1].blk_begin) : 0;
+        int w = seq_read(0);
+        int nblk = w >= 0 ? __ldg(&p.items[w].blk_end) - __ldg(&p.items[w].blk_begin) : 0;
+        for (; w >= 0; ++it) {
+            const int wn = seq_read(it + 1);
+            const int nblk_next = wn >= 0 ? __ldg(&p.items[wn].blk_end) - __ldg(&p.items[wn].blk_begin) : 0;
             for (int j = 0; j < nblk; ++j, ++pJ) {
                 // EW: O is pre-zeroed, so every PV accumulates; else the first block of each
                 // warpgroup in the item overwrites
@@ -424,6 +478,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 __syncwarp();
             }
             nblk = nblk_next;
+            w = wn;
         }
     } else if (KT<RM>::kEW && warp >= 12) {
         // ============================ epilogue warpgroup (RM = 1) ============================
@@ -436,9 +491,11 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         const uint32_t qbase = (uint32_t)(wq * 32) << 16;
         uint32_t J = 0;
         int it = 0;
-        WorkItem wi = item_begin < item_end ? load_item(p.items, item_begin) : WorkItem{};
-        for (int w = item_begin; w < item_end; ++w, ++it) {
-            const WorkItem wn = (w + 1 < item_end) ? load_item(p.items, w + 1) : wi;
+        int w = seq_read(0);
+        WorkItem wi = w >= 0 ? load_item(p.items, w) : WorkItem{};
+        for (; w >= 0; ++it) {
+            const int wnx = seq_read(it + 1);
+            const WorkItem wn = wnx >= 0 ? load_item(p.items, wnx) : wi;
             const int h = it & 1;
             const int off = wi.node0;
             const int rows = min(64, wi.T * p.g - wi.mtile * 64);
@@ -564,6 +621,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             }
             J += nblk;
             wi = wn;
+            w = wnx;
         }
     } else if (KT<RM>::kEW && warp >= 4) {
         // ============================ softmax (RM = 1, half-split rows) ============================
@@ -588,9 +646,11 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         }
         uint32_t J = 0;
         int it = 0;
-        WorkItem wi = item_begin < item_end ? load_item(p.items, item_begin) : WorkItem{};
-        for (int w = item_begin; w < item_end; ++w, ++it) {
-            const WorkItem wn = (w + 1 < item_end) ? load_item(p.items, w + 1) : wi;   // prefetch
+        int w = seq_read(0);
+        WorkItem wi = w >= 0 ? load_item(p.items, w) : WorkItem{};
+        for (; w >= 0; ++it) {
+            const int wnx = seq_read(it + 1);
+            const WorkItem wn = wnx >= 0 ? load_item(p.items, wnx) : wi;   // prefetch
             const int h = it & 1;
             const uint32_t lane_base = (uint32_t)(wq * 32 + 16 * h) << 16;
             const uint32_t o_mine = tmem + lane_base + grp * D;
@@ -750,6 +810,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             if (lane == 0) mbar_arrive(&bars->ml_ready[h]);
             J += nblk;
             wi = wn;
+            w = wnx;
         }
     } else if (warp >= 4) {
         // ============================ softmax + epilogue ============================
@@ -760,9 +821,11 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         const uint32_t o_mine = tmem + lane_base + grp * D;
         uint32_t J = 0;
         int it = 0;
-        WorkItem wi = item_begin < item_end ? load_item(p.items, item_begin) : WorkItem{};
-        for (int w = item_begin; w < item_end; ++w, ++it) {
-            const WorkItem wn = (w + 1 < item_end) ? load_item(p.items, w + 1) : wi;   // prefetch
+        int w = seq_read(0);
+        WorkItem wi = w >= 0 ? load_item(p.items, w) : WorkItem{};
+        for (; w >= 0; ++it) {
+            const int wnx = seq_read(it + 1);
+            const WorkItem wn = wnx >= 0 ? load_item(p.items, wnx) : wi;   // prefetch
             const int P = wi.P;
             const int off = wi.node0;
             const int T = wi.T;
@@ -1177,6 +1240,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             }
             J += nblk;
             wi = wn;
+            w = wnx;
         }
         if (wq == 0 && lane == 0) bulk_wait_all();   // output TMA stores complete before exit
     }
@@ -1184,6 +1248,14 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     __syncthreads();
     tc_fence_after();
     if (warp == 2) tmem_dealloc<C::kTmemCols>(tmem);
+    if (p.dyn && threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(p.qctr + 1, 1) == (int)gridDim.x - 1) {   // last CTA out: ready for the next launch
+            p.qctr[0] = 0;
+            p.qctr[1] = 0;
+            __threadfence();
+        }
+    }
     if (p.trace && threadIdx.x == 0) p.trace[((size_t)blockIdx.x * kTraceJ + kTraceJ - 1) * 16 + 15] = globaltimer_ns();
 }
 

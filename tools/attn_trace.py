@@ -93,6 +93,11 @@ def main():
     res["cta0_items"] = items[cta[0]:cta[1]].tolist()
     g0 = t[:, 255, 14].copy()
     g1 = t[:, 255, 15].copy()
+    smid = t[:, 255, 13].copy().astype(int)
+    t[:, 255, 13] = 0
+    res["per_cta"] = {"smid": smid.tolist(), "start_ns": (g0 - g0.min()).tolist(), "end_ns": (g1 - g0.min()).tolist(),
+                      "blocks": [int(sum(items[i, 4] - items[i, 3] for i in range(cta[c], cta[c + 1]))) for c in range(n)],
+                      "items": [int(cta[c + 1] - cta[c]) for c in range(n)]}
     ok = (g0 > 0) & (g1 > 0)
     res["globaltimer_us"] = {"kernel_span": float((g1[ok].max() - g0[ok].min()) / 1e3),
                              "start_skew": float((g0[ok].max() - g0[ok].min()) / 1e3),
