@@ -410,7 +410,18 @@ static rs_status launch_attn(const rs_attn_plan* pl, const void* q, const void* 
         attr_set[D == 128][rm] = true;
     }
     const int threads = rm == 1 ? KT<1>::kThreads : KT<2>::kThreads;
-    kern<<<pl->n_ctas, threads, smem_bytes, st>>>(tmQ, tmK, tmV, tmO, prm);
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)pl->n_ctas);
+    lc.blockDim = dim3((unsigned)threads);
+    lc.dynamicSmemBytes = (size_t)smem_bytes;
+    lc.stream = st;
+    cudaLaunchAttribute la[1];
+    static const bool pdl = !(getenv("RS_ATTN_PDL") && getenv("RS_ATTN_PDL")[0] == '0');
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = la;
+    lc.numAttrs = pdl ? 1 : 0;
+    RS_CUDA_CHECK(cudaLaunchKernelEx(&lc, kern, tmQ, tmK, tmV, tmO, prm));
     RS_LAUNCH_CHECK();
     return RS_OK;
 }

@@ -284,6 +284,13 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = bars->tmem_base;
+    // Programmatic dependent launch: the next layer's grid may be scheduled now (its CTAs start
+    // as this grid's CTAs exit). Only reads of K/V pages, item tables and block tables (inputs no
+    // earlier grid writes) may precede griddep_wait(): the producer warps stream the first key
+    // blocks while the previous grid drains; Q, the tree masks, outputs and the shared split-KV
+    // workspace are touched only after it.
+    griddep_launch_dependents();
+    if (warp >= 4) griddep_wait();
     if (warp == 0 || warp == 3) {
         // ============================ TMA producers ============================
         // warp 0: Q tiles + K pages; warp 3: V pages (whole warp runs the loop; one elected lane
@@ -329,7 +336,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             int wnx = seq(1);
             WorkItem wi = load_item(p.items, w);
             WorkItem wn = wnx >= 0 ? load_item(p.items, wnx) : wi;
-            if (isK) issue_q(wi, 0);
+            const int q0_at = min(wi.blk_end - wi.blk_begin, C::KS) - 1;   // first Q after the first K ring fill
             int pg_cur = page_chunk(wi, 0);
             // warm L2 with the first blocks of this CTA
             for (int k = 0; k < pf && k < wi.blk_end - wi.blk_begin; ++k) {
@@ -352,6 +359,10 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                     const int cnt = min(32, nb - base);
                     for (int k = 0; k < cnt; ++k, ++J) {
                         const int j = base + k;
+                        if (isK && it == 0 && j == q0_at) {
+                            griddep_wait();
+                            issue_q(wi, 0);
+                        }
                         if (isK && has_next && j == q_next_at) issue_q(wn, it + 1);
                         // L2 prefetch of block j + pf (this item or the next one)
                         if (do_pf) {

@@ -69,6 +69,14 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// Wait until the preceding grid of the stream has completed and its memory is visible.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Allow the next grid of the stream to be scheduled (its CTAs start as SMs free up).
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ------------------------------------------------------------------ clusters / DSMEM
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;

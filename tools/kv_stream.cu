@@ -135,5 +135,40 @@ int main() {
     run("K,V separate, blocks shuffled globally", tk, tv, false, true);
     CUtensorMap tk2 = mk(big, rows), tv2 = mk((char*)big + bytes + (1 << 20) * 3 + 4096 * 5, rows);
     run("K,V in one alloc, V offset by odd amount", tk2, tv2, false, false);
+    // like the verify step: every launch reads a different layer's cache (8 layers rotating)
+    {
+        std::vector<CUtensorMap> tks, tvs;
+        for (int l = 0; l < 8; ++l) {
+            void *kk, *vv;
+            cudaMalloc(&kk, bytes);
+            cudaMalloc(&vv, bytes);
+            cudaMemset(kk, 1, bytes);
+            cudaMemset(vv, 1, bytes);
+            tks.push_back(mk(kk, rows));
+            tvs.push_back(mk(vv, rows));
+        }
+        std::vector<int> rk((size_t)sms * per, 0), rv((size_t)sms * per, 0);
+        for (int i = 0; i < total; ++i) {
+            const int b = i / (Hkv * npg), h = (i / npg) % Hkv, j = i % npg;
+            rk[i] = (perm[b * npg + j] * Hkv + h) * 64;
+            rv[i] = rk[i];
+        }
+        int *dk, *dv;
+        cudaMalloc(&dk, rk.size() * 4); cudaMalloc(&dv, rv.size() * 4);
+        cudaMemcpy(dk, rk.data(), rk.size() * 4, cudaMemcpyHostToDevice);
+        cudaMemcpy(dv, rv.data(), rv.size() * 4, cudaMemcpyHostToDevice);
+        unsigned long long* sink; cudaMalloc(&sink, 8);
+        const int smem = 2 * SLOTS * kTile + 2048;
+        cudaEvent_t a, e; cudaEventCreate(&a); cudaEventCreate(&e);
+        for (int w = 0; w < 8; ++w) kv_kernel<<<sms, 128, smem>>>(tks[w], tvs[w], dk, dv, per, sink);
+        cudaEventRecord(a);
+        for (int r = 0; r < 32; ++r) kv_kernel<<<sms, 128, smem>>>(tks[r % 8], tvs[r % 8], dk, dv, per, sink);
+        cudaEventRecord(e);
+        cudaEventSynchronize(e);
+        float ms; cudaEventElapsedTime(&ms, a, e);
+        const double by = 2.0 * sms * per * kTile;
+        printf("%-44s %7.1f us  %7.1f GB/s  err=%s\n", "8 rotating layers (32 launches, mean)", ms * 1e3 / 32,
+               by / (ms * 1e-3 / 32) / 1e9, cudaGetErrorString(cudaGetLastError()));
+    }
     return 0;
 }
