@@ -360,6 +360,9 @@ static rs_status launch_attn(const rs_attn_plan* pl, const void* q, const void* 
                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         RS_REQUIRE(r == CUDA_SUCCESS, RS_ERR_CUDA, "tensor map Q/O failed (%d)", (int)r);
     }
+    // L2 sector promotion of the K/V page loads (RS_ATTN_L2PROMO = 0..3 for measurements)
+    static const int promo_env = getenv("RS_ATTN_L2PROMO") ? atoi(getenv("RS_ATTN_L2PROMO")) : 3;
+    const CUtensorMapL2promotion kv_promo = (CUtensorMapL2promotion)(promo_env & 3);
     const void* kv[2] = {k_pages, v_pages};
     CUtensorMap* tm[2] = {&tmK, &tmV};
     for (int i = 0; i < 2; ++i) {
@@ -369,7 +372,7 @@ static rs_status launch_attn(const rs_attn_plan* pl, const void* q, const void* 
         cuuint32_t es[2] = {1, 1};
         CUresult r = enc(tm[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(kv[i]), dims, strides, box, es,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                         kv_promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         RS_REQUIRE(r == CUDA_SUCCESS, RS_ERR_CUDA, "tensor map KV failed (%d)", (int)r);
     }
     Params prm;
