@@ -34,9 +34,43 @@ WORKLOAD_DESC = {
     "c5g8": "BASELINE configs[4] per-GPU shard at 8 GPUs: Llama-3-70B shapes (64 q / 8 kv, d=128, 80 layers), "
             "16 samples, prefix 8K, 64-node trees, greedy",
     "tiny": "BASELINE configs[0]: 1 sample, prefix 32, 8-node tree, 1 head, d=64, V=1000, greedy",
-    "c3": "BASELINE configs[2]: Llama-3-8B shapes, batch 256, prefixes 512-16K lognormal, trees 4-64, "
-          "rejection sampling (MSS)",
+    "c3": "BASELINE configs[2]: Llama-3-8B shapes, batch 256, prefixes 512-16K lognormal, trees 4-64 "
+          "(drawn per sample), rejection sampling (MSS)",
+    "c3s": "BASELINE configs[2] as the method runs it: Llama-3-8B shapes, batch 256, prefixes 512-16K "
+           "lognormal, every tree = S(n) for the n select_strategy picks (host C++, called every step), "
+           "rejection sampling (MSS)",
 }
+
+
+# select_strategy inputs for configs with ("strategy", n_cand) trees: acceptance
+# fit F (knots) and a cost model t_sd = c_draft + b0 + b1*N_seq + b2*N_draft (seconds): b1 from the
+# measured attention bytes per token (32 layers x 4 KB at ~4.4 TB/s), b2 the per-token GEMM time of
+# an 8B model at the bf16 tensor peak (2 x 8e9 FLOP / 1.5e15), c_draft a ~1 ms draft pass.
+STRATEGY_KX = [0.0, 0.05, 0.2, 0.5, 1.0]
+STRATEGY_KY = [0.0, 0.15, 0.45, 0.75, 0.95]
+STRATEGY_COST = dict(c_draft=1.0e-3, b0=2.0e-4, b1=3.0e-8, b2=1.07e-5, b3=0.0, k_sat=4096.0, seq_bucket=256,
+                     draft_bucket=4)
+
+
+def strategy_trees(cfg, core):
+    """a0 on the host: one n for the batch (Z20) from each sample's candidate draft tree; every
+    sample's verification tree is the root plus its S(n)."""
+    from types import SimpleNamespace
+    from synth import draw_prefix_lengths, make_candidate_tree
+    P = draw_prefix_lengths(np.random.default_rng(cfg.seed), cfg)
+    rng = np.random.default_rng(cfg.seed + 77)
+    cands = [make_candidate_tree(rng, int(cfg.tree[1])) for _ in range(cfg.B)]
+    sel = core.Selector(SimpleNamespace(**STRATEGY_COST), STRATEGY_KX, STRATEGY_KY)
+    res = sel.select(cands, P, n_min=3, n_max=63, patience=2, return_selected=True)
+    n = res["n"]
+    parents = []
+    for b in range(cfg.B):
+        chosen = sorted(int(x) for x in res["selected"][b][:n])
+        idx = {c: i + 1 for i, c in enumerate(chosen)}
+        cp = cands[b][0]
+        par = [-1] + [0 if cp[c] < 0 else idx[int(cp[c])] for c in chosen]   # S(n) is connected
+        parents.append(np.array(par, np.int32))
+    return sel, cands, P, res, parents
 
 
 def _dist():
@@ -193,7 +227,12 @@ def run_ours(args, world, rank, local):
         dist.init_process_group("nccl", device_id=dev)
     cfg = CONFIGS[args.config]
     cfg = type(cfg)(**{**cfg.__dict__, "seed": cfg.seed + 1000 * rank})   # disjoint samples per rank
-    b = make_verify_batch(cfg, device=dev, gen_device=dev)
+    strat = None
+    if cfg.tree[0] == "strategy":
+        strat = strategy_trees(cfg, core)
+        b = make_verify_batch(cfg, device=dev, gen_device=dev, parents=strat[4])
+    else:
+        b = make_verify_batch(cfg, device=dev, gen_device=dev)
     mode = {"greedy": core.GREEDY, "delta": core.SAMPLE_DELTA, "mss": core.SAMPLE_MSS}[cfg.mode]
     step = VerifyStep(b, mode=mode, temperature=cfg.temperature)
     stream = torch.cuda.current_stream()
@@ -226,7 +265,13 @@ def run_ours(args, world, rank, local):
     barrier()
     with sampler:
         start.record(stream)
+        sel_s = 0.0
         for k in range(args.steps):
+            if strat is not None:
+                # a0 (host) for the next step, while the GPU runs the queued graphs
+                t0 = time.perf_counter()
+                strat[0].select(strat[1], strat[2], n_min=3, n_max=63, patience=2)
+                sel_s += time.perf_counter() - t0
             g_mask.replay()
             ev[k][0].record(stream)
             g_attn.replay()
@@ -307,7 +352,12 @@ def run_ours(args, world, rank, local):
                    "l2": "inputs larger than L2: %.1f GB of distinct per-layer KV resident" %
                          (2 * b["k_cache"].numel() * 2 / 1e9),
                    "parallelism": f"dp{world} (independent sample-sharded instances, no collective)",
-                   "attn_plan": info},
+                   "attn_plan": info,
+                   **({"select_strategy": {"n": strat[3]["n"], "T": strat[3]["n"] + 1, "depth": strat[3]["depth"],
+                                           "width": strat[3]["width"], "pred_al": round(strat[3]["al"], 2),
+                                           "pred_t_sd_ms": round(strat[3]["t_sd"] * 1e3, 3),
+                                           "host_ms_per_call": round(sel_s / args.steps * 1e3, 4),
+                                           "in_timed_loop": True}} if strat is not None else {})},
         "clocks": sampler.summary(),
         "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,

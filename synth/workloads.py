@@ -42,7 +42,7 @@ class VerifyConfig:
     L: int
     page_size: int = 64
     prefix: tuple = ("fixed", 1024)          # ("fixed", P) | ("lognormal", median, sigma, lo, hi)
-    tree: tuple = ("fixed", 16)              # ("fixed", T) | ("range", lo, hi) | ("tiny",)
+    tree: tuple = ("fixed", 16)              # ("fixed", T) | ("range", lo, hi) | ("tiny",) | ("strategy", n_cand)
     mode: str = "greedy"                     # greedy | delta | mss
     p_accept: float = 0.8                    # greedy: probability a node's argmax is a child's token
     temperature: float = 1.0
@@ -67,6 +67,12 @@ CONFIGS = {
                        prefix=("lognormal", 2048, 0.784, 512, 16384), tree=("range", 4, 64),
                        mode="mss"),
     # configs[4] per-GPU shard at G=8: 70B shapes, 128/8 samples, prefix 8K, 64-node trees
+    # configs[2] as the method runs it: every sample's verification tree is its S(n) for the ONE n
+    # select_strategy picks for the batch (Z20), from a candidate draft tree of n_cand nodes
+    # (trees given to make_verify_batch by the caller, which runs the selector)
+    "c3s": VerifyConfig("c3s", B=256, Hq=32, Hkv=8, d=128, V=128256, L=32,
+                        prefix=("lognormal", 2048, 0.784, 512, 16384), tree=("strategy", 96),
+                        mode="mss"),
     "c5g8": VerifyConfig("c5g8", B=16, Hq=64, Hkv=8, d=128, V=128256, L=80, prefix=("fixed", 8192),
                          tree=("fixed", 64), mode="greedy"),
 }
@@ -141,7 +147,7 @@ def _children_lists(parent: np.ndarray):
 
 def make_verify_batch(cfg: VerifyConfig, device="cpu", gen_device: Optional[str] = None,
                       layers: Optional[int] = None, spare_pages: int = 0,
-                      with_logits: bool = True) -> dict:
+                      with_logits: bool = True, parents: Optional[list] = None) -> dict:
     """Draw one verify-step batch. All tensors live on `device`; large random tensors are
     drawn with a torch generator on `gen_device` (default: `device`) seeded by cfg.seed."""
     rng = np.random.default_rng(cfg.seed)
@@ -152,12 +158,17 @@ def make_verify_batch(cfg: VerifyConfig, device="cpu", gen_device: Optional[str]
     B, Hq, Hkv, d, ps, V = cfg.B, cfg.Hq, cfg.Hkv, cfg.d, cfg.page_size, cfg.V
 
     P = draw_prefix_lengths(rng, cfg)
-    Tn = _tree_sizes(rng, cfg)
+    if parents is not None:      # verification trees given by the caller (e.g. from select_strategy)
+        parents = [np.asarray(x, dtype=np.int32) for x in parents]
+        Tn = np.array([len(x) for x in parents], dtype=np.int32)
+    else:
+        Tn = _tree_sizes(rng, cfg)
     tree_off = np.zeros(B + 1, dtype=np.int32)
     tree_off[1:] = np.cumsum(Tn)
     NT = int(tree_off[-1])
-    parents = []
-    for b in range(B):
+    given = parents is not None
+    parents = parents if given else []
+    for b in range(B if not given else 0):
         if cfg.tree[0] == "tiny":
             parents.append(np.asarray(TINY_PARENT, dtype=np.int32))
         else:
