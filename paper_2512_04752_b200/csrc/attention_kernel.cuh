@@ -538,7 +538,10 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 const float f0 = w0 * invL, f1 = w1 * invL;
                 const int hh = wi.kvh * p.g + (grow % p.g);
                 __nv_bfloat16* orow = p.out + ((int64_t)(off + node) * p.Hq + hh) * D;
-                float* prow = direct ? nullptr : p.part_o + ((int64_t)wi.part * kM + rr) * D;
+                // split parts keep their normalised partial O in bf16 (like the output): half the
+                // partial traffic; one more bf16 rounding before the merge (< 2^-9 relative)
+                __nv_bfloat16* dst_row = direct ? orow
+                                                : reinterpret_cast<__nv_bfloat16*>(p.part_o) + ((int64_t)wi.part * kM + rr) * D;
                 const uint32_t rowbase = tmem + ((uint32_t)(wq * 32 + 16 * h) << 16);
                 const int cb = (lane & 16) ? D / 2 : 0;   // my columns [cb, cb + D/2)
 #pragma unroll 1
@@ -550,21 +553,15 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
 #pragma unroll
                     for (int c = 0; c < 16; ++c)
                         a[c] = __float_as_uint(__uint_as_float(a[c]) * f0 + __uint_as_float(bb[c]) * f1);
-                    if (warp_active && row_valid) {
-                        if (direct) {
+                    if (warp_active && row_valid && !(p.dbg & 32)) {   // (dbg 32: skip stores, measurement only)
 #pragma unroll
-                            for (int c = 0; c < 16; c += 8) {
-                                uint4 u;
-                                u.x = pack_bf16(__uint_as_float(a[c]), __uint_as_float(a[c + 1]));
-                                u.y = pack_bf16(__uint_as_float(a[c + 2]), __uint_as_float(a[c + 3]));
-                                u.z = pack_bf16(__uint_as_float(a[c + 4]), __uint_as_float(a[c + 5]));
-                                u.w = pack_bf16(__uint_as_float(a[c + 6]), __uint_as_float(a[c + 7]));
-                                *reinterpret_cast<uint4*>(orow + cb + cc + c) = u;
-                            }
-                        } else {
-#pragma unroll
-                            for (int c = 0; c < 16; c += 4)
-                                *reinterpret_cast<uint4*>(prow + cb + cc + c) = make_uint4(a[c], a[c + 1], a[c + 2], a[c + 3]);
+                        for (int c = 0; c < 16; c += 8) {
+                            uint4 u;
+                            u.x = pack_bf16(__uint_as_float(a[c]), __uint_as_float(a[c + 1]));
+                            u.y = pack_bf16(__uint_as_float(a[c + 2]), __uint_as_float(a[c + 3]));
+                            u.z = pack_bf16(__uint_as_float(a[c + 4]), __uint_as_float(a[c + 5]));
+                            u.w = pack_bf16(__uint_as_float(a[c + 6]), __uint_as_float(a[c + 7]));
+                            *reinterpret_cast<uint4*>(dst_row + cb + cc + c) = u;
                         }
                     }
                 }
@@ -613,11 +610,14 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                         for (int q = 0; q < u.n_parts; ++q) {
                             const float lq = __ldcg(p.part_lse + (int64_t)(u.part_base + q) * kM + rr);
                             const float wq2 = (lq == -INFINITY) ? 0.0f : ex2(lq - M) * inv;
-                            const float4* src = reinterpret_cast<const float4*>(
-                                p.part_o + ((int64_t)(u.part_base + q) * kM + rr) * D + c0);
-                            const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
-                            acc[0] += wq2 * x0.x; acc[1] += wq2 * x0.y; acc[2] += wq2 * x0.z; acc[3] += wq2 * x0.w;
-                            acc[4] += wq2 * x1.x; acc[5] += wq2 * x1.y; acc[6] += wq2 * x1.z; acc[7] += wq2 * x1.w;
+                            const uint4 x = __ldcg(reinterpret_cast<const uint4*>(
+                                reinterpret_cast<const __nv_bfloat16*>(p.part_o) + ((int64_t)(u.part_base + q) * kM + rr) * D + c0));
+                            const uint32_t xw[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                acc[2 * e] += wq2 * __uint_as_float(xw[e] << 16);
+                                acc[2 * e + 1] += wq2 * __uint_as_float(xw[e] & 0xFFFF0000u);
+                            }
                         }
                         uint4 o;
                         o.x = pack_bf16(acc[0], acc[1]);
