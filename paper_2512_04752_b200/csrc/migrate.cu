@@ -28,6 +28,10 @@ struct LayerPtrs {
 
 // One CTA per (sample, layer, K|V). Buffer segment of (layer l, sample s):
 //   base + l * 2*Hkv*d*sum(lens) + 2*Hkv*d*prefix(lens, s) ; K first, then V, each [Hkv][len][d].
+// For one (page, head) the cache holds the page's rows contiguously ([pages][Hkv][ps][d]) and the
+// buffer holds that head's tokens contiguously, so the copy is a sequence of contiguous runs of
+// up to ps*d*2 bytes (16 KB at d = 128): all 256 threads stream 16-byte vectors of one run at a
+// time, with the index arithmetic done once per run.
 template <bool PACK>
 __global__ void __launch_bounds__(kThreads)
 kv_pack_kernel(LayerPtrs layers, int Hkv, int d, int ps, const int32_t* __restrict__ block_table, int max_pages,
@@ -35,22 +39,35 @@ kv_pack_kernel(LayerPtrs layers, int Hkv, int d, int ps, const int32_t* __restri
     const int s = blockIdx.x, l = blockIdx.y, kv = blockIdx.z;
     long long total = 0, before = 0;
     for (int i = 0; i < n; ++i) {
-        if (i < s) before += lens[i];
-        total += lens[i];
+        const int li = __ldg(lens + i);
+        if (i < s) before += li;
+        total += li;
     }
-    const int len = lens[s];
+    const int len = __ldg(lens + s);
+    if (len <= 0) return;
     const int vpr = d / 8;                                   // 16-byte vectors per token row
-    const long long seg = ((long long)l * 2 * Hkv * total + 2LL * Hkv * before + (long long)kv * Hkv * len) * vpr;
+    uint4* seg = buf + ((long long)l * 2 * Hkv * total + 2LL * Hkv * before + (long long)kv * Hkv * len) * vpr;
     uint4* cache = reinterpret_cast<uint4*>(kv ? layers.v[l] : layers.k[l]);
-    const int32_t* bt = block_table + (int64_t)rows[s] * max_pages;
-    const long long nvec = (long long)Hkv * len * vpr;
-    for (long long e = threadIdx.x; e < nvec; e += kThreads) {
-        const int c = (int)(e % vpr);
-        const long long ht = e / vpr;
-        const int t = (int)(ht % len), h = (int)(ht / len);
-        const long long co = (((long long)bt[t / ps] * Hkv + h) * ps + (t % ps)) * vpr + c;
-        if (PACK) buf[seg + e] = cache[co];
-        else cache[co] = buf[seg + e];
+    const int32_t* bt = block_table + (int64_t)__ldg(rows + s) * max_pages;
+    const int npg = (len + ps - 1) / ps;
+    for (int run = 0; run < npg * Hkv; ++run) {
+        const int pg = run / Hkv, h = run - pg * Hkv;
+        const int t0 = pg * ps;
+        const int nt = min(ps, len - t0);                     // tokens of this page in the sample
+        uint4* c = cache + (((long long)__ldg(bt + pg) * Hkv + h) * ps) * vpr;
+        uint4* bsg = seg + ((long long)h * len + t0) * vpr;
+        const int nv = nt * vpr;
+        const uint4* src = PACK ? c : bsg;
+        uint4* dst = PACK ? bsg : c;
+        for (int e0 = threadIdx.x; e0 < nv; e0 += 4 * kThreads) {   // 4 loads in flight, then 4 stores
+            uint4 x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (e0 + u * kThreads < nv) x[u] = src[e0 + u * kThreads];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (e0 + u * kThreads < nv) dst[e0 + u * kThreads] = x[u];
+        }
     }
 }
 

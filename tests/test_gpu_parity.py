@@ -279,3 +279,85 @@ def test_attention_full_config2_sampled(cuda_lib):
     og, oref, lg, lref, info = _run_attention(cuda_lib, b, samples=samples)
     mae, rel = _attn_errors(og, oref)
     assert mae <= ATOL and rel <= RTOL_L2, (mae, rel, info)
+
+
+# ------------------------------------------------------------------ full-size, bench launch configuration
+def _c3s_batch(layers=1, with_logits=True):
+    """configs[2] as bench.py runs it (c3s): B = 256 long-tail prefixes, every tree = S(n) from
+    select_strategy (host C++), MSS rejection sampling; generated on the GPU."""
+    import bench
+    cfg = CONFIGS["c3s"]
+    strat = bench.strategy_trees(cfg, cuda_lib_core())
+    return make_verify_batch(cfg, device="cuda", gen_device="cuda", layers=layers, with_logits=with_logits,
+                             parents=strat[4])
+
+
+def cuda_lib_core():
+    from paper_2512_04752_b200 import core
+    return core
+
+
+def test_attention_full_config3s_sampled(cuda_lib):
+    """Long-tail config at full size (B=256, P 512-16K, T from select_strategy) in the launch
+    configuration bench.py times; oracle on 5 sampled samples (longest included)."""
+    b = _c3s_batch(with_logits=False)
+    for k in ("q", "k_cache", "v_cache"):
+        b[k] = b[k].cpu()
+    P = b["prefix_len"]
+    samples = sorted({0, 77, 200, int(np.argmax(P)), int(np.argmin(P))})
+    og, oref, lg, lref, info = _run_attention(cuda_lib, b, samples=samples)
+    mae, rel = _attn_errors(og, oref)
+    assert mae <= ATOL and rel <= RTOL_L2, (mae, rel, info)
+
+
+def test_accept_mss_full_config3s_bit_exact(cuda_lib):
+    """MSS acceptance at full size (B=256, V=128256) through the same call the step makes; the
+    oracle (independent per sample: keyed by gid) checks 6 sampled samples bit for bit."""
+    core = cuda_lib
+    b = _c3s_batch(layers=1)
+    g = core.tree_accept(core.SAMPLE_MSS, b["logits"], _dev(b["parent"]), _dev(b["token"]), _dev(b["tree_off"]),
+                         _dev(b["gid"]), draft_probs=b["draft_probs"], temperature=1.0, seed=11, step=0)
+    g = [x.cpu().numpy() for x in g]
+    to = b["tree_off"]
+    for s in (0, 5, 99, 128, 201, 255):
+        sl = slice(int(to[s]), int(to[s + 1]))
+        lg = tensor_bf16_bits(b["logits"][sl].cpu())
+        o = OAcc.tree_accept(OAcc.MSS, lg, b["parent"][sl], b["token"][sl], np.array([0, sl.stop - sl.start]),
+                             b["gid"][s:s + 1], b["V"], draft_probs=b["draft_probs"][sl].cpu().numpy(),
+                             temperature=1.0, seed=11, step=0)
+        assert g[0][s] == o[0][0] and g[2][s] == o[2][0] and g[3][s] == o[3][0], s
+        np.testing.assert_array_equal(g[1][s], o[1][0])
+
+
+def test_accept_and_compact_full_config2_bit_exact(cuda_lib):
+    """Greedy acceptance and the KV commit of BASELINE configs[1] at full size (B=64, V=128256,
+    32 layers of 8/128 KV) as the step runs them; the oracle checks every sample's walk and the
+    compacted bytes of 4 sampled samples in every layer."""
+    core = cuda_lib
+    cfg = CONFIGS["c2"]
+    b = make_verify_batch(cfg, device="cuda", gen_device="cuda", with_logits=True)
+    g = core.tree_accept(core.GREEDY, b["logits"], _dev(b["parent"]), _dev(b["token"]), _dev(b["tree_off"]),
+                         _dev(b["gid"]))
+    acc, path = g[0], g[1]
+    o = OAcc.tree_accept(OAcc.GREEDY, tensor_bf16_bits(b["logits"].cpu()), b["parent"], b["token"], b["tree_off"],
+                         b["gid"], b["V"])
+    np.testing.assert_array_equal(acc.cpu().numpy(), o[0])
+    np.testing.assert_array_equal(path.cpu().numpy(), o[1])
+    np.testing.assert_array_equal(g[2].cpu().numpy(), o[2])
+    samples = [0, 21, 42, 63]
+    bt = b["block_table"]
+    pages = np.unique(bt[samples])
+    L = cfg.L
+    before = [tensor_bf16_bits(b[c][l].index_select(0, torch.as_tensor(pages, device="cuda").long()).cpu())
+              for c in ("k_cache", "v_cache") for l in range(L)]
+    ks = [b["k_cache"][l] for l in range(L)]
+    vs = [b["v_cache"][l] for l in range(L)]
+    new_len, _ = core.kv_compact(ks, vs, _dev(bt), _dev(b["prefix_len"]), acc, path)
+    after = [tensor_bf16_bits(b[c][l].index_select(0, torch.as_tensor(pages, device="cuda").long()).cpu())
+             for c in ("k_cache", "v_cache") for l in range(L)]
+    remap = {int(p): i for i, p in enumerate(pages)}
+    sub_bt = np.vectorize(lambda x: remap[int(x)])(bt[samples]).astype(np.int32)
+    onl, _ = OC.kv_compact(before, sub_bt, b["prefix_len"][samples], o[0][samples], o[1][samples], 64)
+    np.testing.assert_array_equal(new_len.cpu().numpy()[samples], onl)
+    for x, y in zip(after, before):
+        np.testing.assert_array_equal(x, y)
