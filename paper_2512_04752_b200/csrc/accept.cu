@@ -14,6 +14,8 @@
 //           materialised for MSS (u64 weights per token in the workspace, updated in place);
 //           bonus by inverse CDF: cluster prefix over slice totals, then tile sums + a block
 //           scan inside the owning CTA.
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 #include "sampling.cuh"
 #include "sm100_ptx.cuh"
@@ -162,6 +164,7 @@ __device__ __forceinline__ void allreduce2(unsigned long long& v0, int op0, unsi
         cluster_sync_all();
         // lane c of warp 0 fetches CTA c's pair (all remote loads in flight at once), then a
         // shuffle reduction; the result is broadcast through shared memory
+        // (a st.async push into peers' slots + transaction-count mbarrier measured no faster)
         if (w == 0) {
             const uint32_t c = (uint32_t)lane;
             unsigned long long ra = 0, rb = 0;   // identity of MAX (unsigned), SUM and OR
@@ -283,29 +286,55 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype, cons
                 best = best > k ? best : k;
             };
             if (dtype == RS_DTYPE_BF16 && logits_vec_ok) {
-                // bf16 rows: 8 x 16-byte loads in flight per thread (one memory round trip per
-                // node at the usual slice size)
+                // bf16 rows: kGreedyInflight x 16-byte loads in flight per thread. Per thread:
+                // packed bf16x2 max (__hmax2) and a packed |bits| max for the non-finite check,
+                // then the lowest index holding that max (float equality, so -0 == +0 as in the
+                // oracle's strict '>' scan); the 64-bit key is built once per thread.
                 const uint4* row = reinterpret_cast<const uint4*>(
                     reinterpret_cast<const uint16_t*>(logits) + (int64_t)(off + c) * V);
+                __nv_bfloat162 vmax = __halves2bfloat162(__ushort_as_bfloat16((unsigned short)0xFF80u),
+                                                        __ushort_as_bfloat16((unsigned short)0xFF80u));   // -inf
+                uint32_t amag = 0;
+                int first = -1;
+                float fmax_t = -INFINITY;
                 for (int i0 = vbeg + tid; i0 < vend; i0 += kGreedyInflight * kThreads) {
                     uint4 x[kGreedyInflight];
 #pragma unroll
                     for (int u = 0; u < kGreedyInflight; ++u) {
                         const int i = i0 + u * kThreads;
-                        if (i < vend) x[u] = __ldg(row + i);
+                        x[u] = (i < vend) ? __ldg(row + i) : make_uint4(0xFF7FFF7Fu, 0xFF7FFF7Fu, 0xFF7FFF7Fu, 0xFF7FFF7Fu);   // lowest finite bf16
                     }
+                    __nv_bfloat162 cm = vmax;
 #pragma unroll
                     for (int u = 0; u < kGreedyInflight; ++u) {
-                        const int i = i0 + u * kThreads;
-                        if (i < vend) {
+                        const uint32_t w[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            cm = __hmax2(cm, *reinterpret_cast<const __nv_bfloat162*>(&w[q]));
+                            amag = __vmaxu2(amag, w[q] & 0x7FFF7FFFu);
+                        }
+                    }
+                    const float chunk_max = fmaxf(__bfloat162float(cm.x), __bfloat162float(cm.y));
+                    if (chunk_max > fmax_t) {   // the new max is in this chunk: lowest index of it
+                        fmax_t = chunk_max;
+                        first = -1;
+#pragma unroll
+                        for (int u = 0; u < kGreedyInflight; ++u) {
                             const uint32_t w[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
 #pragma unroll
                             for (int j = 0; j < 8; ++j) {
-                                const uint32_t h = (j & 1) ? (w[j >> 1] & 0xFFFF0000u) : (w[j >> 1] << 16);
-                                upd(i * 8 + j, __uint_as_float(h));
+                                const float h = __uint_as_float((j & 1) ? (w[j >> 1] & 0xFFFF0000u) : (w[j >> 1] << 16));
+                                if (first < 0 && h == chunk_max) first = (i0 + u * kThreads) * 8 + j;
                             }
                         }
                     }
+                    vmax = cm;
+                }
+                // bf16 magnitude bits >= 0x7F80 <=> inf or NaN (padding loads are the lowest finite value)
+                bad = ((amag & 0xFFFFu) >= 0x7F80u || (amag >> 16) >= 0x7F80u) ? 1ull : 0ull;
+                if (first >= 0) {
+                    const float mcan = fmax_t == 0.0f ? 0.0f : fmax_t;   // -0 -> +0: ties by index
+                    best = ((unsigned long long)fkey(mcan) << 32) | (uint32_t)(~(uint32_t)first);
                 }
             } else {
                 for_slice<2>(lv, qv, false, vbeg, vend, [&](int v, float x, float) { upd(v, x); });

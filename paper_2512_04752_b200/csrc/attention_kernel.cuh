@@ -702,7 +702,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->s_free[grp]);
-                if (warp_active) {
+                if (warp_active && !(p.dbg & 16)) {   // (dbg 16: skip softmax math, measurement only)
                     const int kh = (lane & 16) ? 32 : 0;   // first key of my half
                     float mx8[8];
 #pragma unroll

@@ -361,3 +361,24 @@ def test_accept_and_compact_full_config2_bit_exact(cuda_lib):
     np.testing.assert_array_equal(new_len.cpu().numpy()[samples], onl)
     for x, y in zip(after, before):
         np.testing.assert_array_equal(x, y)
+
+
+def test_accept_greedy_signed_zero_tie(cuda_lib):
+    """-0 and +0 are equal logits: the oracle's strict '>' scan keeps the lower vocab id, and so
+    must the GPU's packed max + first-index search (Z6)."""
+    core = cuda_lib
+    V = 4096
+    lg = torch.full((3, V), -1.0, dtype=torch.bfloat16)
+    lg[0, 100] = -0.0
+    lg[0, 3000] = 0.0          # equal to the max, higher id
+    lg[1, 7] = 0.0
+    lg[1, 5] = -0.0            # lower id wins again
+    parent = np.array([-1, 0, 0], np.int32)
+    token = np.array([0, 3000, 100], np.int32)   # child 2 carries the winning token 100
+    tree_off = np.array([0, 3], np.int32)
+    gid = np.array([5], np.int64)
+    g = core.tree_accept(core.GREEDY, lg.cuda(), _dev(parent), _dev(token), _dev(tree_off), _dev(gid))
+    o = OAcc.tree_accept(OAcc.GREEDY, tensor_bf16_bits(lg), parent, token, tree_off, gid, V)
+    assert int(o[0][0]) == 1 and int(o[1][0][1]) == 2
+    for x, y in zip(g, o):
+        np.testing.assert_array_equal(x.cpu().numpy(), y)
