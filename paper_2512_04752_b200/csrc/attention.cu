@@ -5,18 +5,15 @@
 // T_b*g (node, head-in-group) pairs, node-major, padded to 128 (UMMA M = 128). Keys are the
 // sample's logical slots 0..P_b+T_b-1 in 64-key blocks = one KV page each.
 //
-// Persistent kernel, one CTA per SM (grid = plan.n_ctas), warp-specialised:
-//   warp 0      TMA producer: Q tile (3-D tensor map, 2 buffers), per block one K and one V
-//               page tile (2-D tensor map over [pages*Hkv*64, D], SWIZZLE_128B), 4-stage ring.
-//   warp 1      MMA issuer (one thread): S_j = Q K_j^T -> TMEM (2 buffers, 64 fp32 columns);
-//               O += P_j V_j -> TMEM (D fp32 columns), tcgen05.mma kind::f16, M=128.
-//   warp 2      TMEM allocator.
-//   warps 4..7  softmax + epilogue, one query row per thread: tcgen05.ld S, ancestor mask,
-//               online softmax in the exp2 domain with lazy (threshold 2^8) rescaling of O in
-//               TMEM, P (bf16) -> shared memory in the UMMA K-major SW128 layout, final
-//               normalisation and store (or a split-KV partial + combine kernel).
-// The schedule (which units/key ranges each CTA processes, split-KV cuts for load balance)
-// is built on the host by rs_attn_plan_create from the step's lengths and reused by all layers.
+// Persistent kernel, one CTA per SM (grid = plan.n_ctas), warp-specialised (attention_kernel.cuh
+// has the roles): TMA producers for Q/K and V, an S = Q K^T issuer and an O += P V issuer
+// (tcgen05.mma, accumulators in TMEM), two softmax warpgroups taking alternate key blocks, and
+// for plans whose tiles all have T*g <= 64 an epilogue warpgroup with items alternating between
+// the two 16-lane halves of TMEM so one item's epilogue overlaps the next item's blocks.
+// The schedule is built on the host by rs_attn_plan_create from the step's lengths and reused by
+// all layers: unit groups (sample, kv head) with M query tiles run as gangs of M CTAs over the
+// same key blocks (L2 reuse), balanced contiguous fill with split-KV cuts, merged in-kernel by the
+// last CTA of a unit. Consecutive layers are chained with programmatic dependent launch.
 #include <cuda.h>
 #include <cuda_bf16.h>
 

@@ -6,18 +6,20 @@
 // the T_b*g (node, head-in-group) pairs, node-major, padded to 128 (UMMA M = 128); keys are the
 // sample's logical slots in 64-key blocks = one KV page each.
 //
-// Persistent kernel, one CTA per SM, 12 warps, warp-specialised:
-//   warp 0        TMA producer for Q (3-D map, 2 buffers) and K pages (4-slot ring)
-//   warp 3        TMA producer for V pages (6-slot ring; V lives longer than K)
-//   warp 1        MMA issuer, one thread, non-blocking: S_J = Q K_J^T (SS, M=128, N=64, K=D)
-//                 into S[J&1]; O[J&1] += P_J V_J (TS: P from TMEM, V MN-major, N=D)
-//   warp 2        TMEM allocator (512 columns)
-//   warps 4..7    softmax warpgroup 0: blocks with even J      (one query row per thread)
-//   warps 8..11   softmax warpgroup 1: blocks with odd J
+// Persistent kernel, one CTA per SM, warp-specialised:
+//   warp 0        TMA producer for Q tiles and K pages (ring of KS slots); in dynamic mode also
+//                 takes items from the global queue
+//   warp 3        TMA producer for V pages (ring of VS slots)
+//   warp 1        S issuer: S_J = Q K_J^T (SS, M=128, N=64, K=D) into S[J&1]
+//   warp 2        TMEM allocator + PV issuer: O[J&1] += P_J V_J (TS: P from TMEM, V MN-major)
+//   warps 4..7    softmax warpgroup 0: blocks with even J      (rows of a tile: one per thread,
+//   warps 8..11   softmax warpgroup 1: blocks with odd J        or two per thread when R = 16)
+//   warps 12..15  (RM = 1 only) epilogue warpgroup: merge, normalise and store item i while the
+//                 softmax warpgroups run item i+1 in the other 16-lane half of TMEM
 // Each softmax warpgroup keeps its own running max/sum and its own O accumulator in TMEM, so
 // the two run concurrently on alternate key blocks with no per-block synchronisation; the two
-// partial states are merged in the epilogue (exchange of (m, l) through TMEM columns).
-// Online softmax in the exp2 domain with lazy rescaling (threshold 2^8) of O in TMEM.
+// partial states are merged in the epilogue. Online softmax in the exp2 domain with lazy
+// rescaling (threshold 2^8) of O in TMEM.
 #pragma once
 
 #include <cuda.h>
