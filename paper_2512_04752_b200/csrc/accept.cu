@@ -2,8 +2,8 @@
 //
 // One thread-block CLUSTER per sample walks its tree from the root. The vocabulary is split
 // into contiguous slices, one per CTA of the cluster; only the rows of the nodes on the walk
-// are read (the algorithmic bytes are the visited rows), with 128-bit loads,
-// four in flight per thread. Every reduction (argmax, max, integer sums, 128-bit max) is done
+// are read (the algorithmic bytes are the visited rows), with 128-bit loads
+// (greedy: the whole slice in flight at once, eight 16-byte loads per thread). Every reduction (argmax, max, integer sums, 128-bit max) is done
 // per CTA with warp shuffles + shared memory and then all-reduced across the cluster through
 // distributed shared memory, so every CTA takes the same decision; the walk itself (child
 // tests, residual bookkeeping) is replicated.
@@ -11,10 +11,14 @@
 //           bonus = argmax at the last node.
 //   DELTA / MSS: integer weights w_v (exp_spec), Philox uniforms, 128-bit exact tests; the
 //           residual after a rejection is kept implicitly for DELTA (excluded-token list) and
-//           materialised for MSS (u64 weights per token in the workspace, updated in place);
-//           bonus by inverse CDF: cluster prefix over slice totals, then tile sums + a block
-//           scan inside the owning CTA.
+//           materialised for MSS after the first rejection (u32 per token in the workspace,
+//           updated in place; before it the weights are recomputed from the logits); every
+//           pass that defines the current weights leaves per-tile sums in shared memory, so
+//           the bonus (inverse CDF: cluster prefix over slice totals, the tile, then a block
+//           scan inside the owning CTA) needs no extra pass.
 #include <cuda_bf16.h>
+
+#include <cstdlib>
 
 #include "common.cuh"
 #include "sampling.cuh"
@@ -29,8 +33,17 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kTileVecs = kThreads;        // 8-element vectors per inverse-CDF tile
 constexpr int kMaxTiles = 256;             // tiles per CTA slice
 constexpr int kMaxCluster = 8;
+#ifndef RS_ACC_RES_UNROLL
+#define RS_ACC_RES_UNROLL 1
+#endif
+constexpr int kResUnroll = RS_ACC_RES_UNROLL;
+#ifndef RS_ACC_P2_UNROLL
+#define RS_ACC_P2_UNROLL 2
+#endif
+constexpr int kP2Unroll = RS_ACC_P2_UNROLL;   // vectors in flight per thread in the MSS weight-sum pass
+//   // vectors in flight per thread in the MSS residual passes
 #ifndef RS_ACC_INFLIGHT
-#define RS_ACC_INFLIGHT 4
+#define RS_ACC_INFLIGHT 8
 #endif
 constexpr int kGreedyInflight = RS_ACC_INFLIGHT;   // 16-byte loads in flight per thread (greedy, bf16)
 
@@ -55,7 +68,9 @@ __device__ __forceinline__ Raw8 load_raw(const RowView& rv, int i) {
             r.a = __ldg(reinterpret_cast<const uint4*>(p));
         } else {
             uint32_t w[4] = {0, 0, 0, 0};
-            for (int j = 0; j < 8 && v0 + j < rv.V; ++j) w[j >> 1] |= (uint32_t)__ldg(p + j) << (16 * (j & 1));
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (v0 + j < rv.V) w[j >> 1] |= (uint32_t)__ldg(p + j) << (16 * (j & 1));
             r.a = make_uint4(w[0], w[1], w[2], w[3]);
         }
         r.b = make_uint4(0, 0, 0, 0);
@@ -66,7 +81,9 @@ __device__ __forceinline__ Raw8 load_raw(const RowView& rv, int i) {
             r.b = __ldg(reinterpret_cast<const uint4*>(p) + 1);
         } else {
             uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int j = 0; j < 8 && v0 + j < rv.V; ++j) w[j] = __float_as_uint(__ldg(p + j));
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (v0 + j < rv.V) w[j] = __float_as_uint(__ldg(p + j));
             r.a = make_uint4(w[0], w[1], w[2], w[3]);
             r.b = make_uint4(w[4], w[5], w[6], w[7]);
         }
@@ -225,6 +242,100 @@ __device__ __forceinline__ uint64_t delta_weight(uint64_t w, int tok, const Smem
     return w;
 }
 
+// Warp-reduce a per-vector weight sum and add it to the CTA's inverse-CDF tile sum (the 32
+// lanes of a warp always hold vectors of the same tile: tiles are kThreads vectors).
+__device__ __forceinline__ void tile_add(Smem& sm, int tile, unsigned long long s8) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s8 += __shfl_xor_sync(0xffffffffu, s8, o);
+    if ((threadIdx.x & 31) == 0 && s8) atomicAdd(&sm.tile_sum[tile], s8);
+}
+
+__device__ __forceinline__ void clear_tiles(Smem& sm) {
+    for (int k = threadIdx.x; k < kMaxTiles; k += kThreads) sm.tile_sum[k] = 0ull;
+    __syncthreads();
+}
+
+// MSS residual weights of 8 tokens, stored u32 (a residual is shifted so its max has <= 32
+// bits); rows are padded to a multiple of 8 tokens.
+struct W8 {
+    uint4 a, b;
+};
+__device__ __forceinline__ W8 load_w8(const uint32_t* wrow, int i) {
+    const uint4* p = reinterpret_cast<const uint4*>(wrow) + 2 * (int64_t)i;
+    return W8{__ldcg(p), __ldcg(p + 1)};
+}
+__device__ __forceinline__ uint32_t w8_elem(const W8& w, int j) {
+    return j == 0 ? w.a.x : j == 1 ? w.a.y : j == 2 ? w.a.z : j == 3 ? w.a.w
+         : j == 4 ? w.b.x : j == 5 ? w.b.y : j == 6 ? w.b.z : w.b.w;
+}
+
+// Bonus draw by inverse CDF over the current weights of the node (DESIGN.md "Bit-exact
+// sampling"): the smallest token v with sum_{j<=v} w_j > t. The per-tile sums of this CTA's
+// slice are current in sm.tile_sum; a cluster prefix of slice totals finds the owning CTA,
+// its tile sums the tile, and a block scan over weights8(i, w8) (the 8 weights of vector i)
+// the token. Sets `owner` (the CTA whose result is the bonus) and returns its token.
+template <typename F>
+__device__ __forceinline__ int draw_bonus(Smem& sm, int& phase, uint64_t t, int vbeg, int vend, int V, bool& owner,
+                                          F weights8) {
+    const int tid = threadIdx.x;
+    const uint32_t cs = cluster_size(), crank = cluster_rank();
+    const int ntiles = (vend - vbeg + kTileVecs - 1) / kTileVecs;
+    __syncthreads();
+    unsigned long long slice_total = 0;
+    for (int k = 0; k < ntiles; ++k) slice_total += sm.tile_sum[k];
+    unsigned long long before = 0;
+    if (cs > 1) {
+        if (tid == 0) sm.xch[phase][0] = slice_total;
+        cluster_sync_all();
+        for (uint32_t r = 0; r < crank; ++r) before += ld_dsmem_u64(&sm.xch[phase][0], r);
+        phase ^= 1;
+    }
+    owner = slice_total > 0 && before <= t && t < before + slice_total;
+    if (!owner) return -1;
+    if (tid == 0) {
+        unsigned long long run = before;
+        int tile = ntiles - 1;
+        for (int k = 0; k < ntiles; ++k) {
+            if (run + sm.tile_sum[k] > t) { tile = k; break; }
+            run += sm.tile_sum[k];
+        }
+        sm.bcast_i = tile;
+        sm.bcast_u = run;
+        sm.bonus_v = V - 1;
+    }
+    __syncthreads();
+    const int i = vbeg + sm.bcast_i * kTileVecs + tid;
+    const unsigned long long tbase = sm.bcast_u;
+    uint64_t w8[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) w8[j] = 0;
+    if (i < vend) weights8(i, w8);
+    unsigned long long s8 = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s8 += w8[j];
+    unsigned long long incl = s8;
+    const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) sm.scan[wid] = incl;
+    __syncthreads();
+    unsigned long long wbase = tbase;
+    for (int k = 0; k < wid; ++k) wbase += sm.scan[k];
+    const unsigned long long excl = wbase + incl - s8;
+    if (s8 && excl <= t && t < excl + s8) {
+        unsigned long long accum = excl;
+        for (int j = 0; j < 8; ++j) {
+            accum += w8[j];
+            if (accum > t) { sm.bonus_v = i * 8 + j; break; }
+        }
+    }
+    __syncthreads();
+    return sm.bonus_v;
+}
+
 // MODE is a template parameter so the greedy walk compiles without the 128-bit sampling
 // machinery (register budget: 4 CTAs/SM greedy, 2 CTAs/SM sampling).
 template <int MODE>
@@ -234,7 +345,7 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype, cons
                    const int32_t* __restrict__ tree_off, const int64_t* __restrict__ gid, int V, float inv_tau,
                    uint64_t seed, uint64_t step, int32_t* __restrict__ acc_out, int32_t* __restrict__ path_out,
                    int32_t* __restrict__ bonus_out, int32_t* __restrict__ flags_out, bool logits_vec_ok,
-                   bool draft_vec_ok, uint64_t* __restrict__ wbuf) {
+                   bool draft_vec_ok, uint32_t* __restrict__ wbuf, int prefetch_children) {
     (void)mode_rt;
     constexpr int mode = MODE;
     __shared__ Smem sm;
@@ -248,21 +359,18 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype, cons
     int32_t* pth = path_out + (int64_t)b * RS_MAX_TREE;
     int phase = 0;
     if (leader && tid < RS_MAX_TREE) pth[tid] = -1;
-    if (tid == 0) {
-        bool ok = (T >= 1 && T <= RS_MAX_TREE);
-        if (ok) ok = parent[off] == -1;
-        for (int i = 1; ok && i < T; ++i) {
-            const int pp = parent[off + i];
-            ok = (pp >= 0 && pp < i);
-        }
-        sm.flag = ok ? 0 : RS_FLAG_MALFORMED;
+    // tree check in parallel: node i needs parent[i] in [0, i) (root: -1)
+    bool bad_node = !(T >= 1 && T <= RS_MAX_TREE);
+    if (!bad_node && tid < T) {
+        const int pp = parent[off + tid];
+        sm.parent[tid] = pp;
+        sm.token[tid] = token[off + tid];
+        bad_node = tid == 0 ? pp != -1 : !(pp >= 0 && pp < tid);
     }
-    __syncthreads();
-    if (sm.flag) {
+    if (__syncthreads_or(bad_node)) {
         if (leader && tid == 0) { acc_out[b] = 0; bonus_out[b] = -1; flags_out[b] = RS_FLAG_MALFORMED; }
         return;   // uniform across the cluster: no cluster barrier is reached
     }
-    if (tid < T) { sm.parent[tid] = parent[off + tid]; sm.token[tid] = token[off + tid]; }
     const int64_t g = gid[b];
     const int nvec = (V + 7) / 8;
     const int per = (nvec + (int)cs - 1) / (int)cs;
@@ -292,6 +400,10 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype, cons
                 // oracle's strict '>' scan); the 64-bit key is built once per thread.
                 const uint4* row = reinterpret_cast<const uint4*>(
                     reinterpret_cast<const uint16_t*>(logits) + (int64_t)(off + c) * V);
+                // warm L2 with this CTA's slice of every child's row while row c streams: the
+                // next row of the walk is one of them (speculative reads of the siblings)
+                if (prefetch_children && tid > c && tid < T && sm.parent[tid] == c && vend > vbeg)
+                    bulk_prefetch_l2(row + (int64_t)(tid - c) * (V / 8) + vbeg, (uint32_t)(vend - vbeg) * 16u);
                 __nv_bfloat162 vmax = __halves2bfloat162(__ushort_as_bfloat16((unsigned short)0xFF80u),
                                                         __ushort_as_bfloat16((unsigned short)0xFF80u));   // -inf
                 uint32_t amag = 0;
@@ -345,7 +457,7 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype, cons
             for (int x = c + 1; x < T; ++x)
                 if (sm.parent[x] == c && sm.token[x] == am) { next = x; break; }
             if (next < 0) { bonus = am; stop = true; }
-        } else {
+        } else if (mode == RS_ACCEPT_SAMPLE_MSS) {
             // pass 1: row max (+ non-finite check)
             unsigned long long mk = 0, bad = 0;
             for_slice(lv, qv, false, vbeg, vend, [&](int, float x, float) {
@@ -356,23 +468,195 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype, cons
             allreduce2(mk, OP_MAX, bad, OP_OR, sm, phase);
             if (bad) { flags |= RS_FLAG_NONFINITE; break; }
             const float m = fkey_inv((uint32_t)mk);
-            // pass 2: Z = sum w, Zq = sum qw
-            constexpr bool mss = mode == RS_ACCEPT_SAMPLE_MSS;
+            // The weights of node c are implicit (w_v recomputed from the logits) until a
+            // rejection changes them; from then on the residual lives in wrow (u32 per token).
+            // Every pass that defines the current weights also leaves their per-tile sums in
+            // shared memory, so the bonus draw needs no extra pass.
+            const int Vp = (V + 7) & ~7;
+            uint32_t* wrow = wbuf + (int64_t)b * Vp;
+            bool resid = false;
+            // pass 2: Z = sum w, Zq = sum qw (+ tile sums of w)
             unsigned long long zs = 0, zq = 0;
-            // MSS: the current (residual) weights live in wbuf[b][V] (workspace), so residual
-            // passes read one u64 per token instead of re-deriving it from the logits
-            uint64_t* wrow = mss ? wbuf + (int64_t)b * V : nullptr;
-            for_slice<mss ? 2 : 4>(lv, qv, mss, vbeg, vend, [&](int v, float x, float q) {
-                const uint64_t w = rs::target_weight(x, m, inv_tau);
-                zs += w;
-                if (mss) {
-                    zq += rs::draft_weight(q);
-                    wrow[v] = w;
+            clear_tiles(sm);
+            for (int base = vbeg; base < vend; base += kP2Unroll * kThreads) {
+                Raw8 x[kP2Unroll], q[kP2Unroll];
+#pragma unroll
+                for (int u = 0; u < kP2Unroll; ++u) {
+                    const int i = base + u * kThreads + tid;
+                    if (i < vend) { x[u] = load_raw(lv, i); q[u] = load_raw(qv, i); }
                 }
-            });
+#pragma unroll
+                for (int u = 0; u < kP2Unroll; ++u) {
+                    const int i = base + u * kThreads + tid;
+                    unsigned long long s8 = 0;
+                    if (i < vend) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            if (i * 8 + j < V) {
+                                s8 += rs::target_weight(raw_elem(x[u], dtype, j), m, inv_tau);
+                                zq += rs::draft_weight(raw_elem(q[u], RS_DTYPE_F32, j));
+                            }
+                        }
+                    }
+                    zs += s8;
+                    tile_add(sm, (base - vbeg) / kThreads + u, s8);
+                }
+            }
             allreduce2(zs, OP_SUM, zq, OP_SUM, sm, phase);
             uint64_t Z = zs;
-            const uint64_t Zq = mss ? zq : 0ull;
+            const uint64_t Zq = zq;
+            // r_v = max(prev_v * Zq - qw_v * Z, 0) for token j of vector i
+            auto residual1 = [&](int i, int j, const Raw8& x, const W8& w, const Raw8& q) -> u128 {
+                if (i * 8 + j >= V) return 0;
+                const uint64_t prev = resid ? (uint64_t)w8_elem(w, j)
+                                            : rs::target_weight(raw_elem(x, dtype, j), m, inv_tau);
+                const u128 lhs = (u128)prev * Zq;
+                const u128 rhs = (u128)rs::draft_weight(raw_elem(q, RS_DTYPE_F32, j)) * Z;
+                return lhs > rhs ? lhs - rhs : 0;
+            };
+            int rank = 0;
+            for (int x = c + 1; x < T && next < 0; ++x) {
+                if (sm.parent[x] != c) continue;
+                const int tk = sm.token[x];
+                if (tid == 0) {
+                    const int64_t ro = (int64_t)(off + c) * V + tk;
+                    const float l = (dtype == RS_DTYPE_BF16)
+                                        ? rs::bf16_bits_to_f32(reinterpret_cast<const uint16_t*>(logits)[ro])
+                                        : reinterpret_cast<const float*>(logits)[ro];
+                    const uint64_t qw = rs::draft_weight(draft[ro]);
+                    const uint64_t wt = resid ? (uint64_t)__ldcg(wrow + tk) : rs::target_weight(l, m, inv_tau);
+                    const uint32_t U = rs::uniform_word(seed, step, g, (uint32_t)rank, (uint32_t)c);
+                    const bool acc = qw == 0 ? wt > 0 : ((u128)U * ((u128)qw * Z)) < (((u128)wt * Zq) << 32);
+                    sm.bcast_i = acc ? 1 : 0;
+                }
+                __syncthreads();
+                const bool accepted = sm.bcast_i != 0;
+                __syncthreads();
+                if (accepted) { next = x; break; }
+                ++rank;
+                // residual: pass A = its max (the shift), pass B = shifted values written back
+                // (u32) with their sums. An all-zero residual (max 0, quantisation only) keeps
+                // the pre-rejection weights.
+                u128 rmax = 0;
+                for (int base = vbeg; base < vend; base += kResUnroll * kThreads) {
+                    Raw8 xs[kResUnroll], qs[kResUnroll];
+                    W8 ws[kResUnroll];
+#pragma unroll
+                    for (int u = 0; u < kResUnroll; ++u) {
+                        const int i = base + u * kThreads + tid;
+                        if (i < vend) {
+                            if (resid) ws[u] = load_w8(wrow, i); else xs[u] = load_raw(lv, i);
+                            qs[u] = load_raw(qv, i);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < kResUnroll; ++u) {
+                        const int i = base + u * kThreads + tid;
+                        if (i < vend) {
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                const u128 r = residual1(i, j, xs[u], ws[u], qs[u]);
+                                rmax = r > rmax ? r : rmax;
+                            }
+                        }
+                    }
+                }
+                const u128 mxr = allreduce_max128(rmax, sm, phase);
+                if (mxr != 0) {
+                    int sh = rs::bitlen128(mxr) - 32;
+                    if (sh < 0) sh = 0;
+                    unsigned long long zn = 0, dummy = 0;
+                    clear_tiles(sm);
+                    for (int base = vbeg; base < vend; base += kResUnroll * kThreads) {
+                        Raw8 xs[kResUnroll], qs[kResUnroll];
+                        W8 ws[kResUnroll];
+#pragma unroll
+                        for (int u = 0; u < kResUnroll; ++u) {
+                            const int i = base + u * kThreads + tid;
+                            if (i < vend) {
+                                if (resid) ws[u] = load_w8(wrow, i); else xs[u] = load_raw(lv, i);
+                                qs[u] = load_raw(qv, i);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < kResUnroll; ++u) {
+                            const int i = base + u * kThreads + tid;
+                            unsigned long long s8 = 0;
+                            if (i < vend) {
+                                uint32_t wn[8];
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) {
+                                    wn[j] = (uint32_t)(residual1(i, j, xs[u], ws[u], qs[u]) >> sh);
+                                    s8 += wn[j];
+                                }
+                                uint4* p = reinterpret_cast<uint4*>(wrow) + 2 * (int64_t)i;
+                                __stcg(p, make_uint4(wn[0], wn[1], wn[2], wn[3]));
+                                __stcg(p + 1, make_uint4(wn[4], wn[5], wn[6], wn[7]));
+                            }
+                            zn += s8;
+                            tile_add(sm, (base - vbeg) / kThreads + u, s8);
+                        }
+                    }
+                    resid = true;
+                    allreduce2(zn, OP_SUM, dummy, OP_OR, sm, phase);   // (cluster barrier: the
+                    Z = zn;                                             //  new weights are visible)
+                }
+                __syncthreads();
+            }
+            if (next < 0) {
+                const uint32_t U2 = rs::uniform_word(seed, step, g, 0xFFFFFFFFu, (uint32_t)c);
+                const uint64_t t = (uint64_t)(((u128)U2 * Z) >> 32);
+                bonus = draw_bonus(sm, phase, t, vbeg, vend, V, bonus_mine, [&](int i, uint64_t w8[8]) {
+                    if (resid) {
+                        const W8 w = load_w8(wrow, i);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) w8[j] = (i * 8 + j < V) ? w8_elem(w, j) : 0u;
+                    } else {
+                        const Raw8 xr = load_raw(lv, i);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            w8[j] = (i * 8 + j < V) ? rs::target_weight(raw_elem(xr, dtype, j), m, inv_tau) : 0ull;
+                    }
+                });
+                stop = true;
+            }
+        } else {
+            // DELTA: the residual after rejecting child x is the current weights with w_x = 0
+            // (an excluded-token list), so no pass is needed per rejection.
+            unsigned long long mk = 0, bad = 0;
+            for_slice(lv, qv, false, vbeg, vend, [&](int, float x, float) {
+                bad |= isfinite(x) ? 0ull : 1ull;
+                const unsigned long long k = fkey(x);
+                mk = mk > k ? mk : k;
+            });
+            allreduce2(mk, OP_MAX, bad, OP_OR, sm, phase);
+            if (bad) { flags |= RS_FLAG_NONFINITE; break; }
+            const float m = fkey_inv((uint32_t)mk);
+            // pass 2: Z = sum w (+ tile sums of w)
+            unsigned long long zs = 0, dummy = 0;
+            clear_tiles(sm);
+            for (int base = vbeg; base < vend; base += 4 * kThreads) {
+                Raw8 x[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = base + u * kThreads + tid;
+                    if (i < vend) x[u] = load_raw(lv, i);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = base + u * kThreads + tid;
+                    unsigned long long s8 = 0;
+                    if (i < vend) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            if (i * 8 + j < V) s8 += rs::target_weight(raw_elem(x[u], dtype, j), m, inv_tau);
+                    }
+                    zs += s8;
+                    tile_add(sm, (base - vbeg) / kThreads + u, s8);
+                }
+            }
+            allreduce2(zs, OP_SUM, dummy, OP_OR, sm, phase);
+            uint64_t Z = zs;
             if (tid == 0) sm.n_excluded = 0;
             __syncthreads();
             int rank = 0;
@@ -384,19 +668,17 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype, cons
                     const float l = (dtype == RS_DTYPE_BF16)
                                         ? rs::bf16_bits_to_f32(reinterpret_cast<const uint16_t*>(logits)[ro])
                                         : reinterpret_cast<const float*>(logits)[ro];
-                    const uint64_t qw = mss ? rs::draft_weight(draft[ro]) : 0ull;
-                    const uint64_t wt = mss ? __ldcg(wrow + tk)
-                                            : delta_weight(rs::target_weight(l, m, inv_tau), tk, sm);
+                    const uint64_t wt = delta_weight(rs::target_weight(l, m, inv_tau), tk, sm);
                     const uint32_t U = rs::uniform_word(seed, step, g, (uint32_t)rank, (uint32_t)c);
-                    bool acc;
-                    if (mode == RS_ACCEPT_SAMPLE_DELTA)
-                        acc = ((u128)U * Z) < ((u128)wt << 32);
-                    else if (qw == 0)
-                        acc = wt > 0;
-                    else
-                        acc = ((u128)U * ((u128)qw * Z)) < (((u128)wt * Zq) << 32);
+                    const bool acc = ((u128)U * Z) < ((u128)wt << 32);
                     sm.bcast_i = acc ? 1 : 0;
                     sm.bcast_u = wt;
+                    if (!acc) {
+                        // the rejected token leaves the residual: its weight leaves its tile
+                        const int ti = tk / 8;
+                        if (wt && ti >= vbeg && ti < vend) sm.tile_sum[(ti - vbeg) / kTileVecs] -= wt;
+                        sm.excluded[sm.n_excluded++] = tk;
+                    }
                 }
                 __syncthreads();
                 const bool accepted = sm.bcast_i != 0;
@@ -404,144 +686,19 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype, cons
                 __syncthreads();
                 if (accepted) { next = x; break; }
                 ++rank;
-                if (mode == RS_ACCEPT_SAMPLE_DELTA) {
-                    Z -= wt;
-                    if (tid == 0) sm.excluded[sm.n_excluded++] = tk;
-                    __syncthreads();
-                } else {
-                    // residual r_v = max(w_v*Zq - qw_v*Z, 0): cluster max, then shifted sum,
-                    // written back in place. zn = 0 <=> max r = 0 (the shift keeps the max
-                    // >= 2^31), so an all-zero residual is known after the first pass and the
-                    // pre-rejection weights are simply kept.
-                    u128 rmax = 0;
-                    for (int i = vbeg * 8 + tid; i < min(V, vend * 8); i += kThreads) {
-                        const uint64_t qw = rs::draft_weight(__ldg(draft + (int64_t)(off + c) * V + i));
-                        const u128 lhs = (u128)__ldcg(wrow + i) * Zq, rhs = (u128)qw * Z;
-                        const u128 r = lhs > rhs ? lhs - rhs : 0;
-                        if (r > rmax) rmax = r;
-                    }
-                    const u128 mxr = allreduce_max128(rmax, sm, phase);
-                    if (mxr != 0) {
-                        int s = rs::bitlen128(mxr) - 32;
-                        if (s < 0) s = 0;
-                        unsigned long long zn = 0, dummy = 0;
-                        for (int i = vbeg * 8 + tid; i < min(V, vend * 8); i += kThreads) {
-                            const uint64_t qw = rs::draft_weight(__ldg(draft + (int64_t)(off + c) * V + i));
-                            const u128 lhs = (u128)__ldcg(wrow + i) * Zq, rhs = (u128)qw * Z;
-                            const u128 r = lhs > rhs ? lhs - rhs : 0;
-                            const uint64_t wn = (uint64_t)(r >> s);
-                            wrow[i] = wn;
-                            zn += wn;
-                        }
-                        allreduce2(zn, OP_SUM, dummy, OP_OR, sm, phase);   // (cluster barrier: the
-                        Z = zn;                                             //  new weights are visible)
-                    }
-                    __syncthreads();
-                }
+                Z -= wt;
             }
             if (next < 0) {
-                // bonus ~ current residual: t = (U' * Z) >> 32, smallest v with cumsum > t.
-                // (1) per-tile sums of this CTA's slice; (2) cluster prefix of slice totals finds
-                // the owning CTA; (3) it locates the tile, then the element by a block scan.
                 const uint32_t U2 = rs::uniform_word(seed, step, g, 0xFFFFFFFFu, (uint32_t)c);
                 const uint64_t t = (uint64_t)(((u128)U2 * Z) >> 32);
-                const int ntiles = (vend - vbeg + kTileVecs - 1) / kTileVecs;
-                for (int k = tid; k < kMaxTiles; k += kThreads) sm.tile_sum[k] = 0ull;
-                __syncthreads();
-                for (int tile = 0; tile < ntiles; ++tile) {
-                    const int i = vbeg + tile * kTileVecs + tid;
-                    unsigned long long s8 = 0;
-                    if (i < vend) {
-                        if (mss) {
+                bonus = draw_bonus(sm, phase, t, vbeg, vend, V, bonus_mine, [&](int i, uint64_t w8[8]) {
+                    const Raw8 xr = load_raw(lv, i);
 #pragma unroll
-                            for (int j = 0; j < 8; ++j) {
-                                const int v = i * 8 + j;
-                                if (v < V) s8 += __ldcg(wrow + v);
-                            }
-                        } else {
-                            const Raw8 xr = load_raw(lv, i);
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) {
-                                const int v = i * 8 + j;
-                                if (v < V)
-                                    s8 += delta_weight(rs::target_weight(raw_elem(xr, dtype, j), m, inv_tau), v, sm);
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int o = 16; o; o >>= 1) s8 += __shfl_xor_sync(0xffffffffu, s8, o);
-                    if ((tid & 31) == 0 && s8) atomicAdd(&sm.tile_sum[tile], s8);
-                }
-                __syncthreads();
-                unsigned long long slice_total = 0;
-                for (int k = 0; k < ntiles; ++k) slice_total += sm.tile_sum[k];
-                // exclusive prefix of slice totals over the cluster (every CTA computes all)
-                unsigned long long before = 0;
-                if (cs > 1) {
-                    if (tid == 0) sm.xch[phase][0] = slice_total;
-                    cluster_sync_all();
-                    for (uint32_t r = 0; r < crank; ++r) before += ld_dsmem_u64(&sm.xch[phase][0], r);
-                    phase ^= 1;
-                }
-                const bool owner = slice_total > 0 && before <= t && t < before + slice_total;
-                bonus_mine = owner;
-                if (owner) {
-                    if (tid == 0) {
-                        unsigned long long run = before;
-                        int tile = ntiles - 1;
-                        for (int k = 0; k < ntiles; ++k) {
-                            if (run + sm.tile_sum[k] > t) { tile = k; break; }
-                            run += sm.tile_sum[k];
-                        }
-                        sm.bcast_i = tile;
-                        sm.bcast_u = run;
-                        sm.bonus_v = V - 1;
-                    }
-                    __syncthreads();
-                    const int tile = sm.bcast_i;
-                    const unsigned long long base = sm.bcast_u;
-                    const int i = vbeg + tile * kTileVecs + tid;
-                    uint64_t w8[8];
-                    unsigned long long s8 = 0;
-                    if (i < vend) {
-                        Raw8 xr;
-                        if (!mss) xr = load_raw(lv, i);
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            w8[j] = 0;
-                            const int v = i * 8 + j;
-                            if (v < V) {
-                                w8[j] = mss ? __ldcg(wrow + v)
-                                            : delta_weight(rs::target_weight(raw_elem(xr, dtype, j), m, inv_tau), v, sm);
-                                s8 += w8[j];
-                            }
-                        }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) w8[j] = 0;
-                    }
-                    unsigned long long incl = s8;
-                    const int lane = tid & 31, wid = tid >> 5;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
-                        if (lane >= o) incl += y;
-                    }
-                    if (lane == 31) sm.scan[wid] = incl;
-                    __syncthreads();
-                    unsigned long long wbase = base;
-                    for (int k = 0; k < wid; ++k) wbase += sm.scan[k];
-                    const unsigned long long excl = wbase + incl - s8;
-                    if (s8 && excl <= t && t < excl + s8) {
-                        unsigned long long accum = excl;
-                        for (int j = 0; j < 8; ++j) {
-                            accum += w8[j];
-                            if (accum > t) { sm.bonus_v = i * 8 + j; break; }
-                        }
-                    }
-                    __syncthreads();
-                    bonus = sm.bonus_v;
-                }
+                    for (int j = 0; j < 8; ++j)
+                        w8[j] = (i * 8 + j < V) ? delta_weight(rs::target_weight(raw_elem(xr, dtype, j), m, inv_tau),
+                                                               i * 8 + j, sm)
+                                                : 0ull;
+                });
                 stop = true;
             }
         }
@@ -581,7 +738,7 @@ __global__ void exp_spec_kernel(const float* x, int64_t n, float* y) {
 }  // namespace
 
 extern "C" size_t rs_tree_accept_workspace_bytes(int32_t mode, int32_t B, int32_t V) {
-    return mode == RS_ACCEPT_SAMPLE_MSS && B > 0 && V > 0 ? (size_t)B * (size_t)V * sizeof(uint64_t) : 0;
+    return mode == RS_ACCEPT_SAMPLE_MSS && B > 0 && V > 0 ? (size_t)B * (size_t)((V + 7) & ~7) * sizeof(uint32_t) : 0;
 }
 
 extern "C" rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t logits_dtype,
@@ -619,6 +776,9 @@ extern "C" rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t lo
     const int esz = logits_dtype == RS_DTYPE_BF16 ? 2 : 4;
     const bool lvec = ((reinterpret_cast<uintptr_t>(logits) & 15) == 0) && ((int64_t)V * esz % 16 == 0);
     const bool dvec = draft_probs && ((reinterpret_cast<uintptr_t>(draft_probs) & 15) == 0) && (V % 4 == 0);
+    // RS_ACC_PF=1: speculative L2 prefetch of the children rows (greedy). Measured on config 2:
+    // 34.7 -> 38.1 us (2.2x the DRAM bytes; the walk is bound by the cluster barriers), so off.
+    static const int pf = getenv("RS_ACC_PF") ? atoi(getenv("RS_ACC_PF")) : 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(B * cs));
     cfg.blockDim = dim3(kThreads);
@@ -635,7 +795,7 @@ extern "C" rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t lo
                                                  : tree_accept_kernel<RS_ACCEPT_SAMPLE_MSS>;
     RS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, (int)mode, logits, (int)logits_dtype, draft_probs, parent, token,
                                      tree_off, gid, (int)V, inv_tau, seed, step, accepted_len, path, bonus_token,
-                                     status_flags, lvec, dvec, static_cast<uint64_t*>(need ? ws : nullptr)));
+                                     status_flags, lvec, dvec, static_cast<uint32_t*>(need ? ws : nullptr), pf));
     return RS_OK;
 }
 

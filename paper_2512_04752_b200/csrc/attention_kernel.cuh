@@ -194,11 +194,11 @@ __device__ __forceinline__ float ex2_poly(float x) {
     return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 #ifndef RS_ATTN_EXP_EMU
-#define RS_ATTN_EXP_EMU 0   // measured: no gain (the softmax is latency-, not MUFU-bound)
+#define RS_ATTN_EXP_EMU 0   // eighths of the exponentials on the FMA pipe (0: all on MUFU)
 #endif
-// element c of a row block: every 4th (c % 4 == 3) on the FMA pipe
+// element c of a row block: RS_ATTN_EXP_EMU of every 8 on the FMA pipe
 __device__ __forceinline__ float ex2_mix(float x, int c) {
-    if (RS_ATTN_EXP_EMU && (c & 3) == 3) return ex2_poly(x);
+    if (RS_ATTN_EXP_EMU && (c & 7) >= 8 - RS_ATTN_EXP_EMU) return ex2_poly(x);
     return ex2(x);
 }
 
@@ -755,7 +755,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                     for (int k = 0; k < 8; ++k) ls8[k] = 0.0f;
 #pragma unroll
                     for (int c = 0; c < 32; c += 2) {
-                        const float e0 = ex2(fmaf(__uint_as_float(sh[c]), p.scale_log2, -mo));
+                        const float e0 = ex2_mix(fmaf(__uint_as_float(sh[c]), p.scale_log2, -mo), c);
                         const float e1 = ex2_mix(fmaf(__uint_as_float(sh[c + 1]), p.scale_log2, -mo), c + 1);
                         const uint32_t pk = pack_bf16(e0, e1);
                         sh[c >> 1] = pk;
@@ -943,7 +943,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                         for (int k = 0; k < 8; ++k) ls8[k] = 0.0f;
 #pragma unroll
                         for (int c = 0; c < 32; c += 2) {
-                            const float e0 = ex2(fmaf(__uint_as_float(sh[c]), p.scale_log2, -mo));
+                            const float e0 = ex2_mix(fmaf(__uint_as_float(sh[c]), p.scale_log2, -mo), c);
                             const float e1 = ex2_mix(fmaf(__uint_as_float(sh[c + 1]), p.scale_log2, -mo), c + 1);
                             const uint32_t pk = pack_bf16(e0, e1);
                             sh[c >> 1] = pk;
@@ -1027,7 +1027,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                     for (int k = 0; k < 8; ++k) ls8[k] = 0.0f;
 #pragma unroll
                     for (int c = 0; c < 64; c += 2) {
-                        const float e0 = ex2(fmaf(__uint_as_float(sr[c]), p.scale_log2, -mo));
+                        const float e0 = ex2_mix(fmaf(__uint_as_float(sr[c]), p.scale_log2, -mo), c);
                         const float e1 = ex2_mix(fmaf(__uint_as_float(sr[c + 1]), p.scale_log2, -mo), c + 1);
                         const uint32_t pk = pack_bf16(e0, e1);
                         sr[c >> 1] = pk;

@@ -4,7 +4,7 @@
 // node at depth k has index >= k), copy k never reads a slot written by an earlier copy; only a
 // LATER copy can overwrite a slot an earlier one reads. So the rows are processed in chunks of
 // ascending k, each chunk gathered into registers (all loads in flight) before it is scattered.
-// One CTA per (sample, pair of layers); consecutive threads own consecutive 16-byte columns,
+// The move list is built by two warps in parallel (ballot scan). One CTA per (sample, pair of layers); consecutive threads own consecutive 16-byte columns,
 // so every gather/scatter is a coalesced 128-bit access. Identity moves (path[k] == k) are skipped.
 #include "common.cuh"
 
@@ -49,16 +49,31 @@ kv_compact_kernel(LayerPtrs layers, int nl, int Hkv, int d, int ps, const int32_
     if (a <= 0 || nlay <= 0) return;
     const int vpr = d / 8;                                  // 16-byte vectors per (token, head) row
     const int32_t* bt = block_table + (int64_t)b * max_pages;
-    if (threadIdx.x == 0) {
-        int n = 0;
-        for (int k = 1; k <= a; ++k) {
-            const int src = P + pth[k], dst = P + k;
-            if (src == dst) continue;                       // identity moves are skipped
-            s_src[n] = ((int64_t)bt[src / ps] * Hkv * ps + (src % ps)) * vpr;
-            s_dst[n] = ((int64_t)bt[dst / ps] * Hkv * ps + (dst % ps)) * vpr;
-            ++n;
+    // move list in parallel: thread t < 64 takes k = t + 1; the non-identity moves are packed
+    // in ascending k by a two-warp ballot scan (the order the sequential semantics need)
+    {
+        const int t = threadIdx.x;
+        bool mv = false;
+        int64_t so = 0, dso = 0;
+        if (t < RS_MAX_TREE && t + 1 <= a) {
+            const int src = P + pth[t + 1], dst = P + t + 1;
+            mv = src != dst;                                // identity moves are skipped
+            if (mv) {
+                so = ((int64_t)bt[src / ps] * Hkv * ps + (src % ps)) * vpr;
+                dso = ((int64_t)bt[dst / ps] * Hkv * ps + (dst % ps)) * vpr;
+            }
         }
-        s_n = n;
+        __shared__ int s_cnt[2];
+        const unsigned bal = __ballot_sync(0xffffffffu, mv);
+        const int lane = t & 31;
+        if (t == 0 || t == 32) s_cnt[t >> 5] = __popc(bal);
+        __syncthreads();
+        if (mv) {
+            const int pos = __popc(bal & ((1u << lane) - 1u)) + (t >= 32 ? s_cnt[0] : 0);
+            s_src[pos] = so;
+            s_dst[pos] = dso;
+        }
+        if (t == 0) s_n = s_cnt[0] + s_cnt[1];
     }
     __syncthreads();
     const int n = s_n;

@@ -133,6 +133,11 @@ __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* m, int x, int
                  "r"(x), "r"(y)
                  : "memory");
 }
+// L2 prefetch of a contiguous global range (16-byte aligned address, size a multiple of 16).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(p)), "r"(bytes)
+                 : "memory");
+}
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int x,
                                             int y, int z) {
     asm volatile(
