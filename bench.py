@@ -36,6 +36,9 @@ WORKLOAD_DESC = {
     "tiny": "BASELINE configs[0]: 1 sample, prefix 32, 8-node tree, 1 head, d=64, V=1000, greedy",
     "c3": "BASELINE configs[2]: Llama-3-8B shapes, batch 256, prefixes 512-16K lognormal, trees 4-64 "
           "(drawn per sample), rejection sampling (MSS)",
+    "c4": "BASELINE configs[3]: one instance per B200, 256 samples per instance (2048 at 8), long-tail "
+          "response lengths (LMSYS-shaped lognormal, cap 2048), Llama-3-8B shapes + 1 SSM layer, 16-node "
+          "trees, greedy; samples finish and leave; periodic sample reallocation with KV migration (NCCL)",
     "c3s": "BASELINE configs[2] as the method runs it: Llama-3-8B shapes, batch 256, prefixes 512-16K "
            "lognormal, every tree = S(n) for the n select_strategy picks (host C++, called every step), "
            "rejection sampling (MSS)",
@@ -201,17 +204,23 @@ def cpu_baseline(host, cfg, budget_s=12.0):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=None, help="timed steps (default 50; c4: 400)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--realloc", default="on", choices=["on", "off"], help="c4: sample reallocation")
+    ap.add_argument("--cooldown", type=int, default=32, help="c4: steps between reallocation checks (P:300)")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 400 if args.config == "c4" else 50
     world, rank, local = _dist()
     assert args.warmup >= 3, "W >= 3 warm-up steps"
     if args.impl == "reference":
         return run_reference(args, world, rank)
+    if args.config == "c4":
+        return run_c4(args, world, rank, local)
     return run_ours(args, world, rank, local)
 
 
@@ -372,6 +381,147 @@ def run_ours(args, world, rank, local):
         torch.distributed.destroy_process_group()
 
 
+def c4_samples(world, rank, per_rank=256, seed=4):
+    """Config 4 workload: per_rank x world samples, round-robin over the instances (P:151);
+    prompt ~ LogNormal(ln 256, 0.784) in [32, 2048], response LMSYS-shaped capped at 2048
+    (P:349). Drawn from one global RNG so every world size sees the same population."""
+    from synth import lmsys_response_lengths
+    rng = np.random.default_rng(seed)
+    n = per_rank * world
+    prompt = np.clip(np.rint(rng.lognormal(math.log(256.0), 0.784, size=n)), 32, 2048).astype(np.int32)
+    resp = lmsys_response_lengths(rng, n)
+    return [(g, int(prompt[g]), int(resp[g])) for g in range(n) if g % world == rank]
+
+
+def run_c4(args, world, rank, local):
+    """BASELINE configs[3]: the verify loop of one generation instance per GPU over a long-tailed
+    sample set; samples finish and leave, so loads diverge across instances; with --realloc on
+    the instances rebalance every `cooldown` steps (threshold = knee of the measured
+    throughput-vs-samples curve) and migrate KV over NCCL. A step is one verify step of
+    every instance (host planning + one H2D of metadata + kernels + one D2H of results)."""
+    from paper_2512_04752_b200 import core
+    from paper_2512_04752_b200.instance import GenerationInstance
+    from paper_2512_04752_b200.realloc import Rebalancer
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    samples = c4_samples(world, rank)
+    L, Hq, Hkv, d, T = 32, 32, 8, 128, 16
+    need = sum((p + r + T + 63) // 64 for _, p, r in samples)
+    num_pages = int(need * 1.6) + 256
+    inst = GenerationInstance(samples, Hq=Hq, Hkv=Hkv, d=d, L=L, V=128256, T=T, p_accept=0.8, num_pages=num_pages,
+                              max_pages=72, max_batch=int(len(samples) * 1.5), seed=100 + rank, device=dev)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # threshold: knee of this instance's throughput-vs-samples curve (measured, not committed),
+    # taken on rank 0 and broadcast so every instance plans with the same value
+    counts = [8, 16, 32, 64, 96, 128, 192, 256]
+    tput = []
+    for n in counts:
+        inst.step(seed=1, limit=n, commit=False)
+        t0 = time.perf_counter()
+        tok = sum(inst.step(seed=2 + k, limit=n, commit=False) for k in range(3))
+        tput.append(tok / (time.perf_counter() - t0))
+    thr = core.knee_threshold(counts, tput, 0.10)
+    if world > 1:
+        t = torch.tensor([thr], device=dev)
+        torch.distributed.broadcast(t, 0)
+        thr = int(t.item())
+    realloc = args.realloc == "on" and world > 1
+    reb = Rebalancer(thr, cooldown=args.cooldown) if realloc else None
+    comm = core.Comm(rank, world) if realloc else None
+    staging = torch.empty(4 << 30, dtype=torch.uint8, device=dev) if realloc else None
+    scratch = torch.empty(2 * 512 + 512 * 72, dtype=torch.int32, device=dev) if realloc else None
+
+    def one_step(k, timing=False):
+        mig = (0, 0, 0, 0.0)
+        if realloc:
+            t0 = time.perf_counter()
+            sent, recv, moved = inst.rebalance(reb, comm, staging, scratch)
+            mig = (sent, recv, moved, time.perf_counter() - t0)
+        return inst.step(seed=11, timing=timing), mig
+
+    for w in range(args.warmup):
+        one_step(w)
+    barrier()
+    hbm, _, _, peak_src = _peaks()
+    sampler = ClockSampler(local)
+    loads, attn_ms, attn_bytes = [], 0.0, 0.0
+    tokens = 0
+    migrations = []
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        start.record()
+        for k in range(args.steps):
+            loads.append(inst.load)
+            c, mig = one_step(k, timing=True)
+            tokens += c
+            if mig[0] or mig[1]:
+                migrations.append(mig)
+            if inst.last_B:
+                attn_ms += inst.last_attn_ms
+                P = inst.last_prefix.astype(np.float64)
+                attn_bytes += L * float(4 * Hkv * d * np.sum(P + T) + 4 * Hq * d * T * inst.last_B + 8 * T * inst.last_B
+                                        + 4 * np.sum(np.ceil((P + T) / 64)))
+        end.record()
+        torch.cuda.synchronize()
+    barrier()
+    ms = start.elapsed_time(end)
+    tok_all, ms_max = tokens, ms
+    if world > 1:
+        t = torch.tensor([float(tokens)], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t)
+        tok_all = int(t.item())
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_max = float(t.item())
+    value = tok_all / (ms_max / 1e3)
+    gbs = attn_bytes / (attn_ms * 1e-3) / 1e9 if attn_ms > 0 else 0.0
+    mig_bytes = sum(m[2] for m in migrations)
+    mig_s = sum(m[3] for m in migrations)
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"c4: {WORKLOAD_DESC['c4']}", "samples_per_instance": len(samples),
+                   "Hq": Hq, "Hkv": Hkv, "d": d, "L": L, "V": 128256, "tree": ["fixed", T], "accept_mode": "greedy",
+                   "realloc": "on" if realloc else "off", "cooldown": args.cooldown, "threshold": thr,
+                   "knee_profile": {"counts": counts, "tokens_per_s": [round(x, 1) for x in tput]},
+                   "load_first_last": [loads[0] if loads else 0, loads[-1] if loads else 0],
+                   "finished_samples_rank0": inst.finished, "tokens_rank0": tokens,
+                   "l2": "inputs larger than L2: %.1f GB of per-layer KV pools resident" % (
+                       2 * (L + 1) * num_pages * Hkv * 64 * d * 2 / 1e9),
+                   "parallelism": f"dp{world} (sample-sharded instances; collective only for reallocation)"},
+        "clocks": sampler.summary(),
+        "e2e": {"value": round(value, 1), "unit": UNIT,
+                "h2d_bytes_per_step": int(4 * (len(samples) * (2 + 2 * T + 72) + 1) + 8 * len(samples)),
+                "d2h_bytes_per_step": int(8 * len(samples)),
+                "note": "the loop is host-driven end to end: every step uploads its metadata and reads back "
+                        "accepted_len/new_len; Q and logits are produced on the device upstream (bounds above "
+                        "are for the first step's batch)"},
+        "gpu_launches": int(args.steps * (L + 3)),
+        "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(gbs / hbm, 4), "traffic": None, "kernel": "tree_attn_kernel",
+                     "peak_source": peak_src, "attention_share_of_step": round(attn_ms / ms, 4)},
+        "migration": {"events": len(migrations), "samples_moved_rank0": sum(m[0] + m[1] for m in migrations),
+                      "bytes_rank0": int(mig_bytes), "seconds_rank0": round(mig_s, 4),
+                      "GBps_rank0": round(mig_bytes / mig_s / 1e9, 2) if mig_s > 0 else None},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.destroy()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def run_e2e(step, b, n_steps, tokens_per_step, world, dev, barrier, mode, temperature):
     """Same metric end to end through the public API with HOST buffers: every step copies its
     inputs (Q of every layer, logits, draft probabilities for MSS, tree metadata) from pinned
@@ -471,8 +621,14 @@ def run_reference(args, world, rank):
     paper: /root/reference holds only the paper text). Rank 0 only."""
     if rank != 0:
         return
-    from synth import CONFIGS, make_verify_batch
-    cfg = CONFIGS[args.config]
+    from synth import CONFIGS, VerifyConfig, make_verify_batch
+    if args.config == "c4":
+        # c4's verify step on one sample of its population: 8B shapes, prompt + partial response
+        # lengths of the long tail (lognormal around 600 tokens), 16-node tree, greedy
+        cfg = VerifyConfig("c4", B=1, Hq=32, Hkv=8, d=128, V=128256, L=32, prefix=("lognormal", 600, 0.784, 32, 4096),
+                           tree=("fixed", 16), mode="greedy", seed=4)
+    else:
+        cfg = CONFIGS[args.config]
     # one whole sample per step (all L layers), drawn on the CPU with the same recipe
     one = type(cfg)(**{**cfg.__dict__, "B": max(1, args.steps + args.warmup)})
     b = make_verify_batch(one, device="cpu", spare_pages=0)

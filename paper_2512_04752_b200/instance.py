@@ -1,0 +1,320 @@
+"""One generation instance running the speculative verify loop over a long-tailed sample set
+(BASELINE configs[3]). One process per GPU = one instance.
+
+Per step:
+    host: live samples -> page reservations for the tree slots, block tables, lengths, the
+          tree tokens of this step, the attention schedule (rs_attn_plan_create)
+    device: one H2D of the packed metadata, rs_tree_build_mask, rs_tree_verify_attention_layers
+          (L LLM layers), rs_tree_accept, rs_kv_compact (LLM layers + the SSM layer), one D2H
+          of (accepted_len, new_len)
+    host: lengths advance by a_b + 1; a sample whose response is complete leaves and its pages
+          return to the pool (the long tail of P:95-101 shrinks the batch).
+Every `cooldown` steps the instances rebalance (realloc.Rebalancer: all-gathered loads,
+the Eq. 6 greedy plan, sample choice) and move the chosen samples' KV with rs_migrate_samples
+(NCCL send/recv).
+
+Synthetic content: Q and the logits are drawn once at the maximum batch size
+and addressed by batch position (their values only steer acceptance); every step draws new
+tree tokens on the host so that a node's argmax token is one of its children's tokens with
+probability p_accept (greedy acceptance is then random per step). KV pages hold N(0, 1)
+values; prompts are prefilled upstream (their pages are simply reserved).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import core
+from .realloc import Rebalancer, SampleMeta
+
+PAGE = 64
+
+
+@dataclass
+class Sample:
+    gid: int
+    length: int            # committed tokens with K/V in the cache (P_b)
+    remaining: int         # response tokens still to generate
+    pages: np.ndarray      # page ids (logical page j -> pages[j])
+    steps: int = 0
+    accepted: int = 0      # accepted draft tokens so far
+
+    @property
+    def avg_accepted(self) -> float:
+        return self.accepted / self.steps if self.steps else 0.0
+
+
+class GenerationInstance:
+    def __init__(self, samples, *, Hq=32, Hkv=8, d=128, L=32, V=128256, T=16, p_accept=0.8,
+                 num_pages=8192, max_pages=72, max_batch=None, seed=0, device="cuda", branching=(4, 3, 2, 2, 1)):
+        """samples: iterable of (gid, prompt_len, response_len)."""
+        from synth.workloads import random_tree_parents
+        self.dev = torch.device(device)
+        self.Hq, self.Hkv, self.d, self.L, self.V, self.T = Hq, Hkv, d, L, V, T
+        self.p_accept = p_accept
+        self.max_pages = max_pages
+        self.rng = np.random.default_rng(seed)
+        gen = torch.Generator(device=self.dev).manual_seed(seed)
+        self.pool = core.PagePool(num_pages)
+        self.samples: list[Sample] = []
+        for gid, p0, r in samples:
+            pg = self.pool.alloc(self._pages_for(int(p0) + T))
+            if pg is None:
+                raise MemoryError("page pool too small for the initial samples")
+            self.samples.append(Sample(int(gid), int(p0), int(r), pg))
+        self.max_batch = int(max_batch or max(len(self.samples), 1))
+        # one tree shape for every sample (BFS, node 0 = root); children lists for the tokens
+        self.parent = random_tree_parents(np.random.default_rng(seed + 7), T, branching)
+        self.kids = [np.nonzero(self.parent == c)[0] for c in range(T)]
+        # KV stores: L LLM layers + 1 SSM layer, per-layer page pools [pages, Hkv, 64, d]
+        def pool_tensor():
+            t = torch.empty((num_pages, Hkv, PAGE, d), dtype=torch.bfloat16, device=self.dev)
+            return t.normal_(generator=gen)
+        self.k_llm = [pool_tensor() for _ in range(L)]
+        self.v_llm = [pool_tensor() for _ in range(L)]
+        self.k_ssm, self.v_ssm = [pool_tensor()], [pool_tensor()]
+        # synthetic Q and logits at the maximum batch, addressed by batch position
+        NTmax = self.max_batch * T
+        self.q = torch.randn((L, NTmax, Hq, d), generator=gen, device=self.dev).to(torch.bfloat16)
+        logits = torch.randn((NTmax, V), generator=gen, device=self.dev)
+        self.spike = self.rng.integers(0, V, size=NTmax).astype(np.int32)   # argmax token of each row
+        logits[torch.arange(NTmax, device=self.dev), torch.from_numpy(self.spike).long().to(self.dev)] += 12.0
+        self.logits = logits.to(torch.bfloat16)
+        del logits
+        self.out = torch.empty((L, NTmax, Hq, d), dtype=torch.bfloat16, device=self.dev)
+        # packed per-step metadata: prefix_len [B] | tree_off [B+1] | parent [NT] | token [NT] |
+        # block_table [B, max_pages]; one pinned host buffer, one H2D copy
+        cap = self.max_batch * (2 + 2 * T + max_pages) + 1
+        self.meta_h = torch.empty(cap, dtype=torch.int32).pin_memory()
+        self.meta_d = torch.empty(cap, dtype=torch.int32, device=self.dev)
+        self.gid_h = torch.empty(self.max_batch, dtype=torch.int64).pin_memory()
+        self.gid_d = torch.empty(self.max_batch, dtype=torch.int64, device=self.dev)
+        self.res_h = torch.empty(2 * self.max_batch, dtype=torch.int32).pin_memory()
+        self.mask = torch.empty(NTmax, dtype=torch.int64, device=self.dev)
+        self.depth = torch.empty(NTmax, dtype=torch.int32, device=self.dev)
+        self.tflags = torch.empty(self.max_batch, dtype=torch.int32, device=self.dev)
+        self.acc = torch.empty(self.max_batch, dtype=torch.int32, device=self.dev)
+        self.path = torch.empty((self.max_batch, core.MAX_TREE), dtype=torch.int32, device=self.dev)
+        self.bonus = torch.empty(self.max_batch, dtype=torch.int32, device=self.dev)
+        self.aflags = torch.empty(self.max_batch, dtype=torch.int32, device=self.dev)
+        self.res_d = torch.empty(2 * self.max_batch, dtype=torch.int32, device=self.dev)
+        self.ws = core.alloc_workspace(1 << 20, self.dev)
+        self.stream = torch.cuda.Stream(self.dev)
+        self._ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        self.last_attn_ms = 0.0
+        self.step_no = 0
+        self.tokens = 0            # committed tokens (sum of a_b + 1)
+        self.finished = 0
+
+    @staticmethod
+    def _pages_for(n_tokens: int) -> int:
+        return (n_tokens + PAGE - 1) // PAGE
+
+    @property
+    def load(self) -> int:
+        return len(self.samples)
+
+    # ------------------------------------------------------------------ host side of a step
+    def _reserve_tree_slots(self):
+        for s in self.samples:
+            need = self._pages_for(s.length + self.T)
+            if need > self.max_pages:
+                raise RuntimeError(f"sample {s.gid}: {s.length} tokens exceed max_pages")
+            if need > len(s.pages):
+                extra = self.pool.alloc(need - len(s.pages))
+                if extra is None:
+                    raise MemoryError("page pool exhausted")
+                s.pages = np.concatenate([s.pages, extra])
+
+    def _tokens(self, B: int) -> np.ndarray:
+        """Tree tokens of this step: random, except that with probability p_accept one child of
+        each internal node carries its parent's argmax token (the row's spike)."""
+        T = self.T
+        tok = self.rng.integers(0, self.V, size=(B, T)).astype(np.int32)
+        rows = np.arange(B) * T
+        for c in range(T):
+            kids = self.kids[c]
+            if len(kids) == 0:
+                continue
+            hit = self.rng.random(B) < self.p_accept
+            pick = kids[self.rng.integers(0, len(kids), size=B)]
+            b = np.nonzero(hit)[0]
+            tok[b, pick[b]] = self.spike[rows[b] + c]
+        return tok.reshape(-1)
+
+    def _pack_meta(self, B: int):
+        T, mp = self.T, self.max_pages
+        NT = B * T
+        m = self.meta_h.numpy()
+        o = 0
+        pl = m[o:o + B]; o += B
+        to = m[o:o + B + 1]; o += B + 1
+        par = m[o:o + NT]; o += NT
+        tok = m[o:o + NT]; o += NT
+        bt = m[o:o + B * mp].reshape(B, mp); o += B * mp
+        for i, s in enumerate(self.samples):
+            pl[i] = s.length
+            n = len(s.pages)
+            bt[i, :n] = s.pages
+            bt[i, n:] = s.pages[-1]
+            self.gid_h[i] = s.gid
+        to[:] = np.arange(B + 1, dtype=np.int32) * T
+        par[:] = np.tile(self.parent, B)
+        tok[:] = self._tokens(B)
+        return o, pl.copy(), to.copy()
+
+    # ------------------------------------------------------------------ one verify step
+    def step(self, seed: int = 0, limit: int | None = None, commit: bool = True, timing: bool = False):
+        """Run one verify step over the live samples (the first `limit` of them); returns the
+        committed tokens. commit=False leaves the host state untouched (profiling: the tree
+        slots written by the compaction lie beyond the committed lengths). timing=True records
+        the attention time of the step in self.last_attn_ms (CUDA events on the step's stream)."""
+        all_samples = self.samples
+        if limit is not None:
+            self.samples = all_samples[:limit]
+        try:
+            return self._step(seed, commit, timing)
+        finally:
+            if limit is not None and not commit:
+                self.samples = all_samples
+            elif limit is not None:
+                self.samples = self.samples + all_samples[limit:]
+
+    def _step(self, seed, commit, timing):
+        B = len(self.samples)
+        if B == 0:
+            return 0
+        if B > self.max_batch:
+            raise RuntimeError(f"batch {B} exceeds max_batch {self.max_batch}")
+        T, mp, L = self.T, self.max_pages, self.L
+        NT = B * T
+        self._reserve_tree_slots()
+        n, pl_h, to_h = self._pack_meta(B)
+        plan = core.AttnPlan(pl_h, to_h, self.Hq, self.Hkv, self.d, PAGE)
+        if plan.ws_bytes > self.ws.numel():
+            self.ws = core.alloc_workspace(int(plan.ws_bytes * 1.25), self.dev)
+        st = self.stream
+        with torch.cuda.stream(st):
+            self.meta_d[:n].copy_(self.meta_h[:n], non_blocking=True)
+            self.gid_d[:B].copy_(self.gid_h[:B], non_blocking=True)
+            md = self.meta_d
+            o = 0
+            pl = md[o:o + B]; o += B
+            to = md[o:o + B + 1]; o += B + 1
+            par = md[o:o + NT]; o += NT
+            tok = md[o:o + NT]; o += NT
+            bt = md[o:o + B * mp].view(B, mp)
+            core.tree_build_mask(par, to, stream=st, out=(self.mask[:NT], self.depth[:NT], self.tflags[:B]))
+            plan.upload(self.ws, stream=st)
+            call = core.AttentionLayersCall(plan, [self.q[l, :NT] for l in range(L)], self.k_llm, self.v_llm, bt, pl,
+                                            to, self.mask[:NT], 1.0 / math.sqrt(self.d), self.ws,
+                                            [self.out[l, :NT] for l in range(L)])
+            if timing:
+                self._ev[0].record(st)
+            call(st)
+            if timing:
+                self._ev[1].record(st)
+            core.tree_accept(core.GREEDY, self.logits[:NT], par, tok, to, self.gid_d[:B], seed=seed,
+                             step=self.step_no, out=(self.acc[:B], self.path[:B], self.bonus[:B], self.aflags[:B]),
+                             stream=st)
+            core.kv_compact(self.k_llm + self.k_ssm, self.v_llm + self.v_ssm, bt, pl, self.acc[:B], self.path[:B],
+                            PAGE, new_len=self.res_d[B:2 * B], stream=st)
+            self.res_d[:B].copy_(self.acc[:B])
+            self.res_h[:2 * B].copy_(self.res_d[:2 * B], non_blocking=True)
+        st.synchronize()
+        if timing:
+            self.last_attn_ms = self._ev[0].elapsed_time(self._ev[1])
+        self.last_B, self.last_prefix = B, pl_h
+        r = self.res_h.numpy()
+        acc, new_len = r[:B], r[B:2 * B]
+        if not commit:
+            return int(np.sum(np.minimum(acc + 1, [s.remaining for s in self.samples])))
+        committed = 0
+        live = []
+        for i, s in enumerate(self.samples):
+            made = min(int(acc[i]) + 1, s.remaining)
+            committed += made
+            s.length = int(new_len[i])
+            s.remaining -= made
+            s.steps += 1
+            s.accepted += int(acc[i])
+            if s.remaining <= 0:
+                self.pool.free(s.pages)
+                self.finished += 1
+            else:
+                live.append(s)
+        self.samples = live
+        self.tokens += committed
+        self.step_no += 1
+        return committed
+
+    # ------------------------------------------------------------------ reallocation
+    def sample_meta(self):
+        return [SampleMeta(s.gid, s.length, s.avg_accepted, s.remaining, s.steps, s.accepted) for s in self.samples]
+
+    def _chunks(self, metas, cap_bytes):
+        """Consecutive groups of the transfer whose packed KV (LLM + SSM) fits the staging buffer;
+        both ends compute the same groups from the same broadcast list."""
+        out, cur = [], []
+        for m in metas:
+            trial = cur + [m]
+            lens = [x.seq_len for x in trial]
+            need = 2 * (core.kv_pack_elems(self.L, self.Hkv, self.d, lens) + core.kv_pack_elems(1, self.Hkv, self.d, lens))
+            if need > cap_bytes:
+                if not cur:
+                    raise RuntimeError(f"sample {m.gid} ({m.seq_len} tokens) does not fit the staging buffer")
+                out.append(cur)
+                cur = [m]
+            else:
+                cur = trial
+        if cur:
+            out.append(cur)
+        return out
+
+    def rebalance(self, rebalancer: Rebalancer, comm: "core.Comm", staging, scratch, force=False):
+        """Collective over all instances (every rank calls it at the same step). Returns
+        (#samples sent, #received, KV bytes moved by this rank)."""
+        transfers = rebalancer.plan(self.load, force=force)
+        if not transfers:
+            return 0, 0, 0
+        transfers = rebalancer.choose(transfers, self.sample_meta())
+        cap = staging.numel() * staging.element_size()
+        by_gid = {s.gid: s for s in self.samples}
+        sent_gids = set()
+        sent = recv = moved = 0
+        for tr in transfers:
+            if comm.rank not in (tr.src, tr.dst):
+                continue
+            for chunk in self._chunks(tr.samples, cap):
+                gids = [c.gid for c in chunk]
+                lens = [c.seq_len for c in chunk]
+                src_bt = None
+                if comm.rank == tr.src:
+                    rows = np.zeros((len(chunk), self.max_pages), np.int32)
+                    for i, g in enumerate(gids):
+                        pg = by_gid[g].pages
+                        rows[i, :len(pg)] = pg
+                        rows[i, len(pg):] = pg[-1]
+                    src_bt = torch.from_numpy(rows).to(self.dev)
+                rows = core.migrate_samples(comm, tr.src, tr.dst, (self.k_llm, self.v_llm), (self.k_ssm, self.v_ssm),
+                                            PAGE, self.pool if comm.rank == tr.dst else None, gids, lens, src_bt,
+                                            self.max_pages, staging, scratch, self.stream)
+                moved += 2 * (core.kv_pack_elems(self.L, self.Hkv, self.d, lens) +
+                              core.kv_pack_elems(1, self.Hkv, self.d, lens))
+                if comm.rank == tr.src:
+                    for g in gids:
+                        self.pool.free(by_gid.pop(g).pages)
+                        sent_gids.add(g)
+                        sent += 1
+                else:
+                    for i, c in enumerate(chunk):
+                        npg = self._pages_for(c.seq_len)
+                        self.samples.append(Sample(c.gid, c.seq_len, c.remaining, rows[i, :npg].copy(), c.steps,
+                                                   c.accepted))
+                        recv += 1
+        if sent_gids:
+            self.samples = [s for s in self.samples if s.gid not in sent_gids]
+        return sent, recv, moved

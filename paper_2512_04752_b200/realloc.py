@@ -24,6 +24,9 @@ class SampleMeta:
     gid: int
     seq_len: int
     avg_accepted: float
+    remaining: int = 0      # sample state that travels with it (response tokens still to
+    steps: int = 0          # generate, verify steps so far, accepted drafts so far)
+    accepted: int = 0
 
 
 @dataclass

@@ -91,3 +91,27 @@ def test_plan_rejects_bad_trees(core):
         core.AttnPlan([10], [0, 0], 32, 8, 128, 64, 4)
     with pytest.raises(core.RSError):
         core.AttnPlan([10], [0, 4], 32, 8, 96, 64, 4)
+
+
+def test_instance_migration_chunks_fit_staging(core):
+    """Config 4 reallocation: a transfer's samples are cut into consecutive groups whose packed
+    KV (LLM + SSM layers) fits the staging buffer; both ends derive the same groups."""
+    from paper_2512_04752_b200.instance import GenerationInstance
+    from paper_2512_04752_b200.realloc import SampleMeta
+    inst = GenerationInstance.__new__(GenerationInstance)
+    inst.L, inst.Hkv, inst.d = 32, 8, 128
+    per_tok = 2 * 4 * 8 * 128 // 2 * 33            # bytes per token, 33 layers of K+V bf16
+    rng = np.random.default_rng(0)
+    metas = [SampleMeta(g, int(rng.integers(1, 3000)), 0.0) for g in range(40)]
+    cap = 900 * 1024 * 1024
+    groups = inst._chunks(metas, cap)
+    assert [m.gid for g in groups for m in g] == list(range(40))       # order kept, nothing lost
+    for g in groups:
+        need = 2 * (core.kv_pack_elems(32, 8, 128, [m.seq_len for m in g]) +
+                    core.kv_pack_elems(1, 8, 128, [m.seq_len for m in g]))
+        assert need <= cap and need == sum(m.seq_len for m in g) * per_tok
+    for a, b in zip(groups, groups[1:]):                               # greedy: next sample did not fit
+        lens = [m.seq_len for m in a] + [b[0].seq_len]
+        assert 2 * (core.kv_pack_elems(32, 8, 128, lens) + core.kv_pack_elems(1, 8, 128, lens)) > cap
+    with pytest.raises(RuntimeError):
+        inst._chunks([SampleMeta(0, 10 ** 6, 0.0)], cap)
