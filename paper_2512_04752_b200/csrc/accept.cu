@@ -770,6 +770,8 @@ extern "C" rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t lo
     const int nvec = (V + 7) / 8;
     int cs = 1;
     while (cs < kMaxCluster && nvec / (cs * 2) >= kThreads * 2 && (int64_t)B * cs * 2 <= 148 * 4) cs *= 2;
+    static const int cs_env = getenv("RS_ACC_CS") ? atoi(getenv("RS_ACC_CS")) : 0;   // measurements only
+    if (cs_env == 1 || cs_env == 2 || cs_env == 4 || cs_env == 8) cs = cs_env;
     const int per = (nvec + cs - 1) / cs;
     RS_REQUIRE((per + kTileVecs - 1) / kTileVecs <= kMaxTiles, RS_ERR_UNSUPPORTED, "rs_tree_accept: V=%d too large", V);
     const float inv_tau = (mode == RS_ACCEPT_GREEDY) ? 1.0f : 1.0f / temperature;

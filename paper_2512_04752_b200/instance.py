@@ -283,7 +283,7 @@ class GenerationInstance:
         transfers = rebalancer.choose(transfers, self.sample_meta())
         cap = staging.numel() * staging.element_size()
         by_gid = {s.gid: s for s in self.samples}
-        sent_gids = set()
+        sent_gids, received = set(), []
         sent = recv = moved = 0
         for tr in transfers:
             if comm.rank not in (tr.src, tr.dst):
@@ -309,12 +309,11 @@ class GenerationInstance:
                         self.pool.free(by_gid.pop(g).pages)
                         sent_gids.add(g)
                         sent += 1
-                else:
+                if comm.rank == tr.dst:   # (src == dst only in the loopback test: moved in place)
                     for i, c in enumerate(chunk):
                         npg = self._pages_for(c.seq_len)
-                        self.samples.append(Sample(c.gid, c.seq_len, c.remaining, rows[i, :npg].copy(), c.steps,
-                                                   c.accepted))
+                        received.append(Sample(c.gid, c.seq_len, c.remaining, rows[i, :npg].copy(), c.steps,
+                                               c.accepted))
                         recv += 1
-        if sent_gids:
-            self.samples = [s for s in self.samples if s.gid not in sent_gids]
+        self.samples = [s for s in self.samples if s.gid not in sent_gids] + received
         return sent, recv, moved

@@ -69,3 +69,50 @@ def test_instance_step_accept_matches_oracle(cuda_lib):
     np.testing.assert_array_equal(inst.path[:B].cpu().numpy(), path)
     np.testing.assert_array_equal(inst.bonus[:B].cpu().numpy(), bonus)
     assert acc.sum() > 0    # the synthetic tokens do get accepted
+
+
+class _LoopbackRebalancer:
+    """Plans one transfer of `count` samples from instance 0 to itself (the reallocation data
+    plane through a size-1 NCCL communicator: send and receive on the same GPU)."""
+
+    def __init__(self, count):
+        self.count = count
+
+    def plan(self, local_load, force=False):
+        from paper_2512_04752_b200.realloc import Transfer
+        return [Transfer(0, 0, self.count)]
+
+    def choose(self, transfers, metas):
+        transfers[0].samples = sorted(metas, key=lambda m: (m.seq_len, m.gid))[:self.count]
+        return transfers
+
+
+def test_instance_rebalance_loopback_moves_kv_bit_exact(cuda_lib):
+    core = cuda_lib
+    inst, samples = _instance(n=12, seed=8)
+    for _ in range(3):
+        inst.step(seed=5)
+    before = {s.gid: (s.length, s.remaining, s.steps, s.accepted, s.pages.copy()) for s in inst.samples}
+    comm = core.Comm(0, 1)
+    staging = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    scratch = torch.empty(2 * 64 + 64 * inst.max_pages, dtype=torch.int32, device="cuda")
+    try:
+        sent, recv, moved = inst.rebalance(_LoopbackRebalancer(5), comm, staging, scratch)
+    finally:
+        comm.destroy()
+    assert sent == recv == 5 and moved > 0
+    assert sorted(s.gid for s in inst.samples) == sorted(before)
+    pools = inst.k_llm + inst.v_llm + inst.k_ssm + inst.v_ssm
+    for s in inst.samples:
+        L0, R0, st0, a0, pg0 = before[s.gid]
+        assert (s.length, s.remaining, s.steps, s.accepted) == (L0, R0, st0, a0)
+        if not np.array_equal(s.pages[:len(pg0)], pg0):            # a moved sample: new pages, same bytes
+            for t in pools:
+                old = t[torch.as_tensor(pg0, device="cuda").long()]
+                new = t[torch.as_tensor(s.pages, device="cuda").long()]
+                # committed slots only: token j of the sample -> (page j // 64, row j % 64)
+                for j in range(0, s.length, 7):
+                    assert torch.equal(old[j // 64, :, j % 64], new[j // 64, :, j % 64])
+    while inst.load:                                              # the moved samples keep generating
+        inst.step(seed=6)
+    assert inst.finished == len(samples) and inst.pool.free_count() == 256
