@@ -49,7 +49,7 @@ typedef enum {
     RS_ERR_WORKSPACE = 11          /* workspace too small                                   */
 } rs_status;
 
-enum { RS_FLAG_MALFORMED = 1, RS_FLAG_NONFINITE = 2 };
+enum { RS_FLAG_MALFORMED = 1, RS_FLAG_NONFINITE = 2, RS_FLAG_INSUFFICIENT = 4 };
 enum { RS_ACCEPT_GREEDY = 0, RS_ACCEPT_SAMPLE_DELTA = 1, RS_ACCEPT_SAMPLE_MSS = 2 };
 enum { RS_DTYPE_BF16 = 0, RS_DTYPE_F32 = 1 };
 #define RS_MAX_TREE 64
@@ -70,6 +70,32 @@ const char* rs_version(void);
 rs_status rs_tree_build_mask(const int32_t* parent, const int32_t* tree_off, int32_t B,
                              uint64_t* tree_mask, int32_t* depth, int32_t* status_flags,
                              void* stream);
+
+/* ===================================================================================== f3
+ * rs_tree_select — the verification trees of a batch, built on the GPU from the draft's
+ * candidate trees for the n chosen by rs_select_strategy ("the selection of n";
+ * P:217-227 layer-level search; readings Z1, Z6, Z9, Z11 in DESIGN.md):
+ *   dl(u) = o(u) * dl(parent(u)); w(u) = F(dl(u)) (F: piecewise linear through the knots as
+ *   np.interp, clamped to [0, 1]); S(n) = the first n pops of the search (queue order: w desc,
+ *   depth asc, id asc); tree = root (node 0, token root_token[b]) + S(n) in ascending candidate
+ *   index with re-indexed parents (a candidate with parent -1 hangs under node 0).
+ *   cand_parent device int32 [NC]  parent candidate index (< i) or -1 (child of the root)
+ *   cand_o      device f64 [NC]    draft acceptance estimates o(u)
+ *   cand_token  device int32 [NC]; cand_off device int32 [B+1] (<= 256 candidates per sample)
+ *   root_token  device int32 [B]   the last committed token of each sample
+ *   n           1..63: every tree gets T = n + 1 nodes (tree_off[b] = b * (n + 1))
+ *   knots_x, knots_y device f64 [n_knots], 2 <= n_knots <= 16, knots_x increasing
+ *   parent_out, token_out, depth_out device int32 [B*(n+1)]; tree_mask_out device u64 [B*(n+1)]
+ *               (exactly what rs_tree_build_mask would give for parent_out)
+ *   status_flags device int32 [B]: RS_FLAG_MALFORMED (candidate parents not topological, or
+ *               > 256 candidates) / RS_FLAG_INSUFFICIENT (the search ran out before n pops);
+ *               such a sample's missing nodes are children of the root with token -1.
+ * Errors: n outside [1, 63] -> RS_ERR_UNSUPPORTED; bad knots / null -> RS_ERR_INVALID_ARG. */
+rs_status rs_tree_select(const int32_t* cand_parent, const double* cand_o, const int32_t* cand_token,
+                         const int32_t* cand_off, const int32_t* root_token, int32_t B, int32_t n,
+                         const double* knots_x, const double* knots_y, int32_t n_knots,
+                         int32_t* parent_out, int32_t* token_out, uint64_t* tree_mask_out,
+                         int32_t* depth_out, int32_t* status_flags, void* stream);
 
 /* ===================================================================================== a2
  * Tree-verification attention (P:76-80 single-pass verification of all tree tokens; P:213

@@ -134,3 +134,23 @@ def select_strategy(trees, prefix_len, knots_x, knots_y, cost: CostModel, n_min=
     return dict(n=n_best, depth=depth, width=width, al=al_prof[n_best - 1], t_sd=t_prof[n_best - 1],
                 objective=al_prof[n_best - 1] / t_prof[n_best - 1], n_stop=n_stop,
                 al_profile=al_prof[:n_stop], t_profile=t_prof[:n_stop])
+
+
+def verification_tree(parent, o, token, root_token, n, knots_x, knots_y):
+    """The verification tree of one sample for a chosen n (the n selected draft nodes are
+    verified in one pass as a tree under the last committed token): node 0 = root (token
+    root_token), then S(n) (the first n nodes of the layer-level search) in ascending
+    candidate index; a candidate whose parent is the virtual root (-1) hangs under node 0.
+    S(n) is closed under parents (a node is popped only after its parent), so the result is
+    topologically ordered. Returns (parent_v, token_v) int32 of length n + 1; raises
+    ValueError("InsufficientNodes") when the search yields fewer than n nodes."""
+    dl = draft_logits(parent, o)
+    w = np.array([acceptance_fit(knots_x, knots_y, x) for x in dl])
+    order = layer_search_order(parent, w, n)
+    if len(order) < n:
+        raise ValueError("InsufficientNodes")
+    chosen = sorted(order)
+    pos = {c: i + 1 for i, c in enumerate(chosen)}
+    par = [-1] + [0 if parent[c] < 0 else pos[int(parent[c])] for c in chosen]
+    tok = [int(root_token)] + [int(token[c]) for c in chosen]
+    return np.array(par, np.int32), np.array(tok, np.int32)

@@ -101,6 +101,28 @@ def tree_build_mask(parent: torch.Tensor, tree_off: torch.Tensor, stream=None, o
     return mask, depth, flags
 
 
+# ------------------------------------------------------------------ f3
+_sig("rs_tree_select", _i32, _P, _P, _P, _P, _P, _i32, _i32, _P, _P, _i32, _P, _P, _P, _P, _P, _P)
+FLAG_INSUFFICIENT = 4
+
+
+def tree_select(cand_parent, cand_o, cand_token, cand_off, root_token, n, knots_x, knots_y, stream=None, out=None):
+    """Verification trees (root + S(n)) for every sample, built on the device. Returns
+    (parent, token, mask, depth, flags); tree b occupies rows b*(n+1) .. b*(n+1)+n."""
+    B = cand_off.numel() - 1
+    dev = cand_parent.device
+    NT = B * (n + 1)
+    if out is None:
+        out = (torch.empty(NT, dtype=torch.int32, device=dev), torch.empty(NT, dtype=torch.int32, device=dev),
+               torch.empty(NT, dtype=torch.int64, device=dev), torch.empty(NT, dtype=torch.int32, device=dev),
+               torch.empty(B, dtype=torch.int32, device=dev))
+    par, tok, mask, dep, flags = out
+    _check(_lib.rs_tree_select(_ptr(cand_parent), _ptr(cand_o), _ptr(cand_token), _ptr(cand_off), _ptr(root_token),
+                               B, int(n), _ptr(knots_x), _ptr(knots_y), knots_x.numel(), _ptr(par), _ptr(tok),
+                               _ptr(mask), _ptr(dep), _ptr(flags), _stream(stream)), "rs_tree_select")
+    return par, tok, mask, dep, flags
+
+
 # ------------------------------------------------------------------ a2
 class AttnPlan:
     """Host schedule for one verify step (lengths of this step), shared by every layer."""
@@ -188,6 +210,19 @@ class AttentionLayersCall:
 
     def __call__(self, stream=None):
         _check(_lib.rs_tree_verify_attention_layers(*self.args, _stream(stream)), "rs_tree_verify_attention_layers")
+
+
+def tree_verify_attention_layers(plan: AttnPlan, L, q_ptrs, k_ptrs, v_ptrs, num_pages, block_table, prefix_len,
+                                 tree_off, tree_mask, Hq, head_dim, sm_scale, out_ptrs, ws, lse_ptrs=None,
+                                 stream=None):
+    """All L layers through rs_tree_verify_attention_layers with pre-built pointer arrays
+    (ptr_array of the per-layer Q / K / V / O tensors), for loops whose batch changes every
+    step (the Q/O rows of this step are the first tree_off[B] rows of each layer tensor)."""
+    _check(_lib.rs_tree_verify_attention_layers(
+        plan.handle, L, q_ptrs, k_ptrs, v_ptrs, int(num_pages), _ptr(block_table), block_table.shape[1],
+        _ptr(prefix_len), _ptr(tree_off), _ptr(tree_mask), plan.B, Hq, plan.Hkv, head_dim, plan.page_size,
+        float(sm_scale), out_ptrs, lse_ptrs, _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)),
+        "rs_tree_verify_attention_layers")
 
 
 # ------------------------------------------------------------------ a3

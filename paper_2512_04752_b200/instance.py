@@ -41,6 +41,14 @@ class Sample:
     pages: np.ndarray      # page ids (logical page j -> pages[j])
     steps: int = 0
     accepted: int = 0      # accepted draft tokens so far
+    bt_row: np.ndarray = None   # block-table row [max_pages] (tail padded with the last page)
+
+    def set_pages(self, pages, max_pages):
+        self.pages = pages
+        row = np.empty(max_pages, np.int32)
+        row[:len(pages)] = pages
+        row[len(pages):] = pages[-1]
+        self.bt_row = row
 
     @property
     def avg_accepted(self) -> float:
@@ -64,7 +72,9 @@ class GenerationInstance:
             pg = self.pool.alloc(self._pages_for(int(p0) + T))
             if pg is None:
                 raise MemoryError("page pool too small for the initial samples")
-            self.samples.append(Sample(int(gid), int(p0), int(r), pg))
+            smp = Sample(int(gid), int(p0), int(r), pg)
+            smp.set_pages(pg, max_pages)
+            self.samples.append(smp)
         self.max_batch = int(max_batch or max(len(self.samples), 1))
         # one tree shape for every sample (BFS, node 0 = root); children lists for the tokens
         self.parent = random_tree_parents(np.random.default_rng(seed + 7), T, branching)
@@ -85,6 +95,8 @@ class GenerationInstance:
         self.logits = logits.to(torch.bfloat16)
         del logits
         self.out = torch.empty((L, NTmax, Hq, d), dtype=torch.bfloat16, device=self.dev)
+        self._ptrs = (core.ptr_array([self.q[l] for l in range(L)]), core.ptr_array(self.k_llm),
+                      core.ptr_array(self.v_llm), core.ptr_array([self.out[l] for l in range(L)]))
         # packed per-step metadata: prefix_len [B] | tree_off [B+1] | parent [NT] | token [NT] |
         # block_table [B, max_pages]; one pinned host buffer, one H2D copy
         cap = self.max_batch * (2 + 2 * T + max_pages) + 1
@@ -104,6 +116,7 @@ class GenerationInstance:
         self.ws = core.alloc_workspace(1 << 20, self.dev)
         self.stream = torch.cuda.Stream(self.dev)
         self._ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        self._tok_next = self._tokens(self.max_batch)
         self.last_attn_ms = 0.0
         self.step_no = 0
         self.tokens = 0            # committed tokens (sum of a_b + 1)
@@ -127,7 +140,7 @@ class GenerationInstance:
                 extra = self.pool.alloc(need - len(s.pages))
                 if extra is None:
                     raise MemoryError("page pool exhausted")
-                s.pages = np.concatenate([s.pages, extra])
+                s.set_pages(np.concatenate([s.pages, extra]), self.max_pages)
 
     def _tokens(self, B: int) -> np.ndarray:
         """Tree tokens of this step: random, except that with probability p_accept one child of
@@ -155,15 +168,13 @@ class GenerationInstance:
         par = m[o:o + NT]; o += NT
         tok = m[o:o + NT]; o += NT
         bt = m[o:o + B * mp].reshape(B, mp); o += B * mp
-        for i, s in enumerate(self.samples):
-            pl[i] = s.length
-            n = len(s.pages)
-            bt[i, :n] = s.pages
-            bt[i, n:] = s.pages[-1]
-            self.gid_h[i] = s.gid
+        smp = self.samples
+        pl[:] = np.fromiter((x.length for x in smp), np.int32, B)
+        bt[:] = np.stack([x.bt_row for x in smp])
+        self.gid_h.numpy()[:B] = np.fromiter((x.gid for x in smp), np.int64, B)
         to[:] = np.arange(B + 1, dtype=np.int32) * T
         par[:] = np.tile(self.parent, B)
-        tok[:] = self._tokens(B)
+        tok[:] = self._tok_next[:NT]
         return o, pl.copy(), to.copy()
 
     # ------------------------------------------------------------------ one verify step
@@ -209,12 +220,11 @@ class GenerationInstance:
             bt = md[o:o + B * mp].view(B, mp)
             core.tree_build_mask(par, to, stream=st, out=(self.mask[:NT], self.depth[:NT], self.tflags[:B]))
             plan.upload(self.ws, stream=st)
-            call = core.AttentionLayersCall(plan, [self.q[l, :NT] for l in range(L)], self.k_llm, self.v_llm, bt, pl,
-                                            to, self.mask[:NT], 1.0 / math.sqrt(self.d), self.ws,
-                                            [self.out[l, :NT] for l in range(L)])
             if timing:
                 self._ev[0].record(st)
-            call(st)
+            qa, ka, va, oa = self._ptrs
+            core.tree_verify_attention_layers(plan, L, qa, ka, va, self.k_llm[0].shape[0], bt, pl, to, self.mask[:NT],
+                                              self.Hq, self.d, 1.0 / math.sqrt(self.d), oa, self.ws, stream=st)
             if timing:
                 self._ev[1].record(st)
             core.tree_accept(core.GREEDY, self.logits[:NT], par, tok, to, self.gid_d[:B], seed=seed,
@@ -224,6 +234,7 @@ class GenerationInstance:
                             PAGE, new_len=self.res_d[B:2 * B], stream=st)
             self.res_d[:B].copy_(self.acc[:B])
             self.res_h[:2 * B].copy_(self.res_d[:2 * B], non_blocking=True)
+        self._tok_next = self._tokens(self.max_batch)   # next step's tree tokens while the GPU works
         st.synchronize()
         if timing:
             self.last_attn_ms = self._ev[0].elapsed_time(self._ev[1])
@@ -312,8 +323,9 @@ class GenerationInstance:
                 if comm.rank == tr.dst:   # (src == dst only in the loopback test: moved in place)
                     for i, c in enumerate(chunk):
                         npg = self._pages_for(c.seq_len)
-                        received.append(Sample(c.gid, c.seq_len, c.remaining, rows[i, :npg].copy(), c.steps,
-                                               c.accepted))
+                        rcv = Sample(c.gid, c.seq_len, c.remaining, None, c.steps, c.accepted)
+                        rcv.set_pages(rows[i, :npg].copy(), self.max_pages)
+                        received.append(rcv)
                         recv += 1
         self.samples = [s for s in self.samples if s.gid not in sent_gids] + received
         return sent, recv, moved

@@ -220,3 +220,40 @@ def test_lmsys_length_distribution():
     x = lmsys_response_lengths(np.random.default_rng(0), 100_000, cap=10**9)
     assert abs(np.median(x) / med - 1) < 0.03
     assert abs(np.percentile(x, 95) / p95 - 1) < 0.05
+
+
+def test_verification_tree_paths_are_candidate_paths():
+    """f3 oracle: the verification tree for n is the root plus S(n); every node's root path
+    spells exactly its candidate's token path (found by walking the candidate parents), the
+    node set is S(n) (so the max-weight connected subtree, pinned above), and the array is
+    topological."""
+    rng = np.random.default_rng(11)
+    kx, ky = [0.0, 0.05, 0.2, 0.5, 1.0], [0.0, 0.15, 0.45, 0.75, 0.95]
+    for trial in range(40):
+        N = int(rng.integers(3, 40))
+        parent, o = make_candidate_tree(rng, N)
+        token = rng.integers(0, 1000, size=N).astype(np.int32)
+        w = [OS.acceptance_fit(kx, ky, x) for x in OS.draft_logits(parent, o)]
+        full = OS.layer_search_order(parent, w, N)
+        for n in sorted({1, 2, len(full) // 2 + 1, len(full)}):
+            pv, tv = OS.verification_tree(parent, o, token, 7, n, kx, ky)
+            assert len(pv) == n + 1 and pv[0] == -1 and tv[0] == 7
+            assert all(0 <= pv[i] < i for i in range(1, n + 1))
+            cand_paths = set()
+            for u in full[:n]:
+                seq, x = [], u
+                while x >= 0:
+                    seq.append(int(token[x]))
+                    x = int(parent[x])
+                cand_paths.add(tuple(reversed(seq)))
+            tree_paths = set()
+            for i in range(1, n + 1):
+                seq, x = [], i
+                while x > 0:
+                    seq.append(int(tv[x]))
+                    x = int(pv[x])
+                tree_paths.add(tuple(reversed(seq)))
+            assert tree_paths == cand_paths
+    with pytest.raises(ValueError):
+        OS.verification_tree(np.array([-1, 0], np.int32), np.array([0.5, 0.5]), np.array([1, 2], np.int32), 0, 3,
+                             kx, ky)
