@@ -346,6 +346,36 @@ def run_ours(args, world, rank, local):
                  "note": "remainder of the step (mask kernel + graph launch gaps)"},
     }
 
+    # ---------------- f3: GPU verification-tree construction (timed alone, outside the step) ----------------
+    if strat is not None:
+        sel_n = strat[3]["n"]
+        cands = strat[1]
+        cpar = torch.as_tensor(np.concatenate([p for p, _ in cands]), dtype=torch.int32, device=dev)
+        co = torch.as_tensor(np.concatenate([o for _, o in cands]), dtype=torch.float64, device=dev)
+        ctok = torch.randint(0, cfg.V, (cpar.numel(),), dtype=torch.int32, device=dev)
+        coff = torch.as_tensor(np.concatenate([[0], np.cumsum([len(p) for p, _ in cands])]), dtype=torch.int32,
+                               device=dev)
+        rtok = torch.zeros(cfg.B, dtype=torch.int32, device=dev)
+        kx = torch.tensor(STRATEGY_KX, dtype=torch.float64, device=dev)
+        ky = torch.tensor(STRATEGY_KY, dtype=torch.float64, device=dev)
+        ts_out = core.tree_select(cpar, co, ctok, coff, rtok, sel_n, kx, ky)
+        g_ts = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_ts):
+            core.tree_select(cpar, co, ctok, coff, rtok, sel_n, kx, ky, stream=torch.cuda.current_stream(), out=ts_out)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g_ts.replay()
+        e0.record()
+        for _ in range(20):
+            g_ts.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        same = bool(torch.equal(ts_out[0].cpu(), torch.as_tensor(b["parent"])))
+        kernels["tree_select"] = {"us_per_call": round(e0.elapsed_time(e1) * 1e3 / 20, 2), "launches": 1,
+                                  "candidates": int(cpar.numel()), "n": sel_n,
+                                  "parents_equal_host_selection": same,
+                                  "note": "f3 (SURVEY 8(f)): rs_tree_select timed alone (CUDA graph, 20 calls), "
+                                          "not part of the step"}
+
     # ---------------- end-to-end through the public API with host buffers ----------------
     e2e = run_e2e(step, b, args.e2e_steps, tokens_per_step, world, dev, barrier, mode, cfg.temperature)
 

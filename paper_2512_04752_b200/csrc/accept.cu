@@ -337,16 +337,19 @@ __device__ __forceinline__ int draw_bonus(Smem& sm, int& phase, uint64_t t, int 
 }
 
 // MODE is a template parameter so the greedy walk compiles without the 128-bit sampling
-// machinery (register budget: 4 CTAs/SM greedy, 2 CTAs/SM sampling).
-template <int MODE>
+// machinery (register budget: 4 CTAs/SM greedy, 2 CTAs/SM sampling); DT (the logits dtype)
+// too, so a bf16 vector occupies 4 registers, not 8.
+template <int MODE, int DT>
 __global__ void __launch_bounds__(kThreads, MODE == RS_ACCEPT_GREEDY ? 4 : 2)
-tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype, const float* __restrict__ draft,
+tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype_rt, const float* __restrict__ draft,
                    const int32_t* __restrict__ parent, const int32_t* __restrict__ token,
                    const int32_t* __restrict__ tree_off, const int64_t* __restrict__ gid, int V, float inv_tau,
                    uint64_t seed, uint64_t step, int32_t* __restrict__ acc_out, int32_t* __restrict__ path_out,
                    int32_t* __restrict__ bonus_out, int32_t* __restrict__ flags_out, bool logits_vec_ok,
                    bool draft_vec_ok, uint32_t* __restrict__ wbuf, int prefetch_children) {
     (void)mode_rt;
+    (void)dtype_rt;
+    constexpr int dtype = DT;
     constexpr int mode = MODE;
     __shared__ Smem sm;
     const uint32_t cs = cluster_size();
@@ -792,9 +795,14 @@ extern "C" rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t lo
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    auto kern = mode == RS_ACCEPT_GREEDY        ? tree_accept_kernel<RS_ACCEPT_GREEDY>
-                : mode == RS_ACCEPT_SAMPLE_DELTA ? tree_accept_kernel<RS_ACCEPT_SAMPLE_DELTA>
-                                                 : tree_accept_kernel<RS_ACCEPT_SAMPLE_MSS>;
+    const bool bf = logits_dtype == RS_DTYPE_BF16;
+    auto kern = mode == RS_ACCEPT_GREEDY
+                    ? (bf ? tree_accept_kernel<RS_ACCEPT_GREEDY, RS_DTYPE_BF16> : tree_accept_kernel<RS_ACCEPT_GREEDY, RS_DTYPE_F32>)
+                : mode == RS_ACCEPT_SAMPLE_DELTA
+                    ? (bf ? tree_accept_kernel<RS_ACCEPT_SAMPLE_DELTA, RS_DTYPE_BF16>
+                          : tree_accept_kernel<RS_ACCEPT_SAMPLE_DELTA, RS_DTYPE_F32>)
+                    : (bf ? tree_accept_kernel<RS_ACCEPT_SAMPLE_MSS, RS_DTYPE_BF16>
+                          : tree_accept_kernel<RS_ACCEPT_SAMPLE_MSS, RS_DTYPE_F32>);
     RS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, (int)mode, logits, (int)logits_dtype, draft_probs, parent, token,
                                      tree_off, gid, (int)V, inv_tau, seed, step, accepted_len, path, bonus_token,
                                      status_flags, lvec, dvec, static_cast<uint32_t*>(need ? ws : nullptr), pf));
