@@ -24,7 +24,8 @@ import torch
 
 __all__ = [
     "VerifyConfig", "CONFIGS", "TINY_PARENT", "random_tree_parents", "draw_prefix_lengths",
-    "make_verify_batch", "make_candidate_tree", "lmsys_response_lengths",
+    "make_verify_batch", "make_candidate_tree", "lmsys_response_lengths", "planted_targets",
+    "make_lm_head_inputs",
 ]
 
 # Tiny config tree: paths [0,1,3,6], [0,1,4,7], [0,2,5].
@@ -284,3 +285,49 @@ def make_candidate_tree(rng: np.random.Generator, n_nodes: int, branching=(4, 3,
     o = rng.beta(beta[0], beta[1], size=n_nodes) * (decay ** depth)
     o = np.clip(o, 1e-6, 1.0)
     return parent.astype(np.int32), o.astype(np.float64)
+
+
+def planted_targets(rng: np.random.Generator, parent: np.ndarray, tree_off: np.ndarray, token: np.ndarray,
+                    V: int, p_accept: float) -> np.ndarray:
+    """Per tree node, the token the target model is made to prefer: with probability p_accept
+    one child's token (so the greedy walk can advance), else a token no child carries."""
+    NT = int(tree_off[-1])
+    tgt = np.zeros(NT, dtype=np.int64)
+    for b in range(len(tree_off) - 1):
+        off = int(tree_off[b])
+        ch = _children_lists(np.asarray(parent[off:int(tree_off[b + 1])]))
+        for c, kids in enumerate(ch):
+            kid_toks = set(int(token[off + x]) for x in kids)
+            if kids and rng.random() < p_accept:
+                tgt[off + c] = token[off + kids[rng.integers(len(kids))]]
+            else:
+                t = int(rng.integers(V))
+                while t in kid_toks:
+                    t = int(rng.integers(V))
+                tgt[off + c] = t
+    return tgt
+
+
+def make_lm_head_inputs(batch: dict, Dm: int, seed: int = 7, device="cpu", gen_device: Optional[str] = None,
+                        p_accept: Optional[float] = None, plant: float = 0.1, noise: float = 0.25) -> dict:
+    """Final hidden states [NT, Dm] and an LM-head weight [V, Dm] (bf16) for the tree nodes of
+    `batch`. W ~ N(0, 1); hidden[r] = plant * W[tgt_r] + noise * N(0, 1), so
+    the target's preferred token at node r is tgt_r (planted_targets) by a wide margin
+    (plant*Dm against a noise sd of ~noise*sqrt(Dm)). The planted token is an input property
+    used to steer acceptance; tests never take it as the expected arg-max."""
+    cfg = batch["cfg"]
+    rng = np.random.default_rng(seed)
+    gen_device = gen_device or device
+    gen = torch.Generator(device=gen_device)
+    gen.manual_seed(seed + 777)
+    V, NT = batch["V"], batch["NT"]
+    pa = cfg.p_accept if p_accept is None else p_accept
+    tgt = planted_targets(rng, batch["parent"], batch["tree_off"], batch["token"], V, pa)
+    w = torch.empty((V, Dm), dtype=torch.bfloat16, device=device)
+    step = 8192
+    for v0 in range(0, V, step):      # bounded fp32 temporaries
+        v1 = min(V, v0 + step)
+        w[v0:v1].copy_(torch.randn((v1 - v0, Dm), generator=gen, device=gen_device).to(torch.bfloat16))
+    t = torch.from_numpy(tgt).to(w.device)
+    h = plant * w[t].float() + noise * torch.randn((NT, Dm), generator=gen, device=gen_device).to(w.device)
+    return dict(hidden=h.to(torch.bfloat16), weight=w, planted=tgt, Dm=Dm)
