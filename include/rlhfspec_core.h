@@ -71,6 +71,35 @@ rs_status rs_tree_build_mask(const int32_t* parent, const int32_t* tree_off, int
                              uint64_t* tree_mask, int32_t* depth, int32_t* status_flags,
                              void* stream);
 
+/* ===================================================================================== f2
+ * LM head fused with greedy acceptance. Verification scores every tree node
+ * in one target pass; the LM head is one of its GEMMs; greedy acceptance
+ * needs only each node's arg-max (DESIGN Z5, Z6). rs_lm_head_argmax computes
+ *     argmax_token[r] = argmax_v  sum_k hidden[r,k] * weight[v,k]      (ties -> lowest v)
+ * with fp32 accumulation on the tensor cores, reducing inside the GEMM epilogue, so the
+ * [rows, V] logits are never written.
+ *   hidden   device bf16 [rows, Dm] (final hidden state of each tree node, node-major as Q)
+ *   weight   device bf16 [V, Dm] (nn.Linear layout); both 16-byte aligned; Dm % 64 == 0
+ *   argmax_token device int32 [rows] out (-1 if a row's logits are all NaN)
+ *   max_logit    device fp32 [rows] out (the fp32 maximum), or NULL
+ *   ws, ws_bytes device workspace >= rs_lm_head_argmax_workspace_bytes(rows), 8-byte aligned
+ * Launches a memset, the GEMM kernel and a finalize kernel on `stream`. */
+size_t rs_lm_head_argmax_workspace_bytes(int32_t rows);
+rs_status rs_lm_head_argmax(const void* hidden, const void* weight, int32_t rows, int32_t V, int32_t Dm,
+                            int32_t* argmax_token, float* max_logit, void* ws, size_t ws_bytes,
+                            void* stream);
+
+/* Greedy walk given the per-node arg-max: from the root, move to the
+ * lowest-index child whose token equals argmax_token[current]; stop when none does.
+ *   argmax_token, parent, token device int32 [NT]; tree_off device int32 [B+1]
+ *   accepted_len [B], path [B,64] (-1 padded), bonus_token [B], status_flags [B]: as
+ *   rs_tree_accept GREEDY. A malformed tree sets RS_FLAG_MALFORMED (accepted_len 0, bonus -1);
+ *   a visited node with argmax_token < 0 sets RS_FLAG_NONFINITE (bonus -1). */
+rs_status rs_tree_accept_greedy_tokens(const int32_t* argmax_token, const int32_t* parent,
+                                       const int32_t* token, const int32_t* tree_off, int32_t B,
+                                       int32_t* accepted_len, int32_t* path, int32_t* bonus_token,
+                                       int32_t* status_flags, void* stream);
+
 /* ===================================================================================== f3
  * rs_tree_select — the verification trees of a batch, built on the GPU from the draft's
  * candidate trees for the n chosen by rs_select_strategy ("the selection of n";

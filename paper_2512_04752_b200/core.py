@@ -519,3 +519,44 @@ def migrate_samples(comm: Comm, src_rank, dst_rank, llm_layers, ssm_layers, page
                                    staging.numel() * staging.element_size(), _ptr(scratch), _stream(stream)),
            "rs_migrate_samples")
     return rows[:n] if comm.rank == dst_rank else None
+
+
+# ------------------------------------------------------------------ f2
+_sig("rs_lm_head_argmax_workspace_bytes", _sz, _i32)
+_sig("rs_lm_head_argmax", _i32, _P, _P, _i32, _i32, _i32, _P, _P, _P, _sz, _P)
+_sig("rs_tree_accept_greedy_tokens", _i32, _P, _P, _P, _P, _i32, _P, _P, _P, _P, _P)
+
+
+def lm_head_argmax_workspace_bytes(rows) -> int:
+    return int(_lib.rs_lm_head_argmax_workspace_bytes(int(rows)))
+
+
+def lm_head_argmax(hidden, weight, out=None, max_logit=True, ws=None, stream=None):
+    """Per-row arg-max of hidden @ weight^T (bf16 in, fp32 accumulate), computed in the GEMM
+    epilogue; returns (argmax_token int32 [rows], max_logit fp32 [rows] or None)."""
+    rows, Dm = hidden.shape
+    V = weight.shape[0]
+    dev = hidden.device
+    if out is None:
+        out = (torch.empty(rows, dtype=torch.int32, device=dev),
+               torch.empty(rows, dtype=torch.float32, device=dev) if max_logit else None)
+    tok, mx = out
+    need = lm_head_argmax_workspace_bytes(rows)
+    if ws is None:
+        ws = torch.empty(max(need, 8), dtype=torch.uint8, device=dev)
+    _check(_lib.rs_lm_head_argmax(_ptr(hidden), _ptr(weight), rows, V, Dm, _ptr(tok), _ptr(mx), _ptr(ws),
+                                  ws.numel(), _stream(stream)), "rs_lm_head_argmax")
+    return tok, mx
+
+
+def tree_accept_greedy_tokens(argmax_token, parent, token, tree_off, out=None, stream=None):
+    B = tree_off.numel() - 1
+    dev = parent.device
+    if out is None:
+        out = (torch.empty(B, dtype=torch.int32, device=dev), torch.empty((B, MAX_TREE), dtype=torch.int32, device=dev),
+               torch.empty(B, dtype=torch.int32, device=dev), torch.empty(B, dtype=torch.int32, device=dev))
+    acc, path, bonus, flags = out
+    _check(_lib.rs_tree_accept_greedy_tokens(_ptr(argmax_token), _ptr(parent), _ptr(token), _ptr(tree_off), B,
+                                             _ptr(acc), _ptr(path), _ptr(bonus), _ptr(flags), _stream(stream)),
+           "rs_tree_accept_greedy_tokens")
+    return acc, path, bonus, flags
