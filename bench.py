@@ -39,11 +39,19 @@ WORKLOAD_DESC = {
     "c4": "BASELINE configs[3]: one instance per B200, 256 samples per instance (2048 at 8), long-tail "
           "response lengths (LMSYS-shaped lognormal, cap 2048), Llama-3-8B shapes + 1 SSM layer, 16-node "
           "trees, greedy; samples finish and leave; periodic sample reallocation with KV migration (NCCL)",
+    "c2lm": "BASELINE configs[1] with the LM head in the step (SURVEY 8(f) f2): Llama-3-8B shapes, batch 64, "
+            "prefix 1K, 16-node tree, greedy acceptance from the nodes' final hidden states (4096) through the "
+            "fused LM-head arg-max (V=128256), logits never materialised",
+    "c5g8lm": "BASELINE configs[4] per-GPU shard at 8 GPUs with the LM head in the step (f2): Llama-3-70B shapes, "
+              "16 samples, prefix 8K, 64-node trees, greedy from hidden states (8192) via the fused LM-head arg-max",
     "c3s": "BASELINE configs[2] as the method runs it: Llama-3-8B shapes, batch 256, prefixes 512-16K "
            "lognormal, every tree = S(n) for the n select_strategy picks (host C++, called every step), "
            "rejection sampling (MSS)",
 }
 
+
+# f2 configs: (base config, hidden size of the model whose LM head feeds acceptance)
+LM_HEAD = {"c2lm": ("c2", 4096), "c5g8lm": ("c5g8", 8192)}
 
 # select_strategy inputs for configs with ("strategy", n_cand) trees: acceptance
 # fit F (knots) and a cost model t_sd = c_draft + b0 + b1*N_seq + b2*N_draft (seconds): b1 from the
@@ -172,8 +180,10 @@ def cpu_baseline(host, cfg, budget_s=12.0):
     from oracle import attention as OA
     from oracle import compact as OC
     from oracle import tree as OT
+    from oracle import lm_head as OLM
     masks, _, _ = OT.batch_masks(host["parent"], host["tree_off"])
-    lg_bits = host["logits"].contiguous().view(torch.int16).numpy().view(np.uint16)
+    lm = "hidden" in host
+    lg_bits = None if lm else host["logits"].contiguous().view(torch.int16).numpy().view(np.uint16)
     t0 = time.perf_counter()
     tokens, done = 0, 0
     L = host["q"].shape[0]
@@ -185,10 +195,16 @@ def cpu_baseline(host, cfg, budget_s=12.0):
                                      np.array([0, sl.stop - sl.start]), masks[sl], cfg.Hkv, cfg.page_size,
                                      host["sm_scale"])
         om = {"greedy": OAcc.GREEDY, "delta": OAcc.DELTA, "mss": OAcc.MSS}[cfg.mode]
-        acc, path, bonus, flags = OAcc.tree_accept(om, lg_bits[sl], host["parent"][sl], host["token"][sl],
-                                                   np.array([0, sl.stop - sl.start]), host["gid"][s:s + 1], cfg.V,
-                                                   draft_probs=host["draft"][sl] if om == OAcc.MSS else None,
-                                                   temperature=cfg.temperature, seed=11, step=0)
+        if lm:
+            lg = np.concatenate([OLM.lm_head_logits(host["hidden"][sl], w) for w in host["w64"]], axis=1)
+            am, _ = OLM.argmax_rows(lg)
+            acc, path, bonus = OLM.greedy_walk(am, host["parent"][sl], host["token"][sl],
+                                               np.array([0, sl.stop - sl.start]))
+        else:
+            acc, path, bonus, flags = OAcc.tree_accept(
+                om, lg_bits[sl], host["parent"][sl], host["token"][sl], np.array([0, sl.stop - sl.start]),
+                host["gid"][s:s + 1], cfg.V, draft_probs=host["draft"][sl] if om == OAcc.MSS else None,
+                temperature=cfg.temperature, seed=11, step=0)
         OC.kv_compact([host["kc_np"][l] for l in range(L)] + [host["vc_np"][l] for l in range(L)],
                       host["block_table"][s:s + 1], host["prefix_len"][s:s + 1], acc, path, cfg.page_size)
         tokens += int(acc[0]) + 1
@@ -197,7 +213,8 @@ def cpu_baseline(host, cfg, budget_s=12.0):
             break
     dt = time.perf_counter() - t0
     return dict(value=tokens / dt, unit=UNIT, cores=1, kind="oracle",
-                sample=f"{done} of {host['B']} samples of the workload, all {L} layers + accept + compact, "
+                sample=f"{done} of {host['B']} samples of the workload, all {L} layers + "
+                       f"{'LM-head arg-max (fp64) + greedy walk' if lm else 'accept'} + compact, "
                        f"numpy fp64 / C, single thread, {dt:.1f} s")
 
 
@@ -227,23 +244,29 @@ def main():
 def run_ours(args, world, rank, local):
     from paper_2512_04752_b200 import core
     from paper_2512_04752_b200.step import VerifyStep
-    from synth import CONFIGS, make_verify_batch
+    from synth import CONFIGS, make_lm_head_inputs, make_verify_batch
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    cfg = CONFIGS[args.config]
+    lm = LM_HEAD.get(args.config)
+    cfg = CONFIGS[lm[0] if lm else args.config]
     cfg = type(cfg)(**{**cfg.__dict__, "seed": cfg.seed + 1000 * rank})   # disjoint samples per rank
     strat = None
     if cfg.tree[0] == "strategy":
         strat = strategy_trees(cfg, core)
         b = make_verify_batch(cfg, device=dev, gen_device=dev, parents=strat[4])
     else:
-        b = make_verify_batch(cfg, device=dev, gen_device=dev)
+        b = make_verify_batch(cfg, device=dev, gen_device=dev, with_logits=lm is None)
     mode = {"greedy": core.GREEDY, "delta": core.SAMPLE_DELTA, "mss": core.SAMPLE_MSS}[cfg.mode]
-    step = VerifyStep(b, mode=mode, temperature=cfg.temperature)
+    lm_in = None
+    if lm is not None:
+        lm_in = make_lm_head_inputs(b, Dm=lm[1], seed=7 + 1000 * rank, device=dev, gen_device=dev)
+        b["hidden"], b["lm_weight"] = lm_in["hidden"], lm_in["weight"]
+    step = VerifyStep(b, mode=mode, temperature=cfg.temperature,
+                      lm_head=None if lm is None else (lm_in["hidden"], lm_in["weight"]))
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -264,7 +287,8 @@ def run_ours(args, world, rank, local):
     # after accept, after compact]
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches_per_step = 1 + step.L + 1 + 1     # mask, L x attention (split-KV merge fused), accept, compact
+    # mask, L x attention (split-KV merge fused), accept (f2: LM-head GEMM + finalize + walk), compact
+    launches_per_step = 1 + step.L + (1 if lm is None else 3) + 1
     # The step's device work is captured once into CUDA graphs (mask | L x attention | accept +
     # compact); every timed step replays them (the launches are still our kernels, counted below).
     g_mask, g_attn, g_acc, g_cmp = step.capture_parts(seed=11, step=0)
@@ -331,7 +355,7 @@ def run_ours(args, world, rank, local):
     # ---------------- per-kernel breakdown (HBM-bound rows against the same peak) ----------------
     path_np, acc_np = res["path"], res["accepted_len"]
     moves = int(sum(int(np.sum(path_np[i, 1:acc_np[i] + 1] != np.arange(1, acc_np[i] + 1))) for i in range(b["B"])))
-    esz = 2 if b["logits"].dtype == torch.bfloat16 else 4
+    esz = 2 if lm is not None or b["logits"].dtype == torch.bfloat16 else 4
     acc_bytes = tokens_per_step * cfg.V * (esz + (4 if mode == core.SAMPLE_MSS else 0))   # visited rows
     cmp_bytes = 2 * moves * step.L * 4 * cfg.Hkv * cfg.d
     kernels = {
@@ -345,6 +369,16 @@ def run_ours(args, world, rank, local):
         "mask": {"ms_per_step": round(ms_per_step - attn_ms - acc_ms - cmp_ms, 4), "launches": 1,
                  "note": "remainder of the step (mask kernel + graph launch gaps)"},
     }
+    if lm is not None:
+        lm_flops = 2.0 * b["NT"] * cfg.V * lm[1]
+        kernels.pop("accept")
+        kernels["lm_head_accept"] = {
+            "ms_per_step": round(acc_ms, 4), "launches": 3, "flops": lm_flops,
+            "TFLOPs": round(lm_flops / (acc_ms * 1e-3) / 1e12, 1),
+            "frac_tensor": round(lm_flops / (acc_ms * 1e-3) / 1e12 / tc_burst, 4), "peak_tflops": tc_burst,
+            "bound": "tensor", "logits_bytes_not_written": int(b["NT"]) * cfg.V * 2,
+            "note": "f2: rs_lm_head_argmax (tcgen05 GEMM [NT x Dm] x [V x Dm]^T, arg-max in the epilogue) "
+                    "+ finalize + rs_tree_accept_greedy_tokens walk"}
 
     # ---------------- f3: GPU verification-tree construction (timed alone, outside the step) ----------------
     if strat is not None:
@@ -392,6 +426,8 @@ def run_ours(args, world, rank, local):
                          (2 * b["k_cache"].numel() * 2 / 1e9),
                    "parallelism": f"dp{world} (independent sample-sharded instances, no collective)",
                    "attn_plan": info,
+                   **({"lm_head": {"hidden": lm[1], "fused_argmax": True, "weight_GB": round(cfg.V * lm[1] * 2 / 1e9, 2)}}
+                      if lm is not None else {}),
                    **({"select_strategy": {"n": strat[3]["n"], "T": strat[3]["n"] + 1, "depth": strat[3]["depth"],
                                            "width": strat[3]["width"], "pred_al": round(strat[3]["al"], 2),
                                            "pred_t_sd_ms": round(strat[3]["t_sd"] * 1e3, 3),
@@ -563,17 +599,22 @@ def run_e2e(step, b, n_steps, tokens_per_step, world, dev, barrier, mode, temper
     compute = torch.cuda.current_stream()
     copy = torch.cuda.Stream()
     # a second step object with its own input buffers (KV caches and metadata layout shared)
+    # per-step inputs: Q of every layer, then logits (or, f2, the nodes' final hidden states; the
+    # LM-head weight is model state, resident like the KV cache), then MSS draft probabilities
     b2 = dict(b)
     b2["q"] = torch.empty_like(step.q)
-    b2["logits"] = torch.empty_like(step.logits)
+    lm = step.hidden is not None
+    if lm:
+        b2["hidden"] = torch.empty_like(step.hidden)
+    else:
+        b2["logits"] = torch.empty_like(step.logits)
     if step.draft is not None:
         b2["draft_probs"] = torch.empty_like(step.draft)
-    step2 = VerifyStep(b2, mode=mode, temperature=temperature)
+    step2 = VerifyStep(b2, mode=mode, temperature=temperature,
+                       lm_head=(b2["hidden"], step.lm_w) if lm else None)
     steps = [step, step2]
-    h_q = torch.empty(step.q.shape, dtype=step.q.dtype, pin_memory=True)
-    h_q.copy_(step.q)
-    h_logits = torch.empty(step.logits.shape, dtype=step.logits.dtype, pin_memory=True)
-    h_logits.copy_(step.logits)
+    ins = [[s.q, s.hidden if lm else s.logits] for s in steps]
+    h_ins = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t) for t in ins[0]]
     metas = [[s.parent, s.token, s.tree_off, s.prefix_len, s.block_table, s.gid] for s in steps]
     h_meta = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t) for t in metas[0]]
     h_draft = None
@@ -581,7 +622,7 @@ def run_e2e(step, b, n_steps, tokens_per_step, world, dev, barrier, mode, temper
         h_draft = torch.empty(step.draft.shape, dtype=step.draft.dtype, pin_memory=True).copy_(step.draft)
     outs = [[s.acc, s.path, s.bonus, s.new_len] for s in steps]
     h_outs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in outs[0]]
-    h2d = h_q.numel() * 2 + h_logits.numel() * 2 + sum(t.numel() * t.element_size() for t in h_meta)
+    h2d = sum(t.numel() * t.element_size() for t in h_ins + h_meta)
     if h_draft is not None:
         h2d += h_draft.numel() * 4
     d2h = sum(t.numel() * t.element_size() for t in h_outs)
@@ -597,8 +638,8 @@ def run_e2e(step, b, n_steps, tokens_per_step, world, dev, barrier, mode, temper
         with torch.cuda.stream(copy):
             if k >= 2:
                 copy.wait_event(done[i])          # buffer i free again (its step finished)
-            st.q.copy_(h_q, non_blocking=True)
-            st.logits.copy_(h_logits, non_blocking=True)
+            for t, h in zip(ins[i], h_ins):
+                t.copy_(h, non_blocking=True)
             for t, h in zip(metas[i], h_meta):
                 t.copy_(h, non_blocking=True)
             if h_draft is not None:
@@ -618,6 +659,8 @@ def run_e2e(step, b, n_steps, tokens_per_step, world, dev, barrier, mode, temper
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     return {"value": round(tokens_per_step * world * n_steps / (ms / 1e3), 1), "unit": UNIT,
+            "inputs": "Q (all layers) + " + ("final hidden states (f2)" if lm else "logits") +
+                      (" + draft probabilities" if step.draft is not None else "") + " + tree metadata",
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": n_steps,
             "ms_per_step": round(ms / n_steps, 3),
             "pipelining": "double-buffered inputs: upload of step k+1 overlaps kernels of step k"}
@@ -634,7 +677,12 @@ def run_cpu_baseline(cfg, b):
     host["prefix_len"], host["block_table"], host["gid"] = b["prefix_len"][:nsamp], b["block_table"][:nsamp], b["gid"][:nsamp]
     host["B"] = nsamp
     host["q"] = b["q"][:, :ns].cpu()
-    host["logits"] = b["logits"][:ns].cpu()
+    if b.get("hidden") is not None:     # f2: the oracle LM head (fp64) on the sampled rows
+        host["hidden"] = b["hidden"][:ns].double().cpu().numpy()
+        host["w64"] = [b["lm_weight"][v0:v0 + 8192].double().cpu().numpy()
+                       for v0 in range(0, b["lm_weight"].shape[0], 8192)]
+    else:
+        host["logits"] = b["logits"][:ns].cpu()
     host["draft"] = b["draft_probs"][:ns].float().cpu().numpy() if b.get("draft_probs") is not None else None
     # only the pages of the sampled samples are copied (the cache itself stays on the GPU)
     pages = np.unique(host["block_table"])

@@ -2,6 +2,9 @@
 
     rs_tree_build_mask -> rs_tree_verify_attention_layers (L layers) -> rs_tree_accept -> rs_kv_compact
 
+With `lm_head=(hidden, weight)` (f2, greedy only) acceptance starts from the nodes' final hidden
+states instead of materialised logits: rs_lm_head_argmax -> rs_tree_accept_greedy_tokens.
+
 Pure orchestration: buffers are torch tensors, every computation is a library call; arguments
 are marshalled once so a step costs four ctypes calls. The device part can be captured into a
 CUDA graph (one launch per step)."""
@@ -14,7 +17,7 @@ from . import core
 
 class VerifyStep:
     def __init__(self, batch: dict, mode: int = core.GREEDY, temperature: float = 1.0, num_ctas: int = 0,
-                 with_lse: bool = False):
+                 with_lse: bool = False, lm_head=None):
         b = batch
         dev = b["q"].device
         self.b = b
@@ -35,7 +38,10 @@ class VerifyStep:
         self.q = b["q"]
         self.k_layers = [b["k_cache"][l] for l in range(self.L)]
         self.v_layers = [b["v_cache"][l] for l in range(self.L)]
-        self.logits = b["logits"]
+        self.logits = b.get("logits")
+        self.hidden, self.lm_w = lm_head if lm_head is not None else (None, None)
+        if self.hidden is not None:
+            assert mode == core.GREEDY, "the fused LM head feeds greedy acceptance only"
         self.draft = b.get("draft_probs") if mode == core.SAMPLE_MSS else None
         NT = self.q.shape[1]
         self.mask = torch.empty(NT, dtype=torch.int64, device=dev)
@@ -53,7 +59,10 @@ class VerifyStep:
         self.bonus = torch.empty(self.B, dtype=torch.int32, device=dev)
         self.flags = torch.empty(self.B, dtype=torch.int32, device=dev)
         self.new_len = torch.empty(self.B, dtype=torch.int32, device=dev)
-        nws = core.accept_workspace_bytes(mode, self.B, self.logits.shape[1])
+        nws = core.accept_workspace_bytes(mode, self.B, b["V"]) if self.hidden is None else 0
+        if self.hidden is not None:
+            self.amax = torch.empty(NT, dtype=torch.int32, device=dev)
+            self.lm_ws = torch.empty(max(core.lm_head_argmax_workspace_bytes(NT), 8), dtype=torch.uint8, device=dev)
         self.accept_ws = torch.empty(max(nws, 16), dtype=torch.uint8, device=dev)   # MSS residual weights
         self.attn_call = core.AttentionLayersCall(
             self.plan, [self.q[l] for l in range(self.L)], self.k_layers, self.v_layers, self.block_table,
@@ -68,6 +77,11 @@ class VerifyStep:
         self.attn_call(stream)
 
     def accept_step(self, seed, step, stream=None):
+        if self.hidden is not None:
+            core.lm_head_argmax(self.hidden, self.lm_w, out=(self.amax, None), ws=self.lm_ws, stream=stream)
+            core.tree_accept_greedy_tokens(self.amax, self.parent, self.token, self.tree_off,
+                                           out=(self.acc, self.path, self.bonus, self.flags), stream=stream)
+            return
         core.tree_accept(self.mode, self.logits, self.parent, self.token, self.tree_off, self.gid,
                          draft_probs=self.draft, temperature=self.temperature, seed=seed, step=step,
                          out=(self.acc, self.path, self.bonus, self.flags), stream=stream, ws=self.accept_ws)

@@ -178,3 +178,22 @@ def test_walk_random_and_edge_cases(cuda_lib):
     ok[[2, 3]] = False
     assert np.array_equal(acc[ok], racc[ok]) and np.array_equal(path[ok], rpath[ok])
     assert not flags[ok].any()
+
+
+def test_verify_step_with_fused_lm_head(cuda_lib):
+    """VerifyStep(lm_head=...) — the bench's c2lm step on one layer: acceptance from hidden
+    states equals the oracle's fp64 arg-max -> walk, and compaction follows the accepted path."""
+    from paper_2512_04752_b200.step import VerifyStep
+    b = make_verify_batch(CONFIGS["c2"], device="cuda", layers=1, with_logits=False)
+    inp = make_lm_head_inputs(b, Dm=4096, device="cuda")
+    st = VerifyStep(b, mode=cuda_lib.GREEDY, lm_head=(inp["hidden"], inp["weight"]))
+    res = st.run(seed=0, step=0)
+    rng = np.random.default_rng(3)
+    amax = st.amax.cpu().numpy()
+    rows = np.sort(rng.choice(b["NT"], size=32, replace=False))
+    ref, tol = _reference(inp["hidden"].double().cpu().numpy()[rows], inp["weight"])
+    assert np.array_equal(amax[rows], LH.argmax_rows(ref)[0])
+    racc, rpath, rbonus = LH.greedy_walk(amax, b["parent"], b["token"], b["tree_off"])
+    assert np.array_equal(res["accepted_len"], racc) and np.array_equal(res["path"], rpath)
+    assert np.array_equal(res["bonus"], rbonus)
+    assert np.array_equal(res["new_len"], b["prefix_len"] + 1 + racc)

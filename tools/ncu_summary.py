@@ -17,7 +17,8 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-OURS = ("tree_attn", "attn_combine", "tree_accept", "accept_kernel", "kv_compact", "tree_mask", "kv_pack")
+OURS = ("tree_attn", "attn_combine", "tree_accept", "accept_kernel", "kv_compact", "tree_mask", "kv_pack", "lm_head",
+        "greedy_walk", "tree_select")
 
 METRICS = [
     "gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second", "dram__bytes_read.sum", "dram__bytes_write.sum",
