@@ -27,15 +27,19 @@ def segment_table(models, lens):
     return segs, off
 
 
-def pack(model_caches, block_tables, lens, page_size):
+def pack(model_caches, block_tables, lens, page_size, starts=None):
     """model_caches: per model a list over layers of (K, V) arrays [pages, Hkv, ps, d].
     block_tables: per sample a page list (same page ids in every layer/model).
+    starts: optional per-sample first token (default 0): the segment then holds tokens
+    starts[s] .. starts[s]+lens[s]-1 — the two-stage migration sends the verified
+    prefix first and the tokens verified meanwhile second, each in this same layout.
     Returns the 1-D buffer (dtype of the caches)."""
     parts = []
     for layers in model_caches:
         for (K, V) in layers:
             for s, n in enumerate(lens):
-                slots = np.arange(int(n))
+                t0 = 0 if starts is None else int(starts[s])
+                slots = np.arange(t0, t0 + int(n))
                 pages = np.asarray(block_tables[s])[slots // page_size]
                 rows = slots % page_size
                 for cache in (K, V):
@@ -46,7 +50,7 @@ def pack(model_caches, block_tables, lens, page_size):
     return np.concatenate(parts)
 
 
-def unpack(buf, model_caches, block_tables, lens, page_size):
+def unpack(buf, model_caches, block_tables, lens, page_size, starts=None):
     """Inverse of pack into the destination caches (modified in place) using the
     destination's block tables."""
     off = 0
@@ -55,7 +59,8 @@ def unpack(buf, model_caches, block_tables, lens, page_size):
             Hkv, d = K.shape[1], K.shape[3]
             for s, n in enumerate(lens):
                 n = int(n)
-                slots = np.arange(n)
+                t0 = 0 if starts is None else int(starts[s])
+                slots = np.arange(t0, t0 + n)
                 pages = np.asarray(block_tables[s])[slots // page_size]
                 rows = slots % page_size
                 for cache in (K, V):

@@ -146,3 +146,45 @@ def test_pack_unpack_round_trip_bytes():
                             a = src[m][l][t][src_bt[s][j // ps], :, j % ps, :]
                             b = dst[m][l][t][dst_bt[s][j // ps], :, j % ps, :]
                             np.testing.assert_array_equal(a, b)
+
+
+def test_two_stage_ranges_compose():
+    """Two-stage migration: stage 1 carries tokens [0, a), stage 2 tokens [a, b)
+    (verified on the source meanwhile). Both buffers use the one-shot layout restricted to the
+    range, and unpacking both reproduces the one-shot migration of [0, b) byte for byte; a
+    buffer's segment (model, layer, sample, K|V, head) is exactly the one-shot segment's token
+    range."""
+    rng = np.random.default_rng(3)
+    ps = 4
+    models = [(1, 1, 8), (2, 2, 8)]
+    for trial in range(15):
+        ns = int(rng.integers(1, 4))
+        b_len = [int(x) for x in rng.integers(1, 15, size=ns)]
+        a_len = [int(rng.integers(0, x + 1)) for x in b_len]
+        need = [(n + ps - 1) // ps for n in b_len]
+        cuts = np.concatenate([[0], np.cumsum(need)])
+        sp, dp = rng.permutation(40), rng.permutation(40)
+        src_bt = [sp[cuts[i]:cuts[i + 1]] for i in range(ns)]
+        dst_bt = [dp[cuts[i]:cuts[i + 1]] for i in range(ns)]
+        src = [[(rng.integers(0, 2**16, size=(40, H, ps, d)).astype(np.uint16),
+                 rng.integers(0, 2**16, size=(40, H, ps, d)).astype(np.uint16)) for _ in range(L)]
+               for (L, H, d) in models]
+        zero = lambda: [[(np.zeros((40, H, ps, d), np.uint16), np.zeros((40, H, ps, d), np.uint16))
+                         for _ in range(L)] for (L, H, d) in models]
+        one, two = zero(), zero()
+        OM.unpack(OM.pack(src, src_bt, b_len, ps), one, dst_bt, b_len, ps)
+        delta = [b - a for a, b in zip(a_len, b_len)]
+        buf1 = OM.pack(src, src_bt, a_len, ps)
+        buf2 = OM.pack(src, src_bt, delta, ps, starts=a_len)
+        assert buf1.size + buf2.size == OM.segment_table(models, b_len)[1]
+        OM.unpack(buf1, two, dst_bt, a_len, ps)
+        OM.unpack(buf2, two, dst_bt, delta, ps, starts=a_len)
+        for m in range(len(models)):
+            for l in range(models[m][0]):
+                for t in range(2):
+                    np.testing.assert_array_equal(one[m][l][t], two[m][l][t])
+        # segment check: first segment of buf2 = tokens [a, b) of head 0.. of sample 0, K, SSM layer 0
+        H, d = models[0][1], models[0][2]
+        full = OM.pack(src, src_bt, b_len, ps)
+        segK = full[:H * b_len[0] * d].reshape(H, b_len[0], d)
+        np.testing.assert_array_equal(buf2[:H * delta[0] * d].reshape(H, delta[0], d), segK[:, a_len[0]:, :])
