@@ -300,6 +300,18 @@ rs_status rs_kv_unpack(void* const* k_layers_host, void* const* v_layers_host, i
                        int32_t Hkv, int32_t head_dim, int32_t page_size, const int32_t* block_table,
                        int32_t max_pages, const int32_t* sample_rows, const int32_t* lens,
                        int32_t n, const void* buf, int64_t buf_offset_elems, void* stream);
+/* Token-range variants (f1): sample i contributes tokens starts[i] .. starts[i]+lens[i]-1
+ * (starts device int32 [n]); the buffer layout is the one above with len = lens[i]. */
+rs_status rs_kv_pack_range(void* const* k_layers_host, void* const* v_layers_host, int32_t L,
+                           int32_t Hkv, int32_t head_dim, int32_t page_size, const int32_t* block_table,
+                           int32_t max_pages, const int32_t* sample_rows, const int32_t* starts,
+                           const int32_t* lens, int32_t n, void* buf, int64_t buf_offset_elems,
+                           void* stream);
+rs_status rs_kv_unpack_range(void* const* k_layers_host, void* const* v_layers_host, int32_t L,
+                             int32_t Hkv, int32_t head_dim, int32_t page_size, const int32_t* block_table,
+                             int32_t max_pages, const int32_t* sample_rows, const int32_t* starts,
+                             const int32_t* lens, int32_t n, const void* buf, int64_t buf_offset_elems,
+                             void* stream);
 
 /* Host page allocator of one instance's paged KV store (same page ids in every layer/model).
  * Allocation is all-or-nothing: RS_ERR_NO_MEMORY and nothing reserved if too few pages are
@@ -347,6 +359,42 @@ rs_status rs_migrate_samples(rs_comm* comm, int32_t src_rank, int32_t dst_rank,
                              const int32_t* lens_host, int32_t n, const int32_t* src_block_table,
                              int32_t max_pages, int32_t* dst_block_table_host, void* staging,
                              size_t staging_bytes, int32_t* device_scratch, void* stream);
+
+/* ===================================================================================== f1
+ * Two-stage sample migration. Both ranks of the pair call each
+ * stage with identical n (other ranks return at once); arguments marked src / dst are read on
+ * that side only. Each stage starts with a small blocking handshake (request, all-or-nothing
+ * page reservation on the destination, answer; refusal -> RS_ERR_NO_MEMORY on both ranks and
+ * nothing is sent), then ENQUEUES pack -> NCCL send/recv -> unpack on `stream` and
+ * returns without waiting: staging, device_scratch and the host block-table rows must stay
+ * valid until `stream` has passed this work.
+ *
+ * Stage 1 — the verified prefix, while both instances keep computing on other streams (later
+ * verification steps write only slots >= lens[i], the Markov property of verification):
+ *   src: gids_host, lens_host [n] (tokens verified at the trigger), reserve_lens_host [n]
+ *        (>= lens: tokens the destination reserves pages for), src_block_table device [n, max_pages]
+ *   dst: pool, dst_block_table_host [n, max_pages] out (reserved rows)
+ *   staging >= 2 * rs_kv_pack_elems(all models, lens) bytes; device_scratch int32 >= 2n + n*max_pages.
+ * Stage 2 — the tokens verified on the source since stage 1 (the sample is paused on the
+ * source from the call): tokens starts[i] .. starts[i]+lens[i]-1. The SSM part is sent and
+ * unpacked first and `ssm_ready_event` (cudaEvent_t, may be NULL) is recorded on the
+ * destination's `stream` once it has landed — drafting may resume there — then the
+ * LLM part follows; the samples may be verified on the destination after `stream` completes.
+ *   src: starts_host, lens_host [n], src_block_table
+ *   dst: pool; dst_block_table_host (in: stage-1 rows, out: extended when a sample outgrew its
+ *        reservation); dst_capacity_host int32 [n] (in/out: tokens the row's pages hold)
+ *   device_scratch int32 >= 3n + n*max_pages. */
+rs_status rs_migrate_stage1(rs_comm* comm, int32_t src_rank, int32_t dst_rank, const rs_kv_desc* kv,
+                            rs_page_pool* pool, const int64_t* gids_host, const int32_t* lens_host,
+                            const int32_t* reserve_lens_host, int32_t n, const int32_t* src_block_table,
+                            int32_t max_pages, int32_t* dst_block_table_host, void* staging,
+                            size_t staging_bytes, int32_t* device_scratch, void* stream);
+rs_status rs_migrate_stage2(rs_comm* comm, int32_t src_rank, int32_t dst_rank, const rs_kv_desc* kv,
+                            rs_page_pool* pool, const int32_t* starts_host, const int32_t* lens_host,
+                            int32_t n, const int32_t* src_block_table, int32_t max_pages,
+                            int32_t* dst_block_table_host, int32_t* dst_capacity_host, void* staging,
+                            size_t staging_bytes, int32_t* device_scratch, void* ssm_ready_event,
+                            void* stream);
 
 #ifdef __cplusplus
 }

@@ -560,3 +560,96 @@ def tree_accept_greedy_tokens(argmax_token, parent, token, tree_off, out=None, s
                                              _ptr(acc), _ptr(path), _ptr(bonus), _ptr(flags), _stream(stream)),
            "rs_tree_accept_greedy_tokens")
     return acc, path, bonus, flags
+
+
+# ------------------------------------------------------------------ f1 (two-stage migration)
+_sig("rs_kv_pack_range", _i32, _P, _P, _i32, _i32, _i32, _i32, _P, _i32, _P, _P, _P, _i32, _P, _i64, _P)
+_sig("rs_kv_unpack_range", _i32, _P, _P, _i32, _i32, _i32, _i32, _P, _i32, _P, _P, _P, _i32, _P, _i64, _P)
+_sig("rs_migrate_stage1", _i32, _P, _i32, _i32, ctypes.POINTER(KVDescC), _P, _P, _P, _P, _i32, _P, _i32, _P, _P, _sz,
+     _P, _P)
+_sig("rs_migrate_stage2", _i32, _P, _i32, _i32, ctypes.POINTER(KVDescC), _P, _P, _P, _i32, _P, _i32, _P, _P, _P, _sz,
+     _P, _P, _P)
+
+
+def kv_pack_range(k_layers, v_layers, block_table, sample_rows, starts, lens, buf, offset_elems=0, stream=None):
+    _, Hkv, ps, d = k_layers[0].shape
+    _check(_lib.rs_kv_pack_range(_layer_ptrs(k_layers), _layer_ptrs(v_layers), len(k_layers), Hkv, d, ps,
+                                 _ptr(block_table), block_table.shape[1], _ptr(sample_rows), _ptr(starts), _ptr(lens),
+                                 lens.numel(), _ptr(buf), int(offset_elems), _stream(stream)), "rs_kv_pack_range")
+    return buf
+
+
+def kv_unpack_range(k_layers, v_layers, block_table, sample_rows, starts, lens, buf, offset_elems=0, stream=None):
+    _, Hkv, ps, d = k_layers[0].shape
+    _check(_lib.rs_kv_unpack_range(_layer_ptrs(k_layers), _layer_ptrs(v_layers), len(k_layers), Hkv, d, ps,
+                                   _ptr(block_table), block_table.shape[1], _ptr(sample_rows), _ptr(starts),
+                                   _ptr(lens), lens.numel(), _ptr(buf), int(offset_elems), _stream(stream)),
+           "rs_kv_unpack_range")
+
+
+def _kv_desc(llm_layers, ssm_layers, page_size):
+    keep = []
+
+    def _model(m):
+        if not m:
+            return None, None, 0, 1, 8
+        k, v = m
+        kp, vp = _layer_ptrs(k), _layer_ptrs(v)
+        keep.extend([kp, vp])
+        return kp, vp, len(k), k[0].shape[1], k[0].shape[3]
+    ks, vs, Ls, Hs, ds = _model(ssm_layers)
+    kl, vl, Ll, Hl, dl = _model(llm_layers)
+    desc = KVDescC(ctypes.cast(ks, _P) if ks else None, ctypes.cast(vs, _P) if vs else None, Ls, Hs, ds,
+                   ctypes.cast(kl, _P), ctypes.cast(vl, _P), Ll, Hl, dl, int(page_size))
+    return desc, keep
+
+
+class TwoStageMigration:
+    """f1: stage1() enqueues the verified prefix [0, lens) on `stream` and returns
+    while the instances keep computing; stage2(new_lens) moves [lens, new_lens) with the SSM part
+    first (`ssm_ready` event recorded on the destination) and the LLM part behind it. Both ranks
+    of the pair drive the same object calls; the staging / scratch buffers stay referenced here
+    until the stream is done."""
+
+    def __init__(self, comm: Comm, src_rank, dst_rank, llm_layers, ssm_layers, page_size, pool: PagePool | None,
+                 max_pages, staging, scratch, stream):
+        self.comm, self.src, self.dst = comm, int(src_rank), int(dst_rank)
+        self.desc, self._keep = _kv_desc(llm_layers, ssm_layers, page_size)
+        self.pool, self.max_pages, self.staging, self.scratch, self.stream = pool, int(max_pages), staging, scratch, stream
+        self.ps = int(page_size)
+        self.rows = None
+        self.capacity = None
+        self.ssm_ready = torch.cuda.Event(enable_timing=True)
+        self.done = torch.cuda.Event(enable_timing=True)
+        self.ssm_ready.record(stream)      # torch creates the CUDA event lazily, on first record
+        self.done.record(stream)
+
+    def stage1(self, gids, lens, reserve_lens, src_block_table):
+        n = len(lens)
+        self.n = n
+        self.lens1 = _host_i32(lens)
+        g = np.ascontiguousarray(gids, dtype=np.int64)
+        rsv = _host_i32(reserve_lens)
+        self.rows = np.zeros((max(n, 1), self.max_pages), np.int32)
+        _check(_lib.rs_migrate_stage1(self.comm._h, self.src, self.dst, ctypes.byref(self.desc),
+                                      self.pool.handle if self.pool is not None else None, _ptr(g), _ptr(self.lens1),
+                                      _ptr(rsv), n, _ptr(src_block_table), self.max_pages, _ptr(self.rows),
+                                      _ptr(self.staging), self.staging.numel() * self.staging.element_size(),
+                                      _ptr(self.scratch), _stream(self.stream)), "rs_migrate_stage1")
+        self.capacity = np.ascontiguousarray(rsv.copy())
+        self.done.record(self.stream)
+
+    def stage2(self, new_lens, src_block_table):
+        starts = self.lens1
+        delta = _host_i32(np.asarray(new_lens) - starts)
+        _check(_lib.rs_migrate_stage2(self.comm._h, self.src, self.dst, ctypes.byref(self.desc),
+                                      self.pool.handle if self.pool is not None else None, _ptr(starts), _ptr(delta),
+                                      self.n, _ptr(src_block_table), self.max_pages, _ptr(self.rows),
+                                      _ptr(self.capacity), _ptr(self.staging),
+                                      self.staging.numel() * self.staging.element_size(), _ptr(self.scratch),
+                                      ctypes.c_void_p(self.ssm_ready.cuda_event) if self.comm.rank == self.dst else None,
+                                      _stream(self.stream)), "rs_migrate_stage2")
+        self.done.record(self.stream)
+
+    def dst_rows(self):
+        return self.rows[:self.n] if self.comm.rank == self.dst else None

@@ -35,7 +35,8 @@ struct LayerPtrs {
 template <bool PACK>
 __global__ void __launch_bounds__(kThreads)
 kv_pack_kernel(LayerPtrs layers, int Hkv, int d, int ps, const int32_t* __restrict__ block_table, int max_pages,
-               const int32_t* __restrict__ rows, const int32_t* __restrict__ lens, int n, uint4* buf) {
+               const int32_t* __restrict__ rows, const int32_t* __restrict__ starts, const int32_t* __restrict__ lens,
+               int n, uint4* buf) {
     const int s = blockIdx.x, l = blockIdx.y, kv = blockIdx.z;
     long long total = 0, before = 0;
     for (int i = 0; i < n; ++i) {
@@ -43,19 +44,20 @@ kv_pack_kernel(LayerPtrs layers, int Hkv, int d, int ps, const int32_t* __restri
         if (i < s) before += li;
         total += li;
     }
-    const int len = __ldg(lens + s);
+    const int len = __ldg(lens + s);                          // tokens [st0, st0 + len) of the sample
+    const int st0 = starts ? __ldg(starts + s) : 0;
     if (len <= 0) return;
     const int vpr = d / 8;                                   // 16-byte vectors per token row
     uint4* seg = buf + ((long long)l * 2 * Hkv * total + 2LL * Hkv * before + (long long)kv * Hkv * len) * vpr;
     uint4* cache = reinterpret_cast<uint4*>(kv ? layers.v[l] : layers.k[l]);
     const int32_t* bt = block_table + (int64_t)__ldg(rows + s) * max_pages;
-    const int npg = (len + ps - 1) / ps;
+    const int pg0 = st0 / ps, npg = (st0 + len - 1) / ps - pg0 + 1;
     for (int run = 0; run < npg * Hkv; ++run) {
-        const int pg = run / Hkv, h = run - pg * Hkv;
-        const int t0 = pg * ps;
-        const int nt = min(ps, len - t0);                     // tokens of this page in the sample
-        uint4* c = cache + (((long long)__ldg(bt + pg) * Hkv + h) * ps) * vpr;
-        uint4* bsg = seg + ((long long)h * len + t0) * vpr;
+        const int pg = pg0 + run / Hkv, h = run % Hkv;
+        const int t0 = max(st0, pg * ps);
+        const int nt = min(st0 + len, (pg + 1) * ps) - t0;   // tokens of the range on this page
+        uint4* c = cache + (((long long)__ldg(bt + pg) * Hkv + h) * ps + (t0 - pg * ps)) * vpr;
+        uint4* bsg = seg + ((long long)h * len + (t0 - st0)) * vpr;
         const int nv = nt * vpr;
         const uint4* src = PACK ? c : bsg;
         uint4* dst = PACK ? bsg : c;
@@ -73,8 +75,8 @@ kv_pack_kernel(LayerPtrs layers, int Hkv, int d, int ps, const int32_t* __restri
 
 template <bool PACK>
 rs_status launch_pack(void* const* k_layers, void* const* v_layers, int32_t L, int32_t Hkv, int32_t d, int32_t ps,
-                      const int32_t* block_table, int32_t max_pages, const int32_t* rows, const int32_t* lens,
-                      int32_t n, void* buf, int64_t off, cudaStream_t st) {
+                      const int32_t* block_table, int32_t max_pages, const int32_t* rows, const int32_t* starts,
+                      const int32_t* lens, int32_t n, void* buf, int64_t off, cudaStream_t st) {
     RS_REQUIRE(L >= 0 && L <= kMaxLayers && Hkv > 0 && d % 8 == 0 && ps > 0 && n >= 0, RS_ERR_INVALID_ARG,
                "rs_kv_pack/unpack: bad sizes");
     RS_REQUIRE(off % 8 == 0 && (reinterpret_cast<uintptr_t>(buf) & 15) == 0, RS_ERR_INVALID_ARG,
@@ -88,7 +90,7 @@ rs_status launch_pack(void* const* k_layers, void* const* v_layers, int32_t L, i
         lp.v[i] = v_layers[i];
     }
     dim3 grid(n, L, 2);
-    kv_pack_kernel<PACK><<<grid, kThreads, 0, st>>>(lp, Hkv, d, ps, block_table, max_pages, rows, lens, n,
+    kv_pack_kernel<PACK><<<grid, kThreads, 0, st>>>(lp, Hkv, d, ps, block_table, max_pages, rows, starts, lens, n,
                                                     reinterpret_cast<uint4*>(static_cast<uint16_t*>(buf) + off));
     RS_LAUNCH_CHECK();
     return RS_OK;
@@ -107,7 +109,26 @@ extern "C" rs_status rs_kv_pack(void* const* k_layers_host, void* const* v_layer
                                 const int32_t* sample_rows, const int32_t* lens, int32_t n, void* buf,
                                 int64_t buf_offset_elems, void* stream) {
     return launch_pack<true>(k_layers_host, v_layers_host, L, Hkv, head_dim, page_size, block_table, max_pages,
-                             sample_rows, lens, n, buf, buf_offset_elems, rs::as_stream(stream));
+                             sample_rows, nullptr, lens, n, buf, buf_offset_elems, rs::as_stream(stream));
+}
+
+extern "C" rs_status rs_kv_pack_range(void* const* k_layers_host, void* const* v_layers_host, int32_t L, int32_t Hkv,
+                                      int32_t head_dim, int32_t page_size, const int32_t* block_table,
+                                      int32_t max_pages, const int32_t* sample_rows, const int32_t* starts,
+                                      const int32_t* lens, int32_t n, void* buf, int64_t buf_offset_elems,
+                                      void* stream) {
+    return launch_pack<true>(k_layers_host, v_layers_host, L, Hkv, head_dim, page_size, block_table, max_pages,
+                             sample_rows, starts, lens, n, buf, buf_offset_elems, rs::as_stream(stream));
+}
+
+extern "C" rs_status rs_kv_unpack_range(void* const* k_layers_host, void* const* v_layers_host, int32_t L,
+                                        int32_t Hkv, int32_t head_dim, int32_t page_size, const int32_t* block_table,
+                                        int32_t max_pages, const int32_t* sample_rows, const int32_t* starts,
+                                        const int32_t* lens, int32_t n, const void* buf, int64_t buf_offset_elems,
+                                        void* stream) {
+    return launch_pack<false>(k_layers_host, v_layers_host, L, Hkv, head_dim, page_size, block_table, max_pages,
+                              sample_rows, starts, lens, n, const_cast<void*>(buf), buf_offset_elems,
+                              rs::as_stream(stream));
 }
 
 extern "C" rs_status rs_kv_unpack(void* const* k_layers_host, void* const* v_layers_host, int32_t L, int32_t Hkv,
@@ -115,7 +136,8 @@ extern "C" rs_status rs_kv_unpack(void* const* k_layers_host, void* const* v_lay
                                   const int32_t* sample_rows, const int32_t* lens, int32_t n, const void* buf,
                                   int64_t buf_offset_elems, void* stream) {
     return launch_pack<false>(k_layers_host, v_layers_host, L, Hkv, head_dim, page_size, block_table, max_pages,
-                              sample_rows, lens, n, const_cast<void*>(buf), buf_offset_elems, rs::as_stream(stream));
+                              sample_rows, nullptr, lens, n, const_cast<void*>(buf), buf_offset_elems,
+                              rs::as_stream(stream));
 }
 
 // ------------------------------------------------------------------ page pool (host)
@@ -384,6 +406,256 @@ extern "C" rs_status rs_migrate_samples(rs_comm* c, int32_t src_rank, int32_t ds
     (void)c; (void)src_rank; (void)dst_rank; (void)kv; (void)pool; (void)gids_host; (void)lens_host; (void)n;
     (void)src_block_table; (void)max_pages; (void)dst_block_table_host; (void)staging; (void)staging_bytes;
     (void)device_scratch; (void)stream;
+    rs::set_error("built without NCCL");
+    return RS_ERR_UNSUPPORTED;
+#endif
+}
+
+// ------------------------------------------------------------------ f1: two-stage migration
+// P:303-318. Stage 1 moves the KV of the tokens verified before the trigger while both instances
+// keep computing: later verification steps only write slots beyond them (Markov property), so
+// the transfer is enqueued on a side stream and the call returns. Stage 2 moves the tokens
+// verified meanwhile with the SSM part first (the destination can resume drafting once it has
+// landed) and the LLM part behind it.
+#ifdef RS_HAVE_NCCL
+namespace {
+// Request src -> dst: [n, bytes, status, -, A[n], B[n]]; the destination decides and answers
+// one status word. Returns RS_OK when the transfer may proceed (on both ranks).
+template <class Decide>
+rs_status handshake(rs_comm* c, int src, int dst, int n, int64_t bytes_src, const int32_t* A_src,
+                    const int32_t* B_src, std::vector<int32_t>& A, std::vector<int32_t>& B, cudaStream_t st,
+                    Decide decide, const char* what) {
+    const bool is_src = c->rank == src, is_dst = c->rank == dst;
+    const int64_t len = 4 + 2 * (int64_t)n;
+    A.assign(n, 0);
+    B.assign(n, 0);
+    if (is_src) {
+        c->h_hdr[0] = n;
+        c->h_hdr[1] = bytes_src;
+        c->h_hdr[2] = 0;
+        c->h_hdr[3] = 0;
+        for (int i = 0; i < n; ++i) {
+            c->h_hdr[4 + i] = A_src[i];
+            c->h_hdr[4 + n + i] = B_src[i];
+            A[i] = A_src[i];
+            B[i] = B_src[i];
+        }
+        RS_CUDA_CHECK(cudaMemcpyAsync(c->d_hdr, c->h_hdr, sizeof(int64_t) * len, cudaMemcpyHostToDevice, st));
+    }
+    rs_status s = p2p(c, src, dst, c->d_hdr, sizeof(int64_t) * len, st);
+    if (s != RS_OK) return s;
+    int64_t status = RS_OK;
+    if (is_dst) {
+        RS_CUDA_CHECK(cudaMemcpyAsync(c->h_hdr, c->d_hdr, sizeof(int64_t) * len, cudaMemcpyDeviceToHost, st));
+        RS_CUDA_CHECK(cudaStreamSynchronize(st));
+        RS_REQUIRE(c->h_hdr[0] == n, RS_ERR_LAYOUT_MISMATCH, "%s: header n %lld != %d", what, (long long)c->h_hdr[0], n);
+        for (int i = 0; i < n; ++i) {
+            A[i] = (int32_t)c->h_hdr[4 + i];
+            B[i] = (int32_t)c->h_hdr[4 + n + i];
+        }
+        status = decide(c->h_hdr[1], A, B);
+        c->h_hdr[2] = status;
+        RS_CUDA_CHECK(cudaMemcpyAsync(c->d_hdr + 2, c->h_hdr + 2, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    }
+    s = p2p(c, dst, src, c->d_hdr + 2, sizeof(int64_t), st);
+    if (s != RS_OK) return s;
+    if (is_src && !is_dst) {
+        RS_CUDA_CHECK(cudaMemcpyAsync(c->h_hdr + 2, c->d_hdr + 2, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        RS_CUDA_CHECK(cudaStreamSynchronize(st));
+        status = c->h_hdr[2];
+    }
+    if (status != RS_OK) {
+        rs::set_error("%s: destination refused the request (status %lld)", what, (long long)status);
+        return status == RS_ERR_NO_MEMORY ? RS_ERR_NO_MEMORY : RS_ERR_WORKSPACE;
+    }
+    return RS_OK;
+}
+
+int64_t model_elems(int L, int Hkv, int d, const std::vector<int32_t>& lens) {
+    return L ? rs_kv_pack_elems(L, Hkv, d, lens.data(), (int32_t)lens.size()) : 0;
+}
+}  // namespace
+#endif
+
+extern "C" rs_status rs_migrate_stage1(rs_comm* c, int32_t src_rank, int32_t dst_rank, const rs_kv_desc* kv,
+                                       rs_page_pool* pool, const int64_t* gids_host, const int32_t* lens_host,
+                                       const int32_t* reserve_lens_host, int32_t n, const int32_t* src_block_table,
+                                       int32_t max_pages, int32_t* dst_block_table_host, void* staging,
+                                       size_t staging_bytes, int32_t* device_scratch, void* stream) {
+#ifdef RS_HAVE_NCCL
+    RS_REQUIRE(c && kv && n >= 0 && n <= 4096 && src_rank >= 0 && dst_rank >= 0 && src_rank < c->world &&
+                   dst_rank < c->world,
+               RS_ERR_INVALID_ARG, "rs_migrate_stage1: bad args");
+    const bool is_src = c->rank == src_rank, is_dst = c->rank == dst_rank;
+    if (!is_src && !is_dst) return RS_OK;
+    cudaStream_t st = rs::as_stream(stream);
+    int64_t bytes = 0;
+    if (is_src) {
+        RS_REQUIRE(lens_host && reserve_lens_host && gids_host, RS_ERR_INVALID_ARG,
+                   "rs_migrate_stage1: src needs lens, reserve_lens and gids");
+        for (int i = 0; i < n; ++i)
+            RS_REQUIRE(reserve_lens_host[i] >= lens_host[i], RS_ERR_INVALID_ARG,
+                       "rs_migrate_stage1: reserve_lens[%d] < lens", i);
+        std::vector<int32_t> ln(lens_host, lens_host + n);
+        bytes = 2 * (model_elems(kv->L_ssm, kv->Hkv_ssm, kv->d_ssm, ln) +
+                     model_elems(kv->L_llm, kv->Hkv_llm, kv->d_llm, ln));
+    }
+    std::vector<int32_t> lens, reserve;
+    rs_status s = handshake(
+        c, src_rank, dst_rank, n, bytes, lens_host, reserve_lens_host, lens, reserve, st,
+        [&](int64_t b, std::vector<int32_t>&, std::vector<int32_t>& rsv) -> int64_t {
+            bytes = b;
+            if ((size_t)b > staging_bytes || !staging || !pool || !dst_block_table_host) return RS_ERR_WORKSPACE;
+            return rs_migrate_reserve(pool, rsv.data(), n, kv->page_size, max_pages, dst_block_table_host);
+        },
+        "rs_migrate_stage1");
+    if (s != RS_OK) return s;
+    RS_REQUIRE(device_scratch && staging && (size_t)bytes <= staging_bytes, RS_ERR_WORKSPACE,
+               "rs_migrate_stage1: staging / device_scratch");
+    int32_t* d_rows = device_scratch;
+    int32_t* d_lens = device_scratch + n;
+    int32_t* d_bt = device_scratch + 2 * n;
+    std::vector<int32_t> rows(n);
+    for (int i = 0; i < n; ++i) rows[i] = i;
+    RS_CUDA_CHECK(cudaMemcpyAsync(d_rows, rows.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+    RS_CUDA_CHECK(cudaMemcpyAsync(d_lens, lens.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+    const int64_t e_ssm = model_elems(kv->L_ssm, kv->Hkv_ssm, kv->d_ssm, lens);
+    if (is_src) {
+        RS_REQUIRE(src_block_table, RS_ERR_INVALID_ARG, "rs_migrate_stage1: src block table required");
+        if (kv->L_ssm) {
+            s = rs_kv_pack(kv->k_ssm, kv->v_ssm, kv->L_ssm, kv->Hkv_ssm, kv->d_ssm, kv->page_size, src_block_table,
+                           max_pages, d_rows, d_lens, n, staging, 0, stream);
+            if (s != RS_OK) return s;
+        }
+        s = rs_kv_pack(kv->k_llm, kv->v_llm, kv->L_llm, kv->Hkv_llm, kv->d_llm, kv->page_size, src_block_table,
+                       max_pages, d_rows, d_lens, n, staging, e_ssm, stream);
+        if (s != RS_OK) return s;
+    }
+    s = p2p(c, src_rank, dst_rank, staging, (size_t)bytes, st);
+    if (s != RS_OK) return s;
+    if (is_dst) {
+        RS_CUDA_CHECK(cudaMemcpyAsync(d_bt, dst_block_table_host, sizeof(int32_t) * n * max_pages,
+                                      cudaMemcpyHostToDevice, st));
+        if (kv->L_ssm) {
+            s = rs_kv_unpack(kv->k_ssm, kv->v_ssm, kv->L_ssm, kv->Hkv_ssm, kv->d_ssm, kv->page_size, d_bt, max_pages,
+                             d_rows, d_lens, n, staging, 0, stream);
+            if (s != RS_OK) return s;
+        }
+        s = rs_kv_unpack(kv->k_llm, kv->v_llm, kv->L_llm, kv->Hkv_llm, kv->d_llm, kv->page_size, d_bt, max_pages,
+                         d_rows, d_lens, n, staging, e_ssm, stream);
+        if (s != RS_OK) return s;
+    }
+    return RS_OK;   // enqueued; the caller waits on `stream` before stage 2
+#else
+    (void)c; (void)src_rank; (void)dst_rank; (void)kv; (void)pool; (void)gids_host; (void)lens_host;
+    (void)reserve_lens_host; (void)n; (void)src_block_table; (void)max_pages; (void)dst_block_table_host;
+    (void)staging; (void)staging_bytes; (void)device_scratch; (void)stream;
+    rs::set_error("built without NCCL");
+    return RS_ERR_UNSUPPORTED;
+#endif
+}
+
+extern "C" rs_status rs_migrate_stage2(rs_comm* c, int32_t src_rank, int32_t dst_rank, const rs_kv_desc* kv,
+                                       rs_page_pool* pool, const int32_t* starts_host, const int32_t* lens_host,
+                                       int32_t n, const int32_t* src_block_table, int32_t max_pages,
+                                       int32_t* dst_block_table_host, int32_t* dst_capacity_host, void* staging,
+                                       size_t staging_bytes, int32_t* device_scratch, void* ssm_ready_event,
+                                       void* stream) {
+#ifdef RS_HAVE_NCCL
+    RS_REQUIRE(c && kv && n >= 0 && n <= 4096 && src_rank >= 0 && dst_rank >= 0 && src_rank < c->world &&
+                   dst_rank < c->world,
+               RS_ERR_INVALID_ARG, "rs_migrate_stage2: bad args");
+    const bool is_src = c->rank == src_rank, is_dst = c->rank == dst_rank;
+    if (!is_src && !is_dst) return RS_OK;
+    cudaStream_t st = rs::as_stream(stream);
+    int64_t bytes = 0;
+    if (is_src) {
+        RS_REQUIRE(starts_host && lens_host, RS_ERR_INVALID_ARG, "rs_migrate_stage2: src needs starts and lens");
+        std::vector<int32_t> ln(lens_host, lens_host + n);
+        bytes = 2 * (model_elems(kv->L_ssm, kv->Hkv_ssm, kv->d_ssm, ln) +
+                     model_elems(kv->L_llm, kv->Hkv_llm, kv->d_llm, ln));
+    }
+    const int ps = kv->page_size;
+    std::vector<int32_t> starts, lens;
+    rs_status s = handshake(
+        c, src_rank, dst_rank, n, bytes, starts_host, lens_host, starts, lens, st,
+        [&](int64_t b, std::vector<int32_t>& stt, std::vector<int32_t>& ln) -> int64_t {
+            bytes = b;
+            if ((size_t)b > staging_bytes || !staging || !pool || !dst_block_table_host || !dst_capacity_host)
+                return RS_ERR_WORKSPACE;
+            // pages beyond each row's reservation, all-or-nothing
+            int64_t extra = 0;
+            for (int i = 0; i < n; ++i) {
+                const int need = (stt[i] + ln[i] + ps - 1) / ps, have = (dst_capacity_host[i] + ps - 1) / ps;
+                if (need > max_pages) return RS_ERR_INVALID_ARG;
+                extra += std::max(0, need - have);
+            }
+            if (extra == 0) return RS_OK;
+            std::vector<int32_t> pages(extra);
+            const rs_status a = rs_page_pool_alloc(pool, (int32_t)extra, pages.data());
+            if (a != RS_OK) return a;
+            int64_t o = 0;
+            for (int i = 0; i < n; ++i) {
+                const int need = (stt[i] + ln[i] + ps - 1) / ps, have = (dst_capacity_host[i] + ps - 1) / ps;
+                int32_t* row = dst_block_table_host + (int64_t)i * max_pages;
+                for (int k = have; k < need; ++k) row[k] = pages[o++];
+                if (need > have)
+                    for (int k = need; k < max_pages; ++k) row[k] = row[need - 1];
+                if (need * ps > dst_capacity_host[i]) dst_capacity_host[i] = std::max(dst_capacity_host[i], need * ps);
+            }
+            return RS_OK;
+        },
+        "rs_migrate_stage2");
+    if (s != RS_OK) return s;
+    RS_REQUIRE(device_scratch && staging && (size_t)bytes <= staging_bytes, RS_ERR_WORKSPACE,
+               "rs_migrate_stage2: staging / device_scratch");
+    int32_t* d_rows = device_scratch;
+    int32_t* d_starts = device_scratch + n;
+    int32_t* d_lens = device_scratch + 2 * n;
+    int32_t* d_bt = device_scratch + 3 * n;
+    std::vector<int32_t> rows(n);
+    for (int i = 0; i < n; ++i) rows[i] = i;
+    RS_CUDA_CHECK(cudaMemcpyAsync(d_rows, rows.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+    RS_CUDA_CHECK(cudaMemcpyAsync(d_starts, starts.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+    RS_CUDA_CHECK(cudaMemcpyAsync(d_lens, lens.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+    if (is_dst)
+        RS_CUDA_CHECK(cudaMemcpyAsync(d_bt, dst_block_table_host, sizeof(int32_t) * n * max_pages,
+                                      cudaMemcpyHostToDevice, st));
+    RS_REQUIRE(!is_src || src_block_table, RS_ERR_INVALID_ARG, "rs_migrate_stage2: src block table required");
+    const int64_t e_ssm = model_elems(kv->L_ssm, kv->Hkv_ssm, kv->d_ssm, lens);
+    // SSM part first: drafting resumes on the destination as soon as it has landed
+    if (kv->L_ssm) {
+        if (is_src) {
+            s = rs_kv_pack_range(kv->k_ssm, kv->v_ssm, kv->L_ssm, kv->Hkv_ssm, kv->d_ssm, ps, src_block_table,
+                                 max_pages, d_rows, d_starts, d_lens, n, staging, 0, stream);
+            if (s != RS_OK) return s;
+        }
+        s = p2p(c, src_rank, dst_rank, staging, (size_t)(2 * e_ssm), st);
+        if (s != RS_OK) return s;
+        if (is_dst) {
+            s = rs_kv_unpack_range(kv->k_ssm, kv->v_ssm, kv->L_ssm, kv->Hkv_ssm, kv->d_ssm, ps, d_bt, max_pages,
+                                   d_rows, d_starts, d_lens, n, staging, 0, stream);
+            if (s != RS_OK) return s;
+        }
+    }
+    if (is_dst && ssm_ready_event) RS_CUDA_CHECK(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ssm_ready_event), st));
+    if (is_src) {
+        s = rs_kv_pack_range(kv->k_llm, kv->v_llm, kv->L_llm, kv->Hkv_llm, kv->d_llm, ps, src_block_table, max_pages,
+                             d_rows, d_starts, d_lens, n, staging, e_ssm, stream);
+        if (s != RS_OK) return s;
+    }
+    s = p2p(c, src_rank, dst_rank, static_cast<uint16_t*>(staging) + e_ssm, (size_t)(bytes - 2 * e_ssm), st);
+    if (s != RS_OK) return s;
+    if (is_dst) {
+        s = rs_kv_unpack_range(kv->k_llm, kv->v_llm, kv->L_llm, kv->Hkv_llm, kv->d_llm, ps, d_bt, max_pages, d_rows,
+                               d_starts, d_lens, n, staging, e_ssm, stream);
+        if (s != RS_OK) return s;
+    }
+    return RS_OK;   // enqueued; the destination verifies the samples after `stream` reaches here
+#else
+    (void)c; (void)src_rank; (void)dst_rank; (void)kv; (void)pool; (void)starts_host; (void)lens_host; (void)n;
+    (void)src_block_table; (void)max_pages; (void)dst_block_table_host; (void)dst_capacity_host; (void)staging;
+    (void)staging_bytes; (void)device_scratch; (void)ssm_ready_event; (void)stream;
     rs::set_error("built without NCCL");
     return RS_ERR_UNSUPPORTED;
 #endif
