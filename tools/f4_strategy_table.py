@@ -1,0 +1,136 @@
+"""f4: the paper's Table 1 experiment on synthetic workloads with
+real kernel timings. For each sample count B, every fixed draft token num n in the paper's range
+(2..48) is run through the verify step on the GPU (L=32 layers of tree attention over
+the long-tail prefixes + acceptance + compaction, CUDA graph), trees = root + S(n) of each
+sample's 96-node candidate tree (select_strategy's own layer-level selection at fixed n).
+
+Throughput model (Eq. 2): committed tokens per step = al(n) + B (al from the
+acceptance fit F(dl) summed over S(n), + one bonus per sample) over the step time
+t(n) = c_draft + t_verify_measured(n) + b2 * N_draft, where b2 * N_draft is the analytic
+time of the target model's dense GEMMs for N_draft = B (n + 1) tokens (8B parameters at the
+bf16 tensor peak: out of scope to run, SURVEY 8(a) a2'). The cost model t_sd is then fitted
+(rs_cost_model_fit) to these measured step times, select_strategy picks n* per B with the
+fitted model and patience-2 early stop, and we report throughput(n*) / max_n throughput(n)
+(the paper's "percentage of optimal", Table 1).
+
+    python tools/f4_strategy_table.py [B list, default 16,64,256]"""
+import json
+import os
+import sys
+from types import SimpleNamespace
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2512_04752_b200 import core  # noqa: E402
+from paper_2512_04752_b200.step import VerifyStep  # noqa: E402
+from synth import CONFIGS, draw_prefix_lengths, make_candidate_tree, make_verify_batch  # noqa: E402
+
+KX = [0.0, 0.05, 0.2, 0.5, 1.0]
+KY = [0.0, 0.15, 0.45, 0.75, 0.95]
+C_DRAFT, B2_GEMM = 1.0e-3, 1.07e-5
+N_GRID = [2, 4, 6, 8, 12, 16, 20, 24, 32, 40, 48]
+
+
+def trees_for(sel, cands, P, n):
+    """root + S(n) per sample at a fixed n (n_min = n_max = n)."""
+    res = sel.select(cands, P, n_min=n, n_max=n, patience=2, return_selected=True)
+    parents = []
+    for b in range(len(cands)):
+        chosen = sorted(int(x) for x in res["selected"][b][:n])
+        idx = {c: i + 1 for i, c in enumerate(chosen)}
+        cp = cands[b][0]
+        parents.append(np.array([-1] + [0 if cp[c] < 0 else idx[int(cp[c])] for c in chosen], np.int32))
+    return parents, res["al"]
+
+
+def retree(base, parents, gen):
+    """The base batch (KV pages for P + 49 slots) with other verification trees (T <= 49)."""
+    b = dict(base)
+    T = np.array([len(p) for p in parents], np.int32)
+    off = np.zeros(len(T) + 1, np.int32)
+    off[1:] = np.cumsum(T)
+    NT = int(off[-1])
+    b.update(parent=np.concatenate(parents).astype(np.int32), T=T, tree_off=off, NT=NT,
+             token=np.random.default_rng(1).integers(0, base["V"], size=NT).astype(np.int32))
+    L, _, Hq, d = base["q"].shape
+    b["q"] = torch.randn((L, NT, Hq, d), generator=gen, device="cuda").to(torch.bfloat16)
+    b["logits"] = torch.randn((NT, base["V"]), generator=gen, device="cuda").to(torch.bfloat16)
+    return b
+
+
+def time_step(b, iters=10):
+    step = VerifyStep(b, mode=core.GREEDY)
+    g = step.capture(seed=1, step=0)
+    for _ in range(3):
+        g.replay()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(iters):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters * 1e-3
+
+
+def main():
+    Bs = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "16,64,256").split(",")]
+    base_cost = SimpleNamespace(c_draft=C_DRAFT, b0=2.0e-4, b1=3.0e-8, b2=B2_GEMM, b3=0.0, k_sat=4096.0,
+                                seq_bucket=256, draft_bucket=4)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    rows, samples = [], []
+    per_B = {}
+    for B in Bs:
+        cfg = CONFIGS["c3s"]
+        cfg = type(cfg)(**{**cfg.__dict__, "B": B, "mode": "greedy", "seed": 100 + B})
+        P = draw_prefix_lengths(np.random.default_rng(cfg.seed), cfg)
+        rng = np.random.default_rng(cfg.seed + 77)
+        cands = [make_candidate_tree(rng, 96) for _ in range(B)]
+        sel = core.Selector(base_cost, KX, KY)
+        par48, _ = trees_for(sel, cands, P, max(N_GRID))
+        base = make_verify_batch(cfg, device="cuda", gen_device="cuda", parents=par48, with_logits=False)
+        meas = {}
+        for n in N_GRID:
+            parents, al = trees_for(sel, cands, P, n)
+            t_ver = time_step(retree(base, parents, gen))
+            t = C_DRAFT + t_ver + B2_GEMM * B * (n + 1)
+            meas[n] = dict(al=al, t_verify=t_ver, t_step=t, tput=(al + B) / t)
+            samples.append((float(np.sum(P)), float(B * (n + 1)), t))
+            print(json.dumps({"B": B, "n": n, "t_verify_ms": round(t_ver * 1e3, 3), "al": round(al, 2),
+                              "tput": round((al + B) / t, 1)}), flush=True)
+        per_B[B] = (cfg, P, cands, base, meas)
+    # fit t_sd to the measured step times (b0..b3; c_draft and k_sat kept) and select n* per B
+    ns_, nd_, ts_ = (np.array(x) for x in zip(*samples))
+    fitted = core.cost_model_fit(ns_, nd_, ts_, base_cost)
+    fit_ns = SimpleNamespace(**{k: getattr(fitted, k) for k, _ in fitted._fields_})
+    for B, (cfg, P, cands, base, meas) in per_B.items():
+        sel = core.Selector(fit_ns, KX, KY)
+        r = sel.select(cands, P, n_min=2, n_max=48, patience=2)
+        n_star = int(r["n"])
+        if n_star not in meas:
+            parents, al = trees_for(sel, cands, P, n_star)
+            t_ver = time_step(retree(base, parents, gen))
+            t = C_DRAFT + t_ver + B2_GEMM * B * (n_star + 1)
+            meas[n_star] = dict(al=al, t_verify=t_ver, t_step=t, tput=(al + B) / t)
+        best_n = max(meas, key=lambda k: meas[k]["tput"])
+        rows.append({"B": B, "n_selected": n_star, "n_best_fixed": best_n,
+                     "tput_selected": round(meas[n_star]["tput"], 1), "tput_best_fixed": round(meas[best_n]["tput"], 1),
+                     "pct_of_optimal": round(100.0 * meas[n_star]["tput"] / meas[best_n]["tput"], 2),
+                     "pred_t_sd_ms": round(r["t_sd"] * 1e3, 3), "meas_t_step_ms": round(meas[n_star]["t_step"] * 1e3, 3),
+                     "curve": {str(k): round(v["tput"], 1) for k, v in sorted(meas.items())},
+                     "t_verify_ms": {str(k): round(v["t_verify"] * 1e3, 3) for k, v in sorted(meas.items())}})
+        del base
+        torch.cuda.empty_cache()
+    out = {"experiment": "f4: Table 1 (P:378-392) synthetic, real verify-step timings on one B200",
+           "fitted_cost_model": {k: getattr(fitted, k) for k, _ in fitted._fields_},
+           "rows": rows,
+           "model": "tput(n) = (al(n) + B) / (c_draft 1 ms + measured verify step + 1.07e-5 s x B(n+1) analytic "
+                    "8B GEMMs); al(n) = sum over S(n) of F(dl)"}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

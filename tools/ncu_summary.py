@@ -103,7 +103,7 @@ def main():
                         f.write(f"| {m} | {d[m][0]} | {d[m][1]} |\n")
                 f.write("\n")
         print(open(os.path.join(prof, f"{tag}_ncu_{name}.md")).read())
-        if name == "attn":
+        if name.startswith("attn"):
             d = res[0]
 
             def mb(m):
