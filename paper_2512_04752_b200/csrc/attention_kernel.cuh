@@ -59,7 +59,11 @@ constexpr int kQConsumers = 15;  // warps that read the ring (all but the fetchi
 constexpr int kKSlots = RS_ATTN_KSLOTS;
 constexpr int kVSlots = RS_ATTN_VSLOTS;
 constexpr bool kStageOut = RS_ATTN_STAGE != 0;   // epilogue output through smem + TMA store
-constexpr int kQBufs = 2;
+#ifndef RS_ATTN_QBUFS
+#define RS_ATTN_QBUFS 2
+#endif
+constexpr int kQBufs = RS_ATTN_QBUFS;   // Q tile buffers (RM 2/3; RM = 1 uses the two halves of one tile)
+static_assert(kQBufs == 2, "the Q producer / S issuer handshake assumes two Q buffers (1 deadlocks)");
 constexpr int kPF = 0;          // L2 prefetch distance in KV blocks (0 = off; measured: no gain)
 constexpr int kThreads = 384;    // 12 warps (RM 2/3)
 // RM = 1 (every tile R = 16): 16 warps; warps 12-15 are an epilogue warpgroup, and consecutive
