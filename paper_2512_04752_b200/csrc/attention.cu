@@ -118,6 +118,18 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
         pl->rmodes |= (R == 16) ? 1 : 2;
         n_tiles += Hkv * M;
     }
+    // Dual items (kernel RM = 4): when every unit group has R = 32 and an even number of query
+    // tiles, an item covers tiles (2s, 2s + 1) and each softmax warpgroup owns one, so each K/V
+    // tile in shared memory feeds twice the MMA work (config 5: L2 -> SM traffic halved). The
+    // gang machinery below then runs on "super tiles" (M / 2 per group). RS_ATTN_DUAL=0: off.
+    bool dual = pl->rmodes == 2 && !(getenv("RS_ATTN_DUAL") && getenv("RS_ATTN_DUAL")[0] == '0');
+    for (const GU& u : gus) dual = dual && (u.M % 2 == 0);
+    if (dual) {
+        for (GU& u : gus) u.M /= 2;
+        n_tiles /= 2;
+        pl->rmodes = 4;
+    }
+    const int tile_mul = dual ? 2 : 1;   // item.mtile = tile_mul * (super) tile index
     const int n_ctas = std::max(1, std::min<int>(num_ctas, std::max(n_tiles, 1)));
     // Gangs: the M tiles of a unit group run on M different CTAs ("a gang") that process the
     // same key-block ranges in the same order at the same time, so the K/V blocks the first CTA
@@ -229,20 +241,27 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
                 for (const Seg& sg : per_g[vv]) {
                     const GU& u = gus[sg.gu];
                     per_cta[cta_base + vv * M + m].push_back(
-                        {u.b, u.kvh, sg.tile >= 0 ? sg.tile : m, sg.start, sg.end, -1, u.R, -1, u.P, u.node0, u.T, 0});
+                        {u.b, u.kvh, tile_mul * (sg.tile >= 0 ? sg.tile : m), sg.start, sg.end, -1, u.R, -1, u.P,
+                         u.node0, u.T, 0});
                 }
         for (int ei = 0; ei < (int)entries.size(); ++ei) {
             if (where_of[ei].size() <= 1) continue;
             const GU& u = gus[entries[ei].first];
             for (int m = 0; m < M; ++m) {
                 const int uid = (int)pl->units.size();
-                const int tile = entries[ei].second >= 0 ? entries[ei].second : m;
-                pl->units.push_back({u.b, u.kvh, tile, (int)where_of[ei].size(), n_parts, u.R});
-                for (auto& wc : where_of[ei]) {
+                const int tile = tile_mul * (entries[ei].second >= 0 ? entries[ei].second : m);
+                const int k = (int)where_of[ei].size();
+                pl->units.push_back({u.b, u.kvh, tile, k, n_parts, u.R});
+                // dual: a second unit for tile + 1 whose k parts follow (item.pad = k)
+                if (dual) pl->units.push_back({u.b, u.kvh, tile + 1, k, n_parts + k, u.R});
+                for (int i = 0; i < k; ++i) {
+                    const auto& wc = where_of[ei][i];
                     WorkItem& it = per_cta[cta_base + wc.first * M + m][wc.second];
-                    it.part = n_parts++;
+                    it.part = n_parts + i;
                     it.unit = uid;
+                    it.pad = dual ? k : 0;
                 }
+                n_parts += tile_mul * k;
             }
         }
         cta_base += G * M;
@@ -401,10 +420,11 @@ static rs_status launch_attn(const rs_attn_plan* pl, const void* q, const void* 
                                                                                                : nullptr;
     // row mode: kernels specialised for plans whose tiles all use R = 16 (half-split rows) or all
     // R = 32, so each carries only the registers of its own softmax path; mixed plans take both.
-    const int rm = pl->rmodes == 1 ? 1 : (pl->rmodes == 2 ? 2 : 3);
-    auto kern = rm == 1 ? tree_attn_kernel<D, 1> : (rm == 2 ? tree_attn_kernel<D, 2> : tree_attn_kernel<D, 3>);
+    const int rm = pl->rmodes == 1 ? 1 : (pl->rmodes == 2 ? 2 : (pl->rmodes == 4 ? 4 : 3));
+    auto kern = rm == 1 ? tree_attn_kernel<D, 1>
+                        : (rm == 2 ? tree_attn_kernel<D, 2> : (rm == 4 ? tree_attn_kernel<D, 4> : tree_attn_kernel<D, 3>));
     const int smem_bytes = rm == 1 ? Cfg<D, 1>::kSmemBytes : Cfg<D, 2>::kSmemBytes;
-    static bool attr_set[2][4] = {};
+    static bool attr_set[2][5] = {};
     if (!attr_set[D == 128][rm]) {
         RS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
         attr_set[D == 128][rm] = true;

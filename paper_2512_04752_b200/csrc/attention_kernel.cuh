@@ -136,6 +136,7 @@ struct Bars {
     int item_ring[8];
     uint32_t tmem_base;
     int merge_flag;
+    int merge_flags[2];                               // RM = 4: one split-KV unit per warpgroup
 };
 
 struct Params {
@@ -212,7 +213,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     return r;
 }
 
-// RM: 1 = every tile has R = 16, 2 = every tile has R = 32, 3 = mixed (both paths compiled in).
+// RM: 1 = every tile has R = 16, 2 = every tile has R = 32, 3 = mixed (both paths compiled in),
+// 4 = "dual": every item covers TWO query tiles (mtile, mtile + 1) of a (sample, kv head) and
+// each softmax warpgroup owns one of them (O0/O1, S0/S1, P0/P1 indexed by the tile): every K/V
+// tile brought into shared memory feeds both tiles' S and PV MMAs, halving the L2 -> SM bytes
+// per FLOP (config 5). The issuers walk "virtual blocks" vb = 2 * key block + tile.
 template <int D, int RM>
 __global__ void __launch_bounds__(KT<RM>::kThreads, 1)
 tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -311,6 +316,29 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         const bool do_pf = pf > 0;
         uint32_t J = 0;
         auto issue_q = [&](const WorkItem& x, int slot_it) {
+            if constexpr (RM == 4) {
+                // both Q buffers: tile mtile -> buffer 0, mtile + 1 -> buffer 1 (used every item)
+                mbar_wait(&bars->q_empty[0], (slot_it & 1) ^ 1);
+                mbar_wait(&bars->q_empty[1], (slot_it & 1) ^ 1);
+                const int R = x.rstride;
+                if (elect_one()) {
+                    for (int t = 0; t < 2; ++t) {
+                        const int row0 = (x.mtile + t) * 4 * R;
+                        uint8_t* qs = smem + C::kOffQ + t * C::kQStride;
+                        mbar_arrive_expect_tx(&bars->q_full[t], 4 * R * 128 * C::kBoxes);
+                        for (int q = 0; q < 4; ++q)
+                            for (int s = 0; s < R; s += 16) {
+                                const int node = x.node0 + (row0 + q * R + s) / p.g;
+#pragma unroll
+                                for (int bx = 0; bx < C::kBoxes; ++bx)
+                                    tma_load_3d(qs + bx * (kM * 128) + (32 * q + s) * 128, &tmQ, &bars->q_full[t],
+                                                bx * 64, x.kvh * p.g, node);
+                            }
+                    }
+                }
+                __syncwarp();
+                return;
+            }
             const int qb = slot_it % kQBufs;
             mbar_wait(&bars->q_empty[qb], ((slot_it / kQBufs) & 1) ^ 1);
             const int R = x.rstride;
@@ -369,7 +397,8 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                             griddep_wait();
                             issue_q(wi, 0);
                         }
-                        if (isK && has_next && j == q_next_at) issue_q(wn, it + 1);
+                        if (RM != 4 && isK && has_next && j == q_next_at) issue_q(wn, it + 1);
+                        if (RM == 4 && isK && it > 0 && j == 0) issue_q(wi, it);
                         // L2 prefetch of block j + pf (this item or the next one)
                         if (do_pf) {
                             const int f = j + pf;
@@ -425,18 +454,27 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         int it = 0;
         int w = seq_read(0);
         int nblk = w >= 0 ? __ldg(&p.items[w].blk_end) - __ldg(&p.items[w].blk_begin) : 0;
+        constexpr bool DU = RM == 4;
         for (; w >= 0; ++it) {
             const int wn = seq_read(it + 1);
             const int nblk_next = wn >= 0 ? __ldg(&p.items[wn].blk_end) - __ldg(&p.items[wn].blk_begin) : 0;
             const int qb = it % kQBufs;
-            mbar_wait(&bars->q_full[qb], (it / kQBufs) & 1);
-            const uint32_t qa = sbase + C::kOffQ + qb * C::kQStride;
-            for (int j = 0; j < nblk; ++j, ++sJ) {
-                mbar_wait(&bars->k_full[sJ % C::KS], (sJ / C::KS) & 1);
+            if (DU) {
+                mbar_wait(&bars->q_full[0], it & 1);
+                mbar_wait(&bars->q_full[1], it & 1);
+            } else {
+                mbar_wait(&bars->q_full[qb], (it / kQBufs) & 1);
+            }
+            // dual: virtual block sJ = 2 * key block + tile; key block counter kJ = sJ >> 1
+            const int nv = DU ? 2 * nblk : nblk;
+            for (int j = 0; j < nv; ++j, ++sJ) {
+                const uint32_t kJ = DU ? (sJ >> 1) : sJ;
+                const uint32_t qa = sbase + C::kOffQ + (DU ? (sJ & 1) : qb) * C::kQStride;
+                if (!DU || (sJ & 1) == 0) mbar_wait(&bars->k_full[kJ % C::KS], (kJ / C::KS) & 1);
                 if (lane == 0) TRACE(sJ, 8);
                 mbar_wait(&bars->s_free[sJ & 1], ((sJ >> 1) & 1) ^ 1);
                 tc_fence_after();
-                const uint32_t ka = sbase + C::kOffK + (sJ % C::KS) * C::kKVBytes;
+                const uint32_t ka = sbase + C::kOffK + (kJ % C::KS) * C::kKVBytes;
                 const uint32_t sd = tmem + C::kColS + (sJ & 1) * kBlockN;
                 if (elect_one()) {
 #pragma unroll
@@ -448,8 +486,15 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                     }
                     TRACE(sJ, 2);
                     umma_commit(&bars->s_full[sJ & 1]);
-                    umma_commit(&bars->k_empty[sJ % C::KS]);
-                    if (j == nblk - 1) umma_commit(&bars->q_empty[qb]);
+                    if (!DU || (sJ & 1) == 1) umma_commit(&bars->k_empty[kJ % C::KS]);
+                    if (j == nv - 1) {
+                        if (DU) {
+                            umma_commit(&bars->q_empty[0]);
+                            umma_commit(&bars->q_empty[1]);
+                        } else {
+                            umma_commit(&bars->q_empty[qb]);
+                        }
+                    }
                 }
                 __syncwarp();
             }
@@ -467,19 +512,22 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         for (; w >= 0; ++it) {
             const int wn = seq_read(it + 1);
             const int nblk_next = wn >= 0 ? __ldg(&p.items[wn].blk_end) - __ldg(&p.items[wn].blk_begin) : 0;
-            for (int j = 0; j < nblk; ++j, ++pJ) {
+            constexpr bool DU = RM == 4;
+            const int nv = DU ? 2 * nblk : nblk;   // dual: virtual block pJ = 2 * key block + tile
+            for (int j = 0; j < nv; ++j, ++pJ) {
                 // EW: O is pre-zeroed, so every PV accumulates; else the first block of each
-                // warpgroup in the item overwrites
+                // warpgroup (dual: of each tile) in the item overwrites
                 const bool first = !KT<RM>::kEW && j < 2;
+                const uint32_t vJ = DU ? (pJ >> 1) : pJ;
                 mbar_wait(&bars->p_full[pJ & 1], (pJ >> 1) & 1);
-                mbar_wait(&bars->v_full[pJ % C::VS], (pJ / C::VS) & 1);
+                if (!DU || (pJ & 1) == 0) mbar_wait(&bars->v_full[vJ % C::VS], (vJ / C::VS) & 1);
                 if (lane == 0) TRACE(pJ, 9);
                 // (EW: the softmax warpgroup re-zeroes its O half before its first P of the item,
                 // after the epilogue of item it-2 released it, so PV needs no wait here)
                 if (!KT<RM>::kEW && j == 0) mbar_wait(&bars->o_free, (it & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t pa = tmem + C::kColP + (pJ & 1) * (kBlockN / 2);
-                const uint32_t va = sbase + C::kOffV + (pJ % C::VS) * C::kKVBytes;
+                const uint32_t va = sbase + C::kOffV + (vJ % C::VS) * C::kKVBytes;
                 const uint32_t od = tmem + (pJ & 1) * D;
                 if (elect_one()) {
                     TRACE(pJ, 5);
@@ -489,7 +537,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                         umma_f16_ts(od, pa + kk * 8, bd, idPV, (first && kk == 0) ? 0u : 1u);
                     }
                     umma_commit(&bars->pv_done[pJ & 1]);
-                    umma_commit(&bars->v_empty[pJ % C::VS]);
+                    if (!DU || (pJ & 1) == 1) umma_commit(&bars->v_empty[vJ % C::VS]);
                     if (KT<RM>::kEW && j == nblk - 1) umma_commit(&bars->o_ready[it & 1]);
                 }
                 __syncwarp();
@@ -850,27 +898,30 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             // R = 16: the tile occupies TMEM lanes 0-15 of each sub-partition; two threads share a
             // row (16x32bx2 TMEM shapes), lanes 0-15 taking keys / columns of the low half and
             // lanes 16-31 those of the high half, so no lane idles.
-            const bool hs = RM == 1 ? true : (RM == 2 ? false : (R == 16));
+            const bool hs = RM == 1 ? true : ((RM == 2 || RM == 4) ? false : (R == 16));
+            constexpr bool DU = RM == 4;
+            const int mt = wi.mtile + (DU ? grp : 0);    // dual: this warpgroup's own tile
             const int hl = hs ? (lane & 15) : lane;      // row lane of this thread
             const int rr = wq * 32 + hl;                 // TMEM lane / UMMA row of my row
             const int rl = wq * R + hl;                  // logical row within the tile
-            const int rows = min(4 * R, T * p.g - wi.mtile * 4 * R);
+            const int rows = min(4 * R, T * p.g - mt * 4 * R);
             const bool warp_active = wq * R < rows;
             const bool row_valid = hl < R && rl < rows;
-            const int grow = wi.mtile * 4 * R + rl;      // row within the unit
+            const int grow = mt * 4 * R + rl;            // row within the unit
             const int node = grow / p.g;
             const uint64_t mask = row_valid ? p.tree_mask[off + node] : 0ull;
             const int key_end = P + T;                   // keys >= key_end do not exist
             const int nblk = wi.blk_end - wi.blk_begin;
+            const int nv = DU ? 2 * nblk : nblk;         // virtual blocks (dual: 2 * key block + tile)
             float m_run = -INFINITY, l_run = 0.0f;
             bool had = false;
             uint32_t Jlast = 0;
             // the block loop is instantiated per row mode so each path keeps only its own registers
             auto block_loop = [&](auto hs_tag) {
             constexpr bool HS = decltype(hs_tag)::value;
-            for (int j = (int)((J & 1) != (uint32_t)grp); j < nblk; j += 2) {
+            for (int j = (int)((J & 1) != (uint32_t)grp); j < nv; j += 2) {
                 const uint32_t Jj = J + j;
-                const int kbase = (wi.blk_begin + j) * kBlockN;
+                const int kbase = (wi.blk_begin + (DU ? (j >> 1) : j)) * kBlockN;
                 mbar_wait(&bars->s_full[grp], (Jj >> 1) & 1);
                 tc_fence_after();
                 if (wq == 0 && lane == 0) TRACE(Jj, 3);
@@ -1049,9 +1100,12 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 // keys past the end of the sample in its last page: zero those V rows so that
                 // garbage (possibly NaN) bytes never meet a zero probability in the MMA
                 const int nvalid = key_end - kbase;
-                if (nvalid < kBlockN) {
-                    const uint32_t s = Jj % C::VS;
-                    mbar_wait(&bars->v_full[s], (Jj / C::VS) & 1);
+                // (dual: the V tile is shared by both tiles; warpgroup 0 zeroes it before its
+                // P is published, and the PV issuer runs tile 0's MMA before tile 1's)
+                if (nvalid < kBlockN && (!DU || grp == 0)) {
+                    const uint32_t vJ = DU ? (Jj >> 1) : Jj;
+                    const uint32_t s = vJ % C::VS;
+                    mbar_wait(&bars->v_full[s], (vJ / C::VS) & 1);
                     if (r < kBlockN && r >= nvalid) {
                         uint8_t* vs = smem + C::kOffV + s * C::kKVBytes;
 #pragma unroll
@@ -1073,6 +1127,110 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             };
             if (hs) block_loop(std::true_type{});
             else block_loop(std::false_type{});
+            if constexpr (RM == 4) {
+                // ---------------- dual epilogue: each warpgroup finishes its own tile ----------------
+                if (had) {
+                    mbar_wait(&bars->pv_done[grp], (Jlast >> 1) & 1);
+                    tc_fence_after();
+                }
+                const bool direct = wi.part < 0;
+                const int part = direct ? -1 : wi.part + grp * wi.pad;   // tile 1's parts follow tile 0's
+                if (warp_active) {
+                    const float invL = (had && l_run > 0.0f) ? 1.0f / l_run : 0.0f;
+                    const int h = wi.kvh * p.g + (grow % p.g);
+                    __nv_bfloat16* orow = p.out + ((int64_t)(off + node) * p.Hq + h) * D;
+                    float* prow = direct ? nullptr : p.part_o + ((int64_t)part * kM + rr) * D;
+#pragma unroll 1
+                    for (int cc = 0; cc < ((p.dbg & 1) ? 0 : D); cc += 16) {
+                        uint32_t a[16];
+                        tmem_ld16(o_mine + cc, a);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) a[c] = __float_as_uint(__uint_as_float(a[c]) * invL);
+                        if (row_valid) {
+                            if (direct) {
+#pragma unroll
+                                for (int c = 0; c < 16; c += 8) {
+                                    uint4 u;
+                                    u.x = pack_bf16(__uint_as_float(a[c]), __uint_as_float(a[c + 1]));
+                                    u.y = pack_bf16(__uint_as_float(a[c + 2]), __uint_as_float(a[c + 3]));
+                                    u.z = pack_bf16(__uint_as_float(a[c + 4]), __uint_as_float(a[c + 5]));
+                                    u.w = pack_bf16(__uint_as_float(a[c + 6]), __uint_as_float(a[c + 7]));
+                                    *reinterpret_cast<uint4*>(orow + cc + c) = u;
+                                }
+                            } else {
+#pragma unroll
+                                for (int c = 0; c < 16; c += 4)
+                                    *reinterpret_cast<uint4*>(prow + cc + c) = make_uint4(a[c], a[c + 1], a[c + 2], a[c + 3]);
+                            }
+                        }
+                    }
+                    if (row_valid) {
+                        const float lse2 = (had && l_run > 0.0f) ? m_run + __log2f(l_run) : -INFINITY;
+                        if (direct) {
+                            if (p.lse) p.lse[(int64_t)(off + node) * p.Hq + h] = lse2 * 0.6931471805599453f;
+                        } else {
+                            p.part_lse[(int64_t)part * kM + rr] = lse2;
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->o_free);
+                if (!direct) {
+                    // this tile's split-KV unit (wi.unit + grp): the warpgroup that completes its
+                    // last part merges all parts
+                    __threadfence();
+                    named_bar_sync(5 + grp, 128);
+                    if (wq == 0 && lane == 0) {
+                        const int unit = wi.unit + grp;
+                        const int old = atomicAdd(&p.unit_counter[unit], 1);
+                        const int last = (old == p.units[unit].n_parts - 1) ? 1 : 0;
+                        if (last) p.unit_counter[unit] = 0;      // ready for the next launch
+                        bars->merge_flags[grp] = last;
+                    }
+                    named_bar_sync(5 + grp, 128);
+                    if (bars->merge_flags[grp] && row_valid && warp_active) {
+                        __threadfence();
+                        const SplitUnit u = p.units[wi.unit + grp];
+                        float M = -INFINITY;
+                        for (int q = 0; q < u.n_parts; ++q)
+                            M = fmaxf(M, __ldcg(p.part_lse + (int64_t)(u.part_base + q) * kM + rr));
+                        float wsum = 0.0f;
+                        for (int q = 0; q < u.n_parts; ++q) {
+                            const float lq = __ldcg(p.part_lse + (int64_t)(u.part_base + q) * kM + rr);
+                            wsum += (lq == -INFINITY) ? 0.0f : ex2(lq - M);
+                        }
+                        const float inv = wsum > 0.0f ? 1.0f / wsum : 0.0f;
+                        const int h = wi.kvh * p.g + (grow % p.g);
+                        __nv_bfloat16* orow = p.out + ((int64_t)(off + node) * p.Hq + h) * D;
+#pragma unroll 1
+                        for (int c0 = 0; c0 < D; c0 += 8) {
+                            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                            for (int q = 0; q < u.n_parts; ++q) {
+                                const float lq = __ldcg(p.part_lse + (int64_t)(u.part_base + q) * kM + rr);
+                                const float wq2 = (lq == -INFINITY) ? 0.0f : ex2(lq - M) * inv;
+                                const float4* src = reinterpret_cast<const float4*>(
+                                    p.part_o + ((int64_t)(u.part_base + q) * kM + rr) * D + c0);
+                                const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
+                                acc[0] += wq2 * x0.x; acc[1] += wq2 * x0.y; acc[2] += wq2 * x0.z; acc[3] += wq2 * x0.w;
+                                acc[4] += wq2 * x1.x; acc[5] += wq2 * x1.y; acc[6] += wq2 * x1.z; acc[7] += wq2 * x1.w;
+                            }
+                            uint4 o;
+                            o.x = pack_bf16(acc[0], acc[1]);
+                            o.y = pack_bf16(acc[2], acc[3]);
+                            o.z = pack_bf16(acc[4], acc[5]);
+                            o.w = pack_bf16(acc[6], acc[7]);
+                            *reinterpret_cast<uint4*>(orow + c0) = o;
+                        }
+                        if (p.lse) p.lse[(int64_t)(off + node) * p.Hq + h] = (M + __log2f(wsum)) * 0.6931471805599453f;
+                    }
+                }
+                J += nv;
+                wi = wn;
+                w = wnx;
+                continue;
+            }
             // ---------------- epilogue: merge the two warpgroups' states ----------------
             if (wq == 0 && lane == 0) TRACE(J + nblk - 1, 6);
             const bool had0 = nblk >= 2 || (J & 1) == 0;

@@ -238,6 +238,10 @@ ATTN_CASES = {
                               prefix=("lognormal", 150, 1.0, 0, 900), tree=("range", 1, 64), seed=22),
     "g8_T64": VerifyConfig("g8", B=3, Hq=64, Hkv=8, d=128, V=10, L=1, prefix=("fixed", 700),
                            tree=("fixed", 64), seed=23),
+    "g4_T64_dual": VerifyConfig("g4d", B=5, Hq=32, Hkv=8, d=128, V=10, L=1, prefix=("lognormal", 300, 1.0, 0, 1500),
+                                tree=("fixed", 64), seed=26),
+    "g8_T60_dual_ragged": VerifyConfig("g8r", B=4, Hq=64, Hkv=8, d=128, V=10, L=1, prefix=("lognormal", 200, 1.0, 0, 900),
+                                       tree=("range", 49, 64), seed=27),
     "d64_g2": VerifyConfig("d64", B=9, Hq=4, Hkv=2, d=64, V=10, L=1, prefix=("lognormal", 90, 1.2, 0, 500),
                            tree=("range", 1, 64), seed=24),
     "qscale8": VerifyConfig("q8", B=5, Hq=32, Hkv=8, d=128, V=10, L=1, prefix=("fixed", 333),
@@ -266,6 +270,34 @@ def test_attention_split_kv_parity(cuda_lib, num_ctas):
     np.testing.assert_allclose(lg, lref, atol=2e-2, rtol=1e-3)
     if num_ctas > 3:      # (with 3 CTAs each tile-count class may get a single gang: no cuts)
         assert info["num_split_units"] > 0
+
+
+@pytest.mark.parametrize("num_ctas", [2, 5, 13])
+def test_attention_dual_split_kv_parity(cuda_lib, num_ctas):
+    """Dual items (two query tiles per CTA, kernel RM = 4: T*g in (384, 512], g = 8) with split-KV
+    cuts: each warpgroup writes its own tile's partial and merges its own unit."""
+    cfg = VerifyConfig("dsplit", B=3, Hq=64, Hkv=8, d=128, V=10, L=1, prefix=("lognormal", 900, 0.8, 100, 3000),
+                       tree=("fixed", 64), seed=40 + num_ctas)
+    b = make_verify_batch(cfg, device="cpu", with_logits=False)
+    og, oref, lg, lref, info = _run_attention(cuda_lib, b, num_ctas=num_ctas)
+    mae, rel = _attn_errors(og, oref)
+    assert mae <= ATOL and rel <= RTOL_L2, (mae, rel, info)
+    np.testing.assert_allclose(lg, lref, atol=2e-2, rtol=1e-3)
+    if num_ctas >= 13:    # (2 or 5 CTAs: whole super-tile gangs, no cuts)
+        assert info["num_split_units"] > 0
+
+
+def test_attention_full_config5_sampled(cuda_lib):
+    """BASELINE configs[4] per-GPU shard at G = 8 (B = 16, P = 8K, T = 64, 64/8 heads: dual items)
+    in the launch configuration bench.py times; oracle on 3 sampled samples."""
+    cfg = CONFIGS["c5g8"]
+    b = make_verify_batch(cfg, device="cuda", gen_device="cuda", layers=1, with_logits=False)
+    for k in ("q", "k_cache", "v_cache"):
+        b[k] = b[k].cpu()
+    og, oref, lg, lref, info = _run_attention(cuda_lib, b, samples=[0, 7, 15])
+    mae, rel = _attn_errors(og, oref)
+    assert mae <= ATOL and rel <= RTOL_L2, (mae, rel, info)
+    np.testing.assert_allclose(lg, lref, atol=2e-2, rtol=1e-3)
 
 
 def test_attention_full_config2_sampled(cuda_lib):
