@@ -41,11 +41,16 @@ def _check_plan(core, P, T, Hq, Hkv, d=128, n=148):
     info = pl.info()
     assert cta[0] == 0 and cta[-1] == len(items) and np.all(np.diff(cta) >= 0)
     g = Hq // Hkv
+    # dual items (kernel RM = 4): every unit R = 32 with an even tile count -> an item covers
+    # tiles (mt, mt + 1); tile 1's split parts follow tile 0's by item.pad
+    dual = all(T[b] * g > 64 and ((T[b] * g + 127) // 128) % 2 == 0 for b in range(len(P)))
     cover = {}
-    for b_, kvh, mt, b0, b1, part, R, unit, Pi, node0, Ti, _ in items:
+    for b_, kvh, mt, b0, b1, part, R, unit, Pi, node0, Ti, pad in items:
         assert (Pi, node0, Ti) == (P[b_], to[b_], T[b_])       # lengths copied into the item
         assert (part < 0) == (unit < 0)
-        cover.setdefault((b_, kvh, mt), []).append((b0, b1, part))
+        for t in ((0, 1) if dual else (0,)):
+            assert not dual or mt % 2 == 0
+            cover.setdefault((b_, kvh, mt + t), []).append((b0, b1, part + t * pad if part >= 0 else -1))
     nsplit = 0
     for b in range(len(P)):
         nblk = (P[b] + T[b] + 63) // 64
