@@ -120,3 +120,25 @@ def test_instance_migration_chunks_fit_staging(core):
         assert 2 * (core.kv_pack_elems(32, 8, 128, lens) + core.kv_pack_elems(1, 8, 128, lens)) > cap
     with pytest.raises(RuntimeError):
         inst._chunks([SampleMeta(0, 10 ** 6, 0.0)], cap)
+
+
+def test_f1_f2_argument_validation(core):
+    """The new entry points reject bad arguments before touching the device (CPU-only checks)."""
+    import ctypes
+    L = core._lib
+    P = ctypes.c_void_p
+    # rs_lm_head_argmax: Dm must be a positive multiple of 64; rows == 0 is a no-op
+    assert L.rs_lm_head_argmax(P(16), P(16), 4, 100, 96, P(16), None, P(16), 64, None) == 1
+    assert L.rs_lm_head_argmax(P(16), P(16), 4, 0, 128, P(16), None, P(16), 64, None) == 1
+    assert L.rs_lm_head_argmax(None, None, 0, 100, 128, None, None, None, 0, None) == 0
+    assert L.rs_lm_head_argmax(P(16), P(16), 4, 100, 128, None, None, P(16), 64, None) == 1
+    assert L.rs_lm_head_argmax(P(16), P(16), 4, 100, 128, P(16), None, P(16), 8, None) == 11   # workspace
+    assert core.lm_head_argmax_workspace_bytes(1000) == 8000
+    # rs_tree_accept_greedy_tokens: B == 0 no-op, null pointers rejected
+    assert L.rs_tree_accept_greedy_tokens(None, None, None, None, 0, None, None, None, None, None) == 0
+    assert L.rs_tree_accept_greedy_tokens(None, None, None, None, 3, None, None, None, None, None) == 1
+    # two-stage migration: a null communicator / descriptor is rejected
+    assert L.rs_migrate_stage1(None, 0, 1, None, None, None, None, None, 1, None, 4, None, None, 0, None,
+                               None) == 1
+    assert L.rs_migrate_stage2(None, 0, 1, None, None, None, None, 1, None, 4, None, None, None, 0, None,
+                               None, None) == 1
