@@ -116,9 +116,18 @@ def main():
             t = C_DRAFT + t_ver + B2_GEMM * B * (n_star + 1)
             meas[n_star] = dict(al=al, t_verify=t_ver, t_step=t, tput=(al + B) / t)
         best_n = max(meas, key=lambda k: meas[k]["tput"])
+        # ladder (Fig. 13 direction): Default = no speculation (T = 1: one token per
+        # sample per step, no draft pass), Spec = a static draft budget (n = 24, the paper's
+        # example of a high fixed n; and n = 6), Selection = n* from select_strategy
+        t_def = time_step(retree(base, [np.array([-1], np.int32) for _ in range(B)], gen))
+        tput_def = B / (t_def + B2_GEMM * B)
         rows.append({"B": B, "n_selected": n_star, "n_best_fixed": best_n,
                      "tput_selected": round(meas[n_star]["tput"], 1), "tput_best_fixed": round(meas[best_n]["tput"], 1),
                      "pct_of_optimal": round(100.0 * meas[n_star]["tput"] / meas[best_n]["tput"], 2),
+                     "ladder_vs_default": {"default": 1.0, "spec_n6": round(meas[6]["tput"] / tput_def, 3),
+                                           "spec_n24": round(meas[24]["tput"] / tput_def, 3),
+                                           "selection": round(meas[n_star]["tput"] / tput_def, 3)},
+                     "default_tput": round(tput_def, 1), "default_t_verify_ms": round(t_def * 1e3, 3),
                      "pred_t_sd_ms": round(r["t_sd"] * 1e3, 3), "meas_t_step_ms": round(meas[n_star]["t_step"] * 1e3, 3),
                      "curve": {str(k): round(v["tput"], 1) for k, v in sorted(meas.items())},
                      "t_verify_ms": {str(k): round(v["t_verify"] * 1e3, 3) for k, v in sorted(meas.items())}})
