@@ -207,6 +207,29 @@ __device__ __forceinline__ float ex2_mix(float x, int c) {
     return ex2(x);
 }
 
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2): one instruction per two elements of a row.
+#ifndef RS_ATTN_F32X2
+#define RS_ATTN_F32X2 0
+#endif
+__device__ __forceinline__ uint64_t f2_pack(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     uint32_t r;
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
@@ -1077,6 +1100,24 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                         }
                     }
                     const float mo = (m_run == -INFINITY) ? 0.0f : m_run;
+#if RS_ATTN_F32X2
+                    {
+                        const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2), nm2 = f2_pack(-mo, -mo);
+                        uint64_t ls2[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+                        for (int c = 0; c < 64; c += 2) {
+                            float x0, x1;
+                            f2_unpack(f2_fma(f2_pack(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), sc2, nm2), x0, x1);
+                            const float e0 = ex2_mix(x0, c), e1 = ex2_mix(x1, c + 1);
+                            sr[c >> 1] = pack_bf16(e0, e1);
+                            ls2[(c >> 1) & 3] = f2_add(ls2[(c >> 1) & 3], f2_pack(e0, e1));
+                        }
+                        float a0, a1, b0, b1;
+                        f2_unpack(f2_add(f2_add(ls2[0], ls2[1]), f2_add(ls2[2], ls2[3])), a0, a1);
+                        (void)b0; (void)b1;
+                        l_run += a0 + a1;
+                    }
+#else
                     float ls8[8];
 #pragma unroll
                     for (int k = 0; k < 8; ++k) ls8[k] = 0.0f;
@@ -1089,6 +1130,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                         ls8[(c >> 1) & 7] += e0 + e1;
                     }
                     l_run += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
+#endif
                     wait_prev_pv();
                     tmem_st32(tmem + lane_base + C::kColP + grp * (kBlockN / 2),
                               reinterpret_cast<const uint32_t(&)[32]>(sr[0]));
