@@ -329,3 +329,93 @@ class GenerationInstance:
                         recv += 1
         self.samples = [s for s in self.samples if s.gid not in sent_gids] + received
         return sent, recv, moved
+
+    def rebalance_two_stage(self, rebalancer: Rebalancer, comm: "core.Comm", staging, scratch, overlap_steps=1,
+                            seed=0, force=False):
+        """Reallocation with the paper's two-stage migration (f1). Collective over all
+        instances, like rebalance(). Stage 1 (rs_migrate_stage1) enqueues the chosen samples'
+        verified KV on a side stream; every instance then runs `overlap_steps` verify steps — the
+        migrating samples keep generating on their source, which only writes slots beyond the
+        prefix in flight (Markov property); stage 2 (rs_migrate_stage2) moves the tokens
+        committed meanwhile, SSM part first, and the samples change hands with their updated
+        state. Only samples that cannot finish during the overlap are chosen. Returns
+        (#sent, #received, KV bytes moved by this rank, timing dict in ms)."""
+        transfers = rebalancer.plan(self.load, force=force)
+        if not transfers:
+            return 0, 0, 0, {}
+        guard = overlap_steps * self.T                 # a step commits at most T tokens per sample
+        transfers = rebalancer.choose(transfers, [m for m in self.sample_meta() if m.remaining > guard])
+        cap = staging.numel() * staging.element_size()
+        side = torch.cuda.Stream(device=self.dev)
+        ev = lambda: torch.cuda.Event(enable_timing=True)
+
+        def src_rows(gids):
+            by_gid = {x.gid: x for x in self.samples}
+            rows = np.zeros((len(gids), self.max_pages), np.int32)
+            for i, g in enumerate(gids):
+                pg = by_gid[g].pages
+                rows[i, :len(pg)] = pg
+                rows[i, len(pg):] = pg[-1]
+            return torch.from_numpy(rows).to(self.dev)
+
+        jobs = []
+        for tr in transfers:
+            if comm.rank not in (tr.src, tr.dst) or not tr.samples:
+                continue
+            gids = [c.gid for c in tr.samples]
+            len1 = [c.seq_len for c in tr.samples]
+            reserve = [l + guard for l in len1]
+            need = 2 * (core.kv_pack_elems(self.L, self.Hkv, self.d, reserve) +
+                        core.kv_pack_elems(1, self.Hkv, self.d, reserve))
+            if need > cap:
+                raise RuntimeError(f"two-stage migration needs {need} staging bytes > {cap}")
+            mig = core.TwoStageMigration(comm, tr.src, tr.dst, (self.k_llm, self.v_llm), (self.k_ssm, self.v_ssm),
+                                         PAGE, self.pool if comm.rank == tr.dst else None, self.max_pages, staging,
+                                         scratch, side)
+            e = [ev() for _ in range(4)]
+            e[0].record(side)
+            mig.stage1(gids, len1, reserve, src_rows(gids) if comm.rank == tr.src else None)
+            e[1].record(side)
+            jobs.append((tr, mig, gids, e))
+        for k in range(overlap_steps):                 # computation continues while stage 1 streams
+            self.step(seed=seed + k)
+        # the sources' updated sample state, on every rank (collective, in plan order)
+        state = {}
+        by_gid = {x.gid: x for x in self.samples}
+        for tr in transfers:
+            mine = None
+            if comm.rank == tr.src:
+                mine = [(g.gid, by_gid[g.gid].length, by_gid[g.gid].remaining, by_gid[g.gid].steps,
+                         by_gid[g.gid].accepted) for g in tr.samples]
+            state[id(tr)] = rebalancer.share(tr, mine)
+        sent = recv = moved = 0
+        sent_gids, received, timing = set(), [], {}
+        for tr, mig, gids, e in jobs:
+            upd = state[id(tr)]
+            len2 = [u[1] for u in upd]
+            e[2].record(side)
+            mig.stage2(len2, src_rows(gids) if comm.rank == tr.src else None)
+            e[3].record(side)
+            side.synchronize()
+            timing = {"stage1_ms": e[0].elapsed_time(e[1]), "stage2_stall_ms": e[2].elapsed_time(e[3]),
+                      "delta_tokens": int(sum(len2) - sum(c.seq_len for c in tr.samples))}
+            if comm.rank == tr.dst:
+                timing["ssm_ready_ms"] = e[2].elapsed_time(mig.ssm_ready)
+            moved += 2 * (core.kv_pack_elems(self.L, self.Hkv, self.d, len2) +
+                          core.kv_pack_elems(1, self.Hkv, self.d, len2))
+            if comm.rank == tr.src:
+                self._migrated_from = {g: by_gid[g].pages.copy() for g in gids}   # (tests: old pages)
+                for g in gids:
+                    self.pool.free(by_gid[g].pages)
+                    sent_gids.add(g)
+                    sent += 1
+            if comm.rank == tr.dst:
+                rows = mig.dst_rows()
+                for i, (g, length, rem, steps, acc) in enumerate(upd):
+                    npg = self._pages_for(int(mig.capacity[i]))
+                    rcv = Sample(g, length, rem, None, steps, acc)
+                    rcv.set_pages(rows[i, :npg].copy(), self.max_pages)
+                    received.append(rcv)
+                    recv += 1
+        self.samples = [x for x in self.samples if x.gid not in sent_gids] + received
+        return sent, recv, moved, timing

@@ -90,6 +90,13 @@ class Rebalancer:
             tr.samples = payload[0]
         return transfers
 
+    def share(self, tr: Transfer, payload):
+        """Collective: the source's payload for transfer tr (any picklable object), on every rank."""
+        obj = [payload]
+        src_global = dist.get_global_rank(self.pg, tr.src) if self.pg is not None else tr.src
+        dist.broadcast_object_list(obj, src=src_global, group=self.pg)
+        return obj[0]
+
 
 def execute(transfers: list[Transfer], comm: "core.Comm", llm_layers, ssm_layers, page_size: int,
             pool: "core.PagePool", block_table_of, max_pages: int, staging, scratch, stream=None):

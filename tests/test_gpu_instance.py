@@ -82,6 +82,9 @@ class _LoopbackRebalancer:
         from paper_2512_04752_b200.realloc import Transfer
         return [Transfer(0, 0, self.count)]
 
+    def share(self, tr, payload):
+        return payload
+
     def choose(self, transfers, metas):
         transfers[0].samples = sorted(metas, key=lambda m: (m.seq_len, m.gid))[:self.count]
         return transfers
@@ -115,4 +118,43 @@ def test_instance_rebalance_loopback_moves_kv_bit_exact(cuda_lib):
                     assert torch.equal(old[j // 64, :, j % 64], new[j // 64, :, j % 64])
     while inst.load:                                              # the moved samples keep generating
         inst.step(seed=6)
+    assert inst.finished == len(samples) and inst.pool.free_count() == 256
+
+
+def test_instance_rebalance_two_stage_loopback(cuda_lib):
+    """f1 in the generation loop: stage 1 streams the chosen samples' prefixes while the instance
+    runs a verify step (the migrating samples included), stage 2 moves the tokens committed
+    meanwhile (SSM first). Every committed token of a moved sample is bit-identical in its new
+    pages (LLM and SSM pools), its state carries the overlap step, and the run completes with
+    every page back in the pool."""
+    core = cuda_lib
+    inst, samples = _instance(n=12, seed=9)
+    for _ in range(2):
+        inst.step(seed=5)
+    comm = core.Comm(0, 1)
+    staging = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    scratch = torch.empty(3 * 64 + 64 * inst.max_pages, dtype=torch.int32, device="cuda")
+    steps_before = {s.gid: s.steps for s in inst.samples}
+    try:
+        sent, recv, moved, timing = inst.rebalance_two_stage(_LoopbackRebalancer(4), comm, staging, scratch,
+                                                             overlap_steps=1, seed=7)
+    finally:
+        comm.destroy()
+    assert sent == recv == 4 and moved > 0
+    assert timing["stage2_stall_ms"] >= 0 and timing["delta_tokens"] > 0 and "ssm_ready_ms" in timing
+    old = inst._migrated_from
+    pools = inst.k_llm + inst.v_llm + inst.k_ssm + inst.v_ssm
+    by_gid = {s.gid: s for s in inst.samples}
+    assert set(old) <= set(by_gid)
+    for g, pg0 in old.items():
+        s = by_gid[g]
+        assert s.steps == steps_before[g] + 1                      # the overlap step counted
+        assert not np.array_equal(s.pages[:len(pg0)], pg0)        # new pages
+        for t in pools:
+            a = t[torch.as_tensor(pg0, device="cuda").long()]
+            b = t[torch.as_tensor(s.pages, device="cuda").long()]
+            for j in range(s.length):                              # every committed token
+                assert torch.equal(a[j // 64, :, j % 64], b[j // 64, :, j % 64]), (g, j)
+    while inst.load:
+        inst.step(seed=8)
     assert inst.finished == len(samples) and inst.pool.free_count() == 256
