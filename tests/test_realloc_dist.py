@@ -44,8 +44,12 @@ def _worker(rank, world, port, seed, thr, outdir):
         out_g = {s.gid for tr in trs if tr.src == rank for s in tr.samples}
         kept = [s for s in mine if s.gid not in out_g]
         got = [s for tr in trs if tr.dst == rank for s in tr.samples]
+        # two-stage migration's state hand-over (f1): each source shares its updated sample
+        # state after the overlap steps; every rank sees the source's payload, in plan order
+        shared = [rb.share(t, [(s.gid, s.seq_len + 3) for s in t.samples] if t.src == rank else None) for t in trs]
         res = dict(plan=[(t.src, t.dst, t.count) for t in trs],
                    chosen={t.src: [s.gid for s in t.samples] for t in trs},
+                   shared=shared,
                    final=sorted(s.gid for s in kept + got))
         np.save(os.path.join(outdir, f"r{rank}.npy"), np.array([res], dtype=object), allow_pickle=True)
     finally:
@@ -67,6 +71,9 @@ def test_rebalancer_gloo(world, seed, thr):
     for s, dd, k in ref_plan:
         ref_choice = OR.choose_samples([(x.gid, x.seq_len, x.avg_accepted) for x in samples[s]], k)
         assert sorted(res[0]["chosen"][s]) == sorted(ref_choice)
+    for r in range(world):                                           # share(): the source's payload everywhere
+        for (s, dd, k), sh in zip(ref_plan, res[r]["shared"]):
+            assert [g for g, _ in sh] == res[0]["chosen"][s] and len(sh) == k
     final_loads = [len(res[r]["final"]) for r in range(world)]
     assert final_loads == OR.apply_plan(loads, ref_plan)
     all_final = sorted(g for r in range(world) for g in res[r]["final"])
