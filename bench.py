@@ -229,6 +229,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--realloc", default="on", choices=["on", "off"], help="c4: sample reallocation")
     ap.add_argument("--cooldown", type=int, default=32, help="c4: steps between reallocation checks (P:300)")
+    ap.add_argument("--migration", default="blocking", choices=["blocking", "two-stage"],
+                    help="c4: stop-the-world rs_migrate_samples or the two-stage migration (f1, P:303-318)")
     args = ap.parse_args()
     if args.steps is None:
         args.steps = 400 if args.config == "c4" else 50
@@ -510,15 +512,24 @@ def run_c4(args, world, rank, local):
     reb = Rebalancer(thr, cooldown=args.cooldown) if realloc else None
     comm = core.Comm(rank, world) if realloc else None
     staging = torch.empty(4 << 30, dtype=torch.uint8, device=dev) if realloc else None
-    scratch = torch.empty(2 * 512 + 512 * 72, dtype=torch.int32, device=dev) if realloc else None
+    scratch = torch.empty(3 * 512 + 512 * 72, dtype=torch.int32, device=dev) if realloc else None
+    stalls = []
 
     def one_step(k, timing=False):
         mig = (0, 0, 0, 0.0)
+        tok0 = inst.tokens
         if realloc:
             t0 = time.perf_counter()
-            sent, recv, moved = inst.rebalance(reb, comm, staging, scratch)
+            if args.migration == "two-stage":   # (its overlap step is a verify step of this loop)
+                sent, recv, moved, tm = inst.rebalance_two_stage(reb, comm, staging, scratch, overlap_steps=1,
+                                                                 seed=11)
+                if tm:
+                    stalls.append(tm["stage2_stall_ms"])
+            else:
+                sent, recv, moved = inst.rebalance(reb, comm, staging, scratch)
             mig = (sent, recv, moved, time.perf_counter() - t0)
-        return inst.step(seed=11, timing=timing), mig
+        inst.step(seed=11, timing=timing)
+        return inst.tokens - tok0, mig
 
     for w in range(args.warmup):
         one_step(w)
@@ -565,6 +576,7 @@ def run_c4(args, world, rank, local):
         "config": {"workload": f"c4: {WORKLOAD_DESC['c4']}", "samples_per_instance": len(samples),
                    "Hq": Hq, "Hkv": Hkv, "d": d, "L": L, "V": 128256, "tree": ["fixed", T], "accept_mode": "greedy",
                    "realloc": "on" if realloc else "off", "cooldown": args.cooldown, "threshold": thr,
+                   "migration": args.migration,
                    "knee_profile": {"counts": counts, "tokens_per_s": [round(x, 1) for x in tput]},
                    "load_first_last": [loads[0] if loads else 0, loads[-1] if loads else 0],
                    "finished_samples_rank0": inst.finished, "tokens_rank0": tokens,
@@ -584,7 +596,8 @@ def run_c4(args, world, rank, local):
                      "peak_source": peak_src, "attention_share_of_step": round(attn_ms / ms, 4)},
         "migration": {"events": len(migrations), "samples_moved_rank0": sum(m[0] + m[1] for m in migrations),
                       "bytes_rank0": int(mig_bytes), "seconds_rank0": round(mig_s, 4),
-                      "GBps_rank0": round(mig_bytes / mig_s / 1e9, 2) if mig_s > 0 else None},
+                      "GBps_rank0": round(mig_bytes / mig_s / 1e9, 2) if mig_s > 0 else None,
+                      **({"two_stage_stall_ms_rank0": [round(x, 3) for x in stalls]} if stalls else {})},
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
