@@ -86,7 +86,8 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
                page_size);
     const int g = Hq / Hkv;
     // per-item overhead (epilogue, Q load) in KV-block units; RS_ATTN_OVH overrides (tuning only)
-    const int kOvhBlocks = getenv("RS_ATTN_OVH") ? std::max(0, atoi(getenv("RS_ATTN_OVH"))) : kOvhBlocksDefault;
+    const bool ovh_env = getenv("RS_ATTN_OVH") != nullptr;
+    int kOvhBlocks = ovh_env ? std::max(0, atoi(getenv("RS_ATTN_OVH"))) : kOvhBlocksDefault;
     RS_REQUIRE(g <= 16 && (16 % g) == 0, RS_ERR_UNSUPPORTED, "rs_attn_plan_create: group size %d (need g | 16)", g);
     if (num_ctas <= 0) {
         int dev = 0, sms = 148;
@@ -130,6 +131,10 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
         pl->rmodes = 4;
     }
     const int tile_mul = dual ? 2 : 1;   // item.mtile = tile_mul * (super) tile index
+    // per-item overhead by kernel mode (measured sweeps): the 16-warp kernel hides its
+    // epilogue behind the next item (2 blocks); the 12-warp kernels run it inline (~5k cycles,
+    // ~4-6 blocks); a dual item's block carries two tiles of work, so its overhead is ~1 block
+    if (!ovh_env) kOvhBlocks = dual ? 1 : (pl->rmodes == 1 ? kOvhBlocksDefault : 6);
     const int n_ctas = std::max(1, std::min<int>(num_ctas, std::max(n_tiles, 1)));
     // Gangs: the M tiles of a unit group run on M different CTAs ("a gang") that process the
     // same key-block ranges in the same order at the same time, so the K/V blocks the first CTA

@@ -30,7 +30,13 @@ def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "c2"
     layers = int(sys.argv[2]) if len(sys.argv) > 2 else 4
     cfg = CONFIGS[name]
-    b = make_verify_batch(cfg, device="cuda", gen_device="cuda", layers=layers)
+    if cfg.tree[0] == "strategy":   # c3s: verification trees = S(n) from select_strategy, as bench.py
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        import bench
+        strat = bench.strategy_trees(cfg, core)
+        b = make_verify_batch(cfg, device="cuda", gen_device="cuda", layers=layers, parents=strat[4])
+    else:
+        b = make_verify_batch(cfg, device="cuda", gen_device="cuda", layers=layers)
     mode = {"greedy": core.GREEDY, "delta": core.SAMPLE_DELTA, "mss": core.SAMPLE_MSS}[cfg.mode]
     st = VerifyStep(b, mode=mode)
     st.device_step()
