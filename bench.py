@@ -725,10 +725,25 @@ def run_reference(args, world, rank):
         cfg = VerifyConfig("c4", B=1, Hq=32, Hkv=8, d=128, V=128256, L=32, prefix=("lognormal", 600, 0.784, 32, 4096),
                            tree=("fixed", 16), mode="greedy", seed=4)
     else:
-        cfg = CONFIGS[args.config]
+        cfg = CONFIGS[LM_HEAD[args.config][0] if args.config in LM_HEAD else args.config]
     # one whole sample per step (all L layers), drawn on the CPU with the same recipe
     one = type(cfg)(**{**cfg.__dict__, "B": max(1, args.steps + args.warmup)})
-    b = make_verify_batch(one, device="cpu", spare_pages=0)
+    parents = None
+    if cfg.tree[0] == "strategy":
+        # c3s: the batch's n from the oracle's select_strategy over the whole batch's candidate
+        # trees (same draws as strategy_trees), each sample's tree from the oracle's S(n)
+        from oracle import strategy as OS
+        from synth import draw_prefix_lengths, make_candidate_tree
+        P = draw_prefix_lengths(np.random.default_rng(cfg.seed), cfg)
+        rng = np.random.default_rng(cfg.seed + 77)
+        cands = [make_candidate_tree(rng, int(cfg.tree[1])) for _ in range(cfg.B)]
+        c = STRATEGY_COST
+        cost = OS.CostModel(c["c_draft"], c["b0"], c["b1"], c["b2"], c["b3"], c["k_sat"], c["seq_bucket"],
+                            c["draft_bucket"])
+        n = OS.select_strategy(cands, P, STRATEGY_KX, STRATEGY_KY, cost, n_min=3, n_max=63, patience=2)["n"]
+        parents = [OS.verification_tree(p_, o_, np.zeros(len(p_), np.int32), 0, n, STRATEGY_KX, STRATEGY_KY)[0]
+                   for p_, o_ in cands[:one.B]]
+    b = make_verify_batch(one, device="cpu", spare_pages=0, parents=parents)
     L = b["q"].shape[0]
     from oracle import accept as OAcc
     from oracle import attention as OA
