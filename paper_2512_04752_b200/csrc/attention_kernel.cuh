@@ -208,6 +208,11 @@ __device__ __forceinline__ float ex2_mix(float x, int c) {
 }
 
 // Packed fp32 pairs (sm_100 FFMA2 / FADD2): one instruction per two elements of a row.
+#ifndef RS_ATTN_DU_EPI
+#define RS_ATTN_DU_EPI 16   // dual-item epilogue: O columns read from TMEM per wait (16 | 32 | 64)
+#endif
+constexpr int kDuEpi = RS_ATTN_DU_EPI;
+
 #ifndef RS_ATTN_F32X2
 #define RS_ATTN_F32X2 0
 #endif
@@ -1183,16 +1188,18 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                     __nv_bfloat16* orow = p.out + ((int64_t)(off + node) * p.Hq + h) * D;
                     float* prow = direct ? nullptr : p.part_o + ((int64_t)part * kM + rr) * D;
 #pragma unroll 1
-                    for (int cc = 0; cc < ((p.dbg & 1) ? 0 : D); cc += 16) {
-                        uint32_t a[16];
-                        tmem_ld16(o_mine + cc, a);
+                    for (int cc = 0; cc < ((p.dbg & 1) ? 0 : D); cc += kDuEpi) {
+                        uint32_t a[kDuEpi];                  // kDuEpi columns in flight per TMEM wait
+#pragma unroll
+                        for (int q = 0; q < kDuEpi / 16; ++q)
+                            tmem_ld16(o_mine + cc + 16 * q, *reinterpret_cast<uint32_t(*)[16]>(a + 16 * q));
                         tmem_wait_ld();
 #pragma unroll
-                        for (int c = 0; c < 16; ++c) a[c] = __float_as_uint(__uint_as_float(a[c]) * invL);
+                        for (int c = 0; c < kDuEpi; ++c) a[c] = __float_as_uint(__uint_as_float(a[c]) * invL);
                         if (row_valid) {
                             if (direct) {
 #pragma unroll
-                                for (int c = 0; c < 16; c += 8) {
+                                for (int c = 0; c < kDuEpi; c += 8) {
                                     uint4 u;
                                     u.x = pack_bf16(__uint_as_float(a[c]), __uint_as_float(a[c + 1]));
                                     u.y = pack_bf16(__uint_as_float(a[c + 2]), __uint_as_float(a[c + 3]));
@@ -1202,7 +1209,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                                 }
                             } else {
 #pragma unroll
-                                for (int c = 0; c < 16; c += 4)
+                                for (int c = 0; c < kDuEpi; c += 4)
                                     *reinterpret_cast<uint4*>(prow + cc + c) = make_uint4(a[c], a[c + 1], a[c + 2], a[c + 3]);
                             }
                         }
