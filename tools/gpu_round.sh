@@ -7,7 +7,6 @@ timeout 900 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke exit $?" >> $OUT/smoke.log
 timeout 400 python bench.py > $OUT/bench_c2.json 2> $OUT/bench_c2.err
 timeout 400 python bench.py --config c3s --no-cpu-baseline > $OUT/bench_c3s.json 2> $OUT/bench_c3s.err
-RS_CORE_LIB=paper_2512_04752_b200/_variants/res2/librlhfspec_core.so timeout 400 python bench.py --config c3s --no-cpu-baseline --steps 20 > $OUT/bench_c3s_res2.json 2> $OUT/bench_c3s_res2.err
 timeout 600 python bench.py --config c4 > $OUT/bench_c4.json 2> $OUT/bench_c4.err
 timeout 400 python bench.py --config c5g8 --steps 20 --no-cpu-baseline > $OUT/bench_c5g8.json 2> $OUT/bench_c5g8.err
 ls $OUT
