@@ -132,3 +132,39 @@ def test_two_stage_self_nccl_overlapped(cuda_lib):
     finally:
         side.synchronize()
         comm.destroy()
+
+
+def test_two_stage_zero_delta_and_llm_only(cuda_lib):
+    """Edge cases: stage 2 with no tokens verified meanwhile (an empty transfer) and a store with
+    no SSM model; the prefix moved by stage 1 is intact and nothing else changes."""
+    core = cuda_lib
+    llm = _batch(L=2, Hkv=8, d=128, B=4, seed=13, spare=64)
+    bt = llm["block_table"]
+    maxp = bt.shape[1]
+    K, V, kc, vc = _layers(llm)
+    used = set(np.unique(bt).tolist())
+    pool = core.PagePool(llm["num_pages"])
+    taken = pool.alloc(llm["num_pages"])
+    pool.free([p for p in taken.tolist() if p not in used])
+    sel = np.array([0, 2], np.int64)
+    len1 = llm["prefix_len"][sel].astype(np.int32)
+    comm = core.Comm(0, 1)
+    side = torch.cuda.Stream()
+    try:
+        staging = torch.empty(core.kv_pack_elems(2, 8, 128, len1), dtype=torch.int16, device="cuda")
+        scratch = torch.empty(3 * 2 + 2 * maxp, dtype=torch.int32, device="cuda")
+        mig = core.TwoStageMigration(comm, 0, 0, (K, V), None, 64, pool, maxp, staging, scratch, side)
+        mig.stage1(llm["gid"][sel], len1, len1, _dev(bt[sel]))
+        free_mid = pool.free_count()
+        mig.stage2(len1, _dev(bt[sel]))                # nothing verified meanwhile
+        side.synchronize()
+        assert pool.free_count() == free_mid            # no extra pages
+        rows = mig.dst_rows()
+        for cache in (kc, vc):
+            bits = tensor_bf16_bits(cache)
+            for i, s in enumerate(sel):
+                t = np.arange(int(len1[i]))
+                np.testing.assert_array_equal(bits[:, rows[i, t // 64], :, t % 64], bits[:, bt[s, t // 64], :, t % 64])
+    finally:
+        side.synchronize()
+        comm.destroy()
