@@ -197,3 +197,20 @@ def test_verify_step_with_fused_lm_head(cuda_lib):
     assert np.array_equal(res["accepted_len"], racc) and np.array_equal(res["path"], rpath)
     assert np.array_equal(res["bonus"], rbonus)
     assert np.array_equal(res["new_len"], b["prefix_len"] + 1 + racc)
+
+
+def test_lm_head_argmax_all_negative_ragged_tail(cuda_lib):
+    """Every logit negative and V ragged (1000 = 3 full 256-wide tiles + 232): the zero-filled
+    columns past V must never win; the maximum sits in the tail tile for some rows."""
+    rng = np.random.default_rng(12)
+    rows, V, Dm = 70, 1000, 128
+    H = np.abs(rng.standard_normal((rows, Dm))) + 0.1
+    W = -np.abs(rng.standard_normal((V, Dm))) - 0.1
+    W[997] = -0.01                       # the least negative row: the arg-max, in the ragged tile
+    Hd, Wd = _dev_bf16(H), _dev_bf16(W)
+    tok, mx = cuda_lib.lm_head_argmax(Hd, Wd)
+    torch.cuda.synchronize()
+    t = tok.cpu().numpy()
+    assert np.all(t == 997)
+    assert np.all(mx.cpu().numpy() < 0)
+    _check_rows(t, mx.cpu().numpy(), Hd.double().cpu().numpy(), Wd, min_exact=1.0)
