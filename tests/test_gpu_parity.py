@@ -242,6 +242,8 @@ ATTN_CASES = {
                                 tree=("fixed", 64), seed=26),
     "g8_T60_dual_ragged": VerifyConfig("g8r", B=4, Hq=64, Hkv=8, d=128, V=10, L=1, prefix=("lognormal", 200, 1.0, 0, 900),
                                        tree=("range", 49, 64), seed=27),
+    "g8_T48_gang3": VerifyConfig("g8t48", B=3, Hq=64, Hkv=8, d=128, V=10, L=1, prefix=("fixed", 650),
+                                 tree=("fixed", 48), seed=29),
     "d64_g8_dual": VerifyConfig("d64d", B=3, Hq=16, Hkv=2, d=64, V=10, L=1, prefix=("lognormal", 400, 1.0, 0, 2000),
                                 tree=("range", 49, 64), seed=28),
     "d64_g2": VerifyConfig("d64", B=9, Hq=4, Hkv=2, d=64, V=10, L=1, prefix=("lognormal", 90, 1.2, 0, 500),
