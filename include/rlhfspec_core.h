@@ -116,10 +116,14 @@ rs_status rs_tree_accept_greedy_tokens(const int32_t* argmax_token, const int32_
  *   knots_x, knots_y device f64 [n_knots], 2 <= n_knots <= 16, knots_x increasing
  *   parent_out, token_out, depth_out device int32 [B*(n+1)]; tree_mask_out device u64 [B*(n+1)]
  *               (exactly what rs_tree_build_mask would give for parent_out)
- *   status_flags device int32 [B]: RS_FLAG_MALFORMED (candidate parents not topological, or
- *               > 256 candidates) / RS_FLAG_INSUFFICIENT (the search ran out before n pops);
- *               such a sample's missing nodes are children of the root with token -1.
- * Errors: n outside [1, 63] -> RS_ERR_UNSUPPORTED; bad knots / null -> RS_ERR_INVALID_ARG. */
+ *   status_flags device int32 [B]: RS_FLAG_MALFORMED (candidate parents not topological, an
+ *               o(u) outside [0, 1] or NaN, > 256 candidates, knots not strictly increasing in x
+ *               and non-decreasing in y (checked on the device: every sample flagged), or a
+ *               selected node whose parent was not selected — its token is then -1) /
+ *               RS_FLAG_INSUFFICIENT (the search ran out before n pops); such a sample's missing
+ *               nodes are children of the root with token -1, which rs_tree_accept flags.
+ * Errors: n outside [1, 63] -> RS_ERR_UNSUPPORTED; n_knots outside [2, 16] / null ->
+ * RS_ERR_INVALID_ARG. */
 rs_status rs_tree_select(const int32_t* cand_parent, const double* cand_o, const int32_t* cand_token,
                          const int32_t* cand_off, const int32_t* root_token, int32_t B, int32_t n,
                          const double* knots_x, const double* knots_y, int32_t n_knots,
@@ -156,6 +160,17 @@ rs_status rs_attn_plan_info(const rs_attn_plan* plan, int32_t* num_ctas, int32_t
  * sub-partition R, split unit or -1, prefix_len, tree_off, tree size, 0). Either may be NULL. */
 rs_status rs_attn_plan_items(const rs_attn_plan* plan, int32_t* cta_off, int32_t* items);
 void rs_attn_plan_destroy(rs_attn_plan* plan);
+/* Programmatic dependent launch (PDL). Every attention launch may begin while the previous
+ * kernel on the stream drains; by default it reads NOTHING written by kernels (K/V, block
+ * table, Q, masks) before that kernel has completed (griddepcontrol.wait). enable = 1 lets the
+ * K/V producers stream the PREFIX blocks (every slot < P_b) and read the block table early: set
+ * it only when no kernel that may still be running when the attention launch is enqueued writes
+ * the prefix K/V pages or the block table (e.g. the previous step's rs_kv_compact is separated
+ * from this launch by another kernel, as in a verify step: mask build, then the layers). Blocks
+ * holding tree slots (P_b + i) are always read after the wait, so the tree K/V may be written by
+ * the kernel immediately before (the QKV/RoPE projection). Applies to later launches with this
+ * plan. */
+rs_status rs_attn_plan_set_early_prefix(rs_attn_plan* plan, int32_t enable);
 /* Profiling hook: when buf (device, >= num_ctas*256*8*8 bytes) is set, every attention launch
  * records clock64() per (CTA, block, event) — see csrc/attention.cu. NULL disables. */
 rs_status rs_attn_set_trace(void* buf, size_t bytes);
@@ -201,7 +216,10 @@ rs_status rs_tree_verify_attention_layers(
  *   accepted_len device int32 [B]  out: a_b (accepted drafts, bonus excluded)
  *   path         device int32 [B, 64] out: path[b][0..a_b] local node ids (path[b][0]=0), -1 padded
  *   bonus_token  device int32 [B]  out: the bonus token (-1 on a flagged sample)
- *   status_flags device int32 [B]  out: RS_FLAG_* bits
+ *   status_flags device int32 [B]  out: RS_FLAG_* bits. RS_FLAG_MALFORMED (accepted_len 0,
+ *               bonus -1): T_b outside [1, 64], parent[0] != -1, parent[i] outside [0, i), or a
+ *               draft node (i >= 1) whose token is outside [0, V) (e.g. rs_tree_select's -1 pad).
+ *               RS_FLAG_NONFINITE: a visited row holds NaN/Inf (walk stops there, bonus -1).
  *   ws, ws_bytes: device workspace >= rs_tree_accept_workspace_bytes(mode, B, V) bytes, 16-byte
  *               aligned (MSS keeps each sample's residual weights there; 0 bytes otherwise:
  *               NULL allowed); too small -> RS_ERR_WORKSPACE. */

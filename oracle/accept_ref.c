@@ -179,9 +179,12 @@ int oracle_tree_accept(int mode, const void* logits, int logits_is_bf16, const f
         accepted_len[b] = 0;
         bonus[b] = -1;
         flags[b] = 0;
-        /* tree validation (reading Z1): 1 <= T <= 64, parent[0] = -1, 0 <= parent[i] < i */
+        /* tree validation (reading Z1): 1 <= T <= 64, parent[0] = -1, 0 <= parent[i] < i, and
+         * every draft node's token is a vocabulary id, 0 <= token[i] < V for i >= 1 (the root's
+         * token is the last committed one and is never tested) */
         int ok = (T >= 1 && T <= MAX_TREE && parent[off] == -1);
-        for (int i = 1; ok && i < T; ++i) ok = (parent[off + i] >= 0 && parent[off + i] < i);
+        for (int i = 1; ok && i < T; ++i)
+            ok = (parent[off + i] >= 0 && parent[off + i] < i && token[off + i] >= 0 && token[off + i] < V);
         if (!ok) { flags[b] = FLAG_MALFORMED; continue; }
 
         int c = 0, a = 0;

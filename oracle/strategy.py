@@ -143,7 +143,15 @@ def verification_tree(parent, o, token, root_token, n, knots_x, knots_y):
     candidate index; a candidate whose parent is the virtual root (-1) hangs under node 0.
     S(n) is closed under parents (a node is popped only after its parent), so the result is
     topologically ordered. Returns (parent_v, token_v) int32 of length n + 1; raises
-    ValueError("InsufficientNodes") when the search yields fewer than n nodes."""
+    ValueError("InsufficientNodes") when the search yields fewer than n nodes and
+    ValueError("MalformedTree") when F's knots are not monotone (x strictly increasing, y
+    non-decreasing), an o(u) is outside [0, 1], or S(n) is not closed under parents."""
+    kx, ky = np.asarray(knots_x, float), np.asarray(knots_y, float)
+    if not (np.all(np.isfinite(kx)) and np.all(np.isfinite(ky)) and np.all(np.diff(kx) > 0)
+            and np.all(np.diff(ky) >= 0)):
+        raise ValueError("MalformedTree")      # F must be monotone piecewise linear (P:192)
+    if not all(0.0 <= float(x) <= 1.0 for x in o):
+        raise ValueError("MalformedTree")      # o(u) is a probability (P:80)
     dl = draft_logits(parent, o)
     w = np.array([acceptance_fit(knots_x, knots_y, x) for x in dl])
     order = layer_search_order(parent, w, n)
@@ -151,6 +159,8 @@ def verification_tree(parent, o, token, root_token, n, knots_x, knots_y):
         raise ValueError("InsufficientNodes")
     chosen = sorted(order)
     pos = {c: i + 1 for i, c in enumerate(chosen)}
+    if any(parent[c] >= 0 and int(parent[c]) not in pos for c in chosen):
+        raise ValueError("MalformedTree")      # S(n) not closed under parents
     par = [-1] + [0 if parent[c] < 0 else pos[int(parent[c])] for c in chosen]
     tok = [int(root_token)] + [int(token[c]) for c in chosen]
     return np.array(par, np.int32), np.array(tok, np.int32)

@@ -44,6 +44,7 @@ _sig("rs_attn_plan_upload", _i32, _P, _P, _sz, _P)
 _sig("rs_attn_plan_info", _i32, _P, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32))
 _sig("rs_attn_plan_destroy", None, _P)
 _sig("rs_attn_plan_items", _i32, _P, _P, _P)
+_sig("rs_attn_plan_set_early_prefix", _i32, _P, _i32)
 _sig("rs_attn_set_trace", _i32, _P, _sz)
 _sig("rs_tree_verify_attention", _i32, _P, _P, _P, _P, _i64, _P, _i32, _P, _P, _P, _i32, _i32, _i32,
      _i32, _i32, _f32, _P, _P, _P, _sz, _P)
@@ -127,7 +128,8 @@ def tree_select(cand_parent, cand_o, cand_token, cand_off, root_token, n, knots_
 class AttnPlan:
     """Host schedule for one verify step (lengths of this step), shared by every layer."""
 
-    def __init__(self, prefix_len_host, tree_off_host, Hq, Hkv, head_dim, page_size=64, num_ctas=0):
+    def __init__(self, prefix_len_host, tree_off_host, Hq, Hkv, head_dim, page_size=64, num_ctas=0,
+                 early_prefix=False):
         self._pl = _host_i32(prefix_len_host)
         self._to = _host_i32(tree_off_host)
         self.B, self.Hq, self.Hkv, self.head_dim, self.page_size = len(self._pl), Hq, Hkv, head_dim, page_size
@@ -136,6 +138,8 @@ class AttnPlan:
                                         num_ctas, ctypes.byref(h)), "rs_attn_plan_create")
         self.handle = h
         self.ws_bytes = int(_lib.rs_attn_plan_workspace_bytes(h))
+        if early_prefix:
+            _check(_lib.rs_attn_plan_set_early_prefix(h, 1), "rs_attn_plan_set_early_prefix")
 
     def info(self):
         a, b, c = _i32(), _i32(), _i32()
@@ -637,6 +641,7 @@ class TwoStageMigration:
                                       _ptr(self.staging), self.staging.numel() * self.staging.element_size(),
                                       _ptr(self.scratch), _stream(self.stream)), "rs_migrate_stage1")
         self.capacity = np.ascontiguousarray(rsv.copy())
+        self._keep_bt1 = self._hold(src_block_table)
         self.done.record(self.stream)
 
     def stage2(self, new_lens, src_block_table):
@@ -649,7 +654,15 @@ class TwoStageMigration:
                                       self.staging.numel() * self.staging.element_size(), _ptr(self.scratch),
                                       ctypes.c_void_p(self.ssm_ready.cuda_event) if self.comm.rank == self.dst else None,
                                       _stream(self.stream)), "rs_migrate_stage2")
+        self._keep_bt2 = self._hold(src_block_table)
         self.done.record(self.stream)
+
+    def _hold(self, t):
+        """Keep a caller's device tensor alive (and out of the caching allocator's reuse on other
+        streams) until this migration's stream has passed the kernels that read it."""
+        if isinstance(t, torch.Tensor) and t.is_cuda and self.stream is not None:
+            t.record_stream(self.stream)
+        return t
 
     def dst_rows(self):
         return self.rows[:self.n] if self.comm.rank == self.dst else None

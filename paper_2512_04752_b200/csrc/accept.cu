@@ -46,6 +46,13 @@ constexpr int kP2Unroll = RS_ACC_P2_UNROLL;   // vectors in flight per thread in
 #define RS_ACC_INFLIGHT 8
 #endif
 constexpr int kGreedyInflight = RS_ACC_INFLIGHT;   // 16-byte loads in flight per thread (greedy, bf16)
+// measurement switches: compile-time only (tools/build_variant.sh), no runtime getenv
+#ifndef RS_ACC_CS
+#define RS_ACC_CS 0         // force the cluster size (1/2/4/8); 0: by V and B
+#endif
+#ifndef RS_ACC_PF
+#define RS_ACC_PF 0         // greedy: L2 prefetch of the children's rows
+#endif
 
 struct RowView {
     const void* base;
@@ -362,13 +369,15 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype_rt, c
     int32_t* pth = path_out + (int64_t)b * RS_MAX_TREE;
     int phase = 0;
     if (leader && tid < RS_MAX_TREE) pth[tid] = -1;
-    // tree check in parallel: node i needs parent[i] in [0, i) (root: -1)
+    // tree check in parallel: node i needs parent[i] in [0, i) (root: -1) and, for a draft
+    // node (i >= 1), a vocabulary token 0 <= token[i] < V (sampling modes index rows by it)
     bool bad_node = !(T >= 1 && T <= RS_MAX_TREE);
     if (!bad_node && tid < T) {
         const int pp = parent[off + tid];
+        const int tk = token[off + tid];
         sm.parent[tid] = pp;
-        sm.token[tid] = token[off + tid];
-        bad_node = tid == 0 ? pp != -1 : !(pp >= 0 && pp < tid);
+        sm.token[tid] = tk;
+        bad_node = tid == 0 ? pp != -1 : !(pp >= 0 && pp < tid && tk >= 0 && tk < V);
     }
     if (__syncthreads_or(bad_node)) {
         if (leader && tid == 0) { acc_out[b] = 0; bonus_out[b] = -1; flags_out[b] = RS_FLAG_MALFORMED; }
@@ -773,17 +782,16 @@ extern "C" rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t lo
     const int nvec = (V + 7) / 8;
     int cs = 1;
     while (cs < kMaxCluster && nvec / (cs * 2) >= kThreads * 2 && (int64_t)B * cs * 2 <= 148 * 4) cs *= 2;
-    static const int cs_env = getenv("RS_ACC_CS") ? atoi(getenv("RS_ACC_CS")) : 0;   // measurements only
-    if (cs_env == 1 || cs_env == 2 || cs_env == 4 || cs_env == 8) cs = cs_env;
+    if (RS_ACC_CS == 1 || RS_ACC_CS == 2 || RS_ACC_CS == 4 || RS_ACC_CS == 8) cs = RS_ACC_CS;   // variant builds
     const int per = (nvec + cs - 1) / cs;
     RS_REQUIRE((per + kTileVecs - 1) / kTileVecs <= kMaxTiles, RS_ERR_UNSUPPORTED, "rs_tree_accept: V=%d too large", V);
     const float inv_tau = (mode == RS_ACCEPT_GREEDY) ? 1.0f : 1.0f / temperature;
     const int esz = logits_dtype == RS_DTYPE_BF16 ? 2 : 4;
     const bool lvec = ((reinterpret_cast<uintptr_t>(logits) & 15) == 0) && ((int64_t)V * esz % 16 == 0);
     const bool dvec = draft_probs && ((reinterpret_cast<uintptr_t>(draft_probs) & 15) == 0) && (V % 4 == 0);
-    // RS_ACC_PF=1: speculative L2 prefetch of the children rows (greedy). Measured on config 2:
+    // -DRS_ACC_PF=1: speculative L2 prefetch of the children rows (greedy). Measured on config 2:
     // 34.7 -> 38.1 us (2.2x the DRAM bytes; the walk is bound by the cluster barriers), so off.
-    static const int pf = getenv("RS_ACC_PF") ? atoi(getenv("RS_ACC_PF")) : 0;
+    constexpr int pf = RS_ACC_PF;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(B * cs));
     cfg.blockDim = dim3(kThreads);

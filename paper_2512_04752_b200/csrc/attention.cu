@@ -32,6 +32,26 @@ using namespace attn;
 static unsigned long long* g_trace_buf = nullptr;
 static size_t g_trace_bytes = 0;
 static constexpr int kOvhBlocksDefault = 2;   // per-item fixed cost in block units (planning)
+// Ablation / tuning switches are compile-time only (tools/build_variant.sh -D...): the product
+// library has no runtime switch that changes its schedule or results.
+#ifndef RS_ATTN_OVH
+#define RS_ATTN_OVH -1      // per-item overhead in key blocks; -1: by kernel mode
+#endif
+#ifndef RS_ATTN_DUAL
+#define RS_ATTN_DUAL 1      // dual items (RM = 4) when every unit allows them
+#endif
+#ifndef RS_ATTN_DYN
+#define RS_ATTN_DYN 0       // dynamic item queue for RM = 1 plans (measured slower)
+#endif
+#ifndef RS_ATTN_L2PROMO
+#define RS_ATTN_L2PROMO 3   // CUtensorMapL2promotion of the K/V page loads
+#endif
+#ifndef RS_ATTN_DBG
+#define RS_ATTN_DBG 0       // profiling ablations (results wrong if != 0)
+#endif
+#ifndef RS_ATTN_PDL
+#define RS_ATTN_PDL 1       // programmatic dependent launch between consecutive launches
+#endif
 static constexpr int kMinPart = 4;      // smallest split-KV part, in blocks
 
 namespace {
@@ -66,6 +86,7 @@ struct rs_attn_plan {
     int n_parts;
     size_t off_cta, off_items, off_units, off_counter, off_qorder, off_qctr, off_part_o, off_part_lse, ws_bytes;
     int dyn;                    // dynamic item queue (RM = 1 plans)
+    int early_prefix = 0;       // rs_attn_plan_set_early_prefix
     std::vector<int32_t> qorder;
     std::vector<uint8_t> blob;  // [0, off_part_o): header tables, uploaded verbatim
 };
@@ -85,9 +106,9 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
     RS_REQUIRE(page_size == kBlockN, RS_ERR_UNSUPPORTED, "rs_attn_plan_create: page_size %d != 64",
                page_size);
     const int g = Hq / Hkv;
-    // per-item overhead (epilogue, Q load) in KV-block units; RS_ATTN_OVH overrides (tuning only)
-    const bool ovh_env = getenv("RS_ATTN_OVH") != nullptr;
-    int kOvhBlocks = ovh_env ? std::max(0, atoi(getenv("RS_ATTN_OVH"))) : kOvhBlocksDefault;
+    // per-item overhead (epilogue, Q load) in KV-block units; RS_ATTN_OVH >= 0 overrides (tuning builds)
+    const bool ovh_env = RS_ATTN_OVH >= 0;
+    int kOvhBlocks = ovh_env ? RS_ATTN_OVH : kOvhBlocksDefault;
     RS_REQUIRE(g <= 16 && (16 % g) == 0, RS_ERR_UNSUPPORTED, "rs_attn_plan_create: group size %d (need g | 16)", g);
     if (num_ctas <= 0) {
         int dev = 0, sms = 148;
@@ -122,8 +143,8 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
     // Dual items (kernel RM = 4): when every unit group has R = 32 and an even number of query
     // tiles, an item covers tiles (2s, 2s + 1) and each softmax warpgroup owns one, so each K/V
     // tile in shared memory feeds twice the MMA work (config 5: L2 -> SM traffic halved). The
-    // gang machinery below then runs on "super tiles" (M / 2 per group). RS_ATTN_DUAL=0: off.
-    bool dual = pl->rmodes == 2 && !(getenv("RS_ATTN_DUAL") && getenv("RS_ATTN_DUAL")[0] == '0');
+    // gang machinery below then runs on "super tiles" (M / 2 per group). -DRS_ATTN_DUAL=0: off.
+    bool dual = pl->rmodes == 2 && RS_ATTN_DUAL != 0;
     for (const GU& u : gus) dual = dual && (u.M % 2 == 0);
     if (dual) {
         for (GU& u : gus) u.M /= 2;
@@ -284,9 +305,8 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
     // lists position by position (first items of all CTAs, then the second items, ...).
     {
         // measured slower than the balanced static lists at the configs' item sizes (a 17-block
-        // item is ~15 us, too coarse for the tail): off unless RS_ATTN_DYN=1
-        const char* e = getenv("RS_ATTN_DYN");
-        pl->dyn = (pl->rmodes == 1 && e && e[0] == '1') ? 1 : 0;
+        // item is ~15 us, too coarse for the tail): off unless built with -DRS_ATTN_DYN=1
+        pl->dyn = (pl->rmodes == 1 && RS_ATTN_DYN == 1) ? 1 : 0;
         pl->qorder.clear();
         size_t maxlen = 0;
         for (int c = 0; c < n_ctas; ++c) maxlen = std::max(maxlen, per_cta[c].size());
@@ -353,6 +373,12 @@ extern "C" rs_status rs_attn_plan_items(const rs_attn_plan* plan, int32_t* cta_o
 
 extern "C" void rs_attn_plan_destroy(rs_attn_plan* plan) { delete plan; }
 
+extern "C" rs_status rs_attn_plan_set_early_prefix(rs_attn_plan* plan, int32_t enable) {
+    RS_REQUIRE(plan, RS_ERR_INVALID_ARG, "rs_attn_plan_set_early_prefix: null plan");
+    plan->early_prefix = enable ? 1 : 0;
+    return RS_OK;
+}
+
 extern "C" rs_status rs_attn_set_trace(void* buf, size_t bytes) {
     g_trace_buf = static_cast<unsigned long long*>(buf);
     g_trace_bytes = buf ? bytes : 0;
@@ -381,9 +407,8 @@ static rs_status launch_attn(const rs_attn_plan* pl, const void* q, const void* 
                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         RS_REQUIRE(r == CUDA_SUCCESS, RS_ERR_CUDA, "tensor map Q/O failed (%d)", (int)r);
     }
-    // L2 sector promotion of the K/V page loads (RS_ATTN_L2PROMO = 0..3 for measurements)
-    static const int promo_env = getenv("RS_ATTN_L2PROMO") ? atoi(getenv("RS_ATTN_L2PROMO")) : 3;
-    const CUtensorMapL2promotion kv_promo = (CUtensorMapL2promotion)(promo_env & 3);
+    // L2 sector promotion of the K/V page loads (-DRS_ATTN_L2PROMO = 0..3 for measurements)
+    const CUtensorMapL2promotion kv_promo = (CUtensorMapL2promotion)(RS_ATTN_L2PROMO & 3);
     const void* kv[2] = {k_pages, v_pages};
     CUtensorMap* tm[2] = {&tmK, &tmV};
     for (int i = 0; i < 2; ++i) {
@@ -419,8 +444,8 @@ static rs_status launch_attn(const rs_attn_plan* pl, const void* q, const void* 
     prm.scale_log2 = sm_scale * 1.4426950408889634f;
     prm.out = static_cast<__nv_bfloat16*>(out);
     prm.lse = lse;
-    static const int dbg = getenv("RS_ATTN_DBG") ? atoi(getenv("RS_ATTN_DBG")) : 0;   // profiling ablations only
-    prm.dbg = dbg;
+    prm.dbg = RS_ATTN_DBG;   // profiling ablations only (variant builds)
+    prm.early_prefix = pl->early_prefix;
     prm.trace = (g_trace_bytes >= (size_t)pl->n_ctas * kTraceJ * 16 * sizeof(unsigned long long)) ? g_trace_buf
                                                                                                : nullptr;
     // row mode: kernels specialised for plans whose tiles all use R = 16 (half-split rows) or all
@@ -441,7 +466,7 @@ static rs_status launch_attn(const rs_attn_plan* pl, const void* q, const void* 
     lc.dynamicSmemBytes = (size_t)smem_bytes;
     lc.stream = st;
     cudaLaunchAttribute la[1];
-    static const bool pdl = !(getenv("RS_ATTN_PDL") && getenv("RS_ATTN_PDL")[0] == '0');
+    constexpr bool pdl = RS_ATTN_PDL != 0;
     la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     la[0].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = la;

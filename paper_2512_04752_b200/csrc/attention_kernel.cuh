@@ -160,6 +160,7 @@ struct Params {
     int* qctr;                   // dynamic scheduling: [0] next item, [1] CTAs done (zero between launches)
     int n_items;
     int dyn;                     // 1: CTAs take items from the global queue (atomicAdd), 0: static lists
+    int early_prefix;            // 1: prefix K/V pages + block table may be read before griddepcontrol.wait
     int dbg;                     // ablation switches for profiling only (RS_ATTN_DBG; results wrong if != 0):
                                  // 1 skip epilogue O reads/stores, 2 skip softmax math, 4 skip PV MMA
 };
@@ -324,12 +325,16 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     tc_fence_after();
     const uint32_t tmem = bars->tmem_base;
     // Programmatic dependent launch: the next layer's grid may be scheduled now (its CTAs start
-    // as this grid's CTAs exit). Only reads of K/V pages, item tables and block tables (inputs no
-    // earlier grid writes) may precede griddep_wait(): the producer warps stream the first key
-    // blocks while the previous grid drains; Q, the tree masks, outputs and the shared split-KV
-    // workspace are touched only after it.
+    // as this grid's CTAs exit). Before griddep_wait() returns, the preceding grid's writes are
+    // not guaranteed visible. Only the item tables (uploaded by a copy, not a kernel) are read
+    // before it unconditionally. With plan.early_prefix set (rs_attn_plan_set_early_prefix: the
+    // caller guarantees no kernel that may still be running writes the prefix K/V or the block
+    // table), the K and V producers also stream the PREFIX blocks (every slot < P_b) while the
+    // previous grid drains; a block holding any tree slot (written upstream, e.g. by the QKV
+    // projection right before this launch) is loaded only after the producer's own wait. Q, the
+    // tree masks, outputs and the shared split-KV workspace are touched only after it.
     griddep_launch_dependents();
-    if (warp >= 4) griddep_wait();
+    if (warp >= 4 || ((warp == 0 || warp == 3) && !p.early_prefix)) griddep_wait();
     if (warp == 0 || warp == 3) {
         // ============================ TMA producers ============================
         // warp 0: Q tiles + K pages; warp 3: V pages (whole warp runs the loop; one elected lane
@@ -342,6 +347,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         const int kSlots = isK ? C::KS : C::VS;
         const int pf = ((p.dbg >> 8) & 63) ? ((p.dbg >> 8) & 63) : kPF;
         const bool do_pf = pf > 0;
+        bool waited = !p.early_prefix;   // this warp has executed griddep_wait()
         uint32_t J = 0;
         auto issue_q = [&](const WorkItem& x, int slot_it) {
             if constexpr (RM == 4) {
@@ -422,9 +428,11 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                     for (int k = 0; k < cnt; ++k, ++J) {
                         const int j = base + k;
                         if (isK && it == 0 && j == q0_at) {
-                            griddep_wait();
+                            if (!waited) { griddep_wait(); waited = true; }
                             issue_q(wi, 0);
                         }
+                        // a block with a tree slot (slot >= P_b) only after the wait
+                        if (!waited && (wi.blk_begin + j + 1) * kBlockN > wi.P) { griddep_wait(); waited = true; }
                         if (RM != 4 && isK && has_next && j == q_next_at) issue_q(wn, it + 1);
                         if (RM == 4 && isK && it > 0 && j == 0) issue_q(wi, it);
                         // L2 prefetch of block j + pf (this item or the next one)

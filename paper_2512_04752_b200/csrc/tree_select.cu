@@ -67,6 +67,12 @@ tree_select_kernel(const int32_t* __restrict__ cand_parent, const double* __rest
     __shared__ double kx[kMaxKnots], ky[kMaxKnots];
     if (threadIdx.x < nk) { kx[threadIdx.x] = knots_x[threadIdx.x]; ky[threadIdx.x] = knots_y[threadIdx.x]; }
     __syncthreads();
+    // F must be a monotone piecewise-linear fit: knots_x strictly increasing, knots_y
+    // non-decreasing, all finite. Then w = F(dl) is non-increasing along every path (o <= 1), so
+    // S(n) is closed under parents. Invalid knots flag every sample MALFORMED.
+    bool knots_ok = true;
+    for (int j = 0; j < nk; ++j) knots_ok = knots_ok && isfinite(kx[j]) && isfinite(ky[j]);
+    for (int j = 0; j + 1 < nk; ++j) knots_ok = knots_ok && kx[j] < kx[j + 1] && ky[j] <= ky[j + 1];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int b = blockIdx.x * kWarps + wid;
     if (b >= B) return;
@@ -76,16 +82,17 @@ tree_select_kernel(const int32_t* __restrict__ cand_parent, const double* __rest
     const int T = n + 1;
     const int64_t ob = (int64_t)b * T;
     int flags = 0;
-    bool ok = N >= 1 && N <= kMaxCand;
-    // stage the candidates; check the tree (parent[i] in [-1, i))
+    bool ok = knots_ok && N >= 1 && N <= kMaxCand;
+    // stage the candidates; check the tree (parent[i] in [-1, i)) and o(u) in [0, 1]
     bool bad = false;
     if (ok) {
         for (int i = lane; i < N; i += 32) {
             const int p = cand_parent[off + i];
+            const double o = cand_o[off + i];
             sm.par[i] = p;
-            sm.dl[i] = cand_o[off + i];
+            sm.dl[i] = o;
             sm.pos[i] = 0;
-            bad |= !(p >= -1 && p < i);
+            bad |= !(p >= -1 && p < i) || !(o >= 0.0 && o <= 1.0);
         }
     }
     ok = ok && !__any_sync(0xffffffffu, bad);
@@ -153,16 +160,20 @@ tree_select_kernel(const int32_t* __restrict__ cand_parent, const double* __rest
             base += __popc(bal);
         }
         __syncwarp();
+        bool orphan = false;   // a selected node whose parent was not selected (S(n) not closed)
         for (int i = lane; i < N; i += 32) {
             const int p = sm.pos[i];
             if (p) {
                 const int cp = sm.par[i];
+                const bool lost = cp >= 0 && sm.pos[cp] == 0;
+                orphan |= lost;
                 sm.vpar[p] = cp < 0 ? 0 : sm.pos[cp];
                 parent_out[ob + p] = sm.vpar[p];
-                token_out[ob + p] = cand_token[off + i];
+                token_out[ob + p] = lost ? -1 : cand_token[off + i];   // -1: rs_tree_accept flags it
                 depth_out[ob + p] = sm.dep[i] + 1;
             }
         }
+        if (__any_sync(0xffffffffu, orphan)) flags |= RS_FLAG_MALFORMED;
     } else {
         flags |= RS_FLAG_MALFORMED;
     }

@@ -309,7 +309,8 @@ class GenerationInstance:
                         pg = by_gid[g].pages
                         rows[i, :len(pg)] = pg
                         rows[i, len(pg):] = pg[-1]
-                    src_bt = torch.from_numpy(rows).to(self.dev)
+                    with torch.cuda.stream(self.stream):   # allocated + copied on the stream that reads it
+                        src_bt = torch.from_numpy(rows).to(self.dev)
                 rows = core.migrate_samples(comm, tr.src, tr.dst, (self.k_llm, self.v_llm), (self.k_ssm, self.v_ssm),
                                             PAGE, self.pool if comm.rank == tr.dst else None, gids, lens, src_bt,
                                             self.max_pages, staging, scratch, self.stream)
@@ -350,13 +351,17 @@ class GenerationInstance:
         ev = lambda: torch.cuda.Event(enable_timing=True)
 
         def src_rows(gids):
+            # Allocated and copied ON the side stream that the pack kernels read it from: the copy
+            # is ordered before them, and the caching allocator only reuses the block for later
+            # side-stream work (core.TwoStageMigration also keeps it referenced until `done`).
             by_gid = {x.gid: x for x in self.samples}
             rows = np.zeros((len(gids), self.max_pages), np.int32)
             for i, g in enumerate(gids):
                 pg = by_gid[g].pages
                 rows[i, :len(pg)] = pg
                 rows[i, len(pg):] = pg[-1]
-            return torch.from_numpy(rows).to(self.dev)
+            with torch.cuda.stream(side):
+                return torch.from_numpy(rows).to(self.dev)
 
         jobs = []
         for tr in transfers:

@@ -82,7 +82,12 @@ class Rebalancer:
                 gid = np.array([s.gid for s in local_samples], np.int64)
                 sl = np.array([s.seq_len for s in local_samples], np.int32)
                 aa = np.array([s.avg_accepted for s in local_samples], np.float64)
-                chosen = set(core.choose_samples(gid, sl, aa, tr.count))
+                # never more than the source has eligible (the caller may filter its samples,
+                # e.g. two-stage migration keeps only those that outlive the overlap): a short
+                # or empty payload is broadcast instead of failing here while the other ranks
+                # wait in the collective below; the destination takes what it receives
+                k = min(int(tr.count), len(local_samples))
+                chosen = set(core.choose_samples(gid, sl, aa, k)) if k > 0 else set()
                 payload = [[s for s in local_samples if s.gid in chosen]]
                 payload[0].sort(key=lambda s: (s.seq_len, s.avg_accepted, s.gid))
             src_global = dist.get_global_rank(self.pg, tr.src) if self.pg is not None else tr.src

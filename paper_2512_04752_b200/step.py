@@ -47,9 +47,12 @@ class VerifyStep:
         self.mask = torch.empty(NT, dtype=torch.int64, device=dev)
         self.depth = torch.empty(NT, dtype=torch.int32, device=dev)
         self.tflags = torch.empty(self.B, dtype=torch.int32, device=dev)
-        # host-side plan from this step's lengths (shared by all layers)
+        # host-side plan from this step's lengths (shared by all layers). early_prefix: the prefix
+        # K/V (written by the previous step's compaction) may stream before the preceding grid
+        # completes, because the mask kernel (a plain launch) always sits between the compaction
+        # and the first attention layer, and attention layers write no K/V (header: PDL)
         self.plan = core.AttnPlan(b["prefix_len"], b["tree_off"], self.Hq, self.Hkv, self.d, self.ps,
-                                  num_ctas=num_ctas)
+                                  num_ctas=num_ctas, early_prefix=True)
         self.ws = core.alloc_workspace(self.plan.ws_bytes, dev)
         self.plan.upload(self.ws)
         self.attn_out = torch.empty((self.L, NT, self.Hq, self.d), dtype=torch.bfloat16, device=dev)

@@ -58,18 +58,41 @@ def test_philox_device_bit_exact(cuda_lib):
         assert list(out[i]) == list(OAcc.philox4x32_10(ctr[i], key))
 
 
-def test_exp_spec_device_bit_exact(cuda_lib):
+def test_exp_spec_device_bit_exact_exhaustive(cuda_lib):
+    """SURVEY 8(c) pin: EVERY fp32 value in [-32, 0] (bit patterns 0x80000000 .. 0xC2000000,
+    1.107e9 values, -0 included) gives the same bits on the GPU as in the C oracle; plus the
+    values just below -32 (both return 0), +0 and NaN. The oracle runs in threads over slices
+    (ctypes releases the GIL); the comparison is on the device."""
+    import concurrent.futures as cf
+    import os
     core = cuda_lib
-    # every 7th fp32 bit pattern in [-32, 0] (~1.6e8 values) plus all of [-2^-10, 0]
-    hi = np.float32(-32.0).view(np.uint32)
-    for start in range(0x80000000, int(hi) + 1, 1 << 26):
-        bits = np.arange(start, min(start + (1 << 26), int(hi) + 1), 7, dtype=np.uint64).astype(np.uint32)
+    lo, hi = 0x80000000, int(np.float32(-32.0).view(np.uint32))
+    chunk = 1 << 26
+    nthr = max(1, min(32, os.cpu_count() or 1))
+    ex = cf.ThreadPoolExecutor(nthr)
+
+    def oracle(bits):
         x = bits.view(np.float32)
-        y = core.exp_spec(_dev(x)).cpu().numpy()
-        np.testing.assert_array_equal(y.view(np.uint32), OAcc.exp_spec_array(x).view(np.uint32))
-    x = -np.random.default_rng(2).random(1 << 20).astype(np.float32) * np.float32(2**-10)
-    y = core.exp_spec(_dev(x)).cpu().numpy()
-    np.testing.assert_array_equal(y.view(np.uint32), OAcc.exp_spec_array(x).view(np.uint32))
+        y = np.empty_like(x)
+        parts = np.array_split(np.arange(x.size), nthr)
+        def run(ix):
+            if ix.size:
+                y[ix[0]:ix[-1] + 1] = OAcc.exp_spec_array(x[ix[0]:ix[-1] + 1])
+        list(ex.map(run, parts))
+        return y
+    checked = 0
+    for start in range(lo, hi + 1, chunk):
+        end = min(start + chunk, hi + 1)
+        bits = np.arange(start, end, dtype=np.uint64).astype(np.uint32)
+        y_ref = torch.from_numpy(oracle(bits).view(np.int32)).cuda()
+        y = core.exp_spec(torch.from_numpy(bits.view(np.float32)).cuda())
+        neq = int((y.view(torch.int32) != y_ref).sum().item())
+        assert neq == 0, (hex(start), neq)
+        checked += end - start
+    assert checked == hi - lo + 1 == 1107296257
+    edge = np.array([-32.000004, -33.0, -88.0, -1e30, 0.0, np.nan], np.float32)
+    y = core.exp_spec(_dev(edge)).cpu().numpy()
+    np.testing.assert_array_equal(y.view(np.uint32), OAcc.exp_spec_array(edge).view(np.uint32))
 
 
 # ------------------------------------------------------------------ a3 accept
@@ -133,6 +156,73 @@ def test_accept_sampling_bit_exact(cuda_lib, mode, V, temp):
         g, o = _run_accept_both(core, b, logits, m, temperature=temp, seed=1234 + step, step=step)
         for x, y in zip(g, o):
             np.testing.assert_array_equal(x, y)
+
+
+def _accept_np_both(core, mode, logits_f32, parent, token, tree_off, gid, V, draft=None, seed=0, step=0):
+    """One call on each side with plain numpy inputs (bf16 logits)."""
+    lg = torch.as_tensor(np.asarray(logits_f32, np.float32)).to(torch.bfloat16)
+    g = core.tree_accept(mode, lg.cuda(), _dev(np.asarray(parent, np.int32)), _dev(np.asarray(token, np.int32)),
+                         _dev(np.asarray(tree_off, np.int32)), _dev(np.asarray(gid, np.int64)),
+                         draft_probs=None if draft is None else _dev(np.asarray(draft, np.float32)),
+                         seed=seed, step=step)
+    g = [x.cpu().numpy() for x in g]
+    o = OAcc.tree_accept(mode, tensor_bf16_bits(lg), parent, token, tree_off, gid, V,
+                         draft_probs=draft, seed=seed, step=step)
+    return g, o
+
+
+def test_accept_degenerate_residual_gpu(cuda_lib):
+    """The MSS all-zero-residual fallback (pre-rejection weights kept) on the GPU, bit-exact vs
+    the oracle, on the two pinned constructions of tests/test_oracle_accept.py (draft mass 0;
+    q exactly proportional to p), batched over gids, at a small and the full vocabulary."""
+    core = cuda_lib
+    for V in (16, 128256):
+        support = [1, 3, 4, 6]
+        n = 24
+        l = np.full((4, V), -100.0, np.float32)
+        l[:, support] = 0.0
+        l[3] = -100.0
+        l[3, 5] = 0.0
+        q0 = np.zeros((4, V), np.float32)
+        qp = np.zeros((4, V), np.float32)
+        qp[:, support] = 0.25
+        par1 = np.tile(np.array([-1, 0, 0, 0], np.int32), n)
+        tok1 = np.tile(np.array([0, 9, 11, 3], np.int32), n)
+        off = (np.arange(n + 1) * 4).astype(np.int32)
+        for q, expect_acc in ((q0, 0), (qp, 1)):
+            g, o = _accept_np_both(core, core.SAMPLE_MSS, np.tile(l, (n, 1)), par1, tok1, off, np.arange(n), V,
+                                   draft=np.tile(q, (n, 1)), seed=77, step=5)
+            for x, y in zip(g, o):
+                np.testing.assert_array_equal(x, y)
+            assert np.all(g[0] == expect_acc) and np.all(g[3] == 0)
+        # q0 with the in-support child present too: kept weights -> qw_x = 0, w_x > 0 -> accepted
+        g, o = _accept_np_both(core, core.SAMPLE_MSS, np.tile(l, (n, 1)), par1, tok1, off, np.arange(n), V,
+                               draft=np.tile(q0, (n, 1)), seed=1, step=2)
+        for x, y in zip(g, o):
+            np.testing.assert_array_equal(x, y)
+
+
+def test_accept_out_of_vocabulary_token_gpu(cuda_lib):
+    """A draft token outside [0, V) flags the sample MALFORMED in every mode (no row is indexed
+    by it); other samples of the batch are unaffected."""
+    core = cuda_lib
+    V = 1000
+    rng = np.random.default_rng(5)
+    n = 6
+    par = np.tile(np.array([-1, 0, 0, 1], np.int32), n)
+    tok = rng.integers(0, V, size=4 * n).astype(np.int32)
+    tok[4 * 1 + 2] = -1
+    tok[4 * 3 + 3] = V
+    tok[4 * 4 + 0] = -1                      # the root's token is never tested
+    off = (np.arange(n + 1) * 4).astype(np.int32)
+    l = rng.standard_normal((4 * n, V)).astype(np.float32)
+    q = np.asarray(torch.softmax(torch.randn(4 * n, V), -1).numpy(), np.float32)
+    for mode in (core.GREEDY, core.SAMPLE_DELTA, core.SAMPLE_MSS):
+        g, o = _accept_np_both(core, mode, l, par, tok, off, np.arange(n), V,
+                               draft=q if mode == core.SAMPLE_MSS else None, seed=9, step=1)
+        for x, y in zip(g, o):
+            np.testing.assert_array_equal(x, y)
+        assert list(g[3]) == [0, 1, 0, 1, 0, 0]
 
 
 def test_accept_sampling_distribution_gpu(cuda_lib):

@@ -74,3 +74,31 @@ def test_tree_select_ragged_and_flags(cuda_lib):
         assert flags[b] == 0
         np.testing.assert_array_equal(par[sl], pv)
         np.testing.assert_array_equal(tok[sl], tv)
+
+
+def test_tree_select_invalid_knots_and_probabilities(cuda_lib):
+    """Knots that do not make F monotone flag every sample MALFORMED (device check); an o(u)
+    outside [0, 1] or NaN flags its own sample only. The oracle raises MalformedTree for both."""
+    core = cuda_lib
+    n = 8
+    trees, toks, off, root = _cands(8, 40, seed=9)
+    bad_o = trees[2][1].copy()
+    bad_o[5] = 1.25
+    trees[2] = (trees[2][0], bad_o)
+    nan_o = trees[6][1].copy()
+    nan_o[0] = np.nan
+    trees[6] = (trees[6][0], nan_o)
+    _, _, _, _, flags = _run(core, trees, toks, off, root, n)
+    assert list(np.nonzero(flags)[0]) == [2, 6] and flags[2] == core.FLAG_MALFORMED
+    for b in (2, 6):
+        with pytest.raises(ValueError, match="MalformedTree"):
+            OS.verification_tree(trees[b][0], trees[b][1], toks[b], root[b], n, KX, KY)
+    d = lambda x, dt: torch.as_tensor(np.ascontiguousarray(x)).to(dt).cuda()
+    trees, toks, off, root = _cands(8, 40, seed=10)
+    par = d(np.concatenate([p for p, _ in trees]), torch.int32)
+    o = d(np.concatenate([q for _, q in trees]), torch.float64)
+    tok = d(np.concatenate(toks), torch.int32)
+    for kx, ky in (([0.0, 0.5, 0.5, 1.0], [0.0, 0.2, 0.4, 0.9]), ([0.0, 0.5, 1.0], [0.0, 0.6, 0.4])):
+        out = core.tree_select(par, o, tok, d(off, torch.int32), d(root, torch.int32), n, d(kx, torch.float64),
+                               d(ky, torch.float64))
+        assert (out[4].cpu().numpy() == core.FLAG_MALFORMED).all()

@@ -295,3 +295,63 @@ def test_rng_keyed_by_gid_not_position():
         np.testing.assert_array_equal(a[perm], b)
     r3 = A.tree_accept(A.MSS, lg, par, tok, tree_off, gid, V_SMALL, draft_probs=dp, seed=3, step=10)
     assert not all(np.array_equal(a, b) for a, b in zip(r1, r3))
+
+
+# ---------------------------------------------------------------- malformed tokens, degenerate residual
+def test_out_of_vocabulary_token_is_malformed():
+    """A draft node whose token is outside [0, V) (rs_tree_select pads with -1) makes the tree
+    malformed in every mode (reading Z5: rows are indexed by the child's token); the root's
+    token is never tested, so -1 there is fine."""
+    V = 8
+    l = np.zeros((3, V), np.float32)
+    q = softmax64(np.zeros((3, V)))
+    for bad in (-1, V, V + 100):
+        for mode in (A.GREEDY, A.DELTA, A.MSS):
+            acc, path, bonus, flags = A.tree_accept(mode, bf16_bits(l), [-1, 0, 0], [0, 2, bad], [0, 3],
+                                                    [0], V, draft_probs=q if mode == A.MSS else None)
+            assert flags[0] == A.FLAG_MALFORMED and acc[0] == 0 and bonus[0] == -1, (bad, mode)
+    acc, _, bonus, flags = A.tree_accept(A.GREEDY, bf16_bits(l), [-1, 0], [-1, 3], [0, 2], [0], V)
+    assert flags[0] == 0 and bonus[0] == 0
+
+
+def _uniform_support_logits(V, support, rows):
+    l = np.full((rows, V), -100.0, np.float32)     # exp(-100) underflows exp_spec -> weight 0
+    l[:, support] = 0.0                              # weight exactly 2^32 each
+    return l
+
+
+def test_mss_degenerate_residual_zero_draft_mass():
+    """Degenerate residual (DESIGN "Bit-exact sampling": an all-zero residual keeps the
+    pre-rejection weights). A draft row whose mass quantises to 0 (Zq = 0) rejects every child
+    of zero target weight (qw_x = 0 -> accept iff w_x > 0) and leaves r = max(w*0 - 0*Z, 0) = 0.
+    The bonus is then drawn from the ORIGINAL target p: with p uniform on k = 4 tokens of
+    weight 2^32 each (Z = 4*2^32), t = U'*Z >> 32 = 4*U' and the bonus is support[4*U' >> 32]
+    (closed form; U' = Philox word 0 at counter (0xFFFFFFFF, 0, step, gid), key = seed, pinned
+    by the Random123 vectors)."""
+    V, support = 16, [1, 3, 4, 6]
+    l = bf16_bits(_uniform_support_logits(V, support, 3))
+    q = np.zeros((3, V), np.float32)                 # Zq = 0
+    for gid in range(40):
+        acc, path, bonus, flags = A.tree_accept(A.MSS, l, [-1, 0, 0], [0, 9, 11], [0, 3], [gid], V,
+                                                draft_probs=q, seed=77, step=5)
+        u2 = int(A.philox4x32_10([0xFFFFFFFF, 0, 5, gid], [77, 0])[0])
+        assert flags[0] == 0 and acc[0] == 0
+        assert bonus[0] == support[(4 * u2) >> 32], gid
+
+
+def test_mss_degenerate_residual_proportional_draft():
+    """q exactly proportional to p (p uniform on 4 tokens, q = 1/4 on them): rejecting a child
+    outside the support leaves r_v = w_v*Zq - qw_v*Z = 2^32*2^32 - 2^30*2^34 = 0 for every v, so
+    the pre-rejection weights are kept and the next child (in the support) is accepted with
+    certainty (U*(qw*Z) = U*2^64 < 2^32*(w*Zq) = 2^96). Had the residual been taken as the
+    all-zero vector, Z = 0 and that child would be rejected."""
+    V, support = 16, [1, 3, 4, 6]
+    l = _uniform_support_logits(V, support, 4)
+    l[3] = -100.0
+    l[3, 5] = 0.0                                    # leaf row: bonus deterministic (token 5)
+    q = np.zeros((4, V), np.float32)
+    q[:, support] = 0.25
+    for gid in range(20):
+        acc, path, bonus, flags = A.tree_accept(A.MSS, bf16_bits(l), [-1, 0, 0, 0], [0, 9, 11, 3], [0, 4],
+                                                [gid], V, draft_probs=q, seed=3, step=gid)
+        assert flags[0] == 0 and acc[0] == 1 and list(path[0, :2]) == [0, 3] and bonus[0] == 5

@@ -257,3 +257,64 @@ def test_verification_tree_paths_are_candidate_paths():
     with pytest.raises(ValueError):
         OS.verification_tree(np.array([-1, 0], np.int32), np.array([0.5, 0.5]), np.array([1, 2], np.int32), 0, 3,
                              kx, ky)
+
+
+# ----------------------------------------------------------------- F and t_sd, hand-evaluated
+# The acceptance fit F ("a piecewise linear function ... fitted from offline profiling
+# data") and the cost regression are pinned by values worked out by hand below,
+# independent of np.interp / the oracle's formula, so a planted mistake (extrapolation past the
+# last knot, a wrong segment, no clamp, a squared relu, a dropped term) fails one of them.
+KX = [0.0, 0.05, 0.2, 0.5, 1.0]
+KY = [0.0, 0.15, 0.45, 0.75, 0.95]
+
+
+@pytest.mark.parametrize("x,expect", [
+    (0.0, 0.0), (0.05, 0.15), (0.2, 0.45), (0.5, 0.75), (1.0, 0.95),   # at the knots
+    (0.025, 0.075),       # 0 + (0.025 - 0) / 0.05 * 0.15
+    (0.1, 0.25),          # 0.15 + (0.1 - 0.05) / 0.15 * 0.30
+    (0.35, 0.60),         # 0.45 + (0.35 - 0.2) / 0.3 * 0.30
+    (0.75, 0.85),         # 0.75 + (0.75 - 0.5) / 0.5 * 0.20
+    (0.9, 0.91),          # 0.75 + 0.4 / 0.5 * 0.20
+    (-0.3, 0.0),          # left of the first knot: constant F(x0) (no extrapolation)
+    (1.7, 0.95),          # right of the last knot: constant 0.95, not 0.95 + 0.7 * 0.4
+])
+def test_acceptance_fit_hand_values(x, expect):
+    assert OS.acceptance_fit(KX, KY, x) == pytest.approx(expect, abs=1e-12)
+
+
+def test_acceptance_fit_clamps_to_unit_interval():
+    # knots outside [0, 1]: F is a probability, so values clip to [0, 1]
+    kx, ky = [0.0, 1.0], [-0.5, 1.5]
+    assert OS.acceptance_fit(kx, ky, 0.1) == 0.0          # raw -0.3 -> 0
+    assert OS.acceptance_fit(kx, ky, 0.5) == pytest.approx(0.5)
+    assert OS.acceptance_fit(kx, ky, 0.9) == 1.0          # raw 1.3 -> 1
+
+
+def test_cost_regression_hand_values():
+    # t_sd = c_draft + b0 + b1 N_seq + b2 N_draft + b3 relu(N_draft - k_sat) N_draft
+    cm = OS.CostModel(c_draft=1.0, b0=2.0, b1=0.5, b2=0.25, b3=0.125, k_sat=10)
+    # relu inactive: 1 + 2 + 0.5*4 + 0.25*8 = 7
+    assert cm.regression(4, 8) == pytest.approx(7.0)
+    # relu active: 1 + 2 + 0.5*4 + 0.25*14 + 0.125*(14-10)*14 = 1 + 2 + 2 + 3.5 + 7 = 15.5
+    assert cm.regression(4, 14) == pytest.approx(15.5)
+    # at the saturation point the relu term is 0: 1 + 2 + 0 + 0.25*10 = 5.5
+    assert cm.regression(0, 10) == pytest.approx(5.5)
+    # bucket cache: (300, 15) evaluates at the bucket's lower corner (256, 12)   (Z12)
+    # 1 + 2 + 0.5*256 + 0.25*12 + 0.125*2*12 = 3 + 128 + 3 + 3 = 137
+    assert cm.t_sd(300, 15) == pytest.approx(137.0)
+
+
+def test_verification_tree_rejects_invalid_fit_and_probabilities():
+    rng = np.random.default_rng(3)
+    p, o = make_candidate_tree(rng, 30)
+    tok = np.arange(30, dtype=np.int32)
+    OS.verification_tree(p, o, tok, 7, 6, KX, KY)                         # valid
+    for kx, ky in (([0, 0.5, 0.5, 1], [0, .2, .4, .9]),                  # x not strictly increasing
+                   ([0, 0.5, 1], [0, .6, .4]),                           # y decreasing (F not monotone)
+                   ([0, 0.5, 1], [0, np.nan, .9])):
+        with pytest.raises(ValueError, match="MalformedTree"):
+            OS.verification_tree(p, o, tok, 7, 6, kx, ky)
+    bad = o.copy()
+    bad[4] = 1.5
+    with pytest.raises(ValueError, match="MalformedTree"):
+        OS.verification_tree(p, bad, tok, 7, 6, KX, KY)

@@ -80,3 +80,39 @@ def test_rebalancer_gloo(world, seed, thr):
     assert all_final == sorted(x.gid for s in samples for x in s)   # conservation, no duplicates
     for s, dd, _ in ref_plan:                                        # Eq. 6 constraints
         assert final_loads[s] >= thr and final_loads[dd] <= thr
+
+
+def _worker_filtered(rank, world, port, seed, thr, outdir):
+    """Sources offer only a filtered subset (as two-stage migration does: samples that outlive
+    the overlap), possibly fewer than the planned count: the choice is clamped and broadcast
+    (short or empty payload) instead of failing on the source while the others wait."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2512_04752_b200.realloc import Rebalancer
+        rb = Rebalancer(threshold=thr, cooldown=1)
+        mine = _samples_of(rank, seed)
+        trs = rb.choose(rb.plan(len(mine)), [s for s in mine if s.seq_len > 28])
+        res = dict(plan=[(t.src, t.dst, t.count) for t in trs], chosen={t.src: [s.gid for s in t.samples] for t in trs})
+        np.save(os.path.join(outdir, f"r{rank}.npy"), np.array([res], dtype=object), allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,seed,thr", [(2, 0, 25), (4, 1, 18)])
+def test_rebalancer_choose_clamps_to_eligible(world, seed, thr):
+    with tempfile.TemporaryDirectory() as d:
+        mp.start_processes(_worker_filtered, args=(world, _free_port(), seed, thr, d), nprocs=world, join=True,
+                           start_method="spawn")
+        res = [np.load(os.path.join(d, f"r{r}.npy"), allow_pickle=True)[0] for r in range(world)]
+    samples = [_samples_of(r, seed) for r in range(world)]
+    plan = OR.plan_reallocation([len(s) for s in samples], thr)
+    assert plan
+    short = 0
+    for s, dd, k in plan:
+        elig = [(x.gid, x.seq_len, x.avg_accepted) for x in samples[s] if x.seq_len > 28]
+        short += len(elig) < k                                 # the case the clamp exists for
+        ref = OR.choose_samples(elig, min(k, len(elig))) if elig else []
+        for r in range(world):
+            assert sorted(res[r]["chosen"][s]) == sorted(ref)
+    assert short > 0
