@@ -219,7 +219,8 @@ rs_status rs_tree_verify_attention_layers(
  *   status_flags device int32 [B]  out: RS_FLAG_* bits. RS_FLAG_MALFORMED (accepted_len 0,
  *               bonus -1): T_b outside [1, 64], parent[0] != -1, parent[i] outside [0, i), or a
  *               draft node (i >= 1) whose token is outside [0, V) (e.g. rs_tree_select's -1 pad).
- *               RS_FLAG_NONFINITE: a visited row holds NaN/Inf (walk stops there, bonus -1).
+ *               RS_FLAG_NONFINITE: a visited row holds NaN/Inf logits, or (MSS) its draft row
+ *               holds a value outside [0, 1] or NaN (walk stops there, bonus -1).
  *   ws, ws_bytes: device workspace >= rs_tree_accept_workspace_bytes(mode, B, V) bytes, 16-byte
  *               aligned (MSS keeps each sample's residual weights there; 0 bytes otherwise:
  *               NULL allowed); too small -> RS_ERR_WORKSPACE. */

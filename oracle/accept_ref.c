@@ -209,7 +209,17 @@ int oracle_tree_accept(int mode, const void* logits, int logits_is_bf16, const f
                     break;
                 }
                 uint64_t Zq = 0;
-                if (mode == MODE_MSS) Zq = draft_weights(draft_probs, row, V, qw);
+                if (mode == MODE_MSS) {
+                    /* the draft row must be a probability vector: every q_v in [0, 1] (reading
+                     * Z15 extended: otherwise the sample is flagged like a non-finite row) */
+                    int okq = 1;
+                    for (int v = 0; v < V && okq; ++v) {
+                        float qv = draft_probs[row * (int64_t)V + v];
+                        okq = (qv >= 0.0f && qv <= 1.0f);
+                    }
+                    if (!okq) { flags[b] |= FLAG_NONFINITE; break; }
+                    Zq = draft_weights(draft_probs, row, V, qw);
+                }
                 for (int k = 0; k < nch; ++k) {
                     int x = ch[k];
                     int tk = token[off + x];

@@ -737,6 +737,451 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype_rt, c
     if (cs > 1) cluster_sync_all();
 }
 
+// ============================================================================ MSS, row in smem
+// SAMPLE_MSS with the visited row kept ON CHIP. One cluster of CS CTAs (16 where the device
+// allows the non-portable size, else 8) per sample; CTA r owns the vocabulary slice
+// [r*per, (r+1)*per) (in 8-token vectors) and keeps per token two u32 words in shared memory:
+//   wsl: the target weight w_v (<= 2^32), stored as w_v, or 0xFFFFFFFF for w_v = 2^32 (only a
+//        row maximum has e = 1; every other w_v <= 2^32 - 2^8, so the code is unambiguous);
+//        after the node's first rejection the shifted residual (a plain u32, "resid" state);
+//   qsl: the draft weight qw_v = trunc(q_v * 2^32), encoded the same way (q_v in [0, 1]).
+// A visited node costs ONE pass over HBM (logits + q: the algorithmic bytes): pass L loads the
+// row (raw logits parked in wsl) with its max, a validity flag and Zq; pass E turns wsl into
+// weights with Z and the inverse-CDF tile sums. A rejection runs over shared memory only:
+// pass A computes every r_v = max(w_v Zq - qw_v Z, 0) once in 128 bits and stores it per
+// 8-token vector as r_v >> t (t = max(0, bitlen(vector max) - 32), a byte per vector; an
+// all-zero vector keeps its old words and is marked 0xFF); pass B applies the global shift
+// s = max(0, bitlen(max r) - 32) >= t as (r >> t) >> (s - t) = r >> s (exact), with the sums.
+// If every r_v is 0 (quantisation only) nothing was overwritten: the weights are kept.
+// Children's current (w, qw) are published by the owner CTA of their token into small arrays
+// before the cluster barrier that ends pass E / pass B; child tests read them through DSMEM, so
+// no barrier is needed between a node's tests and the next row's loads. The bonus is the
+// inverse CDF of the current weights (draw_bonus).
+constexpr int kMssThreads = kThreads;   // == kTileVecs: one vector per thread per tile row
+
+struct MssSmem {
+    unsigned long long childw[RS_MAX_TREE];   // current w of child x's token (owner CTA only)
+    unsigned long long childq[RS_MAX_TREE];   // qw of child x's token
+};
+
+// Block + cluster all-reduce of three u64 values (ops op[0..2]); same result in every thread.
+__device__ __forceinline__ void allreduce3(unsigned long long v[3], const int op[3], Smem& sm, int& phase) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o; o >>= 1)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) v[k] = op_apply(op[k], v[k], __shfl_xor_sync(0xffffffffu, v[k], o));
+    __syncthreads();
+    if (lane == 0) { sm.red[w][0] = v[0]; sm.red[w][1] = v[1]; sm.scan[w] = v[2]; }
+    __syncthreads();
+    unsigned long long a[3] = {sm.red[0][0], sm.red[0][1], sm.scan[0]};
+    for (int k = 1; k < kWarps; ++k) {
+        a[0] = op_apply(op[0], a[0], sm.red[k][0]);
+        a[1] = op_apply(op[1], a[1], sm.red[k][1]);
+        a[2] = op_apply(op[2], a[2], sm.scan[k]);
+    }
+    const uint32_t cs = cluster_size();
+    if (cs > 1) {
+        if (threadIdx.x == 0) { sm.xch[phase][0] = a[0]; sm.xch[phase][1] = a[1]; sm.xch[phase][2] = a[2]; }
+        cluster_sync_all();
+        if (w == 0) {
+            const uint32_t c = (uint32_t)lane;
+            unsigned long long r[3] = {0, 0, 0};
+            if (c < cs) {
+#pragma unroll
+                for (int k = 0; k < 3; ++k) r[k] = ld_dsmem_u64(&sm.xch[phase][k], c);
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1)
+#pragma unroll
+                for (int k = 0; k < 3; ++k) r[k] = op_apply(op[k], r[k], __shfl_xor_sync(0xffffffffu, r[k], o));
+            if (lane == 0) { sm.red[0][0] = r[0]; sm.red[0][1] = r[1]; sm.scan[0] = r[2]; }
+        }
+        __syncthreads();
+        a[0] = sm.red[0][0];
+        a[1] = sm.red[0][1];
+        a[2] = sm.scan[0];
+        phase ^= 1;
+    }
+    __syncthreads();   // sm.red / sm.scan are reused by the next reduction
+    v[0] = a[0];
+    v[1] = a[1];
+    v[2] = a[2];
+}
+
+__device__ __forceinline__ uint64_t wdec(uint32_t x) { return x == 0xFFFFFFFFu ? (1ull << 32) : (uint64_t)x; }
+
+// trunc(e * 2^32) for e in [0, 1], ENCODED as u32 (2^32 -> 0xFFFFFFFF): e * 2^32 is exact and
+// cvt.rzi.u32.f32 saturates, so e = 1 gives 0xFFFFFFFF and every e < 1 its exact truncation
+// (<= 2^32 - 2^8); 0, -0 and subnormals give 0 (= __float2ull_rz(e * 2^32) for all e in [0, 1]).
+__device__ __forceinline__ uint32_t f2w(float e) { return __float2uint_rz(__fmul_rn(e, 4294967296.0f)); }
+// sum of 8 encoded weights as the true 64-bit sum
+__device__ __forceinline__ unsigned long long wsum8(const uint32_t e[8]) {
+    unsigned long long s = 0;
+    uint32_t tops = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { s += e[j]; tops += e[j] == 0xFFFFFFFFu ? 1u : 0u; }
+    return s + tops;
+}
+
+// r = max(x*S - y*T, 0) for ENCODED 33-bit weights x, y (0xFFFFFFFF = 2^32) and S, T < 2^64 with
+// x*S, y*T < 2^95: three 32-bit limbs (r2:r1:r0) with carry chains (exact; DESIGN "Bit-exact
+// sampling": r_v = max(w_v Zq - qw_v Z, 0)).
+struct R96 {
+    uint32_t r0, r1, r2;
+};
+__device__ __forceinline__ R96 resid96(uint32_t x, bool xtop, uint64_t S, uint32_t y, bool ytop, uint64_t T) {
+    const uint32_t s0 = (uint32_t)S, s1 = (uint32_t)(S >> 32), t0 = (uint32_t)T, t1 = (uint32_t)(T >> 32);
+    // x = 2^32 is encoded 0xFFFFFFFF: x*S = enc*S + S (the +S is added at limb 0)
+    const uint32_t xs0 = xtop ? s0 : 0u, xs1 = xtop ? s1 : 0u;
+    const uint32_t yt0 = ytop ? t0 : 0u, yt1 = ytop ? t1 : 0u;
+    uint32_t a0, a1, a2, b0, b1, b2;
+    asm("{\n\t"
+        "mul.lo.u32 %0, %6, %7;\n\t"
+        "mul.hi.u32 %1, %6, %7;\n\t"
+        "mad.lo.cc.u32 %1, %6, %8, %1;\n\t"
+        "madc.hi.u32 %2, %6, %8, 0;\n\t"
+        "add.cc.u32 %0, %0, %9;\n\t"
+        "addc.cc.u32 %1, %1, %10;\n\t"
+        "addc.u32 %2, %2, 0;\n\t"
+        "mul.lo.u32 %3, %11, %12;\n\t"
+        "mul.hi.u32 %4, %11, %12;\n\t"
+        "mad.lo.cc.u32 %4, %11, %13, %4;\n\t"
+        "madc.hi.u32 %5, %11, %13, 0;\n\t"
+        "add.cc.u32 %3, %3, %14;\n\t"
+        "addc.cc.u32 %4, %4, %15;\n\t"
+        "addc.u32 %5, %5, 0;\n\t"
+        "}"
+        : "=&r"(a0), "=&r"(a1), "=&r"(a2), "=&r"(b0), "=&r"(b1), "=&r"(b2)
+        : "r"(x), "r"(s0), "r"(s1), "r"(xs0), "r"(xs1), "r"(y), "r"(t0), "r"(t1), "r"(yt0), "r"(yt1));
+    uint32_t d0, d1, d2;
+    asm("{\n\t"
+        "sub.cc.u32 %0, %3, %6;\n\t"
+        "subc.cc.u32 %1, %4, %7;\n\t"
+        "subc.u32 %2, %5, %8;\n\t"
+        "}"
+        : "=r"(d0), "=r"(d1), "=r"(d2)
+        : "r"(a0), "r"(a1), "r"(a2), "r"(b0), "r"(b1), "r"(b2));
+    const uint32_t keep = (uint32_t)((int32_t)d2 >> 31) ^ 0xFFFFFFFFu;   // 0 if A < B
+    return R96{d0 & keep, d1 & keep, d2 & keep};
+}
+__device__ __forceinline__ int r96_bitlen(const R96& r) {
+    return r.r2 ? 96 - __clz(r.r2) : (r.r1 ? 64 - __clz(r.r1) : 32 - __clz(r.r0));
+}
+// low 32 bits of r >> t, 0 <= t < 64
+__device__ __forceinline__ uint32_t r96_shr32(const R96& r, int t) {
+    return t < 32 ? __funnelshift_rc(r.r0, r.r1, t) : __funnelshift_rc(r.r1, r.r2, t - 32);
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kMssThreads, 3)
+mss_accept_kernel(const void* __restrict__ logits, const float* __restrict__ draft,
+                  const int32_t* __restrict__ parent, const int32_t* __restrict__ token,
+                  const int32_t* __restrict__ tree_off, const int64_t* __restrict__ gid, int V, float inv_tau,
+                  uint64_t seed, uint64_t step, int32_t* __restrict__ acc_out, int32_t* __restrict__ path_out,
+                  int32_t* __restrict__ bonus_out, int32_t* __restrict__ flags_out, bool logits_vec_ok,
+                  bool draft_vec_ok) {
+    __shared__ Smem sm;
+    __shared__ MssSmem ms;
+    extern __shared__ __align__(16) uint4 mss_dyn[];
+    const uint32_t cs = cluster_size();
+    const uint32_t crank = cluster_rank();
+    const int b = blockIdx.x / cs;
+    const int tid = threadIdx.x;
+    const bool leader = crank == 0;
+    const int off = tree_off[b];
+    const int T = tree_off[b + 1] - off;
+    int32_t* pth = path_out + (int64_t)b * RS_MAX_TREE;
+    int phase = 0;
+    if (leader && tid < RS_MAX_TREE) pth[tid] = -1;
+    bool bad_node = !(T >= 1 && T <= RS_MAX_TREE);
+    if (!bad_node && tid < T) {
+        const int pp = parent[off + tid];
+        const int tk = token[off + tid];
+        sm.parent[tid] = pp;
+        sm.token[tid] = tk;
+        bad_node = tid == 0 ? pp != -1 : !(pp >= 0 && pp < tid && tk >= 0 && tk < V);
+    }
+    if (__syncthreads_or(bad_node)) {
+        if (leader && tid == 0) { acc_out[b] = 0; bonus_out[b] = -1; flags_out[b] = RS_FLAG_MALFORMED; }
+        return;
+    }
+    const int64_t g = gid[b];
+    const int nvec = (V + 7) / 8;
+    const int per = (nvec + (int)cs - 1) / (int)cs;
+    const int vbeg = min(nvec, (int)crank * per), vend = min(nvec, vbeg + per);
+    uint32_t* wsl = reinterpret_cast<uint32_t*>(mss_dyn);   // [per * 8]
+    uint32_t* qsl = wsl + (size_t)per * 8;                  // [per * 8]
+    uint8_t* vex = reinterpret_cast<uint8_t*>(qsl + (size_t)per * 8);   // [per] residual vector shift
+    int c = 0, a = 0, bonus = -1, flags = 0;
+    bool bonus_mine = leader;
+    if (leader && tid == 0) pth[0] = 0;
+    __syncthreads();
+    // owner CTA: publish the current (w, qw) of the children x > after of node c (tid < T)
+    auto publish = [&](int after, bool resid_state) {
+        __syncthreads();   // this CTA's shared-memory weights are complete
+        const int x = tid;
+        if (x < T && x > after && sm.parent[x] == c) {
+            const int tk = sm.token[x];
+            const int ti = tk >> 3;
+            if (ti >= vbeg && ti < vend) {
+                const int lo = tk - vbeg * 8;
+                ms.childw[x] = resid_state ? (uint64_t)wsl[lo] : wdec(wsl[lo]);
+                ms.childq[x] = wdec(qsl[lo]);
+            }
+        }
+    };
+    for (;;) {
+        const RowView lv{logits, (int64_t)(off + c), V, DT, logits_vec_ok};
+        const RowView qv{draft, (int64_t)(off + c), V, RS_DTYPE_F32, draft_vec_ok};
+        // ---- pass L: the row from HBM into shared memory; max, validity, Zq
+        // (bf16 logits stay packed: the first 16 bytes of the vector's w words hold the 8 raw
+        // values until pass E expands them)
+        unsigned long long red[3] = {0, 0, 0};
+        {
+            float fmx = -INFINITY;
+            uint32_t amag = 0, qbad = 0;
+            unsigned long long zq = 0;
+            for (int i0 = vbeg + tid; i0 < vend; i0 += 2 * kMssThreads) {
+                Raw8 x[2], q[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int i = i0 + u * kMssThreads;
+                    if (i < vend) { x[u] = load_raw(lv, i); q[u] = load_raw(qv, i); }
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int i = i0 + u * kMssThreads;
+                    if (i >= vend) continue;
+                    const bool full = (i + 1) * 8 <= V;
+                    const uint32_t qb[8] = {q[u].a.x, q[u].a.y, q[u].a.z, q[u].a.w, q[u].b.x, q[u].b.y, q[u].b.z, q[u].b.w};
+                    uint32_t qe[8], qu[8];
+                    if (full) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) qu[j] = qb[j];
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) qu[j] = i * 8 + j < V ? qb[j] : 0u;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        // a probability: bits <= 1.0f, or -0
+                        qbad |= (qu[j] > 0x3F800000u && qu[j] != 0x80000000u) ? 1u : 0u;
+                        qe[j] = f2w(__uint_as_float(qu[j]));
+                    }
+                    zq += wsum8(qe);
+                    uint4* wp = reinterpret_cast<uint4*>(wsl + (size_t)(i - vbeg) * 8);
+                    uint4* qp = reinterpret_cast<uint4*>(qsl + (size_t)(i - vbeg) * 8);
+                    qp[0] = make_uint4(qe[0], qe[1], qe[2], qe[3]);
+                    qp[1] = make_uint4(qe[4], qe[5], qe[6], qe[7]);
+                    if (DT == RS_DTYPE_BF16) {
+                        uint32_t w4[4] = {x[u].a.x, x[u].a.y, x[u].a.z, x[u].a.w};
+                        uint32_t wm[4] = {w4[0], w4[1], w4[2], w4[3]};   // for the validity check
+                        if (!full) {
+#pragma unroll
+                            for (int j = 0; j < 8; ++j)   // padding: -inf (weight 0), not checked
+                                if (i * 8 + j >= V) {
+                                    const uint32_t keepm = (j & 1) ? 0x0000FFFFu : 0xFFFF0000u;
+                                    w4[j >> 1] = (w4[j >> 1] & keepm) | ((j & 1) ? 0xFF800000u : 0x0000FF80u);
+                                    wm[j >> 1] &= keepm;
+                                }
+                        }
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const uint32_t wv = w4[k];
+                            amag = __vmaxu2(amag, wm[k] & 0x7FFF7FFFu);
+                            fmx = fmaxf(fmx, fmaxf(__uint_as_float(wv << 16), __uint_as_float(wv & 0xFFFF0000u)));
+                        }
+                        wp[0] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                    } else {
+                        uint32_t lw[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const float l = (full || i * 8 + j < V) ? raw_elem(x[u], DT, j) : -INFINITY;
+                            qbad |= ((full || i * 8 + j < V) && !isfinite(l)) ? 1u : 0u;
+                            fmx = fmaxf(fmx, l);
+                            lw[j] = __float_as_uint(l);
+                        }
+                        wp[0] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+                        wp[1] = make_uint4(lw[4], lw[5], lw[6], lw[7]);
+                    }
+                }
+            }
+            // bf16: magnitude bits >= 0x7F80 <=> inf or NaN (padding lanes are not in amag)
+            const bool lbad = DT == RS_DTYPE_BF16 ? ((amag & 0xFFFFu) >= 0x7F80u || (amag >> 16) >= 0x7F80u) : false;
+            red[0] = fkey(fmx);
+            red[1] = (qbad || lbad) ? 1ull : 0ull;
+            red[2] = zq;
+        }
+        {
+            const int ops[3] = {OP_MAX, OP_OR, OP_SUM};
+            allreduce3(red, ops, sm, phase);
+        }
+        if (red[1]) { flags |= RS_FLAG_NONFINITE; break; }
+        const float m = fkey_inv((uint32_t)red[0]);
+        const uint64_t Zq = red[2];
+        // ---- pass E (shared memory): w_v = trunc(exp_spec((l_v - m) * inv_tau) * 2^32) and Z
+        // (the inverse-CDF tile sums are built only for the bonus draw, below)
+        unsigned long long zs = 0, dummy = 0;
+        for (int base = vbeg; base < vend; base += kMssThreads) {
+            const int i = base + tid;
+            unsigned long long s8 = 0;
+            if (i < vend) {
+                uint4* wp = reinterpret_cast<uint4*>(wsl + (size_t)(i - vbeg) * 8);
+                uint32_t lw[8];
+                if (DT == RS_DTYPE_BF16) {
+                    const uint4 a0 = wp[0];
+                    const uint32_t w4[4] = {a0.x, a0.y, a0.z, a0.w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) { lw[2 * k] = w4[k] << 16; lw[2 * k + 1] = w4[k] & 0xFFFF0000u; }
+                } else {
+                    const uint4 a0 = wp[0], a1 = wp[1];
+                    lw[0] = a0.x; lw[1] = a0.y; lw[2] = a0.z; lw[3] = a0.w;
+                    lw[4] = a1.x; lw[5] = a1.y; lw[6] = a1.z; lw[7] = a1.w;
+                }
+                uint32_t en[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)   // w = trunc(exp_spec((l - m) * inv_tau) * 2^32)
+                    en[j] = f2w(rs::exp_spec(__fmul_rn(__fsub_rn(__uint_as_float(lw[j]), m), inv_tau)));
+                s8 = wsum8(en);
+                wp[0] = make_uint4(en[0], en[1], en[2], en[3]);
+                wp[1] = make_uint4(en[4], en[5], en[6], en[7]);
+            }
+            zs += s8;
+        }
+        publish(c, false);
+        allreduce2(zs, OP_SUM, dummy, OP_OR, sm, phase);   // (cluster barrier: published values visible)
+        uint64_t Z = zs;
+        bool resid = false;
+        int rank = 0, next = -1;
+        for (int x = c + 1; x < T && next < 0; ++x) {
+            if (sm.parent[x] != c) continue;
+            const int tk = sm.token[x];
+            if (tid == 0) {
+                const uint32_t owner = (uint32_t)((tk >> 3) / per);
+                const uint64_t wt = ld_dsmem_u64(&ms.childw[x], owner);
+                const uint64_t qw = ld_dsmem_u64(&ms.childq[x], owner);
+                const uint32_t U = rs::uniform_word(seed, step, g, (uint32_t)rank, (uint32_t)c);
+                const bool acc = qw == 0 ? wt > 0 : ((u128)U * ((u128)qw * Z)) < (((u128)wt * Zq) << 32);
+                sm.bcast_i = acc ? 1 : 0;
+            }
+            __syncthreads();
+            const bool accepted = sm.bcast_i != 0;
+            __syncthreads();
+            if (accepted) { next = x; break; }
+            ++rank;
+            // pass A: r_v in 128 bits, once; stored per vector as r >> t with t in vex
+            unsigned long long bl = 0, dummy2 = 0;
+            for (int i = vbeg + tid; i < vend; i += kMssThreads) {
+                uint4* wp = reinterpret_cast<uint4*>(wsl + (size_t)(i - vbeg) * 8);
+                const uint4* qp = reinterpret_cast<const uint4*>(qsl + (size_t)(i - vbeg) * 8);
+                const uint4 a0 = wp[0], a1 = wp[1], b0 = qp[0], b1 = qp[1];
+                const uint32_t ww[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                const uint32_t qq[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                R96 r[8];
+                R96 ro{0, 0, 0};   // bitlen(max_j r_j) = bitlen(OR_j r_j)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    r[j] = resid96(ww[j], !resid && ww[j] == 0xFFFFFFFFu, Zq, qq[j], qq[j] == 0xFFFFFFFFu, Z);
+                    ro.r0 |= r[j].r0;
+                    ro.r1 |= r[j].r1;
+                    ro.r2 |= r[j].r2;
+                }
+                const int vb = r96_bitlen(ro);
+                bl = bl > (unsigned long long)vb ? bl : (unsigned long long)vb;
+                if (vb == 0) {
+                    vex[i - vbeg] = 0xFF;                // all-zero vector: old words kept
+                } else {
+                    const int t = vb > 32 ? vb - 32 : 0;
+                    vex[i - vbeg] = (uint8_t)t;
+                    uint32_t mt[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) mt[j] = r96_shr32(r[j], t);
+                    wp[0] = make_uint4(mt[0], mt[1], mt[2], mt[3]);
+                    wp[1] = make_uint4(mt[4], mt[5], mt[6], mt[7]);
+                }
+            }
+            allreduce2(bl, OP_MAX, dummy2, OP_OR, sm, phase);
+            if (bl != 0) {
+                // pass B: w <- (r >> t) >> (s - t) = r >> s, s = max(0, bitlen - 32); Z, tile sums
+                const int sh = (int)bl > 32 ? (int)bl - 32 : 0;
+                unsigned long long zn = 0, dummy3 = 0;
+                for (int base = vbeg; base < vend; base += kMssThreads) {
+                    const int i = base + tid;
+                    unsigned long long s8 = 0;
+                    if (i < vend) {
+                        uint4* wp = reinterpret_cast<uint4*>(wsl + (size_t)(i - vbeg) * 8);
+                        const int t = vex[i - vbeg];
+                        uint32_t wn[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                        if (t != 0xFF) {
+                            const uint4 a0 = wp[0], a1 = wp[1];
+                            const uint32_t ww[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                            const int d = sh - t;
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                wn[j] = d >= 32 ? 0u : (ww[j] >> d);
+                                s8 += wn[j];
+                            }
+                        }
+                        wp[0] = make_uint4(wn[0], wn[1], wn[2], wn[3]);
+                        wp[1] = make_uint4(wn[4], wn[5], wn[6], wn[7]);
+                    }
+                    zn += s8;
+                }
+                resid = true;
+                publish(x, true);
+                allreduce2(zn, OP_SUM, dummy3, OP_OR, sm, phase);   // (cluster barrier: visible)
+                Z = zn;
+            }
+            __syncthreads();
+        }
+        if (next < 0) {
+            const uint32_t U2 = rs::uniform_word(seed, step, g, 0xFFFFFFFFu, (uint32_t)c);
+            const uint64_t t = (uint64_t)(((u128)U2 * Z) >> 32);
+            const bool rs_ = resid;
+            // per-tile sums of the current weights (this CTA's slice), then the inverse CDF
+            clear_tiles(sm);
+            for (int base = vbeg; base < vend; base += kMssThreads) {
+                const int i = base + tid;
+                unsigned long long s8 = 0;
+                if (i < vend) {
+                    const uint4* wp = reinterpret_cast<const uint4*>(wsl + (size_t)(i - vbeg) * 8);
+                    const uint4 a0 = wp[0], a1 = wp[1];
+                    const uint32_t ww[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                    if (rs_) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) s8 += ww[j];
+                    } else {
+                        s8 = wsum8(ww);
+                    }
+                }
+                tile_add(sm, (base - vbeg) / kMssThreads, s8);
+            }
+            bonus = draw_bonus(sm, phase, t, vbeg, vend, V, bonus_mine, [&](int i, uint64_t w8[8]) {
+                const uint4* wp = reinterpret_cast<const uint4*>(wsl + (size_t)(i - vbeg) * 8);
+                const uint4 a0 = wp[0], a1 = wp[1];
+                const uint32_t ww[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+                for (int j = 0; j < 8; ++j) w8[j] = rs_ ? (uint64_t)ww[j] : wdec(ww[j]);
+            });
+            break;
+        }
+        c = next;
+        ++a;
+        if (leader && tid == 0) pth[a] = c;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        if (leader) {
+            acc_out[b] = a;
+            flags_out[b] = flags;
+            if (flags & RS_FLAG_NONFINITE) bonus_out[b] = -1;
+        }
+        if (!(flags & RS_FLAG_NONFINITE) && bonus_mine) bonus_out[b] = bonus;
+    }
+    if (cs > 1) cluster_sync_all();
+}
+
 __global__ void philox_kernel(const uint4* ctr, int64_t n, uint2 key, uint4* out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) out[i] = rs::philox4x32_10(ctr[i], key);
@@ -750,7 +1195,78 @@ __global__ void exp_spec_kernel(const float* x, int64_t n, float* y) {
 }  // namespace
 
 extern "C" size_t rs_tree_accept_workspace_bytes(int32_t mode, int32_t B, int32_t V) {
-    return mode == RS_ACCEPT_SAMPLE_MSS && B > 0 && V > 0 ? (size_t)B * (size_t)((V + 7) & ~7) * sizeof(uint32_t) : 0;
+    (void)mode; (void)B; (void)V;
+    return 0;   // MSS keeps the residual on chip (mss_accept_kernel); no mode needs workspace
+}
+
+// per CTA: w and qw words (64 B per 8-token vector) + one residual shift byte per vector
+static size_t mss_smem_bytes(int nvec, int cs) {
+    const size_t per = (size_t)((nvec + cs - 1) / cs);
+    return (per * 65 + 15) / 16 * 16;
+}
+
+// MSS launch: cluster size = 16 (non-portable) when the device can co-schedule it, else 8, and
+// never more CTAs than give every CTA >= 256 vectors; dynamic shared memory = per * 64 bytes.
+static rs_status launch_mss(bool bf, const void* logits, const float* draft, const int32_t* parent,
+                            const int32_t* token, const int32_t* tree_off, const int64_t* gid, int B, int V,
+                            float inv_tau, uint64_t seed, uint64_t step, int32_t* acc, int32_t* path, int32_t* bonus,
+                            int32_t* flags, bool lvec, bool dvec, cudaStream_t st) {
+    auto kern = bf ? mss_accept_kernel<RS_DTYPE_BF16> : mss_accept_kernel<RS_DTYPE_F32>;
+    const int nvec = (V + 7) / 8;
+    static int max_cs = 0;            // 16 if a 16-CTA cluster of this kernel can be resident, else 8
+    static size_t attr_smem[2] = {0, 0};
+    int cs = 1;
+    while (cs < 16 && nvec / (cs * 2) >= kMssThreads) cs *= 2;
+    const size_t smem = mss_smem_bytes(nvec, cs);
+    size_t& cur = attr_smem[bf ? 0 : 1];
+    if (cur < smem) {
+        RS_REQUIRE(smem <= 200 * 1024, RS_ERR_UNSUPPORTED, "rs_tree_accept: V=%d too large for MSS", V);
+        RS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        cur = smem;
+    }
+    if (max_cs == 0) {
+        max_cs = 8;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+            cudaLaunchConfig_t q = {};
+            q.gridDim = dim3(16);
+            q.blockDim = dim3(kMssThreads);
+            q.dynamicSmemBytes = mss_smem_bytes(nvec, 16);
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = 16;
+            qa[0].val.clusterDim.y = 1;
+            qa[0].val.clusterDim.z = 1;
+            q.attrs = qa;
+            q.numAttrs = 1;
+            int n = 0;
+            if (cudaOccupancyMaxActiveClusters(&n, kern, &q) == cudaSuccess && n > 0) max_cs = 16;
+        }
+        cudaGetLastError();
+    }
+    if (cs > max_cs) {
+        cs = max_cs;
+        const size_t sm2 = mss_smem_bytes(nvec, cs);
+        if (cur < sm2) {
+            RS_REQUIRE(sm2 <= 200 * 1024, RS_ERR_UNSUPPORTED, "rs_tree_accept: V=%d too large for MSS", V);
+            RS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+            cur = sm2;
+        }
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(B * cs));
+    cfg.blockDim = dim3(kMssThreads);
+    cfg.dynamicSmemBytes = mss_smem_bytes(nvec, cs);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    RS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, logits, draft, parent, token, tree_off, gid, V, inv_tau, seed, step,
+                                     acc, path, bonus, flags, lvec, dvec));
+    return RS_OK;
 }
 
 extern "C" rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t logits_dtype,
@@ -804,6 +1320,9 @@ extern "C" rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t lo
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const bool bf = logits_dtype == RS_DTYPE_BF16;
+    if (mode == RS_ACCEPT_SAMPLE_MSS) return launch_mss(bf, logits, draft_probs, parent, token, tree_off, gid, B, V,
+                                                        inv_tau, seed, step, accepted_len, path, bonus_token,
+                                                        status_flags, lvec, dvec, cfg.stream);
     auto kern = mode == RS_ACCEPT_GREEDY
                     ? (bf ? tree_accept_kernel<RS_ACCEPT_GREEDY, RS_DTYPE_BF16> : tree_accept_kernel<RS_ACCEPT_GREEDY, RS_DTYPE_F32>)
                 : mode == RS_ACCEPT_SAMPLE_DELTA

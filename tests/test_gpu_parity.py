@@ -189,17 +189,44 @@ def test_accept_degenerate_residual_gpu(cuda_lib):
         par1 = np.tile(np.array([-1, 0, 0, 0], np.int32), n)
         tok1 = np.tile(np.array([0, 9, 11, 3], np.int32), n)
         off = (np.arange(n + 1) * 4).astype(np.int32)
-        for q, expect_acc in ((q0, 0), (qp, 1)):
+        # both drafts: the two out-of-support children are rejected with an all-zero residual, the
+        # kept weights accept the in-support child (q0: qw_x = 0, w_x > 0; qp: certain), bonus 5
+        for q in (q0, qp):
             g, o = _accept_np_both(core, core.SAMPLE_MSS, np.tile(l, (n, 1)), par1, tok1, off, np.arange(n), V,
                                    draft=np.tile(q, (n, 1)), seed=77, step=5)
             for x, y in zip(g, o):
                 np.testing.assert_array_equal(x, y)
-            assert np.all(g[0] == expect_acc) and np.all(g[3] == 0)
-        # q0 with the in-support child present too: kept weights -> qw_x = 0, w_x > 0 -> accepted
-        g, o = _accept_np_both(core, core.SAMPLE_MSS, np.tile(l, (n, 1)), par1, tok1, off, np.arange(n), V,
-                               draft=np.tile(q0, (n, 1)), seed=1, step=2)
+            assert np.all(g[0] == 1) and np.all(g[1][:, 1] == 3) and np.all(g[2] == 5) and np.all(g[3] == 0)
+        # q0 without the in-support child: nothing accepted, bonus from the ORIGINAL p (support)
+        par3, tok3 = np.tile(np.array([-1, 0, 0], np.int32), n), np.tile(np.array([0, 9, 11], np.int32), n)
+        off3 = (np.arange(n + 1) * 3).astype(np.int32)
+        l3 = np.tile(l[:3], (n, 1))
+        g, o = _accept_np_both(core, core.SAMPLE_MSS, l3, par3, tok3, off3, np.arange(n), V,
+                               draft=np.tile(q0[:3], (n, 1)), seed=1, step=2)
         for x, y in zip(g, o):
             np.testing.assert_array_equal(x, y)
+        assert np.all(g[0] == 0) and np.isin(g[2], support).all() and np.all(g[3] == 0)
+
+
+def test_accept_mss_invalid_draft_rows_gpu(cuda_lib):
+    """MSS: a visited node whose draft row holds a value outside [0, 1] or NaN is flagged
+    NONFINITE (walk stops, bonus -1) exactly as in the oracle; unvisited bad rows are ignored."""
+    core = cuda_lib
+    V, n = 128256, 12
+    rng = np.random.default_rng(8)
+    par = np.tile(np.array([-1, 0, 1, 0], np.int32), n)
+    tok = np.tile(np.array([0, 2, 3, 7], np.int32), n)
+    off = (np.arange(n + 1) * 4).astype(np.int32)
+    l = rng.standard_normal((4 * n, V)).astype(np.float32)
+    l[0::4, 2] = 40.0
+    q = np.full((4 * n, V), 1.0 / V, np.float32)
+    for s_ in range(n):
+        r = 4 * s_ + (1 if s_ % 3 else 3)          # node 1 (visited) or node 3 (never visited)
+        q[r, rng.integers(V)] = [1.5, -0.5, np.nan][s_ % 3]
+    g, o = _accept_np_both(core, core.SAMPLE_MSS, l, par, tok, off, np.arange(n), V, draft=q, seed=4, step=2)
+    for x, y in zip(g, o):
+        np.testing.assert_array_equal(x, y)
+    assert (g[3][1::3] == core.FLAG_NONFINITE).all() and (g[3][0::3] == 0).all()
 
 
 def test_accept_out_of_vocabulary_token_gpu(cuda_lib):

@@ -355,3 +355,27 @@ def test_mss_degenerate_residual_proportional_draft():
         acc, path, bonus, flags = A.tree_accept(A.MSS, bf16_bits(l), [-1, 0, 0, 0], [0, 9, 11, 3], [0, 4],
                                                 [gid], V, draft_probs=q, seed=3, step=gid)
         assert flags[0] == 0 and acc[0] == 1 and list(path[0, :2]) == [0, 3] and bonus[0] == 5
+
+
+def test_mss_draft_row_must_be_probabilities():
+    """MSS: a visited node whose draft row holds a value outside [0, 1] (or NaN) is flagged like
+    a non-finite row (walk stops there, bonus -1); rows never visited are not checked."""
+    V = 8
+    l = np.zeros((3, V), np.float32)
+    l[0, 2] = 30.0                                     # child token 2 is (almost) certain at the root
+    q = softmax64(np.zeros((3, V))).astype(np.float32)
+    q[0, 2] = 1.0
+    for bad in (1.5, -0.25, np.nan):
+        qb = q.copy()
+        qb[1, 5] = bad                                 # row of node 1 (visited after accepting it)
+        acc, path, bonus, flags = A.tree_accept(A.MSS, bf16_bits(l), [-1, 0, 1], [0, 2, 3], [0, 3], [0], V,
+                                                draft_probs=qb)
+        assert flags[0] == A.FLAG_NONFINITE and acc[0] == 1 and bonus[0] == -1, bad
+        qb = q.copy()
+        qb[2, 5] = bad                                 # never visited when node 2 is rejected
+        l2 = l.copy()
+        l2[1, :] = 0.0
+        l2[1, 0] = 30.0                                # node 1's row: child token 3 rejected
+        acc, path, bonus, flags = A.tree_accept(A.MSS, bf16_bits(l2), [-1, 0, 1], [0, 2, 3], [0, 3], [0], V,
+                                                draft_probs=qb)
+        assert flags[0] == 0 and acc[0] == 1
