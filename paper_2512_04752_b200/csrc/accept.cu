@@ -817,10 +817,13 @@ __device__ __forceinline__ uint64_t wdec(uint32_t x) { return x == 0xFFFFFFFFu ?
 __device__ __forceinline__ uint32_t f2w(float e) { return __float2uint_rz(__fmul_rn(e, 4294967296.0f)); }
 // sum of 8 encoded weights as the true 64-bit sum
 __device__ __forceinline__ unsigned long long wsum8(const uint32_t e[8]) {
-    unsigned long long s = 0;
+    const unsigned long long s = ((unsigned long long)e[0] + e[1] + e[2]) + ((unsigned long long)e[3] + e[4] + e[5]) +
+                                 ((unsigned long long)e[6] + e[7]);
+    const uint32_t mn = min(min(min(~e[0], ~e[1]), min(~e[2], ~e[3])), min(min(~e[4], ~e[5]), min(~e[6], ~e[7])));
+    if (mn != 0u) return s;                     // no 0xFFFFFFFF code in the vector (the usual case)
     uint32_t tops = 0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) { s += e[j]; tops += e[j] == 0xFFFFFFFFu ? 1u : 0u; }
+    for (int j = 0; j < 8; ++j) tops += e[j] == 0xFFFFFFFFu ? 1u : 0u;
     return s + tops;
 }
 

@@ -167,3 +167,21 @@ def test_bench_reference_arm_contract():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["config"]["workload"].startswith("tiny")
+
+
+def test_sampling_kernels_have_no_fused_multiply_add():
+    """The bit-exact sampling arithmetic (exp_spec) is a fixed sequence of separately
+    rounded fp32 multiplies and adds: the SASS of every acceptance kernel must contain no FFMA /
+    FFMA2 (a contraction would change low bits and break parity with the C oracle)."""
+    import shutil
+    import subprocess
+    from paper_2512_04752_b200 import build as B
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    obj = os.path.join(B.BUILD, "accept.cu.o")
+    if not os.path.exists(obj):
+        B.build(verbose=False)
+    sass = subprocess.run([tool, "-sass", obj], capture_output=True, text=True, check=True).stdout
+    funcs = [f for f in sass.split("Function : ")[1:] if "accept" in f.split("\n")[0] or "exp_spec" in f.split("\n")[0]]
+    assert len(funcs) >= 6
+    for f in funcs:
+        assert "FFMA" not in f, f.split("\n")[0]

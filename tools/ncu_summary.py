@@ -17,7 +17,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-OURS = ("tree_attn", "attn_combine", "tree_accept", "accept_kernel", "kv_compact", "tree_mask", "kv_pack", "lm_head",
+OURS = ("tree_attn", "attn_combine", "tree_accept", "mss_accept", "accept_kernel", "kv_compact", "tree_mask", "kv_pack", "lm_head",
         "greedy_walk", "tree_select")
 
 METRICS = [
@@ -35,7 +35,7 @@ METRICS = [
 
 
 def short(name):
-    m = re.search(r"(tree_attn_kernel|attn_combine\w*|tree_accept\w*|accept_kernel\w*|kv_compact\w*|tree_mask\w*|"
+    m = re.search(r"(tree_attn_kernel|mss_accept_kernel|attn_combine\w*|tree_accept\w*|accept_kernel\w*|kv_compact\w*|tree_mask\w*|"
                   r"kv_pack\w*)", name)
     return m.group(1) if m else name[:60]
 
