@@ -44,6 +44,9 @@ WORKLOAD_DESC = {
             "fused LM-head arg-max (V=128256), logits never materialised",
     "c5g8lm": "BASELINE configs[4] per-GPU shard at 8 GPUs with the LM head in the step (f2): Llama-3-70B shapes, "
               "16 samples, prefix 8K, 64-node trees, greedy from hidden states (8192) via the fused LM-head arg-max",
+    "c5": "BASELINE configs[4]: Llama-3-70B shapes (64 q / 8 kv, d=128, 80 layers), batch 128 sample-sharded "
+          "over the N GPUs (128/N per GPU), prefix 8K, 64-node trees, greedy; when 80 layers of KV do not fit one "
+          "GPU (N <= 2) a pool of 16 distinct layer buffers is cycled (every launch still reads a full layer)",
     "c3s": "BASELINE configs[2] as the method runs it: Llama-3-8B shapes, batch 256, prefixes 512-16K "
            "lognormal, every tree = S(n) for the n select_strategy picks (host C++, called every step), "
            "rejection sampling (MSS)",
@@ -89,6 +92,43 @@ def _dist():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def _relaunch(n):
+    """`python bench.py --gpus N` outside torchrun: re-exec under torch.distributed.run with N
+    ranks on this node (127.0.0.1 rendezvous); rank 0 prints the line. Returns the exit code."""
+    import socket
+    import subprocess
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def _device(local):
+    """One process per GPU; when ranks outnumber the visible GPUs (a 1-GPU test box) ranks share
+    devices round-robin."""
+    n = max(1, torch.cuda.device_count())
+    return torch.device("cuda", local % n)
+
+
+def _pg_init(world, dev):
+    """Control-plane process group for the bench's barriers and max-over-ranks timing (gloo: CPU
+    scalars, works when ranks share a device). The data path has no collective; reallocation's KV
+    transfers run in the library (NCCL) or over peer memory, not through this group."""
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+
+
+def _allreduce(x, op="max"):
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return float(t.item())
 
 
 class ClockSampler:
@@ -173,49 +213,115 @@ def attention_algorithmic(b):
     return by, fl
 
 
-def cpu_baseline(host, cfg, budget_s=12.0):
-    """The oracle as it stands, on the host cores, on a bounded sample of the workload: whole
-    samples through all L layers of attention + acceptance + compaction."""
+def _oracle_sample(job):
+    """One whole sample of the workload through the CPU oracle (test infrastructure), in its own
+    process with one BLAS/OpenMP thread: the sample's shape (P, tree) is the GPU run's, its
+    q/K/V/logits are drawn from the same seeded recipe (synth). Timed: attention over
+    `layers_run` of the L layers (extrapolated to L), acceptance and compaction in full. Returns
+    (tokens committed, seconds)."""
+    import threadpoolctl
+    threadpoolctl.threadpool_limits(1)
+    torch.set_num_threads(1)
     from oracle import accept as OAcc
     from oracle import attention as OA
     from oracle import compact as OC
     from oracle import tree as OT
-    from oracle import lm_head as OLM
-    masks, _, _ = OT.batch_masks(host["parent"], host["tree_off"])
-    lm = "hidden" in host
-    lg_bits = None if lm else host["logits"].contiguous().view(torch.int16).numpy().view(np.uint16)
+    from synth import VerifyConfig, make_verify_batch
+    cfg = VerifyConfig(**{**job["cfg"], "B": 1, "prefix": ("fixed", int(job["P"])), "seed": int(job["seed"])})
+    L = cfg.L
+    lr = max(1, min(L, int(job["layers_run"])))
+    # only the layers that are run are drawn (bounded memory at 70B / 8K shapes)
+    b = make_verify_batch(cfg, device="cpu", layers=lr,
+                          parents=[np.asarray(job["parent"], np.int32)] if job["parent"] is not None else None)
+    T = int(b["T"][0])
+    masks, _, _ = OT.batch_masks(b["parent"], b["tree_off"])
+    lg = b["logits"].contiguous().view(torch.int16).numpy().view(np.uint16)
+    kc = [b["k_cache"][l].double().numpy() for l in range(lr)]
+    vc = [b["v_cache"][l].double().numpy() for l in range(lr)]
+    q = [b["q"][l].double().numpy() for l in range(lr)]
+    dp = b["draft_probs"].float().numpy() if cfg.mode == "mss" else None
+    om = {"greedy": OAcc.GREEDY, "delta": OAcc.DELTA, "mss": OAcc.MSS}[cfg.mode]
     t0 = time.perf_counter()
-    tokens, done = 0, 0
-    L = host["q"].shape[0]
-    for s in range(host["B"]):
-        sl = slice(int(host["tree_off"][s]), int(host["tree_off"][s + 1]))
-        for l in range(L):
-            OA.tree_verify_attention(host["q"][l][sl].double().numpy(), host["kc_np"][l], host["vc_np"][l],
-                                     host["block_table"][s:s + 1], host["prefix_len"][s:s + 1],
-                                     np.array([0, sl.stop - sl.start]), masks[sl], cfg.Hkv, cfg.page_size,
-                                     host["sm_scale"])
-        om = {"greedy": OAcc.GREEDY, "delta": OAcc.DELTA, "mss": OAcc.MSS}[cfg.mode]
-        if lm:
-            lg = np.concatenate([OLM.lm_head_logits(host["hidden"][sl], w) for w in host["w64"]], axis=1)
-            am, _ = OLM.argmax_rows(lg)
-            acc, path, bonus = OLM.greedy_walk(am, host["parent"][sl], host["token"][sl],
-                                               np.array([0, sl.stop - sl.start]))
-        else:
-            acc, path, bonus, flags = OAcc.tree_accept(
-                om, lg_bits[sl], host["parent"][sl], host["token"][sl], np.array([0, sl.stop - sl.start]),
-                host["gid"][s:s + 1], cfg.V, draft_probs=host["draft"][sl] if om == OAcc.MSS else None,
-                temperature=cfg.temperature, seed=11, step=0)
-        OC.kv_compact([host["kc_np"][l] for l in range(L)] + [host["vc_np"][l] for l in range(L)],
-                      host["block_table"][s:s + 1], host["prefix_len"][s:s + 1], acc, path, cfg.page_size)
-        tokens += int(acc[0]) + 1
-        done += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    dt = time.perf_counter() - t0
-    return dict(value=tokens / dt, unit=UNIT, cores=1, kind="oracle",
-                sample=f"{done} of {host['B']} samples of the workload, all {L} layers + "
-                       f"{'LM-head arg-max (fp64) + greedy walk' if lm else 'accept'} + compact, "
-                       f"numpy fp64 / C, single thread, {dt:.1f} s")
+    for l in range(lr):
+        OA.tree_verify_attention(q[l], kc[l], vc[l], b["block_table"], b["prefix_len"], b["tree_off"], masks,
+                                 cfg.Hkv, cfg.page_size, b["sm_scale"])
+    t_attn = (time.perf_counter() - t0) * L / lr
+    t1 = time.perf_counter()
+    acc, path, _, _ = OAcc.tree_accept(om, lg, b["parent"], b["token"], b["tree_off"], b["gid"], cfg.V, draft_probs=dp,
+                                       temperature=cfg.temperature, seed=11, step=0)
+    t_acc = time.perf_counter() - t1
+    t2 = time.perf_counter()
+    OC.kv_compact(kc + vc, b["block_table"], b["prefix_len"], acc, path, cfg.page_size)
+    t_cmp = (time.perf_counter() - t2) * L / lr
+    return int(acc[0]) + 1, t_attn + t_acc + t_cmp, T
+
+
+def oracle_throughput(cfg, prefix_len, parents, n_procs, rounds=1, layers_run=None, seed0=50000, warmup_rounds=0):
+    """The oracle on `n_procs` host cores at once (one process per core, one thread each): every
+    process runs `rounds` whole samples of the workload (shapes taken from the GPU batch in
+    order, values redrawn from the same recipe). Aggregate rate = sum over processes of
+    tokens / busy seconds (the processes run concurrently). Returns (rate, samples, seconds,
+    layers_run)."""
+    import multiprocessing as mp
+    L = cfg.L
+    if layers_run is None:
+        # bound the fp64 attention: the mean sample's cost scales with P; ~2 s of attention per
+        # sample at the configs' shapes
+        pm = float(np.mean(prefix_len))
+        per_layer = 1.2e-9 * cfg.Hq * cfg.d * pm * 20       # measured order of the einsum oracle (s)
+        layers_run = int(max(1, min(L, 2.0 / max(per_layer, 1e-6))))
+    base = {k: v for k, v in cfg.__dict__.items()}
+    jobs = []
+    for r in range(warmup_rounds + rounds):
+        for w in range(n_procs):
+            i = (r * n_procs + w) % len(prefix_len)
+            jobs.append(dict(cfg=base, P=int(prefix_len[i]), parent=None if parents is None else parents[i],
+                             seed=seed0 + r * n_procs + w, layers_run=layers_run))
+    ctx = mp.get_context("spawn")
+    env_keep = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}
+    os.environ.update(OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
+    try:
+        with ctx.Pool(n_procs) as pool:
+            res = pool.map(_oracle_sample, jobs, chunksize=1)
+    finally:
+        for k, v in env_keep.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    per_proc = {}
+    res = res[warmup_rounds * n_procs:]
+    for j, (tok, sec, _) in enumerate(res):
+        w = j % n_procs
+        a = per_proc.setdefault(w, [0, 0.0])
+        a[0] += tok
+        a[1] += sec
+    rate = sum(t / s for t, s in per_proc.values())
+    return rate, len(res), sum(s for _, s in per_proc.values()), layers_run
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_cpu_baseline(cfg, b, parents=None):
+    """cpu_baseline: the oracle on ALL host cores (one process each) plus a 1-core run, on
+    bounded samples of the workload (the GPU batch's sample shapes)."""
+    n = host_cores()
+    P = np.asarray(b["prefix_len"])
+    t0 = time.perf_counter()
+    rate_n, ns_n, sec_n, lr = oracle_throughput(cfg, P, parents, n)
+    rate_1, ns_1, sec_1, _ = oracle_throughput(cfg, P, parents, 1, layers_run=lr)
+    wall = time.perf_counter() - t0
+    return dict(value=round(rate_n, 4), unit=UNIT, cores=n, kind="oracle", value_1core=round(rate_1, 4),
+                sample=f"{ns_n} whole samples on {n} cores at once (one process and one BLAS thread each) + "
+                       f"{ns_1} on 1 core; sample shapes = the GPU batch's first samples (P, tree), values redrawn "
+                       f"from the same synth recipe; attention and compaction timed on {lr} of {cfg.L} layers and "
+                       f"scaled to {cfg.L}, accept in full; numpy fp64 + C; {sec_n:.1f} core-s + {sec_1:.1f} s "
+                       f"timed, {wall:.0f} s wall with data generation")
 
 
 def main():
@@ -223,7 +329,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None, help="timed steps (default 50; c4: 400)")
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c3s",
+                    help="default c3s = BASELINE configs[2] (the largest single-GPU config) as the method runs it")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -234,7 +341,10 @@ def main():
     args = ap.parse_args()
     if args.steps is None:
         args.steps = 400 if args.config == "c4" else 50
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_relaunch(args.gpus))
     world, rank, local = _dist()
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
     assert args.warmup >= 3, "W >= 3 warm-up steps"
     if args.impl == "reference":
         return run_reference(args, world, rank)
@@ -248,20 +358,29 @@ def run_ours(args, world, rank, local):
     from paper_2512_04752_b200.step import VerifyStep
     from synth import CONFIGS, make_lm_head_inputs, make_verify_batch
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+    dev = _device(local)
+    torch.cuda.set_device(dev)
+    _pg_init(world, dev)
     lm = LM_HEAD.get(args.config)
-    cfg = CONFIGS[lm[0] if lm else args.config]
+    n_buf = None
+    if args.config == "c5":
+        # configs[4]: B = 128 sample-sharded over the ranks (static split, no exchange)
+        assert 128 % world == 0, "c5 splits 128 samples evenly over the GPUs"
+        cfg = type(CONFIGS["c5g8"])(**{**CONFIGS["c5g8"].__dict__, "name": "c5", "B": 128 // world})
+        pages = cfg.B * -(-(cfg.prefix[1] + cfg.tree[1]) // cfg.page_size)
+        per_layer = 2 * pages * cfg.Hkv * cfg.page_size * cfg.d * 2
+        n_buf = cfg.L if cfg.L * per_layer <= 100e9 else 16
+    else:
+        cfg = CONFIGS[lm[0] if lm else args.config]
     cfg = type(cfg)(**{**cfg.__dict__, "seed": cfg.seed + 1000 * rank})   # disjoint samples per rank
     strat = None
     if cfg.tree[0] == "strategy":
         strat = strategy_trees(cfg, core)
         b = make_verify_batch(cfg, device=dev, gen_device=dev, parents=strat[4])
     else:
-        b = make_verify_batch(cfg, device=dev, gen_device=dev, with_logits=lm is None)
+        b = make_verify_batch(cfg, device=dev, gen_device=dev, with_logits=lm is None, layers=n_buf)
+    if n_buf is not None and n_buf < cfg.L:
+        b["L_logical"] = cfg.L
     mode = {"greedy": core.GREEDY, "delta": core.SAMPLE_DELTA, "mss": core.SAMPLE_MSS}[cfg.mode]
     lm_in = None
     if lm is not None:
@@ -323,9 +442,7 @@ def run_ours(args, world, rank, local):
     acc_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps
     cmp_ms = sum(e[2].elapsed_time(e[3]) for e in ev) / args.steps
     if world > 1:
-        t = torch.tensor([elapsed_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        elapsed_ms = float(t.item())
+        elapsed_ms = _allreduce(elapsed_ms, "max")
     ms_per_step = elapsed_ms / args.steps
     value = tokens_per_step * world * args.steps / (elapsed_ms / 1e3)
 
@@ -434,6 +551,7 @@ def run_ours(args, world, rank, local):
                    "l2": "inputs larger than L2: %.1f GB of distinct per-layer KV resident" %
                          (2 * b["k_cache"].numel() * 2 / 1e9),
                    "parallelism": f"dp{world} (independent sample-sharded instances, no collective)",
+                   **({"layer_buffers": n_buf} if n_buf is not None and n_buf < cfg.L else {}),
                    "attn_plan": info,
                    **({"lm_head": {"hidden": lm[1], "fused_argmax": True, "weight_GB": round(cfg.V * lm[1] * 2 / 1e9, 2)}}
                       if lm is not None else {}),
@@ -449,7 +567,7 @@ def run_ours(args, world, rank, local):
         "kernels": kernels,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = run_cpu_baseline(cfg, b)
+        line["cpu_baseline"] = run_cpu_baseline(cfg, b, parents=None if strat is None else strat[4])
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -478,11 +596,9 @@ def run_c4(args, world, rank, local):
     from paper_2512_04752_b200.instance import GenerationInstance
     from paper_2512_04752_b200.realloc import Rebalancer
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+    dev = _device(local)
+    torch.cuda.set_device(dev)
+    _pg_init(world, dev)
     samples = c4_samples(world, rank)
     L, Hq, Hkv, d, T = 32, 32, 8, 128, 16
     need = sum((p + r + T + 63) // 64 for _, p, r in samples)
@@ -506,7 +622,7 @@ def run_c4(args, world, rank, local):
         tput.append(tok / (time.perf_counter() - t0))
     thr = core.knee_threshold(counts, tput, 0.10)
     if world > 1:
-        t = torch.tensor([thr], device=dev)
+        t = torch.tensor([thr], dtype=torch.int64)
         torch.distributed.broadcast(t, 0)
         thr = int(t.item())
     realloc = args.realloc == "on" and world > 1
@@ -560,12 +676,8 @@ def run_c4(args, world, rank, local):
     ms = start.elapsed_time(end)
     tok_all, ms_max = tokens, ms
     if world > 1:
-        t = torch.tensor([float(tokens)], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t)
-        tok_all = int(t.item())
-        t = torch.tensor([ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms_max = float(t.item())
+        tok_all = int(_allreduce(tokens, "sum"))
+        ms_max = _allreduce(ms, "max")
     value = tok_all / (ms_max / 1e3)
     gbs = attn_bytes / (attn_ms * 1e-3) / 1e9 if attn_ms > 0 else 0.0
     mig_bytes = sum(m[2] for m in migrations)
@@ -633,8 +745,10 @@ def run_e2e(step, b, n_steps, tokens_per_step, world, dev, barrier, mode, temper
     step2 = VerifyStep(b2, mode=mode, temperature=temperature,
                        lm_head=(b2["hidden"], step.lm_w) if lm else None)
     steps = [step, step2]
-    ins = [[s.q, s.hidden if lm else s.logits] for s in steps]
-    h_ins = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t) for t in ins[0]]
+    q_reps = -(-step.L // step.q.shape[0])    # pooled layer buffers: upload Q once per logical layer
+    ins = [[s.q] * q_reps + [s.hidden if lm else s.logits] for s in steps]
+    h_q = torch.empty(step.q.shape, dtype=step.q.dtype, pin_memory=True).copy_(step.q)
+    h_ins = [h_q] * q_reps + [torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t) for t in ins[0][q_reps:]]
     metas = [[s.parent, s.token, s.tree_off, s.prefix_len, s.block_table, s.gid] for s in steps]
     h_meta = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t) for t in metas[0]]
     h_draft = None
@@ -675,9 +789,7 @@ def run_e2e(step, b, n_steps, tokens_per_step, world, dev, barrier, mode, temper
     barrier()
     ms = s.elapsed_time(e)
     if world > 1:
-        t = torch.tensor([ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = _allreduce(ms, "max")
     return {"value": round(tokens_per_step * world * n_steps / (ms / 1e3), 1), "unit": UNIT,
             "inputs": "Q (all layers) + " + ("final hidden states (f2)" if lm else "logits") +
                       (" + draft probabilities" if step.draft is not None else "") + " + tree metadata",
@@ -686,111 +798,54 @@ def run_e2e(step, b, n_steps, tokens_per_step, world, dev, barrier, mode, temper
             "pipelining": "double-buffered inputs: upload of step k+1 overlaps kernels of step k"}
 
 
-def run_cpu_baseline(cfg, b):
-    """Oracle on host cores over whole samples (bounded ~12 s)."""
-    L = b["q"].shape[0]
-    nsamp = min(b["B"], 8)
-    host = {k: b[k] for k in ("parent", "token", "tree_off", "prefix_len", "block_table", "gid", "sm_scale")}
-    ns = int(b["tree_off"][nsamp])
-    host["tree_off"] = b["tree_off"][:nsamp + 1]
-    host["parent"], host["token"] = b["parent"][:ns], b["token"][:ns]
-    host["prefix_len"], host["block_table"], host["gid"] = b["prefix_len"][:nsamp], b["block_table"][:nsamp], b["gid"][:nsamp]
-    host["B"] = nsamp
-    host["q"] = b["q"][:, :ns].cpu()
-    if b.get("hidden") is not None:     # f2: the oracle LM head (fp64) on the sampled rows
-        host["hidden"] = b["hidden"][:ns].double().cpu().numpy()
-        host["w64"] = [b["lm_weight"][v0:v0 + 8192].double().cpu().numpy()
-                       for v0 in range(0, b["lm_weight"].shape[0], 8192)]
-    else:
-        host["logits"] = b["logits"][:ns].cpu()
-    host["draft"] = b["draft_probs"][:ns].float().cpu().numpy() if b.get("draft_probs") is not None else None
-    # only the pages of the sampled samples are copied (the cache itself stays on the GPU)
-    pages = np.unique(host["block_table"])
-    remap = {int(p): i for i, p in enumerate(pages)}
-    host["block_table"] = np.vectorize(lambda x: remap[int(x)])(host["block_table"]).astype(np.int32)
-    idx = torch.as_tensor(pages, device=b["k_cache"].device, dtype=torch.long)
-    host["kc_np"] = [b["k_cache"][l].index_select(0, idx).double().cpu().numpy() for l in range(L)]
-    host["vc_np"] = [b["v_cache"][l].index_select(0, idx).double().cpu().numpy() for l in range(L)]
-    return cpu_baseline(host, cfg)
-
-
 def run_reference(args, world, rank):
     """Reference arm: the CPU oracle as it stands (no reference implementation exists for this
-    paper: /root/reference holds only the paper text). Rank 0 only."""
+    paper: /root/reference holds only the paper text), on all host cores (one process per core).
+    Each step = one whole sample per core of the workload (shapes as the GPU arm draws them,
+    values from the same recipe), W warm-up steps untimed. Rank 0 only."""
     if rank != 0:
         return
-    from synth import CONFIGS, VerifyConfig, make_verify_batch
+    from synth import CONFIGS, VerifyConfig, draw_prefix_lengths
+    parents = None
     if args.config == "c4":
-        # c4's verify step on one sample of its population: 8B shapes, prompt + partial response
+        # c4's verify step on samples of its population: 8B shapes, prompt + partial response
         # lengths of the long tail (lognormal around 600 tokens), 16-node tree, greedy
-        cfg = VerifyConfig("c4", B=1, Hq=32, Hkv=8, d=128, V=128256, L=32, prefix=("lognormal", 600, 0.784, 32, 4096),
+        cfg = VerifyConfig("c4", B=256, Hq=32, Hkv=8, d=128, V=128256, L=32, prefix=("lognormal", 600, 0.784, 32, 4096),
                            tree=("fixed", 16), mode="greedy", seed=4)
+        P = draw_prefix_lengths(np.random.default_rng(cfg.seed), cfg)
     else:
         cfg = CONFIGS[LM_HEAD[args.config][0] if args.config in LM_HEAD else args.config]
-    # one whole sample per step (all L layers), drawn on the CPU with the same recipe
-    one = type(cfg)(**{**cfg.__dict__, "B": max(1, args.steps + args.warmup)})
-    parents = None
-    if cfg.tree[0] == "strategy":
-        # c3s: the batch's n from the oracle's select_strategy over the whole batch's candidate
-        # trees (same draws as strategy_trees), each sample's tree from the oracle's S(n)
-        from oracle import strategy as OS
-        from synth import draw_prefix_lengths, make_candidate_tree
         P = draw_prefix_lengths(np.random.default_rng(cfg.seed), cfg)
-        rng = np.random.default_rng(cfg.seed + 77)
-        cands = [make_candidate_tree(rng, int(cfg.tree[1])) for _ in range(cfg.B)]
-        c = STRATEGY_COST
-        cost = OS.CostModel(c["c_draft"], c["b0"], c["b1"], c["b2"], c["b3"], c["k_sat"], c["seq_bucket"],
-                            c["draft_bucket"])
-        n = OS.select_strategy(cands, P, STRATEGY_KX, STRATEGY_KY, cost, n_min=3, n_max=63, patience=2)["n"]
-        parents = [OS.verification_tree(p_, o_, np.zeros(len(p_), np.int32), 0, n, STRATEGY_KX, STRATEGY_KY)[0]
-                   for p_, o_ in cands[:one.B]]
-    b = make_verify_batch(one, device="cpu", spare_pages=0, parents=parents)
-    L = b["q"].shape[0]
-    from oracle import accept as OAcc
-    from oracle import attention as OA
-    from oracle import compact as OC
-    from oracle import tree as OT
-    masks, _, _ = OT.batch_masks(b["parent"], b["tree_off"])
-    lg_bits = b["logits"].contiguous().view(torch.int16).numpy().view(np.uint16)
-    kc = [b["k_cache"][l].double().numpy() for l in range(L)]
-    vc = [b["v_cache"][l].double().numpy() for l in range(L)]
-    tokens = 0
-    t_total = 0.0
-    budget_s = float(os.environ.get("RS_REF_BUDGET_S", "150"))
-    layers_run = L
-    for s in range(args.warmup + args.steps):
-        sl = slice(int(b["tree_off"][s]), int(b["tree_off"][s + 1]))
-        t0 = time.perf_counter()
-        ta = time.perf_counter()
-        for l in range(layers_run):
-            OA.tree_verify_attention(b["q"][l][sl].double().numpy(), kc[l], vc[l], b["block_table"][s:s + 1],
-                                     b["prefix_len"][s:s + 1], np.array([0, sl.stop - sl.start]), masks[sl], cfg.Hkv,
-                                     cfg.page_size, b["sm_scale"])
-        t_attn = (time.perf_counter() - ta) * L / layers_run        # layers not run: extrapolated
-        om = {"greedy": OAcc.GREEDY, "delta": OAcc.DELTA, "mss": OAcc.MSS}[cfg.mode]
-        dp = b["draft_probs"][sl].float().numpy() if om == OAcc.MSS else None
-        acc, path, _, _ = OAcc.tree_accept(om, lg_bits[sl], b["parent"][sl], b["token"][sl],
-                                           np.array([0, sl.stop - sl.start]), b["gid"][s:s + 1], cfg.V,
-                                           draft_probs=dp, temperature=cfg.temperature, seed=11, step=s)
-        OC.kv_compact(kc + vc, b["block_table"][s:s + 1], b["prefix_len"][s:s + 1], acc, path, cfg.page_size)
-        dt = (time.perf_counter() - t0) - (t_attn * layers_run / L) + t_attn
-        if s == 0 and dt * (args.warmup + args.steps) > budget_s:
-            layers_run = max(1, int(L * budget_s / (dt * (args.warmup + args.steps))))
-        if s >= args.warmup:
-            t_total += dt
-            tokens += int(acc[0]) + 1
-    value = tokens / t_total
-    line = {"impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t_total / args.steps, 3),
+        if cfg.tree[0] == "strategy":
+            # c3s: the batch's n from the oracle's select_strategy over the batch's candidate trees
+            # (same draws as strategy_trees), each sample's tree from the oracle's S(n)
+            from oracle import strategy as OS
+            from synth import make_candidate_tree
+            rng = np.random.default_rng(cfg.seed + 77)
+            cands = [make_candidate_tree(rng, int(cfg.tree[1])) for _ in range(cfg.B)]
+            c = STRATEGY_COST
+            cost = OS.CostModel(c["c_draft"], c["b0"], c["b1"], c["b2"], c["b3"], c["k_sat"], c["seq_bucket"],
+                                c["draft_bucket"])
+            n = OS.select_strategy(cands, P, STRATEGY_KX, STRATEGY_KY, cost, n_min=3, n_max=63, patience=2)["n"]
+            parents = [OS.verification_tree(p_, o_, np.zeros(len(p_), np.int32), 0, n, STRATEGY_KX, STRATEGY_KY)[0]
+                       for p_, o_ in cands]
+    ncores = host_cores()
+    t0 = time.perf_counter()
+    rate, nsamp, busy, lr = oracle_throughput(cfg, P, parents, ncores, rounds=args.steps, warmup_rounds=args.warmup)
+    wall = time.perf_counter() - t0
+    ms_step = 1e3 * busy / max(1, nsamp) * 1.0       # per-core seconds per sample = one step on each core
+    line = {"impl": "reference", "metric": METRIC, "value": round(rate, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": f"{args.config}: {WORKLOAD_DESC.get(args.config, args.config)}",
-                       "step": "one whole sample of the workload through all layers (bounded sample)"},
-            "cpu_baseline": {"value": round(value, 2), "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{args.steps} whole samples; attention timed on {layers_run} of {L} layers "
-                                       f"per sample and scaled to {L}; accept + compact in full; numpy fp64 + C, "
-                                       f"single thread"},
-            "e2e": {"value": round(value, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                       "step": f"one whole sample of the workload per host core ({ncores} processes at once)"},
+            "cpu_baseline": {"value": round(rate, 3), "unit": UNIT, "cores": ncores, "kind": "oracle",
+                             "sample": f"{nsamp} whole samples ({args.steps} steps x {ncores} cores, {args.warmup} "
+                                       f"warm-up steps untimed); attention and compaction timed on {lr} of "
+                                       f"{cfg.L} layers and scaled to {cfg.L}; accept in full; numpy fp64 + C, one thread per "
+                                       f"process; {wall:.0f} s wall"},
+            "e2e": {"value": round(rate, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 

@@ -24,7 +24,12 @@ class VerifyStep:
         self.mode = mode
         self.temperature = temperature
         self.B, self.Hq, self.Hkv, self.d, self.ps = b["B"], b["Hq"], b["Hkv"], b["d"], b["page_size"]
-        self.L = b["q"].shape[0]
+        # b["L_logical"] > the number of layer buffers: a pool of distinct layer buffers (Q, K, V)
+        # cycled so a deep model's step fits in memory (config 5 at 2 GPUs: SURVEY 8(d)); logical
+        # layer l uses buffer l % pool, every launch still reads a full layer of K/V from HBM
+        n_buf = b["q"].shape[0]
+        self.L = int(b.get("L_logical", n_buf))
+        self.layer_buf = [l % n_buf for l in range(self.L)]
         self.sm_scale = b["sm_scale"]
 
         def t32(x):
@@ -36,8 +41,8 @@ class VerifyStep:
         self.block_table = t32(b["block_table"])
         self.gid = torch.as_tensor(b["gid"], dtype=torch.int64).to(dev)
         self.q = b["q"]
-        self.k_layers = [b["k_cache"][l] for l in range(self.L)]
-        self.v_layers = [b["v_cache"][l] for l in range(self.L)]
+        self.k_layers = [b["k_cache"][i] for i in self.layer_buf]
+        self.v_layers = [b["v_cache"][i] for i in self.layer_buf]
         self.logits = b.get("logits")
         self.hidden, self.lm_w = lm_head if lm_head is not None else (None, None)
         if self.hidden is not None:
@@ -68,7 +73,7 @@ class VerifyStep:
             self.lm_ws = torch.empty(max(core.lm_head_argmax_workspace_bytes(NT), 8), dtype=torch.uint8, device=dev)
         self.accept_ws = torch.empty(max(nws, 16), dtype=torch.uint8, device=dev)   # MSS residual weights
         self.attn_call = core.AttentionLayersCall(
-            self.plan, [self.q[l] for l in range(self.L)], self.k_layers, self.v_layers, self.block_table,
+            self.plan, [self.q[i] for i in self.layer_buf], self.k_layers, self.v_layers, self.block_table,
             self.prefix_len, self.tree_off, self.mask, self.sm_scale, self.ws,
             [self.attn_out[l] for l in range(self.L)], None if self.lse is None else [self.lse[l] for l in range(self.L)])
         self.graph = None
