@@ -336,6 +336,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--realloc", default="on", choices=["on", "off"], help="c4: sample reallocation")
     ap.add_argument("--cooldown", type=int, default=32, help="c4: steps between reallocation checks (P:300)")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="c4: KV migration over peer memory (one push kernel, CUDA IPC) or NCCL send/recv")
     ap.add_argument("--migration", default="blocking", choices=["blocking", "two-stage"],
                     help="c4: stop-the-world rs_migrate_samples or the two-stage migration (f1, P:303-318)")
     args = ap.parse_args()
@@ -627,9 +629,15 @@ def run_c4(args, world, rank, local):
         thr = int(t.item())
     realloc = args.realloc == "on" and world > 1
     reb = Rebalancer(thr, cooldown=args.cooldown) if realloc else None
-    comm = core.Comm(rank, world) if realloc else None
-    staging = torch.empty(4 << 30, dtype=torch.uint8, device=dev) if realloc else None
-    scratch = torch.empty(3 * 512 + 512 * 72, dtype=torch.int32, device=dev) if realloc else None
+    # KV transport: peer memory (rs_peer_push into the destination's pages over CUDA IPC / NVLink;
+    # works when ranks share a GPU) or NCCL send/recv through a staging buffer (one GPU per rank)
+    if realloc and args.transport == "peer":
+        comm = inst.connect_peers(rank)
+        staging = scratch = None
+    else:
+        comm = core.Comm(rank, world) if realloc else None
+        staging = torch.empty(4 << 30, dtype=torch.uint8, device=dev) if realloc else None
+        scratch = torch.empty(3 * 512 + 512 * 72, dtype=torch.int32, device=dev) if realloc else None
     stalls = []
 
     def one_step(k, timing=False):
@@ -689,7 +697,8 @@ def run_c4(args, world, rank, local):
         "config": {"workload": f"c4: {WORKLOAD_DESC['c4']}", "samples_per_instance": len(samples),
                    "Hq": Hq, "Hkv": Hkv, "d": d, "L": L, "V": 128256, "tree": ["fixed", T], "accept_mode": "greedy",
                    "realloc": "on" if realloc else "off", "cooldown": args.cooldown, "threshold": thr,
-                   "migration": args.migration,
+                   "migration": args.migration, "transport": args.transport if realloc else None,
+                   "gpus_visible": torch.cuda.device_count(),
                    "knee_profile": {"counts": counts, "tokens_per_s": [round(x, 1) for x in tput]},
                    "load_first_last": [loads[0] if loads else 0, loads[-1] if loads else 0],
                    "finished_samples_rank0": inst.finished, "tokens_rank0": tokens,

@@ -415,6 +415,44 @@ rs_status rs_migrate_stage2(rs_comm* comm, int32_t src_rank, int32_t dst_rank, c
                             size_t staging_bytes, int32_t* device_scratch, void* ssm_ready_event,
                             void* stream);
 
+/* ===================================================================================== a5 (peer memory)
+ * KV migration over peer memory (P:302-327 on B200): the instances' KV stores are registered
+ * once (rs_peer_create on each rank, the host blob of rs_peer_export sent to every other rank
+ * over the caller's control plane, rs_peer_import there: CUDA IPC mappings of the peer's page
+ * pools, NVLink P2P when the instances are on different GPUs). A migration is then ONE kernel
+ * on the source: every (page, kv head) run of the samples' token range is read from the local
+ * pools and stored straight into the destination's reserved pages — pack, transfer and unpack
+ * of P:321-327 in one pass, with no staging buffer. The allocation handshake of P:325 is the
+ * caller's: the destination reserves pages (rs_migrate_reserve, all-or-nothing; refusal ->
+ * nothing is pushed and the source keeps its samples) and sends its block-table rows back.
+ * Completion: the source records its inter-process event after the push (rs_peer_signal), tells
+ * the destination over the control plane, and the destination's stream waits on it
+ * (rs_peer_wait) before anything reads the new pages. The pools must outlive the rs_peer objects
+ * of every rank that imported them. */
+typedef struct rs_peer rs_peer;
+/* Register this rank's store (pointers kept until rs_peer_destroy; 16-byte aligned pools). */
+rs_status rs_peer_create(const rs_kv_desc* kv, int32_t rank, rs_peer** out);
+/* Size of the registration blob (host bytes): header + one IPC handle / offset per layer pool. */
+size_t rs_peer_blob_bytes(const rs_peer* peer);
+rs_status rs_peer_export(const rs_peer* peer, uint8_t* blob, size_t bytes);
+/* Map the store of the rank named in `blob` (same KV shapes, else RS_ERR_LAYOUT_MISMATCH; a
+ * blob from this process is used by raw pointer). Each rank may be imported once. */
+rs_status rs_peer_import(rs_peer* peer, const uint8_t* blob, size_t bytes);
+/* Source side: copy tokens starts[i] .. starts[i]+lens[i]-1 (starts NULL = from 0) of sample i
+ * from this rank's pages (row i of src_block_table) into dst_rank's pages (row i of
+ * dst_block_table, the rows the destination reserved), every layer of the models selected by
+ * `parts` (bit 0 = SSM, bit 1 = LLM; SSM launched first). src/dst block tables: device int32
+ * [n, max_pages]; starts, lens: device int32 [n]. Enqueued on `stream`. */
+rs_status rs_peer_push(rs_peer* peer, int32_t dst_rank, const int32_t* src_block_table,
+                       const int32_t* dst_block_table, int32_t max_pages, const int32_t* starts,
+                       const int32_t* lens, int32_t n, int32_t parts, void* stream);
+/* Record this rank's event `which` (0 = push done, 1 = SSM part landed) on `stream`. */
+rs_status rs_peer_signal(rs_peer* peer, int32_t which, void* stream);
+/* Make `stream` wait for src_rank's most recent rs_peer_signal(which) — call it only after the
+ * source has told you (control plane) that the signal is enqueued. */
+rs_status rs_peer_wait(rs_peer* peer, int32_t src_rank, int32_t which, void* stream);
+void rs_peer_destroy(rs_peer* peer);
+
 #ifdef __cplusplus
 }
 #endif

@@ -666,3 +666,80 @@ class TwoStageMigration:
 
     def dst_rows(self):
         return self.rows[:self.n] if self.comm.rank == self.dst else None
+
+
+# ------------------------------------------------------------------ a5 over peer memory
+_sig("rs_peer_create", _i32, ctypes.POINTER(KVDescC), _i32, ctypes.POINTER(_P))
+_sig("rs_peer_blob_bytes", _sz, _P)
+_sig("rs_peer_export", _i32, _P, _P, _sz)
+_sig("rs_peer_import", _i32, _P, _P, _sz)
+_sig("rs_peer_push", _i32, _P, _i32, _P, _P, _i32, _P, _P, _i32, _i32, _P)
+_sig("rs_peer_signal", _i32, _P, _i32, _P)
+_sig("rs_peer_wait", _i32, _P, _i32, _i32, _P)
+_sig("rs_peer_destroy", None, _P)
+
+PEER_SSM, PEER_LLM = 1, 2
+PEER_DONE, PEER_SSM_READY = 0, 1
+
+
+class PeerStore:
+    """This rank's KV store registered for peer-memory migration (rs_peer_*). export() gives the
+    host blob other ranks import(); push() copies sample token ranges into a peer's reserved
+    pages (one kernel per model); signal()/wait() carry completion as an inter-process event."""
+
+    def __init__(self, llm_layers, ssm_layers, page_size, rank: int):
+        self.desc, self._keep = _kv_desc(llm_layers, ssm_layers, page_size)
+        self._h = _P()
+        _check(_lib.rs_peer_create(ctypes.byref(self.desc), int(rank), ctypes.byref(self._h)), "rs_peer_create")
+        self.rank = int(rank)
+        self._hold = []
+
+    def export(self) -> bytes:
+        n = int(_lib.rs_peer_blob_bytes(self._h))
+        buf = np.zeros(n, np.uint8)
+        _check(_lib.rs_peer_export(self._h, _ptr(buf), n), "rs_peer_export")
+        return buf.tobytes()
+
+    def import_(self, blob: bytes):
+        buf = np.frombuffer(blob, np.uint8).copy()
+        _check(_lib.rs_peer_import(self._h, _ptr(buf), buf.size), "rs_peer_import")
+
+    def push(self, dst_rank, src_block_table, dst_block_table, lens, starts=None, parts=PEER_SSM | PEER_LLM,
+             stream=None):
+        """src/dst_block_table: device int32 [n, max_pages]; lens/starts: device int32 [n]. The
+        tensors are kept referenced on `stream` until it passes the kernels."""
+        n = int(lens.numel())
+        _check(_lib.rs_peer_push(self._h, int(dst_rank), _ptr(src_block_table), _ptr(dst_block_table),
+                                 int(src_block_table.shape[1]), _ptr(starts) if starts is not None else None,
+                                 _ptr(lens), n, int(parts), _stream(stream)), "rs_peer_push")
+        if stream is not None:
+            for t in (src_block_table, dst_block_table, lens, starts):
+                if isinstance(t, torch.Tensor):
+                    t.record_stream(stream)
+
+    def signal(self, which=PEER_DONE, stream=None):
+        _check(_lib.rs_peer_signal(self._h, int(which), _stream(stream)), "rs_peer_signal")
+
+    def wait(self, src_rank, which=PEER_DONE, stream=None):
+        _check(_lib.rs_peer_wait(self._h, int(src_rank), int(which), _stream(stream)), "rs_peer_wait")
+
+    def destroy(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.rs_peer_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.destroy()
+
+
+def peer_connect(store: PeerStore, pg=None):
+    """Collective over the torch.distributed group: every rank exports its blob, all-gathers
+    the others' and imports them (its own too: pid-local, raw pointers)."""
+    import torch.distributed as dist
+    blob = store.export()
+    world = dist.get_world_size(pg)
+    blobs = [None] * world
+    dist.all_gather_object(blobs, blob, group=pg)
+    for b in blobs:
+        store.import_(b)
+    return store

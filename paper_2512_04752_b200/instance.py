@@ -287,7 +287,11 @@ class GenerationInstance:
 
     def rebalance(self, rebalancer: Rebalancer, comm: "core.Comm", staging, scratch, force=False):
         """Collective over all instances (every rank calls it at the same step). Returns
-        (#samples sent, #received, KV bytes moved by this rank)."""
+        (#samples sent, #received, KV bytes moved by this rank). `comm` is the NCCL communicator
+        (rs_migrate_samples: pack -> send/recv -> unpack through `staging`) or this instance's
+        core.PeerStore (rs_peer_push straight into the destination's pages; staging unused)."""
+        if isinstance(comm, core.PeerStore):
+            return self._rebalance_peer(rebalancer, comm, force)
         transfers = rebalancer.plan(self.load, force=force)
         if not transfers:
             return 0, 0, 0
@@ -340,7 +344,10 @@ class GenerationInstance:
         prefix in flight (Markov property); stage 2 (rs_migrate_stage2) moves the tokens
         committed meanwhile, SSM part first, and the samples change hands with their updated
         state. Only samples that cannot finish during the overlap are chosen. Returns
-        (#sent, #received, KV bytes moved by this rank, timing dict in ms)."""
+        (#sent, #received, KV bytes moved by this rank, timing dict in ms). With a core.PeerStore
+        as `comm` both stages are rs_peer_push kernels on a side stream (staging unused)."""
+        if isinstance(comm, core.PeerStore):
+            return self._rebalance_two_stage_peer(rebalancer, comm, overlap_steps, seed, force)
         transfers = rebalancer.plan(self.load, force=force)
         if not transfers:
             return 0, 0, 0, {}
@@ -422,5 +429,176 @@ class GenerationInstance:
                     rcv.set_pages(rows[i, :npg].copy(), self.max_pages)
                     received.append(rcv)
                     recv += 1
+        self.samples = [x for x in self.samples if x.gid not in sent_gids] + received
+        return sent, recv, moved, timing
+
+    # ------------------------------------------------------------------ migration over peer memory
+    def connect_peers(self, rank: int, pg=None) -> "core.PeerStore":
+        """Register this instance's KV pools (LLM + SSM) for peer-memory migration and map every
+        other instance's (collective over the torch.distributed group)."""
+        store = core.PeerStore((self.k_llm, self.v_llm), (self.k_ssm, self.v_ssm), PAGE, rank)
+        return core.peer_connect(store, pg)
+
+    def _kv_bytes(self, lens) -> int:
+        return 2 * (core.kv_pack_elems(self.L, self.Hkv, self.d, lens) + core.kv_pack_elems(1, self.Hkv, self.d, lens))
+
+    def _src_rows(self, gids, stream):
+        """Device block-table rows of this instance's samples `gids`, allocated and copied on the
+        stream whose kernels read them."""
+        by_gid = {x.gid: x for x in self.samples}
+        rows = np.stack([by_gid[g].bt_row for g in gids]).astype(np.int32)
+        with torch.cuda.stream(stream):
+            return torch.from_numpy(rows).to(self.dev, non_blocking=False)
+
+    def _to_dev(self, x, stream):
+        with torch.cuda.stream(stream):
+            return torch.from_numpy(np.ascontiguousarray(x, dtype=np.int32)).to(self.dev)
+
+    def _rebalance_peer(self, rebalancer: Rebalancer, store: "core.PeerStore", force=False):
+        """Stop-the-world reallocation with peer-memory migration. Per transfer (plan order, every
+        rank takes part in the control-plane broadcasts): the destination reserves pages for the
+        chosen samples all-or-nothing and broadcasts its rows (None = refused: the source
+        keeps its samples); the source pushes every layer's KV into those pages with one kernel
+        per model (SSM first) on the instance stream, records its event and broadcasts that it
+        did; the destination's stream waits on the event, so its next step sees the pages."""
+        transfers = rebalancer.plan(self.load, force=force)
+        if not transfers:
+            return 0, 0, 0
+        transfers = rebalancer.choose(transfers, self.sample_meta())
+        rank = store.rank
+        sent = recv = moved = 0
+        sent_gids, received = set(), []
+        for tr in transfers:
+            if not tr.samples:
+                continue
+            lens = [c.seq_len for c in tr.samples]
+            gids = [c.gid for c in tr.samples]
+            rows = self.pool.reserve(lens, PAGE, self.max_pages) if rank == tr.dst else None
+            rows = rebalancer.share_from(tr.dst, rows)
+            if rows is None:
+                continue                                   # refused: nothing moves
+            if rank == tr.src:
+                st = self.stream
+                store.push(tr.dst, self._src_rows(gids, st), self._to_dev(rows, st), self._to_dev(lens, st),
+                           stream=st)
+                store.signal(core.PEER_DONE, st)
+                by_gid = {x.gid: x for x in self.samples}
+                self._migrated = {g: (by_gid[g].bt_row.copy(), by_gid[g].length) for g in gids}   # (tests)
+                for g in gids:
+                    self.pool.free(by_gid[g].pages)        # reused only by later work on this stream
+                    sent_gids.add(g)
+                    sent += 1
+                moved += self._kv_bytes(lens)
+            rebalancer.share_from(tr.src, True)            # the source's signal is enqueued
+            if rank == tr.dst:
+                store.wait(tr.src, core.PEER_DONE, self.stream)
+                for i, c in enumerate(tr.samples):
+                    npg = self._pages_for(c.seq_len)
+                    rcv = Sample(c.gid, c.seq_len, c.remaining, None, c.steps, c.accepted)
+                    rcv.set_pages(np.asarray(rows[i, :npg]).copy(), self.max_pages)
+                    received.append(rcv)
+                    recv += 1
+                moved += self._kv_bytes(lens)
+        self.samples = [s for s in self.samples if s.gid not in sent_gids] + received
+        return sent, recv, moved
+
+    def _rebalance_two_stage_peer(self, rebalancer: Rebalancer, store: "core.PeerStore", overlap_steps=1, seed=0,
+                                  force=False):
+        """Two-stage migration (f1) over peer memory. Stage 1: the destination reserves
+        pages for the verified length plus the tokens the overlap can add, the source pushes the
+        verified prefix on a side stream and every instance keeps verifying (the source writes
+        only slots beyond the prefix in flight). Stage 2: the source shares the samples'
+        updated state, the destination extends a row that outgrew its reservation, and the
+        source pushes the tokens committed meanwhile, SSM part first (its event lets the
+        destination resume drafting), then the LLM part; the destination's stream waits
+        on the source's events."""
+        transfers = rebalancer.plan(self.load, force=force)
+        if not transfers:
+            return 0, 0, 0, {}
+        guard = overlap_steps * self.T
+        transfers = rebalancer.choose(transfers, [m for m in self.sample_meta() if m.remaining > guard])
+        rank = store.rank
+        side = torch.cuda.Stream(device=self.dev)
+        ev = lambda: torch.cuda.Event(enable_timing=True)
+        jobs = []
+        for tr in transfers:
+            if not tr.samples:
+                continue
+            gids = [c.gid for c in tr.samples]
+            len1 = [c.seq_len for c in tr.samples]
+            reserve = [l + guard for l in len1]
+            rows = self.pool.reserve(reserve, PAGE, self.max_pages) if rank == tr.dst else None
+            rows = rebalancer.share_from(tr.dst, rows)
+            if rows is None:
+                continue
+            e = [ev() for _ in range(4)]
+            if rank == tr.src:
+                side.wait_stream(self.stream)
+                e[0].record(side)
+                store.push(tr.dst, self._src_rows(gids, side), self._to_dev(rows, side), self._to_dev(len1, side),
+                           stream=side)
+                e[1].record(side)
+            jobs.append((tr, gids, len1, np.asarray(rows).copy(), [self._pages_for(r) for r in reserve], e))
+        for k in range(overlap_steps):                 # computation continues while stage 1 streams
+            self.step(seed=seed + k)
+        by_gid = {x.gid: x for x in self.samples}
+        sent = recv = moved = 0
+        sent_gids, received, timing = set(), [], {}
+        for tr, gids, len1, rows, have, e in jobs:
+            mine = None
+            if rank == tr.src:
+                mine = [(g, by_gid[g].length, by_gid[g].remaining, by_gid[g].steps, by_gid[g].accepted) for g in gids]
+            upd = rebalancer.share(tr, mine)
+            len2 = [u[1] for u in upd]
+            if rank == tr.dst:                         # extend rows that outgrew the reservation
+                need = [self._pages_for(l) for l in len2]
+                extra = sum(max(0, n - h) for n, h in zip(need, have))
+                pages = self.pool.alloc(extra) if extra else np.zeros(0, np.int32)
+                if pages is None:
+                    raise MemoryError("two-stage migration: destination pool exhausted at stage 2")
+                o = 0
+                for i, (n, h) in enumerate(zip(need, have)):
+                    if n > h:
+                        rows[i, h:n] = pages[o:o + n - h]
+                        rows[i, n:] = rows[i, n - 1]
+                        o += n - h
+                        have[i] = n
+            rows = rebalancer.share_from(tr.dst, rows if rank == tr.dst else None)
+            delta = [b - a for a, b in zip(len1, len2)]
+            if rank == tr.src:
+                side.wait_stream(self.stream)          # the overlap steps' KV writes
+                e[2].record(side)
+                sbt, dbt = self._src_rows(gids, side), self._to_dev(rows, side)
+                st_d, dl_d = self._to_dev(len1, side), self._to_dev(delta, side)
+                store.push(tr.dst, sbt, dbt, dl_d, starts=st_d, parts=core.PEER_SSM, stream=side)
+                store.signal(core.PEER_SSM_READY, side)
+                store.push(tr.dst, sbt, dbt, dl_d, starts=st_d, parts=core.PEER_LLM, stream=side)
+                store.signal(core.PEER_DONE, side)
+                e[3].record(side)
+                self.stream.wait_stream(side)          # pages are freed below: later work is ordered after
+                self._migrated = {g: (by_gid[g].bt_row.copy(), by_gid[g].length) for g in gids}   # (tests)
+                for g in gids:
+                    self.pool.free(by_gid[g].pages)
+                    sent_gids.add(g)
+                    sent += 1
+                moved += self._kv_bytes(len2)
+            rebalancer.share_from(tr.src, True)
+            if rank == tr.dst:
+                t0 = ev()
+                t1 = ev()
+                t0.record(self.stream)
+                store.wait(tr.src, core.PEER_SSM_READY, self.stream)
+                store.wait(tr.src, core.PEER_DONE, self.stream)
+                t1.record(self.stream)
+                for i, (g, length, rem, steps, acc) in enumerate(upd):
+                    rcv = Sample(g, length, rem, None, steps, acc)
+                    rcv.set_pages(rows[i, :have[i]].copy(), self.max_pages)
+                    received.append(rcv)
+                    recv += 1
+                moved += self._kv_bytes(len2)
+            if rank == tr.src:
+                side.synchronize()
+                timing = {"stage1_ms": e[0].elapsed_time(e[1]), "stage2_stall_ms": e[2].elapsed_time(e[3]),
+                          "delta_tokens": int(sum(delta))}
         self.samples = [x for x in self.samples if x.gid not in sent_gids] + received
         return sent, recv, moved, timing

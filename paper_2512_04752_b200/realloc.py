@@ -97,8 +97,12 @@ class Rebalancer:
 
     def share(self, tr: Transfer, payload):
         """Collective: the source's payload for transfer tr (any picklable object), on every rank."""
+        return self.share_from(tr.src, payload)
+
+    def share_from(self, rank: int, payload):
+        """Collective: `rank`'s payload (any picklable object), on every rank."""
         obj = [payload]
-        src_global = dist.get_global_rank(self.pg, tr.src) if self.pg is not None else tr.src
+        src_global = dist.get_global_rank(self.pg, rank) if self.pg is not None else rank
         dist.broadcast_object_list(obj, src=src_global, group=self.pg)
         return obj[0]
 

@@ -111,8 +111,9 @@ def main():
                 v = float(v.replace(",", ""))
                 return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
             traffic = mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum")
+            rcfg = name.split("_", 1)[1] if "_" in name else cfg   # prof_attn_<config>.ncu-rep
             json.dump({"dram_bytes_per_launch": int(traffic), "source": f"profiles/{tag}_ncu_{name}.md",
-                       "kernel": d["kernel"]}, open(os.path.join(prof, f"ncu_traffic_{cfg}.json"), "w"), indent=1)
+                       "kernel": d["kernel"]}, open(os.path.join(prof, f"ncu_traffic_{rcfg}.json"), "w"), indent=1)
 
 
 if __name__ == "__main__":
