@@ -66,25 +66,136 @@ STRATEGY_COST = dict(c_draft=1.0e-3, b0=2.0e-4, b1=3.0e-8, b2=1.07e-5, b3=0.0, k
                      draft_bucket=4)
 
 
-def strategy_trees(cfg, core):
-    """a0 on the host: one n for the batch (Z20) from each sample's candidate draft tree; every
-    sample's verification tree is the root plus its S(n)."""
-    from types import SimpleNamespace
-    from synth import draw_prefix_lengths, make_candidate_tree
-    P = draw_prefix_lengths(np.random.default_rng(cfg.seed), cfg)
-    rng = np.random.default_rng(cfg.seed + 77)
-    cands = [make_candidate_tree(rng, int(cfg.tree[1])) for _ in range(cfg.B)]
-    sel = core.Selector(SimpleNamespace(**STRATEGY_COST), STRATEGY_KX, STRATEGY_KY)
-    res = sel.select(cands, P, n_min=3, n_max=63, patience=2, return_selected=True)
-    n = res["n"]
-    parents = []
-    for b in range(cfg.B):
-        chosen = sorted(int(x) for x in res["selected"][b][:n])
-        idx = {c: i + 1 for i, c in enumerate(chosen)}
-        cp = cands[b][0]
-        par = [-1] + [0 if cp[c] < 0 else idx[int(cp[c])] for c in chosen]   # S(n) is connected
-        parents.append(np.array(par, np.int32))
-    return sel, cands, P, res, parents
+# Llama-3-8B: GEMM parameters a verified token passes through (all projections + FFN of 32 layers +
+# the LM head; the embedding lookup is not a GEMM) — the non-attention part of t_sd per token.
+GEMM_PARAMS_8B = 8.03e9   # 8.03e9 total - 0.525e9 embedding table + 0.525e9 LM head
+
+
+class Strategy:
+    """a0 as the method runs it on this box: an rs_ctx whose acceptance fit F comes
+    from profiling data of this workload and whose t_sd regression comes from rs_calibrate (the
+    library's own verification attention timed on a (B, P, T) grid + the dense per-token cost at
+    this box's measured GEMM rate); then one n per batch from the candidate trees."""
+
+    def __init__(self, cfg, core, dev, calibrate=True):
+        from types import SimpleNamespace
+        from synth import draw_prefix_lengths, make_candidate_tree
+        self.core, self.cfg = core, cfg
+        t0 = time.perf_counter()
+        self.ctx = core.Ctx(0, 1, cfg.page_size)
+        self.ctx.set_strategy(SimpleNamespace(**STRATEGY_COST), STRATEGY_KX, STRATEGY_KY)   # prior
+        self.info = {"prior": {"knots": [STRATEGY_KX, STRATEGY_KY], "cost": STRATEGY_COST}}
+        if calibrate:
+            self._fit_acceptance(dev)
+            self._calibrate_cost(dev)
+        self.info["seconds"] = round(time.perf_counter() - t0, 2)
+        c, kx, ky = self.ctx.strategy()
+        self.knots = (kx, ky)
+        self.info["fitted"] = {"knots_x": [round(x, 5) for x in kx], "knots_y": [round(y, 5) for y in ky],
+                               "cost": {k: (round(v, 12) if isinstance(v, float) else v) for k, v in c.items()}}
+        # the batch: prefixes and candidate trees, flattened once for the per-step host call
+        self.P = draw_prefix_lengths(np.random.default_rng(cfg.seed), cfg).astype(np.int32)
+        rng = np.random.default_rng(cfg.seed + 77)
+        self.cands = [make_candidate_tree(rng, int(cfg.tree[1])) for _ in range(cfg.B)]
+        self.flat = self._flatten(self.cands)
+        self.selected = np.full((cfg.B, 63), -1, np.int32)
+        self.res = self.select()
+        self.parents = self._trees(self.cands, self.selected, self.res["n"])
+
+    @staticmethod
+    def _flatten(cands):
+        off = np.zeros(len(cands) + 1, np.int32)
+        off[1:] = np.cumsum([len(p) for p, _ in cands])
+        return (np.concatenate([p for p, _ in cands]).astype(np.int32),
+                np.concatenate([o for _, o in cands]).astype(np.float64), off)
+
+    @staticmethod
+    def _trees(cands, selected, n):
+        """Verification trees: root + S(n) in ascending candidate index (Z21)."""
+        parents, chosen_all = [], []
+        for b in range(len(cands)):
+            chosen = sorted(int(x) for x in selected[b][:n])
+            idx = {c: i + 1 for i, c in enumerate(chosen)}
+            cp = cands[b][0]
+            parents.append(np.array([-1] + [0 if cp[c] < 0 else idx[int(cp[c])] for c in chosen], np.int32))
+            chosen_all.append(chosen)
+        return parents
+
+    def select(self, n_min=3, n_max=63):
+        par, o, off = self.flat
+        return self.ctx.select(par, o, off, self.P, n_min=n_min, n_max=n_max, patience=2, selected=self.selected)
+
+    def _fit_acceptance(self, dev, B=64, n_prof=48, seeds=8):
+        """Offline profiling data for F: a B-sample batch of this workload's recipe (own
+        seed), each verification tree = the first n_prof nodes of its candidate tree's search
+        (every depth represented), MSS acceptance on the GPU for `seeds` RNG streams; a draft node
+        is an observation (dl, accepted) with accepted = 1 iff it is on the accepted path."""
+        from dataclasses import replace
+        from synth import make_candidate_tree, make_verify_batch
+        core = self.core
+        pcfg = replace(self.cfg, B=B, L=1, seed=self.cfg.seed + 5000)
+        rng = np.random.default_rng(pcfg.seed + 77)
+        cands = [make_candidate_tree(rng, int(self.cfg.tree[1])) for _ in range(B)]
+        par, o, off = self._flatten(cands)
+        sel = np.full((B, n_prof), -1, np.int32)
+        self.ctx.select(par, o, off, np.full(B, 1024, np.int32), n_min=n_prof, n_max=n_prof, selected=sel)
+        parents = self._trees(cands, sel, n_prof)
+        dl_c = core.draft_logits(par, o, off)
+        dl_nodes = [dl_c[off[b] + np.array(sorted(int(x) for x in sel[b][:n_prof]))] for b in range(B)]
+        vb = make_verify_batch(pcfg, device=dev, gen_device=dev, parents=parents)
+        d32 = lambda x: torch.as_tensor(np.asarray(x, np.int32), device=dev)
+        args = (vb["logits"], d32(vb["parent"]), d32(vb["token"]), d32(vb["tree_off"]),
+                torch.as_tensor(vb["gid"], device=dev))
+        xs, ys = [], []
+        for s_ in range(seeds):
+            acc, path, _, _ = core.tree_accept(core.SAMPLE_MSS, *args, draft_probs=vb["draft_probs"],
+                                               temperature=self.cfg.temperature, seed=900 + s_, step=s_)
+            acc, path = acc.cpu().numpy(), path.cpu().numpy()
+            for b in range(B):
+                on = set(int(x) for x in path[b][1:acc[b] + 1])
+                xs.append(dl_nodes[b])
+                ys.append(np.array([1.0 if i + 1 in on else 0.0 for i in range(n_prof)]))
+        x, y = np.concatenate(xs), np.concatenate(ys)
+        self.ctx.fit_acceptance(x, y, 16)   # <= 16 knots (rs_tree_select)
+        self.info["acceptance_profile"] = {"observations": int(len(x)), "samples": B, "nodes_per_tree": n_prof,
+                                           "seeds": seeds, "mean_accepted": round(float(y.mean()), 4)}
+        del vb
+        torch.cuda.empty_cache()
+
+    def _calibrate_cost(self, dev, layers_distinct=8):
+        """t_sd regression on this box (rs_calibrate): dense per-token cost from the library's
+        tcgen05 GEMM (rs_lm_head_argmax) rate x the model's GEMM parameters, attention timed on
+        a (B, P, T) grid over 32 layers (8 distinct layer pools cycled: each far larger than L2)."""
+        core, cfg = self.core, self.cfg
+        rows, V, Dm = 4096, cfg.V, 4096
+        h = torch.randn(rows, Dm, device=dev).to(torch.bfloat16)
+        w = (torch.randn(V, Dm, device=dev) * 0.02).to(torch.bfloat16)
+        core.lm_head_argmax(h, w, max_logit=False)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            core.lm_head_argmax(h, w, max_logit=False)
+        e1.record()
+        torch.cuda.synchronize()
+        rate = 2.0 * rows * V * Dm * 5 / (e0.elapsed_time(e1) * 1e-3)
+        dense = 2.0 * GEMM_PARAMS_8B / rate
+        del h, w
+        grid = [(B, P, T) for B in (32, 64) for P in (1024, 2048, 4096) for T in (4, 8, 16, 24, 32, 48, 64)]
+        pages = max(B * -(-(P + T) // cfg.page_size) for B, P, T in grid)
+        kk = [torch.randn(pages, cfg.Hkv, cfg.page_size, cfg.d, device=dev).to(torch.bfloat16)
+              for _ in range(layers_distinct)]
+        vv = [torch.randn(pages, cfg.Hkv, cfg.page_size, cfg.d, device=dev).to(torch.bfloat16)
+              for _ in range(layers_distinct)]
+        self.ctx.register_kv(1, [kk[l % layers_distinct] for l in range(cfg.L)],
+                             [vv[l % layers_distinct] for l in range(cfg.L)])
+        t = self.ctx.calibrate(cfg.Hq, grid, reps=3, dense_s_per_token=dense)
+        self.ctx.register_kv(1, [], [])
+        del kk, vv
+        torch.cuda.empty_cache()
+        self.info["calibration"] = {"gemm_TFLOPs": round(rate / 1e12, 1), "dense_s_per_token": dense,
+                                    "gemm_params": GEMM_PARAMS_8B, "grid": {"B": [32, 64], "P": [1024, 2048, 4096],
+                                                                            "T": [4, 8, 16, 24, 32, 48, 64]},
+                                    "attention_ms": [round(x * 1e3, 3) for x in t]}
 
 
 def _dist():
@@ -334,6 +445,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-calibrate", action="store_true",
+                    help="c3s: keep the prior F / t_sd instead of profiling + rs_calibrate at startup")
     ap.add_argument("--realloc", default="on", choices=["on", "off"], help="c4: sample reallocation")
     ap.add_argument("--cooldown", type=int, default=32, help="c4: steps between reallocation checks (P:300)")
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
@@ -377,8 +490,8 @@ def run_ours(args, world, rank, local):
     cfg = type(cfg)(**{**cfg.__dict__, "seed": cfg.seed + 1000 * rank})   # disjoint samples per rank
     strat = None
     if cfg.tree[0] == "strategy":
-        strat = strategy_trees(cfg, core)
-        b = make_verify_batch(cfg, device=dev, gen_device=dev, parents=strat[4])
+        strat = Strategy(cfg, core, dev, calibrate=not args.no_calibrate)
+        b = make_verify_batch(cfg, device=dev, gen_device=dev, parents=strat.parents)
     else:
         b = make_verify_batch(cfg, device=dev, gen_device=dev, with_logits=lm is None, layers=n_buf)
     if n_buf is not None and n_buf < cfg.L:
@@ -426,7 +539,7 @@ def run_ours(args, world, rank, local):
             if strat is not None:
                 # a0 (host) for the next step, while the GPU runs the queued graphs
                 t0 = time.perf_counter()
-                strat[0].select(strat[1], strat[2], n_min=3, n_max=63, patience=2)
+                strat.select()
                 sel_s += time.perf_counter() - t0
             g_mask.replay()
             ev[k][0].record(stream)
@@ -510,16 +623,16 @@ def run_ours(args, world, rank, local):
 
     # ---------------- f3: GPU verification-tree construction (timed alone, outside the step) ----------------
     if strat is not None:
-        sel_n = strat[3]["n"]
-        cands = strat[1]
+        sel_n = strat.res["n"]
+        cands = strat.cands
         cpar = torch.as_tensor(np.concatenate([p for p, _ in cands]), dtype=torch.int32, device=dev)
         co = torch.as_tensor(np.concatenate([o for _, o in cands]), dtype=torch.float64, device=dev)
         ctok = torch.randint(0, cfg.V, (cpar.numel(),), dtype=torch.int32, device=dev)
         coff = torch.as_tensor(np.concatenate([[0], np.cumsum([len(p) for p, _ in cands])]), dtype=torch.int32,
                                device=dev)
         rtok = torch.zeros(cfg.B, dtype=torch.int32, device=dev)
-        kx = torch.tensor(STRATEGY_KX, dtype=torch.float64, device=dev)
-        ky = torch.tensor(STRATEGY_KY, dtype=torch.float64, device=dev)
+        kx = torch.tensor(strat.knots[0], dtype=torch.float64, device=dev)
+        ky = torch.tensor(strat.knots[1], dtype=torch.float64, device=dev)
         ts_out = core.tree_select(cpar, co, ctok, coff, rtok, sel_n, kx, ky)
         g_ts = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g_ts):
@@ -557,11 +670,12 @@ def run_ours(args, world, rank, local):
                    "attn_plan": info,
                    **({"lm_head": {"hidden": lm[1], "fused_argmax": True, "weight_GB": round(cfg.V * lm[1] * 2 / 1e9, 2)}}
                       if lm is not None else {}),
-                   **({"select_strategy": {"n": strat[3]["n"], "T": strat[3]["n"] + 1, "depth": strat[3]["depth"],
-                                           "width": strat[3]["width"], "pred_al": round(strat[3]["al"], 2),
-                                           "pred_t_sd_ms": round(strat[3]["t_sd"] * 1e3, 3),
+                   **({"select_strategy": {"n": strat.res["n"], "T": strat.res["n"] + 1, "depth": strat.res["depth"],
+                                           "width": strat.res["width"], "pred_al": round(strat.res["al"], 2),
+                                           "pred_t_sd_ms": round(strat.res["t_sd"] * 1e3, 3),
                                            "host_ms_per_call": round(sel_s / args.steps * 1e3, 4),
-                                           "in_timed_loop": True}} if strat is not None else {})},
+                                           "in_timed_loop": True, "strategy_state": strat.info}}
+                      if strat is not None else {})},
         "clocks": sampler.summary(),
         "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
@@ -569,7 +683,7 @@ def run_ours(args, world, rank, local):
         "kernels": kernels,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = run_cpu_baseline(cfg, b, parents=None if strat is None else strat[4])
+        line["cpu_baseline"] = run_cpu_baseline(cfg, b, parents=None if strat is None else strat.parents)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -586,6 +700,35 @@ def c4_samples(world, rank, per_rank=256, seed=4):
     prompt = np.clip(np.rint(rng.lognormal(math.log(256.0), 0.784, size=n)), 32, 2048).astype(np.int32)
     resp = lmsys_response_lengths(rng, n)
     return [(g, int(prompt[g]), int(resp[g])) for g in range(n) if g % world == rank]
+
+
+def raw_p2p_gbps(world, rank, dev, nbytes=1 << 30):
+    """Reference for the migration bandwidth: a raw 1 GiB NCCL send 0 -> 1 on its own NCCL group,
+    device-timed on the receiver. Only when ranks own distinct GPUs (NCCL refuses two ranks on
+    one device); otherwise None with the reason."""
+    import torch.distributed as dist
+    if world < 2:
+        return None
+    if torch.cuda.device_count() < world:
+        return {"GBps": None, "why": f"{world} ranks share {torch.cuda.device_count()} GPU(s): no NVLink pair to measure"}
+    g = dist.new_group(backend="nccl")
+    buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    ms = []
+    for it in range(4):
+        dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        if rank == 0:
+            dist.send(buf, 1, group=g)
+        elif rank == 1:
+            dist.recv(buf, 0, group=g)
+        b.record()
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    t = _allreduce(min(ms[1:]) if rank == 1 else 0.0, "max")
+    del buf
+    return {"GBps": round(nbytes / t / 1e6, 1), "bytes": nbytes, "what": "NCCL send/recv rank 0 -> 1, min of 3"}
 
 
 def run_c4(args, world, rank, local):
@@ -638,7 +781,8 @@ def run_c4(args, world, rank, local):
         comm = core.Comm(rank, world) if realloc else None
         staging = torch.empty(4 << 30, dtype=torch.uint8, device=dev) if realloc else None
         scratch = torch.empty(3 * 512 + 512 * 72, dtype=torch.int32, device=dev) if realloc else None
-    stalls = []
+    stalls, pushes = [], []
+    raw = raw_p2p_gbps(world, rank, dev) if realloc else None
 
     def one_step(k, timing=False):
         mig = (0, 0, 0, 0.0)
@@ -651,7 +795,10 @@ def run_c4(args, world, rank, local):
                 if tm:
                     stalls.append(tm["stage2_stall_ms"])
             else:
+                inst.last_push = None
                 sent, recv, moved = inst.rebalance(reb, comm, staging, scratch)
+                if inst.last_push:
+                    pushes.append(inst.last_push)
             mig = (sent, recv, moved, time.perf_counter() - t0)
         inst.step(seed=11, timing=timing)
         return inst.tokens - tok0, mig
@@ -719,6 +866,13 @@ def run_c4(args, world, rank, local):
         "migration": {"events": len(migrations), "samples_moved_rank0": sum(m[0] + m[1] for m in migrations),
                       "bytes_rank0": int(mig_bytes), "seconds_rank0": round(mig_s, 4),
                       "GBps_rank0": round(mig_bytes / mig_s / 1e9, 2) if mig_s > 0 else None,
+                      "note": "GBps_rank0 = KV bytes / host time of the whole reallocation (plan, "
+                              "handshake, transfer) on rank 0",
+                      "push_kernel": ({"bytes": int(sum(p[0] for p in pushes)),
+                                       "ms": round(sum(p[1] for p in pushes), 3),
+                                       "GBps": round(sum(p[0] for p in pushes) / sum(p[1] for p in pushes) / 1e6, 1)}
+                                      if pushes and sum(p[1] for p in pushes) > 0 else None),
+                      "raw_p2p_reference": raw,
                       **({"two_stage_stall_ms_rank0": [round(x, 3) for x in stalls]} if stalls else {})},
     }
     if rank == 0:

@@ -285,9 +285,79 @@ rs_status rs_select_strategy(rs_selector* sel, const int32_t* cand_parent, const
                              const int32_t* cand_off, const int32_t* prefix_len, int32_t B,
                              int32_t n_min, int32_t n_max, int32_t patience, rs_strategy* out,
                              int32_t* selected);
+/* dl(u) = o(u) * dl(parent(u)) of every candidate (Z9), host arrays as rs_select_strategy. */
+rs_status rs_draft_logits(const int32_t* cand_parent, const double* cand_o, const int32_t* cand_off,
+                          int32_t B, double* dl_out);
+/* The acceptance fit F from observations ("fit a function ... between draft logits and token
+ * acceptance probability based on offline profiling data"; reading Z24): dl, accepted
+ * host double [n] (accepted in [0,1]: 0/1 outcomes or rates); n_buckets equal-width buckets of dl
+ * over [0,1] (dl clipped); per non-empty bucket the mean dl and mean acceptance weighted by its
+ * count; a weighted pool-adjacent-violators pass makes the rates non-decreasing. Writes
+ * *n_knots <= n_buckets knots (x strictly increasing, y non-decreasing) into knots_x/knots_y
+ * (capacity n_buckets). RS_ERR_INVALID_ARG ("InsufficientData") with < 2 distinct dl values. */
+rs_status rs_acceptance_fit(const double* dl, const double* accepted, int64_t n, int32_t n_buckets,
+                            double* knots_x, double* knots_y, int32_t* n_knots);
 /* Least-squares fit of the cost model's b0..b3 (c_draft kept) to measured step times. */
 rs_status rs_cost_model_fit(const double* n_seq, const double* n_draft, const double* t_sec,
                             int32_t n, rs_cost_model* inout);
+
+/* ===================================================================================== ctx
+ * rs_ctx — one generation instance (one process per GPU): non-owning registrations of its KV
+ * pools (model 0 = SSM, 1 = LLM; [num_pages, Hkv, page_size, head_dim] bf16 per layer, kept until
+ * rs_ctx_destroy) and its drafting-strategy state: the acceptance fit F and the t_sd cost model,
+ * with the selector built from them (rs_ctx_selector; pass it to rs_select_strategy). Not
+ * thread-safe; distinct ctxs are independent. */
+typedef struct { int32_t rank, world, page_size; } rs_ctx_desc;
+typedef struct rs_ctx rs_ctx;
+rs_status rs_ctx_create(const rs_ctx_desc* desc, rs_ctx** out);
+rs_status rs_ctx_destroy(rs_ctx* ctx);
+rs_status rs_ctx_register_kv(rs_ctx* ctx, int32_t model, int32_t L, void* const* k_layers,
+                             void* const* v_layers, int32_t num_pages, int32_t Hkv, int32_t head_dim);
+/* Set the cost model (cost may be NULL: kept) and/or F's knots (knots NULL: kept); rebuilds the
+ * selector (empty bucket cache). Invalid knots -> RS_ERR_INVALID_ARG and nothing changes. */
+rs_status rs_ctx_set_strategy(rs_ctx* ctx, const rs_cost_model* cost, const double* knots_x,
+                              const double* knots_y, int32_t n_knots);
+/* *n_knots: in = capacity of knots_x/knots_y (may be NULL), out = number of knots. */
+rs_status rs_ctx_get_strategy(const rs_ctx* ctx, rs_cost_model* cost, double* knots_x, double* knots_y,
+                              int32_t* n_knots);
+/* The ctx's selector (borrowed; NULL until F is set). Invalidated by the next set/fit/calibrate. */
+rs_selector* rs_ctx_selector(rs_ctx* ctx);
+/* Refit F from (dl, accepted) observations (rs_acceptance_fit) — offline profiling data, or the
+ * online data P:192 collects to update the function. */
+rs_status rs_ctx_fit_acceptance(rs_ctx* ctx, const double* dl, const double* accepted, int64_t n,
+                                int32_t n_buckets);
+
+/* rs_calibrate — the offline profiling of the t_sd regression on THIS box:
+ * for every grid point (B[i], P[i], T[i]) a synthetic batch (every sample prefix P, a chain tree
+ * of T nodes, consecutive pages of the registered LLM pools) runs the tree-mask build and the
+ * verification attention of every registered LLM layer (the library's kernels, `reps` timed
+ * repetitions after one warm-up, median, CUDA events on `stream`); the point's step time is
+ *   c_draft + t_attention + dense_s_per_token * B*T
+ * (dense_s_per_token: the verification FFN / projections per verified token, outside this
+ * library — measure them, e.g. with rs_lm_head_argmax's GEMM rate, and pass them in), and
+ * rs_cost_model_fit fits b0..b3 with N_seq = B*P, N_draft = B*T (c_draft, k_sat and the buckets
+ * of the ctx's current cost model are kept). The ctx's selector is rebuilt with the fit. Reads
+ * the registered pools, writes only the caller's q/out scratch and workspace.
+ *   q, out   device bf16 scratch >= max_i B*T*Hq*head_dim elements each (qo_elems)
+ *   ws       device, >= rs_calibrate_workspace_bytes(ctx, desc), 256-byte aligned
+ *   t_attn_out host double [n_points] (measured attention + mask seconds per point) or NULL */
+typedef struct {
+    int32_t Hq;
+    int32_t n_points;
+    const int32_t* B;
+    const int32_t* P;
+    const int32_t* T;
+    int32_t reps;
+    void* q;
+    void* out;
+    size_t qo_elems;
+    void* ws;
+    size_t ws_bytes;
+    double dense_s_per_token;
+    void* stream;
+} rs_calib_desc;
+size_t rs_calibrate_workspace_bytes(const rs_ctx* ctx, const rs_calib_desc* desc);
+rs_status rs_calibrate(rs_ctx* ctx, const rs_calib_desc* desc, double* t_attn_out);
 
 /* ===================================================================================== a6
  * Sample reallocation policy. Host only. */

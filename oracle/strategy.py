@@ -58,6 +58,53 @@ def layer_search_order(parent, weights, n_max):
     return order
 
 
+def fit_acceptance(dl, accepted, n_buckets=20):
+    """F from (dl, accepted) observations ("we fit a function (i.e., F: X->Y) between draft
+    logits and token acceptance probability based on offline profiling data"; SPEC S:128-131:
+    "monotone piecewise-linear F minimizing squared error over bucketed empirical acceptance
+    rates; isotonic-regression pass enforces monotonicity"). Reading Z24, step by step:
+      1. bucket k = min(K-1, floor(dl*K)) over [0, 1] (dl clipped to [0, 1]), K = n_buckets;
+      2. per non-empty bucket: x_k = mean dl, r_k = mean accepted, weight n_k = count
+         (sums accumulated in observation order);
+      3. pool-adjacent-violators over the buckets in ascending k with weights n_k (the
+         weighted least-squares non-decreasing fit of r_k): a new block is appended, then while
+         the previous block's value exceeds the last one's they merge into one block with value
+         (sum of n*y) / (sum of n);
+      4. knots (x_k, y_k), y_k = value of k's block; F interpolates them, constant outside.
+    Returns (knots_x, knots_y). Raises ValueError("InsufficientData") with < 2 distinct dl."""
+    dl = np.asarray(dl, dtype=np.float64)
+    acc = np.asarray(accepted, dtype=np.float64)
+    if len(dl) != len(acc) or len(np.unique(dl)) < 2:
+        raise ValueError("InsufficientData")
+    K = int(n_buckets)
+    sx, sy, cnt = [0.0] * K, [0.0] * K, [0] * K
+    for x, a in zip(dl, acc):
+        xc = min(max(x, 0.0), 1.0)
+        k = min(K - 1, int(np.floor(xc * K)))
+        sx[k] += xc
+        sy[k] += a
+        cnt[k] += 1
+    xs, rs, ws = [], [], []
+    for k in range(K):
+        if cnt[k]:
+            xs.append(sx[k] / cnt[k])
+            rs.append(sy[k] / cnt[k])
+            ws.append(float(cnt[k]))
+    # pool adjacent violators: blocks of (sum n*y, sum n, number of buckets)
+    blocks = []
+    for r, w in zip(rs, ws):
+        blocks.append([r * w, w, 1])
+        while len(blocks) > 1 and blocks[-2][0] / blocks[-2][1] > blocks[-1][0] / blocks[-1][1]:
+            a = blocks.pop()
+            blocks[-1][0] += a[0]
+            blocks[-1][1] += a[1]
+            blocks[-1][2] += a[2]
+    ys = []
+    for sy_, sw, m in blocks:
+        ys.extend([sy_ / sw] * m)
+    return np.array(xs), np.array(ys)
+
+
 class CostModel:
     """t_sd = c_draft + b0 + b1*N_seq + b2*N_draft + b3*relu(N_draft - k_sat)*N_draft (S:174),
     evaluated at the lower corner of its (N_seq, N_draft) bucket (reading Z12)."""

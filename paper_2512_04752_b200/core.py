@@ -341,6 +341,15 @@ class Selector:
             res["selected"] = sel[:B]
         return res
 
+    def select_flat(self, parent, o, off, prefix_len, n_min=2, n_max=48, patience=2, selected=None):
+        """The same call on pre-flattened host arrays (int32 parent [N], float64 o [N], int32 off
+        [B+1], int32 prefix_len [B]); `selected` (int32 [B, n_max]) is filled when given."""
+        B = len(off) - 1
+        out = StrategyC()
+        _check(_lib.rs_select_strategy(self._h, _ptr(parent), _ptr(o), _ptr(off), _ptr(prefix_len), B, n_min, n_max,
+                                       patience, ctypes.byref(out), _ptr(selected)), "rs_select_strategy")
+        return {k: getattr(out, k) for k, _ in StrategyC._fields_}
+
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:
             _lib.rs_selector_destroy(self._h)
@@ -360,6 +369,31 @@ def cost_model_fit(n_seq, n_draft, t_sec, cost):
 _sig("rs_knee_threshold", _i32, _P, _P, _i32, _f64, ctypes.POINTER(_i32))
 _sig("rs_plan_reallocation", _i32, _P, _i32, _i32, _P, _P, _P, ctypes.POINTER(_i32))
 _sig("rs_choose_samples", _i32, _P, _P, _P, _i32, _i32, _P)
+
+
+_sig("rs_acceptance_fit", _i32, _P, _P, _i64, _i32, _P, _P, ctypes.POINTER(_i32))
+
+
+_sig("rs_draft_logits", _i32, _P, _P, _P, _i32, _P)
+
+
+def draft_logits(parent, o, off):
+    """dl of every candidate (flat host arrays as Selector.select_flat)."""
+    dl = np.zeros(len(parent))
+    _check(_lib.rs_draft_logits(_ptr(np.ascontiguousarray(parent, np.int32)), _ptr(np.ascontiguousarray(o, np.float64)),
+                                _ptr(np.ascontiguousarray(off, np.int32)), len(off) - 1, _ptr(dl)), "rs_draft_logits")
+    return dl
+
+
+def acceptance_fit(dl, accepted, n_buckets=20):
+    """F's knots from (dl, accepted) observations (rs_acceptance_fit). Returns (knots_x, knots_y)."""
+    x = np.ascontiguousarray(dl, dtype=np.float64)
+    y = np.ascontiguousarray(accepted, dtype=np.float64)
+    kx, ky = np.zeros(n_buckets), np.zeros(n_buckets)
+    m = _i32()
+    _check(_lib.rs_acceptance_fit(_ptr(x), _ptr(y), len(x), int(n_buckets), _ptr(kx), _ptr(ky), ctypes.byref(m)),
+           "rs_acceptance_fit")
+    return kx[:m.value].copy(), ky[:m.value].copy()
 
 
 def knee_threshold(counts, tput, frac=0.1) -> int:
@@ -743,3 +777,107 @@ def peer_connect(store: PeerStore, pg=None):
     for b in blobs:
         store.import_(b)
     return store
+
+
+# ------------------------------------------------------------------ rs_ctx / rs_calibrate
+class CtxDescC(ctypes.Structure):
+    _fields_ = [("rank", _i32), ("world", _i32), ("page_size", _i32)]
+
+
+class CalibDescC(ctypes.Structure):
+    _fields_ = [("Hq", _i32), ("n_points", _i32), ("B", _P), ("P", _P), ("T", _P), ("reps", _i32), ("q", _P),
+                ("out", _P), ("qo_elems", _sz), ("ws", _P), ("ws_bytes", _sz), ("dense_s_per_token", _f64),
+                ("stream", _P)]
+
+
+_sig("rs_ctx_create", _i32, ctypes.POINTER(CtxDescC), ctypes.POINTER(_P))
+_sig("rs_ctx_destroy", _i32, _P)
+_sig("rs_ctx_register_kv", _i32, _P, _i32, _i32, _P, _P, _i32, _i32, _i32)
+_sig("rs_ctx_set_strategy", _i32, _P, ctypes.POINTER(CostModelC), _P, _P, _i32)
+_sig("rs_ctx_get_strategy", _i32, _P, ctypes.POINTER(CostModelC), _P, _P, ctypes.POINTER(_i32))
+_sig("rs_ctx_selector", _P, _P)
+_sig("rs_ctx_fit_acceptance", _i32, _P, _P, _P, _i64, _i32)
+_sig("rs_calibrate_workspace_bytes", _sz, _P, ctypes.POINTER(CalibDescC))
+_sig("rs_calibrate", _i32, _P, ctypes.POINTER(CalibDescC), _P)
+
+
+class Ctx:
+    """One instance's rs_ctx: KV registrations + the strategy state (F, t_sd) and its selector."""
+
+    def __init__(self, rank=0, world=1, page_size=64):
+        self._h = _P()
+        _check(_lib.rs_ctx_create(ctypes.byref(CtxDescC(rank, world, page_size)), ctypes.byref(self._h)),
+               "rs_ctx_create")
+        self._keep = []
+
+    def register_kv(self, model, k_layers, v_layers):
+        if not k_layers:   # unregister
+            _check(_lib.rs_ctx_register_kv(self._h, int(model), 0, None, None, 0, 1, 1), "rs_ctx_register_kv")
+            return
+        kp, vp = _layer_ptrs(k_layers), _layer_ptrs(v_layers)
+        self._keep += [kp, vp, list(k_layers), list(v_layers)]
+        num_pages, Hkv, _, d = k_layers[0].shape
+        _check(_lib.rs_ctx_register_kv(self._h, int(model), len(k_layers), kp, vp, int(num_pages), int(Hkv), int(d)),
+               "rs_ctx_register_kv")
+
+    def set_strategy(self, cost=None, knots_x=None, knots_y=None):
+        c = _cost_c(cost) if cost is not None else None
+        kx = None if knots_x is None else np.ascontiguousarray(knots_x, dtype=np.float64)
+        ky = None if knots_y is None else np.ascontiguousarray(knots_y, dtype=np.float64)
+        _check(_lib.rs_ctx_set_strategy(self._h, ctypes.byref(c) if c is not None else None, _ptr(kx), _ptr(ky),
+                                        0 if kx is None else len(kx)), "rs_ctx_set_strategy")
+
+    def strategy(self):
+        """(cost model dict, knots_x, knots_y) currently in the ctx."""
+        c = CostModelC()
+        m = _i32(64)
+        kx, ky = np.zeros(64), np.zeros(64)
+        _check(_lib.rs_ctx_get_strategy(self._h, ctypes.byref(c), _ptr(kx), _ptr(ky), ctypes.byref(m)),
+               "rs_ctx_get_strategy")
+        return {k: getattr(c, k) for k, _ in CostModelC._fields_}, kx[:m.value].copy(), ky[:m.value].copy()
+
+    def fit_acceptance(self, dl, accepted, n_buckets=20):
+        x = np.ascontiguousarray(dl, dtype=np.float64)
+        y = np.ascontiguousarray(accepted, dtype=np.float64)
+        _check(_lib.rs_ctx_fit_acceptance(self._h, _ptr(x), _ptr(y), len(x), int(n_buckets)),
+               "rs_ctx_fit_acceptance")
+
+    def calibrate(self, Hq, grid, reps=3, dense_s_per_token=0.0, stream=None):
+        """grid: list of (B, P, T). Returns the measured attention seconds per point; the ctx's cost
+        model is refitted (see rs_calibrate)."""
+        g = np.ascontiguousarray(np.asarray(grid, dtype=np.int32).T)
+        Bs, Ps, Ts = (np.ascontiguousarray(g[i]) for i in range(3))
+        d = self._keep[-2][0].shape[3]
+        elems = int(max(b * t for b, _, t in grid) * Hq * d)
+        dev = self._keep[-2][0].device
+        q = torch.randn(elems, device=dev).to(torch.bfloat16)
+        out = torch.empty(elems, dtype=torch.bfloat16, device=dev)
+        desc = CalibDescC(int(Hq), len(grid), _ptr(Bs), _ptr(Ps), _ptr(Ts), int(reps), _ptr(q), _ptr(out), elems,
+                          None, 0, float(dense_s_per_token), _stream(stream))
+        need = int(_lib.rs_calibrate_workspace_bytes(self._h, ctypes.byref(desc)))
+        if need == 0:
+            raise RSError(8, "rs_calibrate_workspace_bytes: " + _lib.rs_last_error().decode())
+        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+        desc.ws, desc.ws_bytes = _ptr(ws), need
+        t = np.zeros(len(grid))
+        _check(_lib.rs_calibrate(self._h, ctypes.byref(desc), _ptr(t)), "rs_calibrate")
+        return t
+
+    def select(self, parent, o, off, prefix_len, n_min=2, n_max=48, patience=2, selected=None):
+        """rs_select_strategy with the ctx's selector (flat host arrays, see Selector.select_flat)."""
+        h = _lib.rs_ctx_selector(self._h)
+        if not h:
+            raise RSError(1, "rs_ctx: no acceptance fit set")
+        B = len(off) - 1
+        out = StrategyC()
+        _check(_lib.rs_select_strategy(h, _ptr(parent), _ptr(o), _ptr(off), _ptr(prefix_len), B, n_min, n_max,
+                                       patience, ctypes.byref(out), _ptr(selected)), "rs_select_strategy")
+        return {k: getattr(out, k) for k, _ in StrategyC._fields_}
+
+    def destroy(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.rs_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.destroy()

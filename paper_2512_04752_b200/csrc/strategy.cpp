@@ -6,6 +6,7 @@
 //   layer-level search with a max priority queue, S(n) = S(n-1) U {u_max}
 //   objective al/t_sd (Eq. 2), early stop after `patience` consecutive decreases (Eq. 3)
 // and rs_cost_model_fit: least squares of the regression coefficients to measured times.
+#include <algorithm>
 #include <cmath>
 #include <queue>
 #include <unordered_map>
@@ -88,6 +89,16 @@ extern "C" rs_status rs_selector_create(const rs_cost_model* cost, const double*
 
 extern "C" void rs_selector_destroy(rs_selector* sel) { delete sel; }
 
+namespace {
+// Reused per-thread buffers of the selector (no allocation per call once warm).
+struct SelScratch {
+    std::vector<double> dl, w, ow;   // per candidate: dl, w; per (sample, step): w of the popped node
+    std::vector<int> dep, cnt, byd, ord, odep, olen;
+    std::vector<PQItem> heap;
+};
+thread_local SelScratch tls;
+}  // namespace
+
 extern "C" rs_status rs_select_strategy(rs_selector* sel, const int32_t* cand_parent, const double* cand_o,
                                         const int32_t* cand_off, const int32_t* prefix_len, int32_t B, int32_t n_min,
                                         int32_t n_max, int32_t patience, rs_strategy* out, int32_t* selected) {
@@ -95,39 +106,61 @@ extern "C" rs_status rs_select_strategy(rs_selector* sel, const int32_t* cand_pa
     RS_REQUIRE(n_min >= 1 && n_max >= n_min && patience >= 1, RS_ERR_INVALID_ARG,
                "rs_select_strategy: need 1 <= n_min <= n_max, patience >= 1");
     RS_REQUIRE(B >= 1, RS_ERR_EMPTY_TREE, "rs_select_strategy: empty batch");
-    std::vector<std::vector<int>> orders(B);
-    std::vector<std::vector<double>> weights(B);
-    std::vector<std::vector<int>> depths(B);
+    SelScratch& S = tls;
+    S.ord.assign((size_t)B * n_max, -1);   // per sample: the popped candidates in order (S(n) = first n)
+    S.ow.resize((size_t)B * n_max);
+    S.odep.resize((size_t)B * n_max);
+    S.olen.assign(B, 0);
     int feasible = n_max;
     for (int b = 0; b < B; ++b) {
         const int o0 = cand_off[b], N = cand_off[b + 1] - cand_off[b];
+        RS_REQUIRE(N >= 0, RS_ERR_INVALID_ARG, "rs_select_strategy: cand_off not non-decreasing at %d", b);
+        S.dl.resize(N);
+        S.dep.resize(N);
+        S.w.resize(N);
         bool has_root_child = false;
-        std::vector<double> dl(N);
-        std::vector<int> dep(N);
+        int max_dep = 0;
         for (int i = 0; i < N; ++i) {
             const int pa = cand_parent[o0 + i];
             RS_REQUIRE(pa < i, RS_ERR_MALFORMED_TREE, "rs_select_strategy: sample %d node %d parent %d", b, i, pa);
-            dl[i] = cand_o[o0 + i] * (pa < 0 ? 1.0 : dl[pa]);
-            dep[i] = pa < 0 ? 0 : dep[pa] + 1;
+            S.dl[i] = cand_o[o0 + i] * (pa < 0 ? 1.0 : S.dl[pa]);
+            S.dep[i] = pa < 0 ? 0 : S.dep[pa] + 1;
+            max_dep = std::max(max_dep, S.dep[i]);
             has_root_child |= pa < 0;
         }
         RS_REQUIRE(N > 0 && has_root_child, RS_ERR_EMPTY_TREE, "rs_select_strategy: sample %d has no candidates", b);
-        std::vector<double> w(N);
-        for (int i = 0; i < N; ++i) w[i] = acceptance_fit(sel, dl[i]);
-        // layer-level search: at step m push layer m (depth m-1), pop u_max
-        std::priority_queue<PQItem> pq;
-        std::vector<int> order;
+        for (int i = 0; i < N; ++i) S.w[i] = acceptance_fit(sel, S.dl[i]);
+        // nodes grouped by depth (ascending id inside a layer): layer m is one contiguous range
+        S.cnt.assign(max_dep + 2, 0);
+        for (int i = 0; i < N; ++i) ++S.cnt[S.dep[i] + 1];
+        for (int d = 0; d <= max_dep; ++d) S.cnt[d + 1] += S.cnt[d];
+        S.byd.resize(N);
+        for (int i = 0; i < N; ++i) S.byd[S.cnt[S.dep[i]]++] = i;   // cnt[d] ends at the start of d + 1
+        // layer-level search (P:227): at step m push layer m (depth m-1), pop u_max
+        S.heap.clear();
+        int* ord = S.ord.data() + (size_t)b * n_max;
+        int len = 0, lo = 0;
         for (int m = 1; m <= n_max; ++m) {
-            for (int i = 0; i < N; ++i)
-                if (dep[i] == m - 1) pq.push({w[i], dep[i], i});
-            if (pq.empty()) break;
-            order.push_back(pq.top().id);
-            pq.pop();
+            if (m - 1 <= max_dep) {
+                const int hi = S.cnt[m - 1];
+                for (int k = lo; k < hi; ++k) {
+                    const int i = S.byd[k];
+                    S.heap.push_back({S.w[i], S.dep[i], i});
+                    std::push_heap(S.heap.begin(), S.heap.end());
+                }
+                lo = hi;
+            }
+            if (S.heap.empty()) break;
+            std::pop_heap(S.heap.begin(), S.heap.end());
+            const PQItem top = S.heap.back();
+            S.heap.pop_back();
+            ord[len] = top.id;
+            S.ow[(size_t)b * n_max + len] = top.w;
+            S.odep[(size_t)b * n_max + len] = top.depth;
+            ++len;
         }
-        feasible = std::min<int>(feasible, (int)order.size());
-        orders[b] = std::move(order);
-        weights[b] = std::move(w);
-        depths[b] = std::move(dep);
+        S.olen[b] = len;
+        feasible = std::min<int>(feasible, len);
     }
     RS_REQUIRE(feasible >= n_min, RS_ERR_INSUFFICIENT_NODES,
                "rs_select_strategy: only %d candidate steps (n_min %d)", feasible, n_min);
@@ -140,7 +173,7 @@ extern "C" rs_status rs_select_strategy(rs_selector* sel, const int32_t* cand_pa
     bool have_prev = false;
     for (int n = 1; n <= feasible; ++n) {
         double add = 0.0;
-        for (int b = 0; b < B; ++b) add += weights[b][orders[b][n - 1]];
+        for (int b = 0; b < B; ++b) add += S.ow[(size_t)b * n_max + n - 1];
         al += add;
         bool hit = false;
         const double t = t_sd(sel, n_seq, (long long)B * (n + 1), &hit);
@@ -161,19 +194,16 @@ extern "C" rs_status rs_select_strategy(rs_selector* sel, const int32_t* cand_pa
         if (dec >= patience) break;
     }
     int depth = 0, width = 0;
+    int per_layer[RS_MAX_TREE + 2];
     for (int b = 0; b < B; ++b) {
-        std::vector<int> per_layer(RS_MAX_TREE + 1, 0);
+        std::fill(per_layer, per_layer + RS_MAX_TREE + 2, 0);
         for (int k = 0; k < best_n; ++k) {
-            const int d = depths[b][orders[b][k]] + 1;   // verification-tree depth (root = 0)
+            const int d = S.odep[(size_t)b * n_max + k] + 1;   // verification-tree depth (root = 0)
             depth = std::max(depth, d);
             if (d <= RS_MAX_TREE) width = std::max(width, ++per_layer[d]);
         }
     }
-    if (selected) {
-        for (int b = 0; b < B; ++b)
-            for (int k = 0; k < n_max; ++k)
-                selected[(int64_t)b * n_max + k] = k < (int)orders[b].size() ? orders[b][k] : -1;
-    }
+    if (selected) std::copy(S.ord.begin(), S.ord.end(), selected);
     out->n = best_n;
     out->depth = depth;
     out->width = width;
@@ -183,6 +213,67 @@ extern "C" rs_status rs_select_strategy(rs_selector* sel, const int32_t* cand_pa
     out->al = best_al;
     out->t_sd = best_t;
     out->objective = best_obj;
+    return RS_OK;
+}
+
+// dl(u) = o(u) * dl(parent(u)) (reading Z9: the product includes u), per candidate.
+extern "C" rs_status rs_draft_logits(const int32_t* cand_parent, const double* cand_o, const int32_t* cand_off,
+                                     int32_t B, double* dl_out) {
+    RS_REQUIRE(cand_parent && cand_o && cand_off && dl_out && B >= 0, RS_ERR_INVALID_ARG, "rs_draft_logits: bad args");
+    for (int b = 0; b < B; ++b) {
+        const int o0 = cand_off[b], N = cand_off[b + 1] - o0;
+        for (int i = 0; i < N; ++i) {
+            const int pa = cand_parent[o0 + i];
+            RS_REQUIRE(pa < i, RS_ERR_MALFORMED_TREE, "rs_draft_logits: sample %d node %d parent %d", b, i, pa);
+            dl_out[o0 + i] = cand_o[o0 + i] * (pa < 0 ? 1.0 : dl_out[o0 + pa]);
+        }
+    }
+    return RS_OK;
+}
+
+// F from (dl, accepted) observations (reading Z24): K equal-width
+// buckets of dl over [0, 1] -> per non-empty bucket the mean dl and the mean acceptance (weight =
+// count) -> weighted pool-adjacent-violators (non-decreasing least squares) -> knots.
+extern "C" rs_status rs_acceptance_fit(const double* dl, const double* accepted, int64_t n, int32_t n_buckets,
+                                       double* knots_x, double* knots_y, int32_t* n_knots) {
+    RS_REQUIRE(dl && accepted && knots_x && knots_y && n_knots && n >= 0 && n_buckets >= 1, RS_ERR_INVALID_ARG,
+               "rs_acceptance_fit: bad args");
+    bool two = false;
+    for (int64_t i = 1; i < n && !two; ++i) two = dl[i] != dl[0];
+    RS_REQUIRE(two, RS_ERR_INVALID_ARG, "rs_acceptance_fit: InsufficientData (< 2 distinct draft logits)");
+    const int K = n_buckets;
+    std::vector<double> sx(K, 0.0), sy(K, 0.0);
+    std::vector<long long> cnt(K, 0);
+    for (int64_t i = 0; i < n; ++i) {
+        const double x = dl[i] < 0.0 ? 0.0 : (dl[i] > 1.0 ? 1.0 : dl[i]);
+        int k = (int)std::floor(x * K);
+        if (k > K - 1) k = K - 1;
+        sx[k] += x;
+        sy[k] += accepted[i];
+        ++cnt[k];
+    }
+    // blocks of the PAV pass: (sum of n*y, sum of n, first knot index)
+    struct Blk { double sy, sw; int first; };
+    std::vector<Blk> st;
+    int m = 0;
+    for (int k = 0; k < K; ++k) {
+        if (!cnt[k]) continue;
+        const double w = (double)cnt[k], r = sy[k] / w;
+        knots_x[m] = sx[k] / w;
+        st.push_back({r * w, w, m});
+        ++m;
+        while (st.size() > 1 && st[st.size() - 2].sy / st[st.size() - 2].sw > st.back().sy / st.back().sw) {
+            const Blk a = st.back();
+            st.pop_back();
+            st.back().sy += a.sy;
+            st.back().sw += a.sw;
+        }
+    }
+    for (size_t j = 0; j < st.size(); ++j) {
+        const int e = j + 1 < st.size() ? st[j + 1].first : m;
+        for (int i = st[j].first; i < e; ++i) knots_y[i] = st[j].sy / st[j].sw;
+    }
+    *n_knots = m;
     return RS_OK;
 }
 

@@ -120,6 +120,7 @@ class GenerationInstance:
         self.last_attn_ms = 0.0
         self.step_no = 0
         self.tokens = 0            # committed tokens (sum of a_b + 1)
+        self.last_push = None      # (bytes, device ms) of the last peer-memory push this rank sourced
         self.finished = 0
 
     @staticmethod
@@ -467,7 +468,7 @@ class GenerationInstance:
         transfers = rebalancer.choose(transfers, self.sample_meta())
         rank = store.rank
         sent = recv = moved = 0
-        sent_gids, received = set(), []
+        sent_gids, received, pushes = set(), [], []
         for tr in transfers:
             if not tr.samples:
                 continue
@@ -479,8 +480,12 @@ class GenerationInstance:
                 continue                                   # refused: nothing moves
             if rank == tr.src:
                 st = self.stream
-                store.push(tr.dst, self._src_rows(gids, st), self._to_dev(rows, st), self._to_dev(lens, st),
-                           stream=st)
+                sbt, dbt, ln = self._src_rows(gids, st), self._to_dev(rows, st), self._to_dev(lens, st)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                store.push(tr.dst, sbt, dbt, ln, stream=st)
+                e1.record(st)
+                pushes.append((self._kv_bytes(lens), e0, e1))
                 store.signal(core.PEER_DONE, st)
                 by_gid = {x.gid: x for x in self.samples}
                 self._migrated = {g: (by_gid[g].bt_row.copy(), by_gid[g].length) for g in gids}   # (tests)
@@ -500,6 +505,9 @@ class GenerationInstance:
                     recv += 1
                 moved += self._kv_bytes(lens)
         self.samples = [s for s in self.samples if s.gid not in sent_gids] + received
+        if pushes:   # device time of this rank's push kernels (source side)
+            pushes[-1][2].synchronize()
+            self.last_push = (sum(p[0] for p in pushes), sum(p[1].elapsed_time(p[2]) for p in pushes))
         return sent, recv, moved
 
     def _rebalance_two_stage_peer(self, rebalancer: Rebalancer, store: "core.PeerStore", overlap_steps=1, seed=0,

@@ -132,3 +132,60 @@ def test_page_pool_all_or_nothing(core):
         pool.free(a[:1])                                           # double free
     with pytest.raises(core.RSError):
         pool.reserve([64 * 5], page_size=64, max_pages=4)          # longer than a block-table row
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_acceptance_fit_matches_oracle(core, seed):
+    """rs_acceptance_fit (C++) vs oracle.strategy.fit_acceptance on random observations
+    (0/1 outcomes or rates, clipped dl, few or many buckets)."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(2, 4000))
+    dl = rng.random(n) * 1.2 - 0.1
+    acc = (rng.random(n) < np.clip(0.2 + 0.9 * dl, 0, 1)).astype(float) if seed % 2 else rng.random(n)
+    K = int(rng.integers(1, 40))
+    kx, ky = core.acceptance_fit(dl, acc, K)
+    ox, oy = OS.fit_acceptance(dl, acc, K)
+    np.testing.assert_allclose(kx, ox, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(ky, oy, rtol=0, atol=1e-12)
+    with pytest.raises(core.RSError):
+        core.acceptance_fit([0.4] * 5, [1, 0, 1, 0, 1], K)
+
+
+def test_ctx_strategy_state(core):
+    """rs_ctx keeps F and the cost model; a refit replaces F; invalid knots leave it unchanged;
+    the ctx's selector gives the same result as a standalone selector with the same state."""
+    ctx = core.Ctx(rank=0, world=1, page_size=64)
+    with pytest.raises(core.RSError):
+        ctx.select(np.zeros(1, np.int32), np.ones(1), np.array([0, 1], np.int32), np.array([10], np.int32))
+    cost = _cost()
+    ctx.set_strategy(cost, KX, KY)
+    c, kx, ky = ctx.strategy()
+    assert np.array_equal(kx, KX) and np.array_equal(ky, KY) and c["b1"] == cost.b1
+    with pytest.raises(core.RSError):
+        ctx.set_strategy(None, [0.0, 0.5, 0.4], [0.0, 0.5, 0.6])      # x not increasing
+    assert np.array_equal(ctx.strategy()[1], KX)
+    rng = np.random.default_rng(5)
+    dl = rng.random(3000)
+    ctx.fit_acceptance(dl, (rng.random(3000) < 0.2 + 0.7 * dl).astype(float), 10)
+    _, kx2, ky2 = ctx.strategy()
+    assert len(kx2) == 10 and np.all(np.diff(ky2) >= 0)
+    trees = [make_candidate_tree(rng, 60) for _ in range(16)]
+    off = np.zeros(17, np.int32)
+    off[1:] = np.cumsum([len(p) for p, _ in trees])
+    par = np.concatenate([p for p, _ in trees]).astype(np.int32)
+    o = np.concatenate([q for _, q in trees]).astype(np.float64)
+    pl = rng.integers(100, 4000, size=16).astype(np.int32)
+    a = ctx.select(par, o, off, pl, n_min=2, n_max=30)
+    b = core.Selector(cost, kx2, ky2).select_flat(par, o, off, pl, n_min=2, n_max=30)
+    assert a == b
+    ctx.destroy()
+
+
+def test_draft_logits_matches_oracle(core):
+    rng = np.random.default_rng(2)
+    trees = [make_candidate_tree(rng, int(rng.integers(1, 90))) for _ in range(30)]
+    off = np.zeros(31, np.int32)
+    off[1:] = np.cumsum([len(p) for p, _ in trees])
+    dl = core.draft_logits(np.concatenate([p for p, _ in trees]), np.concatenate([o for _, o in trees]), off)
+    ref = np.concatenate([OS.draft_logits(p, o) for p, o in trees])
+    assert np.array_equal(dl, ref)

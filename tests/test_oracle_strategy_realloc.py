@@ -318,3 +318,55 @@ def test_verification_tree_rejects_invalid_fit_and_probabilities():
     bad[4] = 1.5
     with pytest.raises(ValueError, match="MalformedTree"):
         OS.verification_tree(p, bad, tok, 7, 6, KX, KY)
+
+
+# ---------------------------------------------------------------- fit_acceptance
+def test_fit_acceptance_pava_hand_example():
+    """Hand-computed pool-adjacent-violators: bucket rates 0.2, 0.6, 0.4, 0.9 with counts
+    1, 1, 3, 1 -> the violating pair (0.6 | 1 obs, 0.4 | 3 obs) pools to (0.6 + 1.2) / 4 = 0.45;
+    knot x = bucket means of dl."""
+    # K = 4 buckets over [0, 1]: [0, .25) [.25, .5) [.5, .75) [.75, 1]
+    obs = [(0.1, 0.2), (0.3, 0.6), (0.6, 0.4), (0.6, 0.4), (0.7, 0.4), (0.9, 0.9)]
+    kx, ky = OS.fit_acceptance([o[0] for o in obs], [o[1] for o in obs], n_buckets=4)
+    np.testing.assert_allclose(kx, [0.1, 0.3, (0.6 + 0.6 + 0.7) / 3, 0.9], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(ky, [0.2, 0.45, 0.45, 0.9], rtol=0, atol=1e-15)
+
+
+def test_fit_acceptance_pava_cascade_and_empty_buckets():
+    """A later low bucket pools backwards through two earlier blocks: rates 0.5, 0.7, 0.8, 0.1
+    (counts 1 each, buckets 2 and 4 of 6 empty): 0.8 | 0.1 -> 0.45, then 0.7 > 0.45 ->
+    (0.7 + 0.8 + 0.1) / 3; 0.5 < 1.6 / 3 stays."""
+    dl = [0.05, 0.2, 0.55, 0.95]   # buckets 0, 1, 3, 5 of K = 6
+    acc = [0.5, 0.7, 0.8, 0.1]
+    kx, ky = OS.fit_acceptance(dl, acc, n_buckets=6)
+    np.testing.assert_allclose(kx, dl, rtol=0, atol=1e-15)
+    np.testing.assert_allclose(ky, [0.5] + [1.6 / 3] * 3, rtol=0, atol=1e-15)
+
+
+def test_fit_acceptance_spec_examples():
+    """identity target -> F within 0.05 of x on [0, 1]; G(x) = min(1, 0.2 + 0.9x),
+    10k Bernoulli observations -> within 0.05 of G on [0.05, 0.95]; all accepted -> F == 1."""
+    rng = np.random.default_rng(3)
+    for G, lo, hi in ((lambda x: x, 0.0, 1.0), (lambda x: np.minimum(1.0, 0.2 + 0.9 * x), 0.05, 0.95)):
+        dl = rng.random(10000)
+        acc = (rng.random(10000) < G(dl)).astype(float)
+        kx, ky = OS.fit_acceptance(dl, acc, n_buckets=20)
+        xs = np.linspace(lo, hi, 181)
+        F = np.array([OS.acceptance_fit(kx, ky, x) for x in xs])
+        assert np.max(np.abs(F - G(xs))) < 0.05 + (1 / 40 if lo == 0.0 else 0.0)
+        assert np.all(np.diff(ky) >= 0)
+    kx, ky = OS.fit_acceptance(rng.random(500), np.ones(500))
+    assert np.all(ky == 1.0)
+
+
+def test_fit_acceptance_monotone_and_insufficient():
+    rng = np.random.default_rng(11)
+    for _ in range(50):
+        n = int(rng.integers(2, 300))
+        dl = rng.random(n)
+        acc = rng.random(n)
+        kx, ky = OS.fit_acceptance(dl, acc, n_buckets=int(rng.integers(1, 30)))
+        assert np.all(np.diff(kx) > 0) and np.all(np.diff(ky) >= -1e-15)
+        assert np.all(ky >= acc.min() - 1e-15) and np.all(ky <= acc.max() + 1e-15)
+    with pytest.raises(ValueError):
+        OS.fit_acceptance([0.3, 0.3, 0.3], [1, 0, 1])
