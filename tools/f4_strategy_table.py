@@ -4,14 +4,24 @@ real kernel timings. For each sample count B, every fixed draft token num n in t
 the long-tail prefixes + acceptance + compaction, CUDA graph), trees = root + S(n) of each
 sample's 96-node candidate tree (select_strategy's own layer-level selection at fixed n).
 
-Throughput model (Eq. 2): committed tokens per step = al(n) + B (al from the
-acceptance fit F(dl) summed over S(n), + one bonus per sample) over the step time
-t(n) = c_draft + t_verify_measured(n) + b2 * N_draft, where b2 * N_draft is the analytic
-time of the target model's dense GEMMs for N_draft = B (n + 1) tokens (8B parameters at the
-bf16 tensor peak: out of scope to run, SURVEY 8(a) a2'). The cost model t_sd is then fitted
-(rs_cost_model_fit) to these measured step times, select_strategy picks n* per B with the
-fitted model and patience-2 early stop, and we report throughput(n*) / max_n throughput(n)
-(the paper's "percentage of optimal", Table 1).
+Realized acceptance is NOT the selector's prediction: every node's target arg-max is planted
+from a ground truth G(x) = min(1, 0.2 + 0.9 x) of its draft logit that differs from the
+acceptance fit F the selector uses — child x of node c carries c's arg-max with probability
+G(dl_x) / G(dl_c) (root: G = 1; normalised when a node's children sum past 1), so P(x on the
+accepted path) = G(dl_x) — and the greedy acceptance KERNEL walks the trees (3 draws of the
+logits per n). Committed tokens per step = realized accepted drafts + B (bonus) over the step
+time t(n) = c_draft + t_verify_measured(n) + dense * N_draft, dense = the per-token time of an
+8B model's GEMMs at this box's measured tcgen05 GEMM rate (rs_lm_head_argmax), N_draft =
+B (n + 1). The cost model t_sd is fitted (rs_cost_model_fit) to the measured step times,
+select_strategy picks n* per B with F and patience-2 early stop, and the table reports
+realized throughput(n*) / max_n realized throughput(n) (Table 1's "percentage of optimal").
+
+Ladder (Fig. 13 direction): Default (no speculation) -> Spec (static n = 6, 24) ->
+Selection (n*) -> Reallocation. The last rung needs several instances; on this one-GPU box it is
+MODELLED: the long-tailed config-4 population (8 instances x 256 samples, LMSYS-shaped
+responses) is stepped with the per-instance step time measured here at every batch size, once
+with every instance draining on its own (the stage ends with its slowest instance) and once
+with the instances rebalanced to the knee threshold every 32 steps.
 
     python tools/f4_strategy_table.py [B list, default 16,64,256]"""
 import json
@@ -30,20 +40,100 @@ from synth import CONFIGS, draw_prefix_lengths, make_candidate_tree, make_verify
 
 KX = [0.0, 0.05, 0.2, 0.5, 1.0]
 KY = [0.0, 0.15, 0.45, 0.75, 0.95]
-C_DRAFT, B2_GEMM = 1.0e-3, 1.07e-5
+C_DRAFT = 1.0e-3
 N_GRID = [2, 4, 6, 8, 12, 16, 20, 24, 32, 40, 48]
+GEMM_PARAMS_8B = 8.03e9
+
+
+def G(x):
+    """Ground-truth acceptance of a draft node with draft logit x, != the fit F."""
+    return np.minimum(1.0, 0.2 + 0.9 * np.asarray(x, dtype=np.float64))
+
+
+def dense_per_token():
+    """Per verified token: 8B GEMM parameters x 2 FLOP at the measured rs_lm_head_argmax rate."""
+    rows, V, Dm = 4096, 128256, 4096
+    h = torch.randn(rows, Dm, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(V, Dm, device="cuda") * 0.02).to(torch.bfloat16)
+    core.lm_head_argmax(h, w, max_logit=False)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        core.lm_head_argmax(h, w, max_logit=False)
+    e1.record()
+    torch.cuda.synchronize()
+    rate = 2.0 * rows * V * Dm * 5 / (e0.elapsed_time(e1) * 1e-3)
+    return 2.0 * GEMM_PARAMS_8B / rate, rate
+
+
+def realized_accepted(parents, chosen, dl_c, off_c, V, gen, trials=3, seed=0, obs=None):
+    """Mean accepted drafts per step (sum over samples) when the targets follow G: planted
+    arg-max per node, greedy acceptance on the GPU (rs_tree_accept). obs: list that receives
+    (dl, on the accepted path) of every draft node of every trial."""
+    rng = np.random.default_rng(seed)
+    B = len(parents)
+    T = np.array([len(p) for p in parents], np.int32)
+    off = np.zeros(B + 1, np.int32)
+    off[1:] = np.cumsum(T)
+    NT = int(off[-1])
+    parent = np.concatenate(parents).astype(np.int32)
+    token = np.zeros(NT, np.int32)
+    gnode = np.ones(NT)                       # G(dl) per verification node (root: 1)
+    for b in range(B):
+        ch = chosen[b]
+        gnode[off[b] + 1:off[b + 1]] = G(dl_c[off_c[b] + np.asarray(ch, np.int64)]) if len(ch) else []
+        token[off[b]:off[b + 1]] = rng.choice(V, size=T[b], replace=False)
+    d32 = lambda x: torch.as_tensor(np.asarray(x, np.int32), device="cuda")
+    par_d, tok_d, off_d = d32(parent), d32(token), d32(off)
+    gid = torch.arange(B, dtype=torch.int64, device="cuda")
+    total = 0.0
+    for t in range(trials):
+        spike = rng.integers(0, V, size=NT)
+        for b in range(B):
+            o = off[b]
+            kids = [[] for _ in range(T[b])]
+            for i in range(1, T[b]):
+                kids[parents[b][i]].append(i)
+            for c in range(T[b]):
+                if not kids[c]:
+                    continue
+                q = gnode[o + np.array(kids[c])] / gnode[o + c]
+                if q.sum() > 1.0:
+                    q = q / q.sum()
+                u = rng.random()
+                cum = np.cumsum(q)
+                k = int(np.searchsorted(cum, u, side="right"))
+                if k < len(kids[c]):
+                    spike[o + c] = token[o + kids[c][k]]
+                else:                                   # no child: a token no child carries
+                    kt = set(int(token[o + x]) for x in kids[c])
+                    while int(spike[o + c]) in kt:
+                        spike[o + c] = rng.integers(0, V)
+        lg = torch.randn((NT, V), generator=gen, device="cuda")
+        lg[torch.arange(NT, device="cuda"), torch.as_tensor(spike, device="cuda")] += 12.0
+        acc, path, _, _ = core.tree_accept(core.GREEDY, lg.to(torch.bfloat16), par_d, tok_d, off_d, gid)
+        total += float(acc.sum().item())
+        if obs is not None:
+            a, pth = acc.cpu().numpy(), path.cpu().numpy()
+            for b in range(B):
+                on = set(int(x) for x in pth[b][1:a[b] + 1])
+                dls = dl_c[off_c[b] + np.asarray(chosen[b], np.int64)]
+                obs.extend((float(dls[i - 1]), 1.0 if i in on else 0.0) for i in range(1, T[b]))
+        del lg
+    return total / trials
 
 
 def trees_for(sel, cands, P, n):
-    """root + S(n) per sample at a fixed n (n_min = n_max = n)."""
+    """root + S(n) per sample at a fixed n (n_min = n_max = n); also the chosen candidates."""
     res = sel.select(cands, P, n_min=n, n_max=n, patience=2, return_selected=True)
-    parents = []
+    parents, chosen_all = [], []
     for b in range(len(cands)):
         chosen = sorted(int(x) for x in res["selected"][b][:n])
         idx = {c: i + 1 for i, c in enumerate(chosen)}
         cp = cands[b][0]
         parents.append(np.array([-1] + [0 if cp[c] < 0 else idx[int(cp[c])] for c in chosen], np.int32))
-    return parents, res["al"]
+        chosen_all.append(chosen)
+    return parents, res["al"], chosen_all
 
 
 def retree(base, parents, gen):
@@ -76,9 +166,45 @@ def time_step(b, iters=10):
     return e0.elapsed_time(e1) / iters * 1e-3
 
 
+def fleet(curve_B, curve_t, G_inst=8, per_inst=256, T_tok=None, realloc=False, thr=None, cooldown=32, seed=4):
+    """Modelled generation stage of G_inst instances (config-4 population): each step an instance
+    with B samples takes t(B) (interpolated from the measured per-instance step times) and
+    commits tok_per_sample tokens per sample; a sample leaves when its response is done. The
+    stage ends when the last instance is done (synchronous RLHF generation). With
+    realloc, every `cooldown` steps the loads are rebalanced by the library's planner
+    (rs_plan_reallocation, Eq. 6) to the knee threshold. Returns (total tokens, stage seconds)."""
+    import math
+    from synth import lmsys_response_lengths
+    rng = np.random.default_rng(seed)
+    n = G_inst * per_inst
+    resp = lmsys_response_lengths(rng, n).astype(np.float64)
+    inst = [list(resp[i::G_inst]) for i in range(G_inst)]
+    clock = np.zeros(G_inst)
+    tok_ps = T_tok
+    step = 0
+    total = float(resp.sum())
+    tfun = lambda B: float(np.interp(B, curve_B, curve_t)) if B > 0 else 0.0
+    while any(inst):
+        # synchronous steps: instances step independently; track each one's clock
+        for i in range(G_inst):
+            if inst[i]:
+                clock[i] += tfun(len(inst[i]))
+                inst[i] = [r - tok_ps for r in inst[i] if r - tok_ps > 0]
+        step += 1
+        if realloc and step % cooldown == 0:
+            loads = [len(x) for x in inst]
+            if any(l < thr for l in loads) and any(l > thr for l in loads):
+                for s_, d_, c_ in core.plan_reallocation(loads, thr):
+                    inst[s_].sort()
+                    moved, inst[s_] = inst[s_][:c_], inst[s_][c_:]   # shortest first (P:298)
+                    inst[d_] += moved
+    return total, float(clock.max())
+
+
 def main():
     Bs = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "16,64,256").split(",")]
-    base_cost = SimpleNamespace(c_draft=C_DRAFT, b0=2.0e-4, b1=3.0e-8, b2=B2_GEMM, b3=0.0, k_sat=4096.0,
+    dense, rate = dense_per_token()
+    base_cost = SimpleNamespace(c_draft=C_DRAFT, b0=2.0e-4, b1=3.0e-8, b2=dense, b3=0.0, k_sat=4096.0,
                                 seq_bucket=256, draft_bucket=4)
     gen = torch.Generator(device="cuda").manual_seed(5)
     rows, samples = [], []
@@ -89,56 +215,118 @@ def main():
         P = draw_prefix_lengths(np.random.default_rng(cfg.seed), cfg)
         rng = np.random.default_rng(cfg.seed + 77)
         cands = [make_candidate_tree(rng, 96) for _ in range(B)]
+        off_c = np.zeros(B + 1, np.int32)
+        off_c[1:] = np.cumsum([len(p) for p, _ in cands])
+        dl_c = core.draft_logits(np.concatenate([p for p, _ in cands]), np.concatenate([o for _, o in cands]), off_c)
         sel = core.Selector(base_cost, KX, KY)
-        par48, _ = trees_for(sel, cands, P, max(N_GRID))
+        par48, _, _ = trees_for(sel, cands, P, max(N_GRID))
         base = make_verify_batch(cfg, device="cuda", gen_device="cuda", parents=par48, with_logits=False)
         meas = {}
-        for n in N_GRID:
-            parents, al = trees_for(sel, cands, P, n)
+
+        def measure(n):
+            parents, al, chosen = trees_for(sel, cands, P, n)
             t_ver = time_step(retree(base, parents, gen))
-            t = C_DRAFT + t_ver + B2_GEMM * B * (n + 1)
-            meas[n] = dict(al=al, t_verify=t_ver, t_step=t, tput=(al + B) / t)
+            acc = realized_accepted(parents, chosen, dl_c, off_c, cfg.V, gen, seed=n)
+            t = C_DRAFT + t_ver + dense * B * (n + 1)
+            meas[n] = dict(al_pred=al, acc=acc, t_verify=t_ver, t_step=t, tput=(acc + B) / t)
             samples.append((float(np.sum(P)), float(B * (n + 1)), t))
-            print(json.dumps({"B": B, "n": n, "t_verify_ms": round(t_ver * 1e3, 3), "al": round(al, 2),
-                              "tput": round((al + B) / t, 1)}), flush=True)
-        per_B[B] = (cfg, P, cands, base, meas)
+            print(json.dumps({"B": B, "n": n, "t_verify_ms": round(t_ver * 1e3, 3), "al_pred_F": round(al, 2),
+                              "accepted_realized_G": round(acc, 2), "tput": round((acc + B) / t, 1)}), flush=True)
+
+        for n in N_GRID:
+            measure(n)
+        per_B[B] = (cfg, P, cands, base, meas, measure)
     # fit t_sd to the measured step times (b0..b3; c_draft and k_sat kept) and select n* per B
     ns_, nd_, ts_ = (np.array(x) for x in zip(*samples))
     fitted = core.cost_model_fit(ns_, nd_, ts_, base_cost)
     fit_ns = SimpleNamespace(**{k: getattr(fitted, k) for k, _ in fitted._fields_})
-    for B, (cfg, P, cands, base, meas) in per_B.items():
-        sel = core.Selector(fit_ns, KX, KY)
-        r = sel.select(cands, P, n_min=2, n_max=48, patience=2)
-        n_star = int(r["n"])
-        if n_star not in meas:
-            parents, al = trees_for(sel, cands, P, n_star)
-            t_ver = time_step(retree(base, parents, gen))
-            t = C_DRAFT + t_ver + B2_GEMM * B * (n_star + 1)
-            meas[n_star] = dict(al=al, t_verify=t_ver, t_step=t, tput=(al + B) / t)
+    # F from profiling data: 64 other samples of the workload, trees of 48 nodes, the same
+    # planted-G acceptance on the GPU; (dl, on-path) observations -> rs_acceptance_fit
+    pr_rng = np.random.default_rng(999)
+    pc = [make_candidate_tree(pr_rng, 96) for _ in range(64)]
+    po = np.zeros(65, np.int32)
+    po[1:] = np.cumsum([len(p) for p, _ in pc])
+    pdl = core.draft_logits(np.concatenate([p for p, _ in pc]), np.concatenate([o for _, o in pc]), po)
+    ppar, _, pch = trees_for(core.Selector(base_cost, KX, KY), pc, np.full(64, 1024), 48)
+    obs = []
+    realized_accepted(ppar, pch, pdl, po, 128256, gen, trials=4, seed=4242, obs=obs)
+    FX, FY = core.acceptance_fit([o[0] for o in obs], [o[1] for o in obs], 16)
+    for B, (cfg, P, cands, base, meas, measure) in per_B.items():
+        sels = []
+        for kx, ky in ((FX, FY), (KX, KY)):      # fitted F (the method), prior F (mis-specified)
+            r_ = core.Selector(fit_ns, kx, ky).select(cands, P, n_min=2, n_max=48, patience=2)
+            if int(r_["n"]) not in meas:
+                measure(int(r_["n"]))
+            sels.append((int(r_["n"]), r_))
+        (n_star, r), (n_prior, _) = sels
         best_n = max(meas, key=lambda k: meas[k]["tput"])
-        # ladder (Fig. 13 direction): Default = no speculation (T = 1: one token per
-        # sample per step, no draft pass), Spec = a static draft budget (n = 24, the paper's
-        # example of a high fixed n; and n = 6), Selection = n* from select_strategy
+        # Default = no speculation (T = 1: one token per sample per step, no draft pass)
         t_def = time_step(retree(base, [np.array([-1], np.int32) for _ in range(B)], gen))
-        tput_def = B / (t_def + B2_GEMM * B)
-        rows.append({"B": B, "n_selected": n_star, "n_best_fixed": best_n,
-                     "tput_selected": round(meas[n_star]["tput"], 1), "tput_best_fixed": round(meas[best_n]["tput"], 1),
-                     "pct_of_optimal": round(100.0 * meas[n_star]["tput"] / meas[best_n]["tput"], 2),
-                     "ladder_vs_default": {"default": 1.0, "spec_n6": round(meas[6]["tput"] / tput_def, 3),
-                                           "spec_n24": round(meas[24]["tput"] / tput_def, 3),
-                                           "selection": round(meas[n_star]["tput"] / tput_def, 3)},
-                     "default_tput": round(tput_def, 1), "default_t_verify_ms": round(t_def * 1e3, 3),
-                     "pred_t_sd_ms": round(r["t_sd"] * 1e3, 3), "meas_t_step_ms": round(meas[n_star]["t_step"] * 1e3, 3),
-                     "curve": {str(k): round(v["tput"], 1) for k, v in sorted(meas.items())},
-                     "t_verify_ms": {str(k): round(v["t_verify"] * 1e3, 3) for k, v in sorted(meas.items())}})
-        del base
-        torch.cuda.empty_cache()
-    out = {"experiment": "f4: Table 1 (P:378-392) synthetic, real verify-step timings on one B200",
+        tput_def = B / (t_def + dense * B)
+        row = {"B": B, "n_selected": n_star, "n_best_fixed": best_n,
+               "tput_selected": round(meas[n_star]["tput"], 1), "tput_best_fixed": round(meas[best_n]["tput"], 1),
+               "pct_of_optimal": round(100.0 * meas[n_star]["tput"] / meas[best_n]["tput"], 2),
+               "ladder_vs_default": {"default": 1.0, "spec_n6": round(meas[6]["tput"] / tput_def, 3),
+                                     "spec_n24": round(meas[24]["tput"] / tput_def, 3),
+                                     "selection": round(meas[n_star]["tput"] / tput_def, 3)},
+               "default_tput": round(tput_def, 1), "default_t_verify_ms": round(t_def * 1e3, 3),
+               "pred_t_sd_ms": round(r["t_sd"] * 1e3, 3), "meas_t_step_ms": round(meas[n_star]["t_step"] * 1e3, 3),
+               "al_pred_vs_realized_at_n_star": [round(meas[n_star]["al_pred"], 2), round(meas[n_star]["acc"], 2)],
+               "prior_F": {"n_selected": n_prior, "tput": round(meas[n_prior]["tput"], 1),
+                           "pct_of_optimal": round(100.0 * meas[n_prior]["tput"] / meas[best_n]["tput"], 2)},
+               "curve": {str(k): round(v["tput"], 1) for k, v in sorted(meas.items())},
+               "t_verify_ms": {str(k): round(v["t_verify"] * 1e3, 3) for k, v in sorted(meas.items())}}
+        rows.append(row)
+    # Reallocation rung (modelled, see the module docstring): per-instance step time vs batch size
+    # at the selected n of the largest B, measured on the same kernels
+    Bmax = max(per_B)
+    cfg, P, cands, base, meas = per_B[Bmax][:5]
+    n_star = rows[-1]["n_selected"]
+    tok_ps = 1.0 + meas[n_star]["acc"] / Bmax
+    curve_B, curve_t = [], []
+    sel = core.Selector(fit_ns, FX, FY)
+    parents, _, _ = trees_for(sel, cands, P, n_star)
+    for nb in sorted({1, 2, 4, 8, 16, 32, 64, 128, Bmax}):
+        if nb > Bmax:
+            continue
+        sub = dict(base)
+        sub = retree_subset(base, parents, nb, gen)
+        curve_B.append(nb)
+        curve_t.append(C_DRAFT + time_step(sub) + dense * nb * (n_star + 1))
+    tput_curve = [b * tok_ps / t for b, t in zip(curve_B, curve_t)]
+    thr = core.knee_threshold(curve_B, tput_curve, 0.10)
+    tot, t_no = fleet(curve_B, curve_t, T_tok=tok_ps)
+    _, t_re = fleet(curve_B, curve_t, T_tok=tok_ps, realloc=True, thr=thr)
+    realloc = {"modelled": True, "instances": 8, "samples_per_instance": 256, "n": n_star,
+               "tokens_per_sample_step": round(tok_ps, 3), "knee_threshold": thr,
+               "curve_B": curve_B, "curve_step_ms": [round(x * 1e3, 3) for x in curve_t],
+               "curve_tokens_per_s": [round(x, 1) for x in tput_curve],
+               "stage_s_without": round(t_no, 3), "stage_s_with": round(t_re, 3),
+               "gain": round(t_no / t_re, 3)}
+    for row in rows:
+        row["ladder_vs_default"]["reallocation_modelled"] = round(row["ladder_vs_default"]["selection"] * t_no / t_re, 3)
+    out = {"experiment": "f4: Table 1 (P:378-392) synthetic, real verify-step timings on one B200, realized "
+                         "acceptance from a ground truth G != F",
            "fitted_cost_model": {k: getattr(fitted, k) for k, _ in fitted._fields_},
-           "rows": rows,
-           "model": "tput(n) = (al(n) + B) / (c_draft 1 ms + measured verify step + 1.07e-5 s x B(n+1) analytic "
-                    "8B GEMMs); al(n) = sum over S(n) of F(dl)"}
+           "dense_s_per_token": dense, "gemm_TFLOPs": round(rate / 1e12, 1),
+           "fitted_F": {"knots_x": [round(x, 5) for x in FX], "knots_y": [round(y, 5) for y in FY],
+                        "observations": len(obs)},
+           "rows": rows, "reallocation": realloc,
+           "model": "tput(n) = (realized accepted + B) / (c_draft 1 ms + measured verify step + dense x B(n+1)); "
+                    "realized accepted from rs_tree_accept on targets planted from G(x) = min(1, 0.2 + 0.9x); "
+                    "n_selected uses F fitted from profiling observations of the same process (P:192) and the fitted "
+                    "t_sd; prior_F = the hand-set knots KX/KY (mis-specified) for comparison"}
     print(json.dumps(out), flush=True)
+
+
+def retree_subset(base, parents, nb, gen):
+    """The first nb samples of the base batch with the given verification trees."""
+    b = dict(base)
+    b["B"] = nb
+    b["prefix_len"] = base["prefix_len"][:nb]
+    b["block_table"] = base["block_table"][:nb]
+    b["gid"] = base["gid"][:nb]
+    return retree(b, parents[:nb], gen)
 
 
 if __name__ == "__main__":
