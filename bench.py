@@ -253,6 +253,7 @@ class ClockSampler:
 
     def __init__(self, device_index: int, period_s: float = 0.02):
         self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.mem, self.power = [], []
         self.period = period_s
         self._stop = threading.Event()
         self._ok = False
@@ -270,6 +271,8 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.mem.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_MEM))
+                self.power.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
                 r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for k, v in self.REASONS.items():
                     if r & v and k != "gpu_idle":
@@ -293,7 +296,9 @@ class ClockSampler:
         if not self._ok or not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "mem_mhz": statistics.median(self.mem) if self.mem else None,
+                "power_w_median": round(statistics.median(self.power), 1) if self.power else None}
 
 
 def _peaks():

@@ -204,9 +204,8 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
         used += best;
     }
     // Balanced contiguous fill with split-KV cuts over the gangs of one class: unit groups are
-    // poured, in order, into gangs; gang v owns the work interval [v*W/n, (v+1)*W/n) of the
-    // concatenated stream (re-divided whenever a new gang is entered, since each extra split
-    // part costs another kOvhBlocks); parts are never smaller than kMinPart blocks.
+    // poured, in order, into gangs of a common capacity (the smallest that fits, below); parts
+    // are never smaller than kMinPart blocks.
     struct Seg { int gu, tile, start, end; };   // tile -1: every tile of the gang
     std::vector<std::vector<WorkItem>> per_cta(n_ctas);
     int n_parts = 0;
@@ -222,45 +221,56 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
             else if (M == 1 && gangs[gus[gi].M] == 0)
                 for (int m = 0; m < gus[gi].M; ++m) entries.push_back({gi, m});
         }
+        // Balanced fill: the smallest per-gang capacity (blocks + kOvhBlocks per item, so every
+        // extra split part pays its overhead) for which pouring the entries in order into the G
+        // gangs fits, found by bisection; then the fill at that capacity. (A running-average
+        // target drifted: the last gangs absorbed every split overhead, 76 vs 63 blocks of cost
+        // on config 2.)
         std::vector<std::vector<std::pair<int, int>>> where_of(entries.size());
         long long W = 0;
-        for (auto& e : entries) W += gus[e.first].nblk + kOvhBlocks;
-        long long W_eff = W, pos = 0;
-        int v = 0;
-        long long end = (W_eff + G - 1) / G;
-        auto next_gang = [&]() {
-            ++v;
-            end = pos + (W_eff - pos + (G - v) - 1) / (G - v);
-        };
-        for (int ei = 0; ei < (int)entries.size(); ++ei) {
-            const int gi = entries[ei].first;
-            const GU& u = gus[gi];
-            int rem = u.nblk, start = 0;
-            while (rem > 0) {
-                if (v < G - 1 && pos >= end) { next_gang(); continue; }
-                const long long room = (v == G - 1) ? (1ll << 60) : end - pos - kOvhBlocks;
-                int take;
-                if (room >= rem) {
-                    take = rem;
-                } else if (room < kMinPart) {
-                    if (per_g[v].empty()) {
-                        take = rem;               // never leave a gang without work
-                    } else {
-                        next_gang();              // too little room for a useful part: next gang
-                        continue;
-                    }
-                } else {
-                    take = (int)room;
-                    if (rem - take < kMinPart) take = (rem >= 2 * kMinPart) ? rem - kMinPart : rem;
-                }
-                if (!where_of[ei].empty()) W_eff += kOvhBlocks;   // an extra part of a split unit
-                where_of[ei].push_back({v, (int)per_g[v].size()});
-                per_g[v].push_back({gi, entries[ei].second, start, start + take});
-                pos += take + kOvhBlocks;
-                start += take;
-                rem -= take;
-            }
+        int max_nblk = 0;
+        for (auto& e : entries) {
+            W += gus[e.first].nblk + kOvhBlocks;
+            max_nblk = std::max(max_nblk, gus[e.first].nblk);
         }
+        auto fill = [&](long long cap, bool commit) -> bool {
+            int v = 0;
+            long long load = 0;
+            for (int ei = 0; ei < (int)entries.size(); ++ei) {
+                const int gi = entries[ei].first;
+                int rem = gus[gi].nblk, start = 0;
+                while (rem > 0) {
+                    if (v >= G) return false;
+                    const long long room = cap - load - kOvhBlocks;
+                    int take;
+                    if (room >= rem) {
+                        take = rem;
+                    } else {
+                        take = (int)std::min<long long>(room, rem - kMinPart);   // leave >= kMinPart
+                        if (take < kMinPart) {
+                            if (load == 0) take = rem;   // an empty gang takes the whole entry
+                            else { ++v; load = 0; continue; }
+                        }
+                    }
+                    if (commit) {
+                        where_of[ei].push_back({v, (int)per_g[v].size()});
+                        per_g[v].push_back({gi, entries[ei].second, start, start + take});
+                    }
+                    load += take + kOvhBlocks;
+                    start += take;
+                    rem -= take;
+                }
+            }
+            return true;
+        };
+        long long lo = std::max<long long>((W + G - 1) / G, 1), hi = lo + max_nblk + 2 * kOvhBlocks + kMinPart;
+        while (!fill(hi, false)) hi *= 2;
+        while (lo < hi) {
+            const long long mid = (lo + hi) / 2;
+            if (fill(mid, false)) hi = mid;
+            else lo = mid + 1;
+        }
+        fill(lo, true);
         // expand: gang v -> CTAs cta_base + v*M + m (tile m); split units per tile
         for (int vv = 0; vv < G; ++vv)
             for (int m = 0; m < M; ++m)

@@ -433,7 +433,10 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                         }
                         // a block with a tree slot (slot >= P_b) only after the wait
                         if (!waited && (wi.blk_begin + j + 1) * kBlockN > wi.P) { griddep_wait(); waited = true; }
-                        if (RM != 4 && isK && has_next && j == q_next_at) issue_q(wn, it + 1);
+                        if (RM != 4 && isK && has_next && j == q_next_at) {
+                            if (lane == 0) TRACE(J, 11);   // (profiling: next item's Q issued at block J)
+                            issue_q(wn, it + 1);
+                        }
                         if (RM == 4 && isK && it > 0 && j == 0) issue_q(wi, it);
                         // L2 prefetch of block j + pf (this item or the next one)
                         if (do_pf) {
@@ -501,6 +504,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             } else {
                 mbar_wait(&bars->q_full[qb], (it / kQBufs) & 1);
             }
+            if (lane == 0) TRACE(sJ, 10);   // (profiling: this item's Q seen landed)
             // dual: virtual block sJ = 2 * key block + tile; key block counter kJ = sJ >> 1
             const int nv = DU ? 2 * nblk : nblk;
             for (int j = 0; j < nv; ++j, ++sJ) {
@@ -548,6 +552,9 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         for (; w >= 0; ++it) {
             const int wn = seq_read(it + 1);
             const int nblk_next = wn >= 0 ? __ldg(&p.items[wn].blk_end) - __ldg(&p.items[wn].blk_begin) : 0;
+            // keys [key_end, ...) of the sample's last page: their V rows are zeroed below
+            const int key_end = __ldg(&p.items[w].P) + __ldg(&p.items[w].T);
+            const int blk0 = __ldg(&p.items[w].blk_begin);
             constexpr bool DU = RM == 4;
             const int nv = DU ? 2 * nblk : nblk;   // dual: virtual block pJ = 2 * key block + tile
             for (int j = 0; j < nv; ++j, ++pJ) {
@@ -555,8 +562,27 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 // warpgroup (dual: of each tile) in the item overwrites
                 const bool first = !KT<RM>::kEW && j < 2;
                 const uint32_t vJ = DU ? (pJ >> 1) : pJ;
+                if (!DU || (pJ & 1) == 0) {
+                    mbar_wait(&bars->v_full[vJ % C::VS], (vJ / C::VS) & 1);
+                    // Keys past the end of the sample in its last page get P = 0, but their V
+                    // rows hold whatever the page held (possibly NaN bytes, and 0 * NaN = NaN in
+                    // the MMA): zero them here, where the V tile is awaited anyway, so the softmax
+                    // never waits on a V load (a tail block's P used to wait for its V tile, which
+                    // stalled the whole P -> PV -> V-slot chain at every item end).
+                    const int nvalid = key_end - (blk0 + (DU ? (j >> 1) : j)) * kBlockN;
+                    if (nvalid < kBlockN) {
+                        uint8_t* vs = smem + C::kOffV + (vJ % C::VS) * C::kKVBytes;
+                        const int nz = (kBlockN - nvalid) * C::kBoxes * 8;   // 16-byte chunks
+                        for (int q = lane; q < nz; q += 32) {
+                            const int row = nvalid + q / (C::kBoxes * 8), rem = q % (C::kBoxes * 8);
+                            reinterpret_cast<uint4*>(vs + (rem >> 3) * (kBlockN * 128) + row * 128)[rem & 7] =
+                                make_uint4(0, 0, 0, 0);
+                        }
+                        fence_proxy_async_smem();
+                    }
+                    __syncwarp();
+                }
                 mbar_wait(&bars->p_full[pJ & 1], (pJ >> 1) & 1);
-                if (!DU || (pJ & 1) == 0) mbar_wait(&bars->v_full[vJ % C::VS], (vJ / C::VS) & 1);
                 if (lane == 0) TRACE(pJ, 9);
                 // (EW: the softmax warpgroup re-zeroes its O half before its first P of the item,
                 // after the epilogue of item it-2 released it, so PV needs no wait here)
@@ -879,22 +905,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                     first_blk = false;
                 }
                 tmem_wait_st();
-                // keys past the end of the sample in its last page: zero those V rows
-                const int nvalid = key_end - kbase;
-                if (nvalid < kBlockN) {
-                    const uint32_t sl = Jj % C::VS;
-                    mbar_wait(&bars->v_full[sl], (Jj / C::VS) & 1);
-                    if (r < kBlockN && r >= nvalid) {
-                        uint8_t* vs = smem + C::kOffV + sl * C::kKVBytes;
-#pragma unroll
-                        for (int bx = 0; bx < C::kBoxes; ++bx) {
-                            uint4* row = reinterpret_cast<uint4*>(vs + bx * (kBlockN * 128) + r * 128);
-#pragma unroll
-                            for (int c = 0; c < 8; ++c) row[c] = make_uint4(0, 0, 0, 0);
-                        }
-                    }
-                    fence_proxy_async_smem();
-                }
+                // (V rows past the sample's end are zeroed by the PV issuer)
                 tc_fence_before();
                 __syncwarp();
                 if (wq == 0 && lane == 0) TRACE(Jj, 4);
@@ -1152,26 +1163,8 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                     wait_prev_pv();
                 }
                 }   // !hs
-                // keys past the end of the sample in its last page: zero those V rows so that
-                // garbage (possibly NaN) bytes never meet a zero probability in the MMA
-                const int nvalid = key_end - kbase;
-                // (dual: the V tile is shared by both tiles; warpgroup 0 zeroes it before its
-                // P is published, and the PV issuer runs tile 0's MMA before tile 1's)
-                if (nvalid < kBlockN && (!DU || grp == 0)) {
-                    const uint32_t vJ = DU ? (Jj >> 1) : Jj;
-                    const uint32_t s = vJ % C::VS;
-                    mbar_wait(&bars->v_full[s], (vJ / C::VS) & 1);
-                    if (r < kBlockN && r >= nvalid) {
-                        uint8_t* vs = smem + C::kOffV + s * C::kKVBytes;
-#pragma unroll
-                        for (int bx = 0; bx < C::kBoxes; ++bx) {
-                            uint4* row = reinterpret_cast<uint4*>(vs + bx * (kBlockN * 128) + r * 128);
-#pragma unroll
-                            for (int c = 0; c < 8; ++c) row[c] = make_uint4(0, 0, 0, 0);
-                        }
-                    }
-                    fence_proxy_async_smem();
-                }
+                // (V rows past the sample's end are zeroed by the PV issuer before the first MMA
+                // that reads the tile — dual: tile 0's, which it issues before tile 1's)
                 tc_fence_before();
                 __syncwarp();
                 if (wq == 0 && lane == 0) TRACE(Jj, 4);

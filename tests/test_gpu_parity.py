@@ -435,14 +435,15 @@ def test_attention_full_config2_sampled(cuda_lib):
 
 
 # ------------------------------------------------------------------ full-size, bench launch configuration
-def _c3s_batch(layers=1, with_logits=True):
+def _c3s_batch(layers=1, with_logits=True, calibrate=True):
     """configs[2] as bench.py runs it (c3s): B = 256 long-tail prefixes, every tree = S(n) from
-    select_strategy (host C++), MSS rejection sampling; generated on the GPU."""
+    select_strategy (host C++) with F and t_sd calibrated on this GPU exactly as bench.py does
+    (calibrate=False: the prior F / t_sd, a larger n), MSS rejection sampling; generated on the GPU."""
     import bench
     cfg = CONFIGS["c3s"]
-    strat = bench.strategy_trees(cfg, cuda_lib_core())
+    strat = bench.Strategy(cfg, cuda_lib_core(), "cuda", calibrate=calibrate)
     return make_verify_batch(cfg, device="cuda", gen_device="cuda", layers=layers, with_logits=with_logits,
-                             parents=strat[4])
+                             parents=strat.parents)
 
 
 def cuda_lib_core():
@@ -450,10 +451,12 @@ def cuda_lib_core():
     return core
 
 
-def test_attention_full_config3s_sampled(cuda_lib):
+@pytest.mark.parametrize("calibrate", [True, False])
+def test_attention_full_config3s_sampled(cuda_lib, calibrate):
     """Long-tail config at full size (B=256, P 512-16K, T from select_strategy) in the launch
-    configuration bench.py times; oracle on 5 sampled samples (longest included)."""
-    b = _c3s_batch(with_logits=False)
+    configuration bench.py times (calibrated: T*g <= 64, the 16-warp kernel; prior: T*g > 64, the
+    12-warp kernel); oracle on 5 sampled samples (longest included)."""
+    b = _c3s_batch(with_logits=False, calibrate=calibrate)
     for k in ("q", "k_cache", "v_cache"):
         b[k] = b[k].cpu()
     P = b["prefix_len"]

@@ -33,8 +33,8 @@ def main():
     if cfg.tree[0] == "strategy":   # c3s: verification trees = S(n) from select_strategy, as bench.py
         sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
         import bench
-        strat = bench.strategy_trees(cfg, core)
-        b = make_verify_batch(cfg, device="cuda", gen_device="cuda", layers=layers, parents=strat[4])
+        strat = bench.Strategy(cfg, core, "cuda", calibrate=True)
+        b = make_verify_batch(cfg, device="cuda", gen_device="cuda", layers=layers, parents=strat.parents)
     else:
         b = make_verify_batch(cfg, device="cuda", gen_device="cuda", layers=layers)
     mode = {"greedy": core.GREEDY, "delta": core.SAMPLE_DELTA, "mss": core.SAMPLE_MSS}[cfg.mode]

@@ -17,8 +17,8 @@ from synth import CONFIGS, make_verify_batch  # noqa: E402
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 50
 cfg = CONFIGS["c3s"]
 dev = torch.device("cuda", 0)
-strat = bench.strategy_trees(cfg, core)
-b = make_verify_batch(cfg, device=dev, gen_device=dev, layers=1, parents=strat[4])
+strat = bench.Strategy(cfg, core, "cuda", calibrate=True)
+b = make_verify_batch(cfg, device=dev, gen_device=dev, layers=1, parents=strat.parents)
 lg, dp = b["logits"], b["draft_probs"]
 d32 = lambda x: torch.as_tensor(np.asarray(x), dtype=torch.int32, device=dev)
 par, tok, off = d32(b["parent"]), d32(b["token"]), d32(b["tree_off"])
