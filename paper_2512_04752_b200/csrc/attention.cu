@@ -40,8 +40,11 @@ static constexpr int kOvhBlocksDefault = 2;   // per-item fixed cost in block un
 #ifndef RS_ATTN_DUAL
 #define RS_ATTN_DUAL 1      // dual items (RM = 4) when every unit allows them
 #endif
-#ifndef RS_ATTN_DYN
-#define RS_ATTN_DYN 0       // dynamic item queue for RM = 1 plans (measured slower)
+#ifndef RS_ATTN_DYNFRAC
+#define RS_ATTN_DYNFRAC 0   // percent of the work left to a dynamic tail queue (measured slower at 6-20: off)
+#endif
+#ifndef RS_ATTN_DYNPART
+#define RS_ATTN_DYNPART 8   // key blocks per dynamic tail part (at least; cap/16 for long lists)
 #endif
 #ifndef RS_ATTN_L2PROMO
 #define RS_ATTN_L2PROMO 3   // CUtensorMapL2promotion of the K/V page loads
@@ -208,6 +211,8 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
     // are never smaller than kMinPart blocks.
     struct Seg { int gu, tile, start, end; };   // tile -1: every tile of the gang
     std::vector<std::vector<WorkItem>> per_cta(n_ctas);
+    std::vector<Seg> dyn_segs;          // hybrid tail parts of the current class
+    std::vector<WorkItem> dyn_items;    // ... as work items (after every static list)
     int n_parts = 0;
     int cta_base = 0;
     for (int M = 1; M <= 4; ++M) {
@@ -233,14 +238,32 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
             W += gus[e.first].nblk + kOvhBlocks;
             max_nblk = std::max(max_nblk, gus[e.first].nblk);
         }
-        auto fill = [&](long long cap, bool commit) -> bool {
+        // hybrid (single-tile class, no dual items): the static lists take a (1 - DYNFRAC) share
+        // of that capacity and what does not fit becomes small split parts in a global queue
+        // that CTAs pull from once their own list is done (atomic counter): the launch then ends
+        // when the average CTA does, not the slowest (SMs do not all stream HBM at the same rate;
+        // config 2 CTA end times spread 48-62 us with balanced static lists).
+        const bool hybrid = M == 1 && !dual && RS_ATTN_DYNFRAC > 0;
+        int dyn_part = RS_ATTN_DYNPART;
+        auto fill = [&](long long cap, bool commit, bool to_dyn) -> bool {
             int v = 0;
             long long load = 0;
             for (int ei = 0; ei < (int)entries.size(); ++ei) {
                 const int gi = entries[ei].first;
                 int rem = gus[gi].nblk, start = 0;
                 while (rem > 0) {
-                    if (v >= G) return false;
+                    if (v >= G) {
+                        if (!to_dyn) return false;
+                        // the rest of this entry and every later one: tail parts
+                        const int take = rem < dyn_part + kMinPart ? rem : dyn_part;
+                        if (commit) {
+                            where_of[ei].push_back({-1, (int)dyn_segs.size()});
+                            dyn_segs.push_back({gi, entries[ei].second, start, start + take});
+                        }
+                        start += take;
+                        rem -= take;
+                        continue;
+                    }
                     const long long room = cap - load - kOvhBlocks;
                     int take;
                     if (room >= rem) {
@@ -264,13 +287,20 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
             return true;
         };
         long long lo = std::max<long long>((W + G - 1) / G, 1), hi = lo + max_nblk + 2 * kOvhBlocks + kMinPart;
-        while (!fill(hi, false)) hi *= 2;
+        while (!fill(hi, false, false)) hi *= 2;
         while (lo < hi) {
             const long long mid = (lo + hi) / 2;
-            if (fill(mid, false)) hi = mid;
+            if (fill(mid, false, false)) hi = mid;
             else lo = mid + 1;
         }
-        fill(lo, true);
+        dyn_part = std::max<int>(RS_ATTN_DYNPART, (int)(lo / 16));
+        if (hybrid) fill(std::max<long long>(lo * (100 - RS_ATTN_DYNFRAC) / 100, kMinPart + kOvhBlocks), true, true);
+        else fill(lo, true, false);
+        for (const Seg& sg : dyn_segs) {   // (hybrid: M == 1)
+            const GU& u = gus[sg.gu];
+            dyn_items.push_back({u.b, u.kvh, tile_mul * sg.tile, sg.start, sg.end, -1, u.R, -1, u.P, u.node0, u.T, 0});
+        }
+        dyn_segs.clear();
         // expand: gang v -> CTAs cta_base + v*M + m (tile m); split units per tile
         for (int vv = 0; vv < G; ++vv)
             for (int m = 0; m < M; ++m)
@@ -292,7 +322,8 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
                 if (dual) pl->units.push_back({u.b, u.kvh, tile + 1, k, n_parts + k, u.R});
                 for (int i = 0; i < k; ++i) {
                     const auto& wc = where_of[ei][i];
-                    WorkItem& it = per_cta[cta_base + wc.first * M + m][wc.second];
+                    WorkItem& it = wc.first >= 0 ? per_cta[cta_base + wc.first * M + m][wc.second]
+                                                 : dyn_items[wc.second];
                     it.part = n_parts + i;
                     it.unit = uid;
                     it.pad = dual ? k : 0;
@@ -309,25 +340,15 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
     }
     pl->cta_off[n_ctas] = (int)pl->items.size();
     pl->n_ctas = n_ctas;
-    // Dynamic scheduling (every tile R = 16: the 16-warp kernel): CTAs pull items from a global
-    // queue, so a CTA that runs faster (SMs do not all stream HBM at the same rate) takes more
-    // work and the launch ends when the average CTA does. Queue order interleaves the static
-    // lists position by position (first items of all CTAs, then the second items, ...).
-    {
-        // measured slower than the balanced static lists at the configs' item sizes (a 17-block
-        // item is ~15 us, too coarse for the tail): off unless built with -DRS_ATTN_DYN=1
-        pl->dyn = (pl->rmodes == 1 && RS_ATTN_DYN == 1) ? 1 : 0;
-        pl->qorder.clear();
-        size_t maxlen = 0;
-        for (int c = 0; c < n_ctas; ++c) maxlen = std::max(maxlen, per_cta[c].size());
-        for (size_t k = 0; k < maxlen; ++k)
-            for (int c = 0; c < n_ctas; ++c)
-                if (k < per_cta[c].size()) pl->qorder.push_back(pl->cta_off[c] + (int)k);
-        // longest items first, so the launch tail is made of the short split parts
-        std::stable_sort(pl->qorder.begin(), pl->qorder.end(), [&](int x, int y) {
-            return pl->items[x].blk_end - pl->items[x].blk_begin > pl->items[y].blk_end - pl->items[y].blk_begin;
-        });
-    }
+    // Dynamic tail: item indices after the static lists, longest first, pulled by CTAs that
+    // finished their own list (p.dyn); none -> pure static schedule.
+    pl->qorder.clear();
+    for (size_t i = 0; i < dyn_items.size(); ++i) pl->qorder.push_back((int)(pl->items.size() + i));
+    pl->items.insert(pl->items.end(), dyn_items.begin(), dyn_items.end());
+    std::stable_sort(pl->qorder.begin(), pl->qorder.end(), [&](int x, int y) {
+        return pl->items[x].blk_end - pl->items[x].blk_begin > pl->items[y].blk_end - pl->items[y].blk_begin;
+    });
+    pl->dyn = pl->qorder.empty() ? 0 : 1;
     pl->n_parts = n_parts;
     pl->off_cta = 0;
     pl->off_items = align_up(sizeof(int32_t) * (n_ctas + 1), 256);
@@ -441,7 +462,7 @@ static rs_status launch_attn(const rs_attn_plan* pl, const void* q, const void* 
     prm.unit_counter = reinterpret_cast<int*>(w + pl->off_counter);
     prm.qorder = reinterpret_cast<const int32_t*>(w + pl->off_qorder);
     prm.qctr = reinterpret_cast<int*>(w + pl->off_qctr);
-    prm.n_items = (int)pl->items.size();
+    prm.n_items = (int)pl->qorder.size();   // dynamic tail items
     prm.dyn = pl->dyn;
     prm.prefix_len = prefix_len;
     prm.tree_off = tree_off;

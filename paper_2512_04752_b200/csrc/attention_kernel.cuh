@@ -52,7 +52,6 @@ constexpr int kM = 128;          // query rows per work item (UMMA M)
 #endif
 constexpr int kMaxSlots = 8;
 constexpr int kRing = 8;         // dynamic item queue ring depth (shared memory)
-constexpr int kQConsumers = 15;  // warps that read the ring (all but the fetching producer warp 0)
 #ifndef RS_ATTN_STAGE
 #define RS_ATTN_STAGE 0
 #endif
@@ -260,9 +259,9 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     const int lane = threadIdx.x & 31;
     const int item_begin = p.cta_off[blockIdx.x];
     const int item_end = p.cta_off[blockIdx.x + 1];
-    // The CTA's item sequence: static (its plan list) or dynamic (p.dyn: warp 0 takes the next
-    // item of the global queue with atomicAdd and publishes it through a shared-memory ring that
-    // every other warp reads once per position). -1 ends the sequence.
+    // The CTA's item sequence: its static plan list, then (p.dyn) the dynamic tail: warp 0 takes
+    // the next item of the global queue with atomicAdd; every position is published through a
+    // shared-memory ring that every other warp reads once per position. -1 ends the sequence.
     auto seq_read = [&](int it) -> int {   // warp-collective, every warp except warp 0
         if (!p.dyn) return item_begin + it < item_end ? item_begin + it : -1;
         const int sl = it % kRing;
@@ -274,10 +273,13 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     };
     auto seq_fetch = [&](int it) -> int {  // warp 0: produce position it of the sequence
         if (!p.dyn) return item_begin + it < item_end ? item_begin + it : -1;
-        int w = 0;
-        if ((threadIdx.x & 31) == 0) w = atomicAdd(p.qctr, 1);
-        w = __shfl_sync(0xffffffffu, w, 0);
-        w = (w < p.n_items) ? __ldg(p.qorder + w) : -1;
+        int w = item_begin + it;
+        if (w >= item_end) {   // own list done: the next tail item of the global queue
+            griddep_wait();    // (the counter is reset by the previous launch's last CTA)
+            if ((threadIdx.x & 31) == 0) w = atomicAdd(p.qctr, 1);
+            w = __shfl_sync(0xffffffffu, w, 0);
+            w = (w < p.n_items) ? __ldg(p.qorder + w) : -1;
+        }
         const int sl = it % kRing;
         mbar_wait(&bars->item_empty[sl], ((it / kRing) & 1) ^ 1);
         if ((threadIdx.x & 31) == 0) {
@@ -307,7 +309,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         mbar_init(&bars->o_free, 8);
         for (int i = 0; i < kRing; ++i) {
             mbar_init(&bars->item_full[i], 1);
-            mbar_init(&bars->item_empty[i], kQConsumers);
+            mbar_init(&bars->item_empty[i], KT<RM>::kThreads / 32 - 1);   // every warp but warp 0
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bars->o_ready[i], 1);

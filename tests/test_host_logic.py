@@ -39,7 +39,8 @@ def _check_plan(core, P, T, Hq, Hkv, d=128, n=148):
     pl = core.AttnPlan(P, to, Hq, Hkv, d, 64, num_ctas=n)
     cta, items = pl.schedule()
     info = pl.info()
-    assert cta[0] == 0 and cta[-1] == len(items) and np.all(np.diff(cta) >= 0)
+    # static lists first; items past cta[-1] are the dynamic tail (pulled by CTAs that finished)
+    assert cta[0] == 0 and cta[-1] <= len(items) and np.all(np.diff(cta) >= 0)
     g = Hq // Hkv
     # dual items (kernel RM = 4): every unit R = 32 with an even tile count -> an item covers
     # tiles (mt, mt + 1); tile 1's split parts follow tile 0's by item.pad
