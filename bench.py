@@ -77,7 +77,7 @@ class Strategy:
     library's own verification attention timed on a (B, P, T) grid + the dense per-token cost at
     this box's measured GEMM rate); then one n per batch from the candidate trees."""
 
-    def __init__(self, cfg, core, dev, calibrate=True):
+    def __init__(self, cfg, core, dev, calibrate=True, force_n=None):
         from types import SimpleNamespace
         from synth import draw_prefix_lengths, make_candidate_tree
         self.core, self.cfg = core, cfg
@@ -99,7 +99,7 @@ class Strategy:
         self.cands = [make_candidate_tree(rng, int(cfg.tree[1])) for _ in range(cfg.B)]
         self.flat = self._flatten(self.cands)
         self.selected = np.full((cfg.B, 63), -1, np.int32)
-        self.res = self.select()
+        self.res = self.select() if force_n is None else self.select(n_min=force_n, n_max=force_n)
         self.parents = self._trees(self.cands, self.selected, self.res["n"])
 
     @staticmethod
@@ -123,6 +123,8 @@ class Strategy:
 
     def select(self, n_min=3, n_max=63):
         par, o, off = self.flat
+        if self.selected.shape[1] != n_max:      # rows of the selection order are [B, n_max]
+            self.selected = np.full((self.cfg.B, n_max), -1, np.int32)
         return self.ctx.select(par, o, off, self.P, n_min=n_min, n_max=n_max, patience=2, selected=self.selected)
 
     def _fit_acceptance(self, dev, B=64, n_prof=48, seeds=8):
@@ -450,6 +452,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-n", type=int, default=None,
+                    help="c3s: every tree = S(n) for this n under the prior F (profiling runs: the calibrated "
+                         "shapes without the calibration launches)")
     ap.add_argument("--no-calibrate", action="store_true",
                     help="c3s: keep the prior F / t_sd instead of profiling + rs_calibrate at startup")
     ap.add_argument("--realloc", default="on", choices=["on", "off"], help="c4: sample reallocation")
@@ -495,7 +500,7 @@ def run_ours(args, world, rank, local):
     cfg = type(cfg)(**{**cfg.__dict__, "seed": cfg.seed + 1000 * rank})   # disjoint samples per rank
     strat = None
     if cfg.tree[0] == "strategy":
-        strat = Strategy(cfg, core, dev, calibrate=not args.no_calibrate)
+        strat = Strategy(cfg, core, dev, calibrate=not (args.no_calibrate or args.force_n), force_n=args.force_n)
         b = make_verify_batch(cfg, device=dev, gen_device=dev, parents=strat.parents)
     else:
         b = make_verify_batch(cfg, device=dev, gen_device=dev, with_logits=lm is None, layers=n_buf)
