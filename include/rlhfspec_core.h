@@ -1,7 +1,7 @@
 /* rlhfspec_core — C ABI of the RLHFSpec verification hot path on B200 (sm_100a).
  *
  * Paper: RLHFSpec (arXiv 2512.04752), /root/reference/PAPER.md, cited P:<line>.
- * Scope: DESIGN.md §1 / SURVEY.md §8. Readings Z1..Z20: DESIGN.md §2.
+ * Scope: DESIGN.md §1 / SURVEY.md §8. Readings Z1..Z27: DESIGN.md §2.
  *
  * Conventions (all entry points)
  *  - Every call returns rs_status (RS_OK = 0). No exception crosses the ABI. On error,

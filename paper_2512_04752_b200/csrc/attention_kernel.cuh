@@ -69,6 +69,15 @@ constexpr int kThreads = 384;    // 12 warps (RM 2/3)
 // items alternate between the two 16-lane halves of each TMEM sub-partition, so item i's O is
 // normalised and stored while item i+1 already accumulates.
 template <int RM> struct KT { static constexpr bool kEW = (RM == 1); static constexpr int kThreads = kEW ? 512 : 384; };
+// RM = 1: an item's 64 rows are half the TMEM lanes (16 per sub-partition), so its S and PV MMAs
+// are issued with M = 64 at the item's lane half (tcgen05 M = 64 layout: A row m <-> lane
+// (m % 16) + 32 (m / 16), + 16 for the odd half) instead of M = 128 over both items' halves: half
+// the tensor-core work per key block (the M = 128 form computed the other item's rows too). Under
+// the power cap that work sets the SM clock (c3s: no MMAs at all -> 1965 vs 1365 MHz).
+#ifndef RS_ATTN_M64
+#define RS_ATTN_M64 1
+#endif
+constexpr bool kM64 = RS_ATTN_M64 != 0;
 constexpr int kTraceJ = 256;
 
 // Row layout of a tile: logical query row r (node-major (node, head-in-group) pairs of the unit)
@@ -389,8 +398,10 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                         const int node = x.node0 + (row0 + q * R + s) / p.g;
 #pragma unroll
                         for (int bx = 0; bx < C::kBoxes; ++bx)
-                            tma_load_3d(qs + bx * (kM * 128) + (32 * q + s + (KT<RM>::kEW ? 16 * (slot_it & 1) : 0)) * 128, &tmQ, &bars->q_full[qb],
-                                        bx * 64, x.kvh * p.g, node);
+                            tma_load_3d(qs + bx * (kM * 128) +
+                                            (KT<RM>::kEW ? (kM64 ? 64 * (slot_it & 1) + 16 * q + s : 32 * q + s + 16 * (slot_it & 1))
+                                                          : 32 * q + s) * 128,
+                                        &tmQ, &bars->q_full[qb], bx * 64, x.kvh * p.g, node);
                     }
             }
             __syncwarp();
@@ -489,7 +500,8 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     } else if (warp == 1) {
         // ============================ MMA issuer: S = Q K^T ============================
         // Runs ahead as far as the S double buffer allows (S_J needs S_{J-2} consumed).
-        constexpr uint32_t idS = idesc_bf16_f32(kM, kBlockN, 0);
+        constexpr bool S64 = KT<RM>::kEW && kM64;
+        constexpr uint32_t idS = idesc_bf16_f32(S64 ? 64 : kM, kBlockN, 0);
         const uint32_t sbase = smem_u32(smem);
         uint32_t sJ = 0;
         int it = 0;
@@ -511,13 +523,14 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             const int nv = DU ? 2 * nblk : nblk;
             for (int j = 0; j < nv; ++j, ++sJ) {
                 const uint32_t kJ = DU ? (sJ >> 1) : sJ;
-                const uint32_t qa = sbase + C::kOffQ + (DU ? (sJ & 1) : qb) * C::kQStride;
+                // (M = 64: the item's 64 Q rows are contiguous at half it & 1 of the tile)
+                const uint32_t qa = sbase + C::kOffQ + (DU ? (sJ & 1) : qb) * C::kQStride + (S64 ? (it & 1) * 64 * 128 : 0);
                 if (!DU || (sJ & 1) == 0) mbar_wait(&bars->k_full[kJ % C::KS], (kJ / C::KS) & 1);
                 if (lane == 0) TRACE(sJ, 8);
                 mbar_wait(&bars->s_free[sJ & 1], ((sJ >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t ka = sbase + C::kOffK + (kJ % C::KS) * C::kKVBytes;
-                const uint32_t sd = tmem + C::kColS + (sJ & 1) * kBlockN;
+                const uint32_t sd = tmem + C::kColS + (sJ & 1) * kBlockN + (S64 ? (uint32_t)(16 * (it & 1)) << 16 : 0u);
                 if (elect_one()) {
 #pragma unroll
                     for (int k = 0; k < ((p.dbg & 16) ? 0 : D / 16); ++k) {
@@ -545,7 +558,8 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         }
     } else if (warp == 2) {
         // ============================ MMA issuer: O += P V ============================
-        constexpr uint32_t idPV = idesc_bf16_f32(kM, D, 1);
+        constexpr bool P64 = KT<RM>::kEW && kM64;
+        constexpr uint32_t idPV = idesc_bf16_f32(P64 ? 64 : kM, D, 1);
         const uint32_t sbase = smem_u32(smem);
         uint32_t pJ = 0;
         int it = 0;
@@ -590,9 +604,10 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 // after the epilogue of item it-2 released it, so PV needs no wait here)
                 if (!KT<RM>::kEW && j == 0) mbar_wait(&bars->o_free, (it & 1) ^ 1);
                 tc_fence_after();
-                const uint32_t pa = tmem + C::kColP + (pJ & 1) * (kBlockN / 2);
+                const uint32_t lh = P64 ? (uint32_t)(16 * (it & 1)) << 16 : 0u;   // the item's lane half
+                const uint32_t pa = tmem + C::kColP + (pJ & 1) * (kBlockN / 2) + lh;
                 const uint32_t va = sbase + C::kOffV + (vJ % C::VS) * C::kKVBytes;
-                const uint32_t od = tmem + (pJ & 1) * D;
+                const uint32_t od = tmem + (pJ & 1) * D + lh;
                 if (elect_one()) {
                     TRACE(pJ, 5);
 #pragma unroll
