@@ -606,7 +606,8 @@ def run_ours(args, world, rank, local):
     path_np, acc_np = res["path"], res["accepted_len"]
     moves = int(sum(int(np.sum(path_np[i, 1:acc_np[i] + 1] != np.arange(1, acc_np[i] + 1))) for i in range(b["B"])))
     esz = 2 if lm is not None or b["logits"].dtype == torch.bfloat16 else 4
-    acc_bytes = tokens_per_step * cfg.V * (esz + (4 if mode == core.SAMPLE_MSS else 0))   # visited rows
+    qsz = (b["draft_probs"].element_size() if mode == core.SAMPLE_MSS else 0)
+    acc_bytes = tokens_per_step * cfg.V * (esz + qsz)   # visited rows (logits + MSS draft row)
     cmp_bytes = 2 * moves * step.L * 4 * cfg.Hkv * cfg.d
     kernels = {
         "attention": {"ms_per_step": round(attn_ms, 4), "launches": step.L, "bytes": by * step.L,
@@ -931,7 +932,7 @@ def run_e2e(step, b, n_steps, tokens_per_step, world, dev, barrier, mode, temper
     h_outs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in outs[0]]
     h2d = sum(t.numel() * t.element_size() for t in h_ins + h_meta)
     if h_draft is not None:
-        h2d += h_draft.numel() * 4
+        h2d += h_draft.numel() * h_draft.element_size()
     d2h = sum(t.numel() * t.element_size() for t in h_outs)
     copied = [torch.cuda.Event() for _ in range(2)]
     done = [torch.cuda.Event() for _ in range(2)]

@@ -225,6 +225,15 @@ rs_status rs_tree_verify_attention_layers(
  *               aligned (MSS keeps each sample's residual weights there; 0 bytes otherwise:
  *               NULL allowed); too small -> RS_ERR_WORKSPACE. */
 size_t rs_tree_accept_workspace_bytes(int32_t mode, int32_t B, int32_t V);
+/* As rs_tree_accept with the draft probabilities' dtype given: draft_dtype RS_DTYPE_F32 or
+ * RS_DTYPE_BF16 (a bf16 value is used as the fp32 number it denotes, so the arithmetic of
+ * "Bit-exact sampling" is unchanged; a bf16 row is 2/3 of the bytes). rs_tree_accept = the F32 form. */
+rs_status rs_tree_accept_ex(int32_t mode, const void* logits, int32_t logits_dtype, const void* draft_probs,
+                            int32_t draft_dtype, const int32_t* parent, const int32_t* token,
+                            const int32_t* tree_off, const int64_t* gid, int32_t B, int32_t V,
+                            float temperature, uint64_t seed, uint64_t step, int32_t* accepted_len,
+                            int32_t* path, int32_t* bonus_token, int32_t* status_flags, void* ws,
+                            size_t ws_bytes, void* stream);
 rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t logits_dtype,
                          const float* draft_probs, const int32_t* parent, const int32_t* token,
                          const int32_t* tree_off, const int64_t* gid, int32_t B, int32_t V,

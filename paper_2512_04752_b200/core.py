@@ -53,6 +53,8 @@ _sig("rs_tree_verify_attention_layers", _i32, _P, _i32, _P, _P, _P, _i64, _P, _i
 _sig("rs_tree_accept", _i32, _i32, _P, _i32, _P, _P, _P, _P, _P, _i32, _i32, _f32, _u64, _u64, _P, _P,
      _P, _P, _P, _sz, _P)
 _sig("rs_tree_accept_workspace_bytes", _sz, _i32, _i32, _i32)
+_sig("rs_tree_accept_ex", _i32, _i32, _P, _i32, _P, _i32, _P, _P, _P, _P, _i32, _i32, _f32, _u64, _u64, _P, _P,
+     _P, _P, _P, _sz, _P)
 _sig("rs_philox4x32_10", _i32, _P, _i64, _P, _P, _P)
 _sig("rs_exp_spec", _i32, _P, _i64, _P, _P)
 _sig("rs_kv_compact", _i32, _P, _P, _i32, _i64, _i32, _i32, _i32, _P, _i32, _P, _P, _P, _i32, _P, _P, _P)
@@ -248,10 +250,11 @@ def tree_accept(mode, logits, parent, token, tree_off, gid, draft_probs=None, te
         out = (torch.empty(B, dtype=torch.int32, device=dev), torch.empty((B, MAX_TREE), dtype=torch.int32, device=dev),
                torch.empty(B, dtype=torch.int32, device=dev), torch.empty(B, dtype=torch.int32, device=dev))
     acc, path, bonus, flags = out
-    _check(_lib.rs_tree_accept(int(mode), _ptr(logits), dt, _ptr(draft_probs), _ptr(parent), _ptr(token),
-                               _ptr(tree_off), _ptr(gid), B, V, float(temperature), int(seed), int(step), _ptr(acc),
-                               _ptr(path), _ptr(bonus), _ptr(flags), _ptr(ws) if need else None,
-                               ws.numel() if need else 0, _stream(stream)), "rs_tree_accept")
+    qdt = DTYPE_BF16 if (draft_probs is not None and draft_probs.dtype == torch.bfloat16) else DTYPE_F32
+    _check(_lib.rs_tree_accept_ex(int(mode), _ptr(logits), dt, _ptr(draft_probs), qdt, _ptr(parent), _ptr(token),
+                                  _ptr(tree_off), _ptr(gid), B, V, float(temperature), int(seed), int(step), _ptr(acc),
+                                  _ptr(path), _ptr(bonus), _ptr(flags), _ptr(ws) if need else None,
+                                  ws.numel() if need else 0, _stream(stream)), "rs_tree_accept_ex")
     return acc, path, bonus, flags
 
 

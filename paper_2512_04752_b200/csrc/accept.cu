@@ -876,9 +876,9 @@ __device__ __forceinline__ uint32_t r96_shr32(const R96& r, int t) {
     return t < 32 ? __funnelshift_rc(r.r0, r.r1, t) : __funnelshift_rc(r.r1, r.r2, t - 32);
 }
 
-template <int DT>
+template <int DT, int DQ>   // DT: logits dtype, DQ: draft-probability dtype (bf16 values are exact fp32)
 __global__ void __launch_bounds__(kMssThreads, 3)
-mss_accept_kernel(const void* __restrict__ logits, const float* __restrict__ draft,
+mss_accept_kernel(const void* __restrict__ logits, const void* __restrict__ draft,
                   const int32_t* __restrict__ parent, const int32_t* __restrict__ token,
                   const int32_t* __restrict__ tree_off, const int64_t* __restrict__ gid, int V, float inv_tau,
                   uint64_t seed, uint64_t step, int32_t* __restrict__ acc_out, int32_t* __restrict__ path_out,
@@ -936,7 +936,7 @@ mss_accept_kernel(const void* __restrict__ logits, const float* __restrict__ dra
     };
     for (;;) {
         const RowView lv{logits, (int64_t)(off + c), V, DT, logits_vec_ok};
-        const RowView qv{draft, (int64_t)(off + c), V, RS_DTYPE_F32, draft_vec_ok};
+        const RowView qv{draft, (int64_t)(off + c), V, DQ, draft_vec_ok};
         // ---- pass L: the row from HBM into shared memory; max, validity, Zq
         // (bf16 logits stay packed: the first 16 bytes of the vector's w words hold the 8 raw
         // values until pass E expands them)
@@ -957,7 +957,15 @@ mss_accept_kernel(const void* __restrict__ logits, const float* __restrict__ dra
                     const int i = i0 + u * kMssThreads;
                     if (i >= vend) continue;
                     const bool full = (i + 1) * 8 <= V;
-                    const uint32_t qb[8] = {q[u].a.x, q[u].a.y, q[u].a.z, q[u].a.w, q[u].b.x, q[u].b.y, q[u].b.z, q[u].b.w};
+                    uint32_t qb[8];
+                    if (DQ == RS_DTYPE_BF16) {   // bf16 -> the fp32 bit pattern of the same value
+                        const uint32_t h4[4] = {q[u].a.x, q[u].a.y, q[u].a.z, q[u].a.w};
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) { qb[2 * k] = h4[k] << 16; qb[2 * k + 1] = h4[k] & 0xFFFF0000u; }
+                    } else {
+                        qb[0] = q[u].a.x; qb[1] = q[u].a.y; qb[2] = q[u].a.z; qb[3] = q[u].a.w;
+                        qb[4] = q[u].b.x; qb[5] = q[u].b.y; qb[6] = q[u].b.z; qb[7] = q[u].b.w;
+                    }
                     uint32_t qe[8], qu[8];
                     if (full) {
 #pragma unroll
@@ -1210,22 +1218,29 @@ static size_t mss_smem_bytes(int nvec, int cs) {
 
 // MSS launch: cluster size = 16 (non-portable) when the device can co-schedule it, else 8, and
 // never more CTAs than give every CTA >= 256 vectors; dynamic shared memory = per * 64 bytes.
-static rs_status launch_mss(bool bf, const void* logits, const float* draft, const int32_t* parent,
+static rs_status launch_mss(bool bf, bool qbf, const void* logits, const void* draft, const int32_t* parent,
                             const int32_t* token, const int32_t* tree_off, const int64_t* gid, int B, int V,
                             float inv_tau, uint64_t seed, uint64_t step, int32_t* acc, int32_t* path, int32_t* bonus,
                             int32_t* flags, bool lvec, bool dvec, cudaStream_t st) {
-    auto kern = bf ? mss_accept_kernel<RS_DTYPE_BF16> : mss_accept_kernel<RS_DTYPE_F32>;
+    auto kern = bf ? (qbf ? mss_accept_kernel<RS_DTYPE_BF16, RS_DTYPE_BF16> : mss_accept_kernel<RS_DTYPE_BF16, RS_DTYPE_F32>)
+                   : (qbf ? mss_accept_kernel<RS_DTYPE_F32, RS_DTYPE_BF16> : mss_accept_kernel<RS_DTYPE_F32, RS_DTYPE_F32>);
     const int nvec = (V + 7) / 8;
     static int max_cs = 0;            // 16 if a 16-CTA cluster of this kernel can be resident, else 8
-    static size_t attr_smem[2] = {0, 0};
+    static size_t attr_smem[4] = {0, 0, 0, 0};
     int cs = 1;
     while (cs < 16 && nvec / (cs * 2) >= kMssThreads) cs *= 2;
     const size_t smem = mss_smem_bytes(nvec, cs);
-    size_t& cur = attr_smem[bf ? 0 : 1];
+    size_t& cur = attr_smem[(bf ? 0 : 1) + (qbf ? 2 : 0)];
     if (cur < smem) {
         RS_REQUIRE(smem <= 200 * 1024, RS_ERR_UNSUPPORTED, "rs_tree_accept: V=%d too large for MSS", V);
         RS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         cur = smem;
+    }
+    static bool nonportable[4] = {false, false, false, false};
+    if (!nonportable[(bf ? 0 : 1) + (qbf ? 2 : 0)]) {   // per template instance
+        nonportable[(bf ? 0 : 1) + (qbf ? 2 : 0)] = true;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaGetLastError();
     }
     if (max_cs == 0) {
         max_cs = 8;
@@ -1272,6 +1287,14 @@ static rs_status launch_mss(bool bf, const void* logits, const float* draft, con
     return RS_OK;
 }
 
+extern "C" rs_status rs_tree_accept_ex(int32_t mode, const void* logits, int32_t logits_dtype,
+                                       const void* draft_probs, int32_t draft_dtype, const int32_t* parent,
+                                       const int32_t* token, const int32_t* tree_off,
+                                       const int64_t* gid, int32_t B, int32_t V, float temperature,
+                                       uint64_t seed, uint64_t step, int32_t* accepted_len,
+                                       int32_t* path, int32_t* bonus_token, int32_t* status_flags,
+                                       void* ws, size_t ws_bytes, void* stream);
+
 extern "C" rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t logits_dtype,
                                     const float* draft_probs, const int32_t* parent,
                                     const int32_t* token, const int32_t* tree_off,
@@ -1279,11 +1302,25 @@ extern "C" rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t lo
                                     uint64_t seed, uint64_t step, int32_t* accepted_len,
                                     int32_t* path, int32_t* bonus_token, int32_t* status_flags,
                                     void* ws, size_t ws_bytes, void* stream) {
+    return rs_tree_accept_ex(mode, logits, logits_dtype, draft_probs, RS_DTYPE_F32, parent, token, tree_off, gid, B,
+                             V, temperature, seed, step, accepted_len, path, bonus_token, status_flags, ws, ws_bytes,
+                             stream);
+}
+
+extern "C" rs_status rs_tree_accept_ex(int32_t mode, const void* logits, int32_t logits_dtype,
+                                       const void* draft_probs, int32_t draft_dtype, const int32_t* parent,
+                                       const int32_t* token, const int32_t* tree_off,
+                                       const int64_t* gid, int32_t B, int32_t V, float temperature,
+                                       uint64_t seed, uint64_t step, int32_t* accepted_len,
+                                       int32_t* path, int32_t* bonus_token, int32_t* status_flags,
+                                       void* ws, size_t ws_bytes, void* stream) {
     RS_REQUIRE(mode == RS_ACCEPT_GREEDY || mode == RS_ACCEPT_SAMPLE_DELTA ||
                    mode == RS_ACCEPT_SAMPLE_MSS,
                RS_ERR_INVALID_ARG, "rs_tree_accept: bad mode %d", mode);
     RS_REQUIRE(logits_dtype == RS_DTYPE_BF16 || logits_dtype == RS_DTYPE_F32, RS_ERR_INVALID_ARG,
                "rs_tree_accept: bad logits dtype %d", logits_dtype);
+    RS_REQUIRE(draft_dtype == RS_DTYPE_BF16 || draft_dtype == RS_DTYPE_F32, RS_ERR_INVALID_ARG,
+               "rs_tree_accept: bad draft dtype %d", draft_dtype);
     RS_REQUIRE(B >= 0 && V >= 1, RS_ERR_INVALID_ARG, "rs_tree_accept: B=%d V=%d", B, V);
     RS_REQUIRE((mode == RS_ACCEPT_SAMPLE_MSS) == (draft_probs != nullptr), RS_ERR_INVALID_ARG,
                "rs_tree_accept: draft_probs must be given for MSS only");
@@ -1307,7 +1344,8 @@ extern "C" rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t lo
     const float inv_tau = (mode == RS_ACCEPT_GREEDY) ? 1.0f : 1.0f / temperature;
     const int esz = logits_dtype == RS_DTYPE_BF16 ? 2 : 4;
     const bool lvec = ((reinterpret_cast<uintptr_t>(logits) & 15) == 0) && ((int64_t)V * esz % 16 == 0);
-    const bool dvec = draft_probs && ((reinterpret_cast<uintptr_t>(draft_probs) & 15) == 0) && (V % 4 == 0);
+    const bool dvec = draft_probs && ((reinterpret_cast<uintptr_t>(draft_probs) & 15) == 0) &&
+                      (V % (draft_dtype == RS_DTYPE_BF16 ? 8 : 4) == 0);
     // -DRS_ACC_PF=1: speculative L2 prefetch of the children rows (greedy). Measured on config 2:
     // 34.7 -> 38.1 us (2.2x the DRAM bytes; the walk is bound by the cluster barriers), so off.
     constexpr int pf = RS_ACC_PF;
@@ -1323,7 +1361,7 @@ extern "C" rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t lo
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const bool bf = logits_dtype == RS_DTYPE_BF16;
-    if (mode == RS_ACCEPT_SAMPLE_MSS) return launch_mss(bf, logits, draft_probs, parent, token, tree_off, gid, B, V,
+    if (mode == RS_ACCEPT_SAMPLE_MSS) return launch_mss(bf, draft_dtype == RS_DTYPE_BF16, logits, draft_probs, parent, token, tree_off, gid, B, V,
                                                         inv_tau, seed, step, accepted_len, path, bonus_token,
                                                         status_flags, lvec, dvec, cfg.stream);
     auto kern = mode == RS_ACCEPT_GREEDY
@@ -1333,7 +1371,7 @@ extern "C" rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t lo
                           : tree_accept_kernel<RS_ACCEPT_SAMPLE_DELTA, RS_DTYPE_F32>)
                     : (bf ? tree_accept_kernel<RS_ACCEPT_SAMPLE_MSS, RS_DTYPE_BF16>
                           : tree_accept_kernel<RS_ACCEPT_SAMPLE_MSS, RS_DTYPE_F32>);
-    RS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, (int)mode, logits, (int)logits_dtype, draft_probs, parent, token,
+    RS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, (int)mode, logits, (int)logits_dtype, static_cast<const float*>(draft_probs), parent, token,
                                      tree_off, gid, (int)V, inv_tau, seed, step, accepted_len, path, bonus_token,
                                      status_flags, lvec, dvec, static_cast<uint32_t*>(need ? ws : nullptr), pf));
     return RS_OK;

@@ -49,6 +49,7 @@ class VerifyConfig:
     temperature: float = 1.0
     q_scale: float = 1.0
     target_noise: float = 1.0                # sampling: sigma of target-vs-draft logit noise
+    draft_dtype: str = "f32"                 # MSS draft probabilities: "f32" | "bf16" (the SSM's dtype)
     seed: int = 0
 
     @property
@@ -73,7 +74,7 @@ CONFIGS = {
     # (trees given to make_verify_batch by the caller, which runs the selector)
     "c3s": VerifyConfig("c3s", B=256, Hq=32, Hkv=8, d=128, V=128256, L=32,
                         prefix=("lognormal", 2048, 0.784, 512, 16384), tree=("strategy", 96),
-                        mode="mss"),
+                        mode="mss", draft_dtype="bf16"),
     "c5g8": VerifyConfig("c5g8", B=16, Hq=64, Hkv=8, d=128, V=128256, L=80, prefix=("fixed", 8192),
                          tree=("fixed", 64), mode="greedy"),
 }
@@ -250,6 +251,8 @@ def _make_logits(cfg, rng, gen, gen_device, device, parents, tree_off, token, NT
         # draft distribution q_c per row (the SSM's output at node c)
         z = torch.randn((NT, V), generator=gen, device=gen_device, dtype=torch.float32) * 3.0
         q = torch.softmax(z, dim=-1)
+        if cfg.mode == "mss" and cfg.draft_dtype == "bf16":
+            q = q.to(torch.bfloat16).float()   # the distribution the children are drawn from and tested with
         tok = torch.from_numpy(token.astype(np.int64)).to(gen_device)
         for b in range(cfg.B):
             off = int(tree_off[b])
@@ -266,7 +269,10 @@ def _make_logits(cfg, rng, gen, gen_device, device, parents, tree_off, token, NT
         target = torch.log(q) + cfg.target_noise * torch.randn(
             (NT, V), generator=gen, device=gen_device, dtype=torch.float32)
         res["logits"] = target.to(torch.bfloat16).to(device)
-        res["draft_probs"] = q.to(device) if cfg.mode == "mss" else None
+        if cfg.mode == "mss":
+            res["draft_probs"] = (q.to(torch.bfloat16) if cfg.draft_dtype == "bf16" else q).to(device)
+        else:
+            res["draft_probs"] = None
     return res
 
 

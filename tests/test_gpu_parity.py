@@ -114,7 +114,7 @@ def _run_accept_both(core, b, logits, mode, temperature=1.0, seed=11, step=3, pa
     g = [x.cpu().numpy() for x in g]
     lg = tensor_bf16_bits(logits) if logits.dtype == torch.bfloat16 else logits.numpy()
     o = OAcc.tree_accept(mode, lg, parent, b["token"], b["tree_off"], b["gid"], b["V"],
-                         draft_probs=None if dp is None else dp.numpy(), temperature=temperature,
+                         draft_probs=None if dp is None else dp.float().numpy(), temperature=temperature,
                          seed=seed, step=step)
     return g, o
 
@@ -143,13 +143,17 @@ def test_accept_greedy_bit_exact(cuda_lib, cfgname):
         np.testing.assert_array_equal(x, y)
 
 
-@pytest.mark.parametrize("mode,V,temp", [("delta", 1000, 1.0), ("mss", 1000, 1.0), ("mss", 1000, 0.7),
-                                         ("delta", 128256, 1.0), ("mss", 128256, 1.3)])
-def test_accept_sampling_bit_exact(cuda_lib, mode, V, temp):
+@pytest.mark.parametrize("mode,V,temp,qdt", [("delta", 1000, 1.0, "f32"), ("mss", 1000, 1.0, "f32"),
+                                             ("mss", 1000, 0.7, "f32"), ("mss", 1000, 1.0, "bf16"),
+                                             ("delta", 128256, 1.0, "f32"), ("mss", 128256, 1.3, "f32"),
+                                             ("mss", 128256, 1.0, "bf16"), ("mss", 1003, 1.0, "bf16")])
+def test_accept_sampling_bit_exact(cuda_lib, mode, V, temp, qdt):
+    """DELTA / MSS vs the oracle, bit for bit; bf16 draft rows (rs_tree_accept_ex) against the
+    oracle fed the same values as fp32 (V = 1003: rows not 16-byte aligned, the scalar path)."""
     core = cuda_lib
     B = 24 if V < 5000 else 4
     cfg = VerifyConfig("s", B=B, Hq=4, Hkv=1, d=64, V=V, L=1, prefix=("fixed", 5), tree=("range", 2, 40),
-                       mode=mode, seed=7 + V % 13)
+                       mode=mode, seed=7 + V % 13, draft_dtype=qdt)
     b, logits = _accept_case(cfg)
     m = core.SAMPLE_DELTA if mode == "delta" else core.SAMPLE_MSS
     for step in range(3):
@@ -479,7 +483,7 @@ def test_accept_mss_full_config3s_bit_exact(cuda_lib):
         sl = slice(int(to[s]), int(to[s + 1]))
         lg = tensor_bf16_bits(b["logits"][sl].cpu())
         o = OAcc.tree_accept(OAcc.MSS, lg, b["parent"][sl], b["token"][sl], np.array([0, sl.stop - sl.start]),
-                             b["gid"][s:s + 1], b["V"], draft_probs=b["draft_probs"][sl].cpu().numpy(),
+                             b["gid"][s:s + 1], b["V"], draft_probs=b["draft_probs"][sl].float().cpu().numpy(),
                              temperature=1.0, seed=11, step=0)
         assert g[0][s] == o[0][0] and g[2][s] == o[2][0] and g[3][s] == o[3][0], s
         np.testing.assert_array_equal(g[1][s], o[1][0])
