@@ -80,7 +80,7 @@ rs_status rs_tree_build_mask(const int32_t* parent, const int32_t* tree_off, int
  * [rows, V] logits are never written.
  *   hidden   device bf16 [rows, Dm] (final hidden state of each tree node, node-major as Q)
  *   weight   device bf16 [V, Dm] (nn.Linear layout); both 16-byte aligned; Dm % 64 == 0
- *   argmax_token device int32 [rows] out (-1 if a row's logits are all NaN)
+ *   argmax_token device int32 [rows] out (-1 if any logit of the row is NaN or +-Inf: no arg-max, Z15)
  *   max_logit    device fp32 [rows] out (the fp32 maximum), or NULL
  *   ws, ws_bytes device workspace >= rs_lm_head_argmax_workspace_bytes(rows), 8-byte aligned
  * Launches a memset, the GEMM kernel and a finalize kernel on `stream`. */

@@ -34,10 +34,16 @@ def lm_head_logits(hidden, weight):
 
 
 def argmax_rows(logits):
-    """Per-row arg-max (np.argmax returns the first maximal index = lowest vocab id) and max."""
+    """Per-row arg-max (np.argmax returns the first maximal index = lowest vocab id) and max. A
+    row holding any non-finite logit has no arg-max: -1 and NaN (reading Z15: such a row stops
+    the greedy walk with RS_FLAG_NONFINITE, whichever path computed the logits)."""
     lg = np.asarray(logits)
     idx = np.argmax(lg, axis=1).astype(np.int32)
-    return idx, lg[np.arange(lg.shape[0]), idx]
+    mx = lg[np.arange(lg.shape[0]), idx].astype(np.float64)
+    bad = ~np.all(np.isfinite(lg), axis=1)
+    idx[bad] = -1
+    mx[bad] = np.nan
+    return idx, mx
 
 
 def lm_head_argmax(hidden, weight):

@@ -139,6 +139,7 @@ lm_head_argmax_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_cons
             const bool full_tile = v0 + kBN <= V;
             float best = -INFINITY;
             int bi = -1;
+            uint32_t amag = 0;   // max |x| bits of the row's valid columns: >= 0x7F800000 <=> Inf / NaN
 #pragma unroll 1
             for (int c = 0; c < kBN; c += 64) {
                 uint32_t r0[32], r1[32];
@@ -149,22 +150,26 @@ lm_head_argmax_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_cons
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         const float x = __uint_as_float(r0[j]);
+                        amag = max(amag, r0[j] & 0x7FFFFFFFu);
                         if (x > best) { best = x; bi = v0 + c + j; }
                     }
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         const float x = __uint_as_float(r1[j]);
+                        amag = max(amag, r1[j] & 0x7FFFFFFFu);
                         if (x > best) { best = x; bi = v0 + c + 32 + j; }
                     }
                 } else {
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         const float x = __uint_as_float(r0[j]);
+                        if (v0 + c + j < V) amag = max(amag, r0[j] & 0x7FFFFFFFu);
                         if (v0 + c + j < V && x > best) { best = x; bi = v0 + c + j; }
                     }
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         const float x = __uint_as_float(r1[j]);
+                        if (v0 + c + 32 + j < V) amag = max(amag, r1[j] & 0x7FFFFFFFu);
                         if (v0 + c + 32 + j < V && x > best) { best = x; bi = v0 + c + 32 + j; }
                     }
                 }
@@ -173,7 +178,10 @@ lm_head_argmax_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_cons
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars->acc_empty[a]);
             const int row = m * kBM + q * 32 + lane;
-            if (row < rows && bi >= 0) atomicMax(&keys[row], argmax_key(best, bi));
+            // a non-finite logit anywhere in the row: the all-ones key (above every real key) marks
+            // it and finalize reports no arg-max (-1), as rs_tree_accept flags such a row (Z15)
+            if (row < rows && amag >= 0x7F800000u) atomicMax(&keys[row], ~0ull);
+            else if (row < rows && bi >= 0) atomicMax(&keys[row], argmax_key(best, bi));
         }
     }
     tc_fence_before();
@@ -186,7 +194,7 @@ __global__ void lm_head_finalize_kernel(const unsigned long long* __restrict__ k
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= rows) return;
     const unsigned long long k = keys[r];
-    if (k == 0) {                              // every logit NaN: no arg-max
+    if (k == 0 || k == ~0ull) {                // a non-finite logit in the row (or no columns): no arg-max
         tok[r] = -1;
         if (mx) mx[r] = __uint_as_float(0x7fc00000u);
         return;

@@ -94,6 +94,25 @@ def test_lm_head_argmax_nan_row(cuda_lib):
     _check_rows(tok[ok], mx.cpu().numpy()[ok], Hd.double().cpu().numpy()[ok], W, min_exact=0.9)
 
 
+def test_lm_head_argmax_single_inf_logit(cuda_lib):
+    """A row with ONE +Inf logit (fp32 overflow of one product) has no arg-max (-1; Z15 on the
+    fused path, as the oracle's argmax_rows); without the rule the +Inf column would win."""
+    rng = np.random.default_rng(7)
+    H = rng.standard_normal((40, 128))
+    H[:, 0] = np.abs(H[:, 0]) + 0.5                 # every row prefers column 5 (finite)...
+    H[9, 0] = 1e4                                   # ...row 9 overflows there: logit ~ 1e40 -> +Inf
+    W0 = rng.standard_normal((300, 128))
+    W0[5, 0] = 1e36
+    Hd, W = _dev_bf16(H), _dev_bf16(W0)
+    tok, _ = cuda_lib.lm_head_argmax(Hd, W)
+    torch.cuda.synchronize()
+    tok = tok.cpu().numpy()
+    ref, _ = LH.argmax_rows((Hd.double().cpu().numpy() @ W.double().cpu().numpy().T).astype(np.float32))
+    assert tok[9] == -1 and ref[9] == -1
+    others = np.arange(40) != 9
+    assert np.all(tok[others] == 5) and np.all(ref[others] == 5)
+
+
 @pytest.mark.parametrize("name,Dm", [("c2", 4096), ("c5g8", 8192)])
 def test_lm_head_full_size_sampled(cuda_lib, name, Dm):
     """Full config size (c2: 1024 rows x V 128256 x 4096; c5g8: 1024 x 128256 x 8192) in the

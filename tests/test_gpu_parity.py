@@ -425,6 +425,21 @@ def test_attention_full_config5_sampled(cuda_lib):
     np.testing.assert_allclose(lg, lref, atol=2e-2, rtol=1e-3)
 
 
+@pytest.mark.parametrize("gpus", [2, 4])
+def test_attention_full_config5_shard_sampled(cuda_lib, gpus):
+    """BASELINE configs[4] per-GPU shard at G = 2 / 4 (B = 128/G = 64 / 32 samples, P = 8K,
+    T = 64, 64/8 heads), as bench.py --config c5 --gpus G runs each rank; one layer, oracle on 3
+    sampled samples (first, middle, last)."""
+    cfg = CONFIGS["c5g8"]
+    cfg = type(cfg)(**{**cfg.__dict__, "name": "c5", "B": 128 // gpus})
+    b = make_verify_batch(cfg, device="cuda", gen_device="cuda", layers=1, with_logits=False)
+    for k in ("q", "k_cache", "v_cache"):
+        b[k] = b[k].cpu()
+    og, oref, lg, lref, info = _run_attention(cuda_lib, b, samples=[0, cfg.B // 2, cfg.B - 1])
+    mae, rel = _attn_errors(og, oref)
+    assert mae <= ATOL and rel <= RTOL_L2, (mae, rel, info)
+
+
 def test_attention_full_config2_sampled(cuda_lib):
     """BASELINE configs[1] at full size (B=64, P=1K, T=16, 32/8 heads), in the launch
     configuration bench.py times (plan over all SMs); oracle on 6 sampled samples."""

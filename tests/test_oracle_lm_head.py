@@ -135,3 +135,16 @@ def test_walk_special_cases():
     par = np.array([-1, 0, 0, 2]); tok = np.array([0, 4, 4, 5]); am = np.array([4, 9, 5, 1])
     acc, path, bonus = LH.greedy_walk(am, par, tok, np.array([0, 4]))
     assert acc[0] == 1 and path[0, :2].tolist() == [0, 1] and bonus[0] == 9
+
+
+def test_nonfinite_rows_have_no_argmax():
+    """Z15 on the fused path: a row with any NaN or +-Inf logit has no arg-max (-1, NaN), so the
+    walk stops there with RS_FLAG_NONFINITE exactly as rs_tree_accept does on logits; finite
+    rows are untouched (a +Inf would otherwise win, a NaN would be skipped)."""
+    lg = np.array([[0.0, 3.0, 1.0], [0.0, np.inf, 1.0], [np.nan, 3.0, 5.0], [-np.inf, -1.0, -2.0]])
+    idx, mx = LH.argmax_rows(lg)
+    assert idx.tolist() == [1, -1, -1, -1]
+    assert mx[0] == 3.0 and np.isnan(mx[1:]).all()
+    acc, path, bonus = LH.greedy_walk(np.array([-1, 5], np.int32), np.array([-1, 0], np.int32),
+                                       np.array([0, 5], np.int32), np.array([0, 2], np.int32))
+    assert acc[0] == 0 and bonus[0] == -1
