@@ -446,7 +446,11 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                         }
                         // a block with a tree slot (slot >= P_b) only after the wait
                         if (!waited && (wi.blk_begin + j + 1) * kBlockN > wi.P) { griddep_wait(); waited = true; }
-                        if (RM != 4 && isK && has_next && j == q_next_at) {
+                        // RM = 1 with static lists: Q(0) and Q(1) here, then the epilogue warpgroup
+                        // issues Q(it + 2) once item it's epilogue is done (issuing Q here stalled
+                        // the K stream ~2 000 cycles per item: eight small 3-D TMA boxes)
+                        const bool ew_static = KT<RM>::kEW && !p.dyn;
+                        if (RM != 4 && isK && has_next && (ew_static ? (it == 0 && j == q0_at) : j == q_next_at)) {
                             if (lane == 0) TRACE(J, 11);   // (profiling: next item's Q issued at block J)
                             issue_q(wn, it + 1);
                         }
@@ -711,6 +715,26 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars->o_free2[h]);
             if (wq == 0 && lane == 0) TRACE(J + nblk - 1, 7);
+            if (wq == 0 && !p.dyn && item_begin + it + 2 < item_end) {
+                // Q of item it + 2 into lane half h (item it's S MMAs are long done: q_empty[h])
+                const WorkItem x = load_item(p.items, item_begin + it + 2);
+                const int qs_it = it + 2;
+                mbar_wait(&bars->q_empty[qs_it & 1], ((qs_it >> 1) & 1) ^ 1);
+                if (elect_one()) {
+                    mbar_arrive_expect_tx(&bars->q_full[qs_it & 1], 4 * x.rstride * 128 * C::kBoxes);
+                    const int row0 = x.mtile * 4 * x.rstride;
+                    for (int q = 0; q < 4; ++q)
+                        for (int s2 = 0; s2 < x.rstride; s2 += 16) {
+                            const int node = x.node0 + (row0 + q * x.rstride + s2) / p.g;
+#pragma unroll
+                            for (int bx = 0; bx < C::kBoxes; ++bx)
+                                tma_load_3d(smem + C::kOffQ + bx * (kM * 128) +
+                                                (kM64 ? 64 * (qs_it & 1) + 16 * q + s2 : 32 * q + s2 + 16 * (qs_it & 1)) * 128,
+                                            &tmQ, &bars->q_full[qs_it & 1], bx * 64, x.kvh * p.g, node);
+                        }
+                }
+                __syncwarp();
+            }
             if (wi.part >= 0) {
                 // split-KV unit: the CTA that completes its last part merges all parts
                 __threadfence();
