@@ -1314,6 +1314,7 @@ extern "C" rs_status rs_tree_accept_ex(int32_t mode, const void* logits, int32_t
                                        uint64_t seed, uint64_t step, int32_t* accepted_len,
                                        int32_t* path, int32_t* bonus_token, int32_t* status_flags,
                                        void* ws, size_t ws_bytes, void* stream) {
+    rs::bind_device(logits);
     RS_REQUIRE(mode == RS_ACCEPT_GREEDY || mode == RS_ACCEPT_SAMPLE_DELTA ||
                    mode == RS_ACCEPT_SAMPLE_MSS,
                RS_ERR_INVALID_ARG, "rs_tree_accept: bad mode %d", mode);
@@ -1379,6 +1380,7 @@ extern "C" rs_status rs_tree_accept_ex(int32_t mode, const void* logits, int32_t
 
 extern "C" rs_status rs_philox4x32_10(const uint32_t* ctr, int64_t n, const uint32_t* key_host,
                                       uint32_t* out, void* stream) {
+    rs::bind_device(ctr);
     RS_REQUIRE(n >= 0 && key_host, RS_ERR_INVALID_ARG, "rs_philox4x32_10: bad args");
     if (n == 0) return RS_OK;
     philox_kernel<<<(unsigned)((n + 255) / 256), 256, 0, rs::as_stream(stream)>>>(
@@ -1389,6 +1391,7 @@ extern "C" rs_status rs_philox4x32_10(const uint32_t* ctr, int64_t n, const uint
 }
 
 extern "C" rs_status rs_exp_spec(const float* x, int64_t n, float* y, void* stream) {
+    rs::bind_device(x);
     RS_REQUIRE(n >= 0, RS_ERR_INVALID_ARG, "rs_exp_spec: n < 0");
     if (n == 0) return RS_OK;
     exp_spec_kernel<<<(unsigned)((n + 255) / 256), 256, 0, rs::as_stream(stream)>>>(x, n, y);

@@ -376,6 +376,7 @@ extern "C" size_t rs_attn_plan_workspace_bytes(const rs_attn_plan* plan) {
 }
 
 extern "C" rs_status rs_attn_plan_upload(const rs_attn_plan* plan, void* ws, size_t ws_bytes, void* stream) {
+    rs::bind_device(ws);
     RS_REQUIRE(plan && ws, RS_ERR_INVALID_ARG, "rs_attn_plan_upload: null pointer");
     RS_REQUIRE(ws_bytes >= plan->ws_bytes, RS_ERR_WORKSPACE, "rs_attn_plan_upload: workspace %zu < %zu",
                ws_bytes, plan->ws_bytes);
@@ -515,6 +516,7 @@ extern "C" rs_status rs_tree_verify_attention(const rs_attn_plan* plan, const vo
                                               int32_t Hkv, int32_t head_dim, int32_t page_size,
                                               float sm_scale, void* out, float* lse, void* ws,
                                               size_t ws_bytes, void* stream) {
+    rs::bind_device(q);
     RS_REQUIRE(plan, RS_ERR_INVALID_ARG, "rs_tree_verify_attention: null plan");
     RS_REQUIRE(plan->B == B && plan->Hq == Hq && plan->Hkv == Hkv && plan->D == head_dim &&
                    plan->ps == page_size,
@@ -543,6 +545,7 @@ extern "C" rs_status rs_tree_verify_attention_layers(
     const int32_t* prefix_len, const int32_t* tree_off, const uint64_t* tree_mask, int32_t B, int32_t Hq,
     int32_t Hkv, int32_t head_dim, int32_t page_size, float sm_scale, void* const* out_layers,
     float* const* lse_layers, void* ws, size_t ws_bytes, void* stream) {
+    rs::bind_device(block_table);
     RS_REQUIRE(L >= 0 && q_layers && k_layers && v_layers && out_layers, RS_ERR_INVALID_ARG,
                "rs_tree_verify_attention_layers: null layer arrays");
     for (int32_t l = 0; l < L; ++l) {

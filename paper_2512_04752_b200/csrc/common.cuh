@@ -13,6 +13,7 @@
 namespace rs {
 
 void set_error(const char* fmt, ...);
+void bind_device(const void* device_ptr);   // make the owner of device_ptr the current device
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

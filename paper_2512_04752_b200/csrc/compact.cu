@@ -122,6 +122,7 @@ extern "C" rs_status rs_kv_compact(void* const* k_layers_host, void* const* v_la
                                    const int32_t* prefix_len, const int32_t* accepted_len,
                                    const int32_t* path, int32_t B, int32_t* new_len,
                                    int32_t* moves, void* stream) {
+    rs::bind_device(block_table);
     (void)num_pages;
     RS_REQUIRE(B >= 0 && L >= 0 && Hkv > 0 && page_size > 0, RS_ERR_INVALID_ARG, "rs_kv_compact: bad sizes");
     RS_REQUIRE(head_dim % 8 == 0, RS_ERR_UNSUPPORTED, "rs_kv_compact: head_dim %% 8 != 0");

@@ -290,6 +290,7 @@ extern "C" size_t rs_lm_head_argmax_workspace_bytes(int32_t rows) {
 extern "C" rs_status rs_lm_head_argmax(const void* hidden, const void* weight, int32_t rows, int32_t V, int32_t Dm,
                                        int32_t* argmax_token, float* max_logit, void* ws, size_t ws_bytes,
                                        void* stream) {
+    rs::bind_device(hidden);
     RS_REQUIRE(rows >= 0 && V >= 1 && Dm >= kBK && Dm % kBK == 0, RS_ERR_INVALID_ARG,
                "rs_lm_head_argmax: rows=%d V=%d Dm=%d (Dm must be a positive multiple of 64)", rows, V, Dm);
     if (rows == 0) return RS_OK;
@@ -338,6 +339,7 @@ extern "C" rs_status rs_tree_accept_greedy_tokens(const int32_t* argmax_token, c
                                                   const int32_t* token, const int32_t* tree_off, int32_t B,
                                                   int32_t* accepted_len, int32_t* path, int32_t* bonus_token,
                                                   int32_t* status_flags, void* stream) {
+    rs::bind_device(argmax_token);
     RS_REQUIRE(B >= 0, RS_ERR_INVALID_ARG, "rs_tree_accept_greedy_tokens: B=%d", B);
     if (B == 0) return RS_OK;
     RS_REQUIRE(argmax_token && parent && token && tree_off && accepted_len && path && bonus_token && status_flags,

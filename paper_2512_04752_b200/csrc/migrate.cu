@@ -108,6 +108,7 @@ extern "C" rs_status rs_kv_pack(void* const* k_layers_host, void* const* v_layer
                                 int32_t head_dim, int32_t page_size, const int32_t* block_table, int32_t max_pages,
                                 const int32_t* sample_rows, const int32_t* lens, int32_t n, void* buf,
                                 int64_t buf_offset_elems, void* stream) {
+    rs::bind_device(block_table);
     return launch_pack<true>(k_layers_host, v_layers_host, L, Hkv, head_dim, page_size, block_table, max_pages,
                              sample_rows, nullptr, lens, n, buf, buf_offset_elems, rs::as_stream(stream));
 }
@@ -117,6 +118,7 @@ extern "C" rs_status rs_kv_pack_range(void* const* k_layers_host, void* const* v
                                       int32_t max_pages, const int32_t* sample_rows, const int32_t* starts,
                                       const int32_t* lens, int32_t n, void* buf, int64_t buf_offset_elems,
                                       void* stream) {
+    rs::bind_device(block_table);
     return launch_pack<true>(k_layers_host, v_layers_host, L, Hkv, head_dim, page_size, block_table, max_pages,
                              sample_rows, starts, lens, n, buf, buf_offset_elems, rs::as_stream(stream));
 }
@@ -126,6 +128,7 @@ extern "C" rs_status rs_kv_unpack_range(void* const* k_layers_host, void* const*
                                         int32_t max_pages, const int32_t* sample_rows, const int32_t* starts,
                                         const int32_t* lens, int32_t n, const void* buf, int64_t buf_offset_elems,
                                         void* stream) {
+    rs::bind_device(block_table);
     return launch_pack<false>(k_layers_host, v_layers_host, L, Hkv, head_dim, page_size, block_table, max_pages,
                               sample_rows, starts, lens, n, const_cast<void*>(buf), buf_offset_elems,
                               rs::as_stream(stream));
@@ -135,6 +138,7 @@ extern "C" rs_status rs_kv_unpack(void* const* k_layers_host, void* const* v_lay
                                   int32_t head_dim, int32_t page_size, const int32_t* block_table, int32_t max_pages,
                                   const int32_t* sample_rows, const int32_t* lens, int32_t n, const void* buf,
                                   int64_t buf_offset_elems, void* stream) {
+    rs::bind_device(block_table);
     return launch_pack<false>(k_layers_host, v_layers_host, L, Hkv, head_dim, page_size, block_table, max_pages,
                               sample_rows, nullptr, lens, n, const_cast<void*>(buf), buf_offset_elems,
                               rs::as_stream(stream));
@@ -303,6 +307,7 @@ extern "C" rs_status rs_migrate_samples(rs_comm* c, int32_t src_rank, int32_t ds
                                         int32_t n, const int32_t* src_block_table, int32_t max_pages,
                                         int32_t* dst_block_table_host, void* staging, size_t staging_bytes,
                                         int32_t* device_scratch, void* stream) {
+    rs::bind_device(device_scratch);
 #ifdef RS_HAVE_NCCL
     RS_REQUIRE(c && kv && n >= 0 && n <= 4096 && src_rank >= 0 && dst_rank >= 0 && src_rank < c->world &&
                    dst_rank < c->world,
@@ -482,6 +487,7 @@ extern "C" rs_status rs_migrate_stage1(rs_comm* c, int32_t src_rank, int32_t dst
                                        const int32_t* reserve_lens_host, int32_t n, const int32_t* src_block_table,
                                        int32_t max_pages, int32_t* dst_block_table_host, void* staging,
                                        size_t staging_bytes, int32_t* device_scratch, void* stream) {
+    rs::bind_device(device_scratch);
 #ifdef RS_HAVE_NCCL
     RS_REQUIRE(c && kv && n >= 0 && n <= 4096 && src_rank >= 0 && dst_rank >= 0 && src_rank < c->world &&
                    dst_rank < c->world,
@@ -561,6 +567,7 @@ extern "C" rs_status rs_migrate_stage2(rs_comm* c, int32_t src_rank, int32_t dst
                                        int32_t* dst_block_table_host, int32_t* dst_capacity_host, void* staging,
                                        size_t staging_bytes, int32_t* device_scratch, void* ssm_ready_event,
                                        void* stream) {
+    rs::bind_device(device_scratch);
 #ifdef RS_HAVE_NCCL
     RS_REQUIRE(c && kv && n >= 0 && n <= 4096 && src_rank >= 0 && dst_rank >= 0 && src_rank < c->world &&
                    dst_rank < c->world,

@@ -139,6 +139,7 @@ extern "C" rs_status rs_peer_create(const rs_kv_desc* kv, int32_t rank, rs_peer*
             rs::set_error("rs_peer_create: null or unaligned pool pointer");
             return RS_ERR_INVALID_ARG;
         }
+    rs::bind_device(p->ptrs.empty() ? nullptr : p->ptrs[0]);   // events on the pools' device
     for (int e = 0; e < 2; ++e)
         if (cudaEventCreateWithFlags(&p->ev[e], cudaEventDisableTiming | cudaEventInterprocess) != cudaSuccess) {
             rs::set_error("rs_peer_create: cudaEventCreate (interprocess) failed");
@@ -232,6 +233,7 @@ extern "C" rs_status rs_peer_import(rs_peer* p, const uint8_t* blob, size_t byte
 extern "C" rs_status rs_peer_push(rs_peer* p, int32_t dst_rank, const int32_t* src_block_table,
                                   const int32_t* dst_block_table, int32_t max_pages, const int32_t* starts,
                                   const int32_t* lens, int32_t n, int32_t parts, void* stream) {
+    rs::bind_device(src_block_table);
     RS_REQUIRE(p && dst_rank >= 0 && dst_rank < kMaxPeers && n >= 0 && n <= 65535 && max_pages > 0 &&
                    parts >= 0 && parts <= 3,
                RS_ERR_INVALID_ARG, "rs_peer_push: bad args");

@@ -56,6 +56,7 @@ tree_mask_kernel(const int32_t* __restrict__ parent, const int32_t* __restrict__
 extern "C" rs_status rs_tree_build_mask(const int32_t* parent, const int32_t* tree_off, int32_t B,
                                         uint64_t* tree_mask, int32_t* depth, int32_t* status_flags,
                                         void* stream) {
+    rs::bind_device(parent);
     RS_REQUIRE(B >= 0, RS_ERR_INVALID_ARG, "rs_tree_build_mask: B < 0");
     if (B == 0) return RS_OK;
     RS_REQUIRE(parent && tree_off && tree_mask && depth, RS_ERR_INVALID_ARG,

@@ -207,6 +207,7 @@ extern "C" rs_status rs_tree_select(const int32_t* cand_parent, const double* ca
                                     const double* knots_x, const double* knots_y, int32_t n_knots,
                                     int32_t* parent_out, int32_t* token_out, uint64_t* tree_mask_out,
                                     int32_t* depth_out, int32_t* status_flags, void* stream) {
+    rs::bind_device(cand_parent);
     RS_REQUIRE(B >= 0, RS_ERR_INVALID_ARG, "rs_tree_select: B < 0");
     RS_REQUIRE(n >= 1 && n + 1 <= RS_MAX_TREE, RS_ERR_UNSUPPORTED, "rs_tree_select: n=%d outside [1, 63]", n);
     RS_REQUIRE(n_knots >= 2 && n_knots <= kMaxKnots, RS_ERR_INVALID_ARG, "rs_tree_select: %d knots", n_knots);

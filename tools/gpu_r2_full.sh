@@ -8,6 +8,6 @@ timeout 1500 python -m pytest tests -m gpu -q --timeout 300 > $OUT/pytest_gpu.lo
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke exit $?" >> $OUT/smoke.log
 timeout 600 python bench.py > $OUT/bench_default.json 2> $OUT/bench_default.err
 timeout 400 python bench.py --config c2 --no-cpu-baseline > $OUT/bench_c2.json 2> $OUT/bench_c2.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches_default.csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"tree_|kv_|attn|mss_|accept|lm_head|walk" -c 400 --csv --log-file $OUT/launches_default.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --force-n 8 > $OUT/ncu_bench.log 2>&1
 tail -3 $OUT/pytest_gpu.log; tail -1 $OUT/smoke.log; cat $OUT/bench_default.json $OUT/bench_c2.json
