@@ -876,8 +876,13 @@ __device__ __forceinline__ uint32_t r96_shr32(const R96& r, int t) {
     return t < 32 ? __funnelshift_rc(r.r0, r.r1, t) : __funnelshift_rc(r.r1, r.r2, t - 32);
 }
 
+// 3 CTAs per SM (registers and 65 KB of shared memory each); with bf16 drafts 49 KB, so 4 fit
+// when the kernel stays within 64 registers (more clusters in flight: the kernel is latency-bound)
+#ifndef RS_MSS_MINB_BF16
+#define RS_MSS_MINB_BF16 4
+#endif
 template <int DT, int DQ>   // DT: logits dtype, DQ: draft-probability dtype (bf16 values are exact fp32)
-__global__ void __launch_bounds__(kMssThreads, 3)
+__global__ void __launch_bounds__(kMssThreads, DQ == RS_DTYPE_BF16 ? RS_MSS_MINB_BF16 : 3)
 mss_accept_kernel(const void* __restrict__ logits, const void* __restrict__ draft,
                   const int32_t* __restrict__ parent, const int32_t* __restrict__ token,
                   const int32_t* __restrict__ tree_off, const int64_t* __restrict__ gid, int V, float inv_tau,
@@ -914,8 +919,11 @@ mss_accept_kernel(const void* __restrict__ logits, const void* __restrict__ draf
     const int per = (nvec + (int)cs - 1) / (int)cs;
     const int vbeg = min(nvec, (int)crank * per), vend = min(nvec, vbeg + per);
     uint32_t* wsl = reinterpret_cast<uint32_t*>(mss_dyn);   // [per * 8]
-    uint32_t* qsl = wsl + (size_t)per * 8;                  // [per * 8]
-    uint8_t* vex = reinterpret_cast<uint8_t*>(qsl + (size_t)per * 8);   // [per] residual vector shift
+    // draft: qw words [per * 8] (fp32 drafts), or the raw bf16 values [per * 8] (bf16 drafts: half
+    // the shared memory, qw = trunc(q * 2^32) recomputed where used)
+    uint32_t* qsl = wsl + (size_t)per * 8;
+    uint16_t* qsl16 = reinterpret_cast<uint16_t*>(qsl);
+    uint8_t* vex = reinterpret_cast<uint8_t*>(qsl) + (size_t)per * 8 * (DQ == RS_DTYPE_BF16 ? 2 : 4);   // [per]
     int c = 0, a = 0, bonus = -1, flags = 0;
     bool bonus_mine = leader;
     if (leader && tid == 0) pth[0] = 0;
@@ -930,7 +938,8 @@ mss_accept_kernel(const void* __restrict__ logits, const void* __restrict__ draf
             if (ti >= vbeg && ti < vend) {
                 const int lo = tk - vbeg * 8;
                 ms.childw[x] = resid_state ? (uint64_t)wsl[lo] : wdec(wsl[lo]);
-                ms.childq[x] = wdec(qsl[lo]);
+                ms.childq[x] = DQ == RS_DTYPE_BF16 ? wdec(f2w(__uint_as_float((uint32_t)qsl16[lo] << 16)))
+                                                   : wdec(qsl[lo]);
             }
         }
     };
@@ -982,9 +991,15 @@ mss_accept_kernel(const void* __restrict__ logits, const void* __restrict__ draf
                     }
                     zq += wsum8(qe);
                     uint4* wp = reinterpret_cast<uint4*>(wsl + (size_t)(i - vbeg) * 8);
-                    uint4* qp = reinterpret_cast<uint4*>(qsl + (size_t)(i - vbeg) * 8);
-                    qp[0] = make_uint4(qe[0], qe[1], qe[2], qe[3]);
-                    qp[1] = make_uint4(qe[4], qe[5], qe[6], qe[7]);
+                    if (DQ == RS_DTYPE_BF16) {   // the raw values back (padding lanes zero)
+                        *reinterpret_cast<uint4*>(qsl16 + (size_t)(i - vbeg) * 8) =
+                            make_uint4((qu[0] >> 16) | (qu[1] & 0xFFFF0000u), (qu[2] >> 16) | (qu[3] & 0xFFFF0000u),
+                                       (qu[4] >> 16) | (qu[5] & 0xFFFF0000u), (qu[6] >> 16) | (qu[7] & 0xFFFF0000u));
+                    } else {
+                        uint4* qp = reinterpret_cast<uint4*>(qsl + (size_t)(i - vbeg) * 8);
+                        qp[0] = make_uint4(qe[0], qe[1], qe[2], qe[3]);
+                        qp[1] = make_uint4(qe[4], qe[5], qe[6], qe[7]);
+                    }
                     if (DT == RS_DTYPE_BF16) {
                         uint32_t w4[4] = {x[u].a.x, x[u].a.y, x[u].a.z, x[u].a.w};
                         uint32_t wm[4] = {w4[0], w4[1], w4[2], w4[3]};   // for the validity check
@@ -1085,10 +1100,23 @@ mss_accept_kernel(const void* __restrict__ logits, const void* __restrict__ draf
             unsigned long long bl = 0, dummy2 = 0;
             for (int i = vbeg + tid; i < vend; i += kMssThreads) {
                 uint4* wp = reinterpret_cast<uint4*>(wsl + (size_t)(i - vbeg) * 8);
-                const uint4* qp = reinterpret_cast<const uint4*>(qsl + (size_t)(i - vbeg) * 8);
-                const uint4 a0 = wp[0], a1 = wp[1], b0 = qp[0], b1 = qp[1];
+                const uint4 a0 = wp[0], a1 = wp[1];
                 const uint32_t ww[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-                const uint32_t qq[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                uint32_t qq[8];
+                if (DQ == RS_DTYPE_BF16) {
+                    const uint4 h = *reinterpret_cast<const uint4*>(qsl16 + (size_t)(i - vbeg) * 8);
+                    const uint32_t h4[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        qq[2 * k] = f2w(__uint_as_float(h4[k] << 16));
+                        qq[2 * k + 1] = f2w(__uint_as_float(h4[k] & 0xFFFF0000u));
+                    }
+                } else {
+                    const uint4* qp = reinterpret_cast<const uint4*>(qsl + (size_t)(i - vbeg) * 8);
+                    const uint4 b0 = qp[0], b1 = qp[1];
+                    qq[0] = b0.x; qq[1] = b0.y; qq[2] = b0.z; qq[3] = b0.w;
+                    qq[4] = b1.x; qq[5] = b1.y; qq[6] = b1.z; qq[7] = b1.w;
+                }
                 R96 r[8];
                 R96 ro{0, 0, 0};   // bitlen(max_j r_j) = bitlen(OR_j r_j)
 #pragma unroll
@@ -1211,9 +1239,9 @@ extern "C" size_t rs_tree_accept_workspace_bytes(int32_t mode, int32_t B, int32_
 }
 
 // per CTA: w and qw words (64 B per 8-token vector) + one residual shift byte per vector
-static size_t mss_smem_bytes(int nvec, int cs) {
+static size_t mss_smem_bytes(int nvec, int cs, bool qbf) {
     const size_t per = (size_t)((nvec + cs - 1) / cs);
-    return (per * 65 + 15) / 16 * 16;
+    return (per * (qbf ? 49 : 65) + 15) / 16 * 16;
 }
 
 // MSS launch: cluster size = 16 (non-portable) when the device can co-schedule it, else 8, and
@@ -1229,7 +1257,7 @@ static rs_status launch_mss(bool bf, bool qbf, const void* logits, const void* d
     static size_t attr_smem[4] = {0, 0, 0, 0};
     int cs = 1;
     while (cs < 16 && nvec / (cs * 2) >= kMssThreads) cs *= 2;
-    const size_t smem = mss_smem_bytes(nvec, cs);
+    const size_t smem = mss_smem_bytes(nvec, cs, qbf);
     size_t& cur = attr_smem[(bf ? 0 : 1) + (qbf ? 2 : 0)];
     if (cur < smem) {
         RS_REQUIRE(smem <= 200 * 1024, RS_ERR_UNSUPPORTED, "rs_tree_accept: V=%d too large for MSS", V);
@@ -1248,7 +1276,7 @@ static rs_status launch_mss(bool bf, bool qbf, const void* logits, const void* d
             cudaLaunchConfig_t q = {};
             q.gridDim = dim3(16);
             q.blockDim = dim3(kMssThreads);
-            q.dynamicSmemBytes = mss_smem_bytes(nvec, 16);
+            q.dynamicSmemBytes = mss_smem_bytes(nvec, 16, qbf);
             cudaLaunchAttribute qa[1];
             qa[0].id = cudaLaunchAttributeClusterDimension;
             qa[0].val.clusterDim.x = 16;
@@ -1263,7 +1291,7 @@ static rs_status launch_mss(bool bf, bool qbf, const void* logits, const void* d
     }
     if (cs > max_cs) {
         cs = max_cs;
-        const size_t sm2 = mss_smem_bytes(nvec, cs);
+        const size_t sm2 = mss_smem_bytes(nvec, cs, qbf);
         if (cur < sm2) {
             RS_REQUIRE(sm2 <= 200 * 1024, RS_ERR_UNSUPPORTED, "rs_tree_accept: V=%d too large for MSS", V);
             RS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
@@ -1273,7 +1301,7 @@ static rs_status launch_mss(bool bf, bool qbf, const void* logits, const void* d
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(B * cs));
     cfg.blockDim = dim3(kMssThreads);
-    cfg.dynamicSmemBytes = mss_smem_bytes(nvec, cs);
+    cfg.dynamicSmemBytes = mss_smem_bytes(nvec, cs, qbf);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;

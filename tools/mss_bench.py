@@ -17,7 +17,7 @@ from synth import CONFIGS, make_verify_batch  # noqa: E402
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 50
 cfg = CONFIGS["c3s"]
 dev = torch.device("cuda", 0)
-strat = bench.Strategy(cfg, core, "cuda", calibrate=True)
+strat = bench.Strategy(cfg, core, "cuda", calibrate=False, force_n=int(os.environ.get("MSS_N", "8")))
 b = make_verify_batch(cfg, device=dev, gen_device=dev, layers=1, parents=strat.parents)
 lg, dp = b["logits"], b["draft_probs"]
 d32 = lambda x: torch.as_tensor(np.asarray(x), dtype=torch.int32, device=dev)
@@ -54,7 +54,7 @@ for s in range(b["B"]):
         else:
             tests += len(kids)
             rej += len(kids)
-alg = visited * V * 6
+alg = visited * V * (lg.element_size() + dp.element_size())   # logits + draft row
 print(json.dumps(dict(ms=round(ms, 4), B=b["B"], T=int(T[0]), visited_rows=int(visited), child_tests=int(tests),
                       rejections=int(rej), accepted=int(acc.sum()), alg_bytes=int(alg),
                       GBps=round(alg / ms / 1e6, 1), frac_hbm=round(alg / ms / 1e6 / 6536.4, 4))))
