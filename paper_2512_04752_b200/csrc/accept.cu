@@ -177,8 +177,10 @@ __device__ __forceinline__ void allreduce2(unsigned long long& v0, int op0, unsi
         v0 = op_apply(op0, v0, __shfl_xor_sync(0xffffffffu, v0, o));
         v1 = op_apply(op1, v1, __shfl_xor_sync(0xffffffffu, v1, o));
     }
+    __syncwarp();
     __syncthreads();
     if (lane == 0) { sm.red[w][0] = v0; sm.red[w][1] = v1; }
+    __syncwarp();
     __syncthreads();
     unsigned long long a = sm.red[0][0], b = sm.red[0][1];
     for (int k = 1; k < kWarps; ++k) { a = op_apply(op0, a, sm.red[k][0]); b = op_apply(op1, b, sm.red[k][1]); }
@@ -200,7 +202,9 @@ __device__ __forceinline__ void allreduce2(unsigned long long& v0, int op0, unsi
             }
             if (lane == 0) { sm.red[0][0] = ra; sm.red[0][1] = rb; }
         }
-        __syncthreads();
+        __syncwarp();   // (reconverge the warp before the aligned CTA barrier)
+        __syncwarp();
+    __syncthreads();
         a = sm.red[0][0];
         b = sm.red[0][1];
         phase ^= 1;
@@ -219,8 +223,10 @@ __device__ __forceinline__ u128 allreduce_max128(u128 v, Smem& sm, int& phase) {
         u128 v2 = ((u128)hi << 64) | lo;
         if (v2 > v) v = v2;
     }
+    __syncwarp();
     __syncthreads();
     if (lane == 0) { sm.red[w][0] = (unsigned long long)(v >> 64); sm.red[w][1] = (unsigned long long)v; }
+    __syncwarp();
     __syncthreads();
     u128 r = 0;
     for (int k = 0; k < kWarps; ++k) {
@@ -259,6 +265,7 @@ __device__ __forceinline__ void tile_add(Smem& sm, int tile, unsigned long long 
 
 __device__ __forceinline__ void clear_tiles(Smem& sm) {
     for (int k = threadIdx.x; k < kMaxTiles; k += kThreads) sm.tile_sum[k] = 0ull;
+    __syncwarp();
     __syncthreads();
 }
 
@@ -287,6 +294,7 @@ __device__ __forceinline__ int draw_bonus(Smem& sm, int& phase, uint64_t t, int 
     const int tid = threadIdx.x;
     const uint32_t cs = cluster_size(), crank = cluster_rank();
     const int ntiles = (vend - vbeg + kTileVecs - 1) / kTileVecs;
+    __syncwarp();
     __syncthreads();
     unsigned long long slice_total = 0;
     for (int k = 0; k < ntiles; ++k) slice_total += sm.tile_sum[k];
@@ -310,6 +318,7 @@ __device__ __forceinline__ int draw_bonus(Smem& sm, int& phase, uint64_t t, int 
         sm.bcast_u = run;
         sm.bonus_v = V - 1;
     }
+    __syncwarp();
     __syncthreads();
     const int i = vbeg + sm.bcast_i * kTileVecs + tid;
     const unsigned long long tbase = sm.bcast_u;
@@ -328,6 +337,7 @@ __device__ __forceinline__ int draw_bonus(Smem& sm, int& phase, uint64_t t, int 
         if (lane >= o) incl += y;
     }
     if (lane == 31) sm.scan[wid] = incl;
+    __syncwarp();
     __syncthreads();
     unsigned long long wbase = tbase;
     for (int k = 0; k < wid; ++k) wbase += sm.scan[k];
@@ -339,6 +349,7 @@ __device__ __forceinline__ int draw_bonus(Smem& sm, int& phase, uint64_t t, int 
             if (accum > t) { sm.bonus_v = i * 8 + j; break; }
         }
     }
+    __syncwarp();
     __syncthreads();
     return sm.bonus_v;
 }
@@ -390,6 +401,7 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype_rt, c
     int c = 0, a = 0, bonus = -1, flags = 0;
     bool bonus_mine = leader;   // which CTA writes the bonus
     if (leader && tid == 0) pth[0] = 0;
+    __syncwarp();
     __syncthreads();
 
     for (;;) {
@@ -541,9 +553,13 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype_rt, c
                     const bool acc = qw == 0 ? wt > 0 : ((u128)U * ((u128)qw * Z)) < (((u128)wt * Zq) << 32);
                     sm.bcast_i = acc ? 1 : 0;
                 }
-                __syncthreads();
+                __syncwarp();   // (reconverge the warp before the aligned CTA barrier)
+        __syncwarp();
+    __syncthreads();
                 const bool accepted = sm.bcast_i != 0;
-                __syncthreads();
+                __syncwarp();   // (reconverge the warp before the aligned CTA barrier)
+        __syncwarp();
+    __syncthreads();
                 if (accepted) { next = x; break; }
                 ++rank;
                 // residual: pass A = its max (the shift), pass B = shifted values written back
@@ -613,7 +629,9 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype_rt, c
                     allreduce2(zn, OP_SUM, dummy, OP_OR, sm, phase);   // (cluster barrier: the
                     Z = zn;                                             //  new weights are visible)
                 }
-                __syncthreads();
+                __syncwarp();   // (reconverge the warp before the aligned CTA barrier)
+        __syncwarp();
+    __syncthreads();
             }
             if (next < 0) {
                 const uint32_t U2 = rs::uniform_word(seed, step, g, 0xFFFFFFFFu, (uint32_t)c);
@@ -670,7 +688,9 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype_rt, c
             allreduce2(zs, OP_SUM, dummy, OP_OR, sm, phase);
             uint64_t Z = zs;
             if (tid == 0) sm.n_excluded = 0;
-            __syncthreads();
+            __syncwarp();   // (reconverge the warp before the aligned CTA barrier)
+        __syncwarp();
+    __syncthreads();
             int rank = 0;
             for (int x = c + 1; x < T && next < 0; ++x) {
                 if (sm.parent[x] != c) continue;
@@ -692,10 +712,14 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype_rt, c
                         sm.excluded[sm.n_excluded++] = tk;
                     }
                 }
-                __syncthreads();
+                __syncwarp();   // (reconverge the warp before the aligned CTA barrier)
+        __syncwarp();
+    __syncthreads();
                 const bool accepted = sm.bcast_i != 0;
                 const uint64_t wt = sm.bcast_u;
-                __syncthreads();
+                __syncwarp();   // (reconverge the warp before the aligned CTA barrier)
+        __syncwarp();
+    __syncthreads();
                 if (accepted) { next = x; break; }
                 ++rank;
                 Z -= wt;
@@ -718,7 +742,9 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype_rt, c
         c = next;
         ++a;
         if (leader && tid == 0) pth[a] = c;
-        __syncthreads();
+        __syncwarp();   // (reconverge the warp before the aligned CTA barrier)
+        __syncwarp();
+    __syncthreads();
     }
     if (tid == 0) {
         if (leader) {
@@ -771,8 +797,10 @@ __device__ __forceinline__ void allreduce3(unsigned long long v[3], const int op
     for (int o = 16; o; o >>= 1)
 #pragma unroll
         for (int k = 0; k < 3; ++k) v[k] = op_apply(op[k], v[k], __shfl_xor_sync(0xffffffffu, v[k], o));
+    __syncwarp();
     __syncthreads();
     if (lane == 0) { sm.red[w][0] = v[0]; sm.red[w][1] = v[1]; sm.scan[w] = v[2]; }
+    __syncwarp();
     __syncthreads();
     unsigned long long a[3] = {sm.red[0][0], sm.red[0][1], sm.scan[0]};
     for (int k = 1; k < kWarps; ++k) {
@@ -797,12 +825,15 @@ __device__ __forceinline__ void allreduce3(unsigned long long v[3], const int op
                 for (int k = 0; k < 3; ++k) r[k] = op_apply(op[k], r[k], __shfl_xor_sync(0xffffffffu, r[k], o));
             if (lane == 0) { sm.red[0][0] = r[0]; sm.red[0][1] = r[1]; sm.scan[0] = r[2]; }
         }
-        __syncthreads();
+        __syncwarp();   // (reconverge the warp before the aligned CTA barrier)
+        __syncwarp();
+    __syncthreads();
         a[0] = sm.red[0][0];
         a[1] = sm.red[0][1];
         a[2] = sm.scan[0];
         phase ^= 1;
     }
+    __syncwarp();
     __syncthreads();   // sm.red / sm.scan are reused by the next reduction
     v[0] = a[0];
     v[1] = a[1];
