@@ -210,9 +210,16 @@ __device__ __forceinline__ float ex2_poly(float x) {
 #ifndef RS_ATTN_EXP_EMU
 #define RS_ATTN_EXP_EMU 0   // eighths of the exponentials on the FMA pipe (0: all on MUFU)
 #endif
-// element c of a row block: RS_ATTN_EXP_EMU of every 8 on the FMA pipe
+// Dual items (RM = 4, the tensor-bound config 5): two softmax warps per SM sub-partition each
+// need 64 MUFU ex2 per row per key block, as many MUFU cycles as the block's MMAs take; putting
+// RS_ATTN_EXP_EMU_DUAL of every 8 on the FMA pipe measured 312 -> 298 us per layer (c5g8).
+#ifndef RS_ATTN_EXP_EMU_DUAL
+#define RS_ATTN_EXP_EMU_DUAL 2
+#endif
+// element c of a row block: EMU of every 8 on the FMA pipe
+template <int EMU = RS_ATTN_EXP_EMU>
 __device__ __forceinline__ float ex2_mix(float x, int c) {
-    if (RS_ATTN_EXP_EMU && (c & 7) >= 8 - RS_ATTN_EXP_EMU) return ex2_poly(x);
+    if (EMU && (c & 7) >= 8 - EMU) return ex2_poly(x);
     return ex2(x);
 }
 
@@ -988,6 +995,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             // lanes 16-31 those of the high half, so no lane idles.
             const bool hs = RM == 1 ? true : ((RM == 2 || RM == 4) ? false : (R == 16));
             constexpr bool DU = RM == 4;
+            constexpr int kEmu = DU ? RS_ATTN_EXP_EMU_DUAL : RS_ATTN_EXP_EMU;
             const int mt = wi.mtile + (DU ? grp : 0);    // dual: this warpgroup's own tile
             const int hl = hs ? (lane & 15) : lane;      // row lane of this thread
             const int rr = wq * 32 + hl;                 // TMEM lane / UMMA row of my row
@@ -1173,7 +1181,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                         for (int c = 0; c < 64; c += 2) {
                             float x0, x1;
                             f2_unpack(f2_fma(f2_pack(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), sc2, nm2), x0, x1);
-                            const float e0 = ex2_mix(x0, c), e1 = ex2_mix(x1, c + 1);
+                            const float e0 = ex2_mix<kEmu>(x0, c), e1 = ex2_mix<kEmu>(x1, c + 1);
                             sr[c >> 1] = pack_bf16(e0, e1);
                             ls2[(c >> 1) & 3] = f2_add(ls2[(c >> 1) & 3], f2_pack(e0, e1));
                         }
@@ -1188,8 +1196,8 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                     for (int k = 0; k < 8; ++k) ls8[k] = 0.0f;
 #pragma unroll
                     for (int c = 0; c < 64; c += 2) {
-                        const float e0 = ex2_mix(fmaf(__uint_as_float(sr[c]), p.scale_log2, -mo), c);
-                        const float e1 = ex2_mix(fmaf(__uint_as_float(sr[c + 1]), p.scale_log2, -mo), c + 1);
+                        const float e0 = ex2_mix<kEmu>(fmaf(__uint_as_float(sr[c]), p.scale_log2, -mo), c);
+                        const float e1 = ex2_mix<kEmu>(fmaf(__uint_as_float(sr[c + 1]), p.scale_log2, -mo), c + 1);
                         const uint32_t pk = pack_bf16(e0, e1);
                         sr[c >> 1] = pk;
                         ls8[(c >> 1) & 7] += e0 + e1;
