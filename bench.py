@@ -847,6 +847,9 @@ def run_c4(args, world, rank, local):
     value = tok_all / (ms_max / 1e3)
     gbs = attn_bytes / (attn_ms * 1e-3) / 1e9 if attn_ms > 0 else 0.0
     mig_bytes = sum(m[2] for m in migrations)
+    push_b, push_ms = float(sum(p[0] for p in pushes)), float(sum(p[1] for p in pushes))
+    if world > 1:   # push kernels run on the source ranks: totals over every rank
+        push_b, push_ms = _allreduce(push_b, "sum"), _allreduce(push_ms, "sum")
     mig_s = sum(m[3] for m in migrations)
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -879,10 +882,8 @@ def run_c4(args, world, rank, local):
                       "GBps_rank0": round(mig_bytes / mig_s / 1e9, 2) if mig_s > 0 else None,
                       "note": "GBps_rank0 = KV bytes / host time of the whole reallocation (plan, "
                               "handshake, transfer) on rank 0",
-                      "push_kernel": ({"bytes": int(sum(p[0] for p in pushes)),
-                                       "ms": round(sum(p[1] for p in pushes), 3),
-                                       "GBps": round(sum(p[0] for p in pushes) / sum(p[1] for p in pushes) / 1e6, 1)}
-                                      if pushes and sum(p[1] for p in pushes) > 0 else None),
+                      "push_kernel_all_ranks": ({"bytes": int(push_b), "ms": round(push_ms, 3),
+                                                 "GBps": round(push_b / push_ms / 1e6, 1)} if push_ms > 0 else None),
                       "raw_p2p_reference": raw,
                       **({"two_stage_stall_ms_rank0": [round(x, 3) for x in stalls]} if stalls else {})},
     }
