@@ -42,6 +42,14 @@ def main():
     L = int(sys.argv[sys.argv.index("--layers") + 1]) if "--layers" in sys.argv else 8
     reps = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 10
     cfg, b = batch(spec, L)
+    if "--contiguous" in sys.argv:   # (experiment) every sample's pages consecutive in the pool
+        bt = b["block_table"]
+        npg = (b["prefix_len"] + b["T"] + 63) // 64
+        o = 0
+        for i in range(len(npg)):
+            bt[i, :npg[i]] = np.arange(o, o + npg[i])
+            bt[i, npg[i]:] = o + npg[i] - 1
+            o += npg[i]
     dev = "cuda"
     par = torch.as_tensor(b["parent"]).to(dev)
     to = torch.as_tensor(b["tree_off"]).to(dev)
