@@ -189,3 +189,21 @@ def test_draft_logits_matches_oracle(core):
     dl = core.draft_logits(np.concatenate([p for p, _ in trees]), np.concatenate([o for _, o in trees]), off)
     ref = np.concatenate([OS.draft_logits(p, o) for p, o in trees])
     assert np.array_equal(dl, ref)
+
+
+def test_calibrate_validates_before_any_device_work(core):
+    """rs_calibrate / rs_calibrate_workspace_bytes refuse a ctx without a registered LLM KV store,
+    too few grid points and too small Q/O scratch — on the host, before touching the device."""
+    import ctypes
+    ctx = core.Ctx(0, 1, 64)
+    ctx.set_strategy(_cost(), KX, KY)
+    B = np.array([8, 8, 16, 16], np.int32)
+    P = np.array([128, 256, 128, 256], np.int32)
+    T = np.array([4, 8, 4, 8], np.int32)
+    desc = core.CalibDescC(32, 4, B.ctypes.data, P.ctypes.data, T.ctypes.data, 2, None, None, 0, None, 0, 0.0, None)
+    assert core._lib.rs_calibrate_workspace_bytes(ctx._h, ctypes.byref(desc)) == 0
+    st = core._lib.rs_calibrate(ctx._h, ctypes.byref(desc), None)
+    assert st == 1 and b"no LLM KV" in core._lib.rs_last_error()
+    desc.n_points = 3
+    assert core._lib.rs_calibrate(ctx._h, ctypes.byref(desc), None) == 1      # < 4 grid points
+    ctx.destroy()
