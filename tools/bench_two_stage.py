@@ -111,6 +111,58 @@ def main():
         rows = mig.dst_rows()
         pool.free(np.unique(np.concatenate([rows[i, :(int(len2[i]) + ps - 1) // ps] for i in range(n)])))
     comm.destroy()
+    # the same two measurements over peer memory (rs_peer_push: one kernel straight into the
+    # destination's reserved pages; loopback: this process's own store, a device-local copy)
+    store = core.PeerStore((K, V), (Ks, Vs), ps, 0)
+    store.import_(store.export())
+    d32 = lambda x: torch.as_tensor(np.ascontiguousarray(x, np.int32), device="cuda")
+    peer = {}
+    rows = pool.reserve(len1, ps, npg)
+    dbt, ln1 = d32(rows), d32(len1)
+    for rep in range(3):   # stop-the-world push of the whole KV
+        a, z = ev(), ev()
+        torch.cuda.synchronize()
+        a.record(compute)
+        store.push(0, bt, dbt, ln1, stream=compute)
+        z.record(compute)
+        torch.cuda.synchronize()
+        peer["stop_the_world_stall_ms"] = round(a.elapsed_time(z), 3)
+    pool.free(np.unique(rows.ravel()))
+    rows = pool.reserve(len1 + 256, ps, npg)
+    dbt = d32(rows)
+    s0, s1 = ev(), ev()
+    torch.cuda.synchronize()
+    s0.record(side)
+    store.push(0, bt, dbt, ln1, stream=side)
+    s1.record(side)
+    a, z = ev(), ev()
+    a.record(compute)
+    k = 0
+    while not s1.query() or k < 2:
+        g_step.replay()
+        k += 1
+        if k % 4 == 0:
+            compute.synchronize()
+    z.record(compute)
+    torch.cuda.synchronize()
+    acc_per_step = float(step.acc.float().mean().item()) + 1.0
+    len2 = np.minimum(len1 + np.int32(np.ceil(acc_per_step * k)), tok + 256).astype(np.int32)
+    t0, t_ssm, t1 = ev(), ev(), ev()
+    dl2 = d32(len2 - len1)              # (the stage-2 lengths on the device before the clock starts)
+    torch.cuda.synchronize()
+    t0.record(side)
+    store.push(0, bt, dbt, dl2, starts=ln1, parts=core.PEER_SSM, stream=side)
+    t_ssm.record(side)
+    store.push(0, bt, dbt, dl2, starts=ln1, parts=core.PEER_LLM, stream=side)
+    t1.record(side)
+    side.synchronize()
+    peer.update(stage1_ms_overlapped=round(s0.elapsed_time(s1), 3), steps_during_stage1=k,
+                step_ms_during=round(a.elapsed_time(z) / k, 4), two_stage_stall_ms=round(t0.elapsed_time(t1), 3),
+                two_stage_ssm_ready_ms=round(t0.elapsed_time(t_ssm), 3),
+                push_GBps_stage1=round(2 * (core.kv_pack_elems(L, Hkv, d, len1) + core.kv_pack_elems(1, 8, d, len1))
+                                       / (s0.elapsed_time(s1) * 1e-3) / 1e9, 1))
+    pool.free(np.unique(rows.ravel()))
+    store.destroy()
     r = res_runs[-1]
     nbytes = 2 * (core.kv_pack_elems(L, Hkv, d, len1) + core.kv_pack_elems(1, 8, d, len1))
     out = {"samples": n, "tokens_per_sample": tok, "bytes_stage1": int(nbytes),
@@ -122,9 +174,10 @@ def main():
            "stage2_delta_tokens_per_sample": r["delta_tokens"],
            "stall_ratio_two_stage_vs_stw": round(r["stage2_stall_ms"] / t_stw, 4),
            "runs": res_runs,
+           "peer_transport": peer,
            "note": "size-1 NCCL communicator (device-local p2p); LLM 32 layers + SSM 1 layer, Llama-3-8B KV "
                    "shapes; stall = time the migrating samples cannot be verified"}
-    print(json.dumps(out), flush=True)
+    print(json.dumps(out), flush=True)   # (NCCL may print its version line before it)
 
 
 if __name__ == "__main__":
