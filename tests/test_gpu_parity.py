@@ -160,6 +160,10 @@ def test_accept_sampling_bit_exact(cuda_lib, mode, V, temp, qdt):
         g, o = _run_accept_both(core, b, logits, m, temperature=temp, seed=1234 + step, step=step)
         for x, y in zip(g, o):
             np.testing.assert_array_equal(x, y)
+    if mode == "mss":   # fp32 logits with the same draft rows (the other logits-dtype instance)
+        g, o = _run_accept_both(core, b, logits.float(), m, temperature=temp, seed=99, step=7)
+        for x, y in zip(g, o):
+            np.testing.assert_array_equal(x, y)
 
 
 def _accept_np_both(core, mode, logits_f32, parent, token, tree_off, gid, V, draft=None, seed=0, step=0):
