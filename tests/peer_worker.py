@@ -178,6 +178,44 @@ def case_instance(rank, dev, two_stage):
     store.destroy()
 
 
+def case_nccl(rank, dev):
+    """rs_migrate_samples between two processes over NCCL (source-only and destination-only
+    branches, and a refusal). Needs NCCL to accept the two ranks' devices (distinct GPUs)."""
+    from paper_2512_04752_b200 import core
+    Hkv, d, num_pages, maxp = 2, 128, 48, 8
+    llm = _pools(dev, 3, Hkv, d, num_pages, 10 + rank)
+    ssm = _pools(dev, 1, Hkv, d, num_pages, 20 + rank)
+    pool = core.PagePool(num_pages)
+    comm = core.Comm(rank, 2)
+    staging = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
+    scratch = torch.empty(2 * 64 + 64 * maxp, dtype=torch.int32, device=dev)
+    lens = [1, 63, 64, 65, 200]
+    src_rows = np.zeros((len(lens), maxp), np.int32)
+    perm = np.random.default_rng(rank).permutation(num_pages)
+    o = 0
+    for i, n in enumerate(lens):
+        npg = (n + PS - 1) // PS
+        src_rows[i, :npg] = perm[o:o + npg]
+        src_rows[i, npg:] = src_rows[i, npg - 1]
+        o += npg
+    before = _host(ssm) + _host(llm)
+    src_bt = torch.as_tensor(src_rows, device=dev) if rank == 0 else None
+    rows = core.migrate_samples(comm, 0, 1, llm, ssm, PS, pool if rank == 1 else None, list(range(len(lens))), lens,
+                                src_bt, maxp, staging, scratch)
+    src_state = _bcast((before, src_rows) if rank == 0 else None, 0)
+    if rank == 1:
+        torch.cuda.synchronize(dev)
+        got = _host(ssm) + _host(llm)
+        caches, srows = src_state
+        buf = OM.pack([caches[:1], caches[1:]], list(srows), lens, PS)
+        exp = [(a.copy(), b.copy()) for a, b in before]
+        OM.unpack(buf, [exp[:1], exp[1:]], list(rows), lens, PS)
+        for (ga, gb), (ea, eb) in zip(got, exp):
+            assert np.array_equal(ga, ea) and np.array_equal(gb, eb)
+    dist.barrier()
+    comm.destroy()
+
+
 def worker(rank, world, port, case, outdir):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -186,6 +224,8 @@ def worker(rank, world, port, case, outdir):
     try:
         if case == "core":
             case_core(rank, dev)
+        elif case == "nccl":
+            case_nccl(rank, dev)
         else:
             case_instance(rank, dev, two_stage=(case == "two_stage"))
         open(os.path.join(outdir, f"ok{rank}"), "w").write("ok")

@@ -93,3 +93,11 @@ def test_peer_loopback_in_process(cuda_lib):
         other.import_(store.export())
     other.destroy()
     store.destroy()
+
+
+def test_nccl_migrate_two_processes(cuda_lib):
+    """rs_migrate_samples over NCCL between two processes (the source-only and destination-only
+    branches of the handshake and transfer). NCCL needs one GPU per rank: skipped on a one-GPU box."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("NCCL needs one GPU per rank (this box has one); the peer transport covers the two-process path")
+    _run("nccl")
