@@ -521,7 +521,9 @@ rs_status rs_peer_import(rs_peer* peer, const uint8_t* blob, size_t bytes);
  * from this rank's pages (row i of src_block_table) into dst_rank's pages (row i of
  * dst_block_table, the rows the destination reserved), every layer of the models selected by
  * `parts` (bit 0 = SSM, bit 1 = LLM; SSM launched first). src/dst block tables: device int32
- * [n, max_pages]; starts, lens: device int32 [n]. Enqueued on `stream`. */
+ * [n, max_pages]; starts, lens: device int32 [n]. Enqueued on `stream`. Device data is not
+ * validated (the kernel trusts it, like the attention kernel trusts its block table): the caller
+ * guarantees starts[i] + lens[i] <= max_pages * page_size and page ids inside both pools. */
 rs_status rs_peer_push(rs_peer* peer, int32_t dst_rank, const int32_t* src_block_table,
                        const int32_t* dst_block_table, int32_t max_pages, const int32_t* starts,
                        const int32_t* lens, int32_t n, int32_t parts, void* stream);
