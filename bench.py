@@ -534,12 +534,14 @@ def run_ours(args, world, rank, local):
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     # mask, L x attention (split-KV merge fused), accept (f2: LM-head GEMM + finalize + walk), compact
-    launches_per_step = 1 + step.L + (1 if lm is None else 3) + 1
+    launches_per_step = 1 + step.L + (1 if lm is None else 3) + (0 if step.fused_commit else 1)
     # The step's device work is captured once into CUDA graphs (mask | L x attention | accept +
     # compact); every timed step replays them (the launches are still our kernels, counted below).
     g_mask, g_attn, g_acc, g_cmp = step.capture_parts(seed=11, step=0)
     for w in range(args.warmup):
-        g_mask.replay(); g_attn.replay(); g_acc.replay(); g_cmp.replay()
+        g_mask.replay(); g_attn.replay(); g_acc.replay()
+        if g_cmp is not None:
+            g_cmp.replay()
     sampler = ClockSampler(local)
     barrier()
     with sampler:
@@ -557,7 +559,8 @@ def run_ours(args, world, rank, local):
             ev[k][1].record(stream)
             g_acc.replay()
             ev[k][2].record(stream)
-            g_cmp.replay()
+            if g_cmp is not None:
+                g_cmp.replay()
             ev[k][3].record(stream)
         end.record(stream)
         torch.cuda.synchronize()
@@ -620,6 +623,15 @@ def run_ours(args, world, rank, local):
         "mask": {"ms_per_step": round(ms_per_step - attn_ms - acc_ms - cmp_ms, 4), "launches": 1,
                  "note": "remainder of the step (mask kernel + graph launch gaps)"},
     }
+    if step.fused_commit:
+        # one launch commits the K/V in its tail (rs_tree_accept_compact): accept + compact together
+        tot = acc_bytes + cmp_bytes
+        kernels["accept"] = {"ms_per_step": round(acc_ms + cmp_ms, 4), "launches": 1, "bytes": int(tot),
+                             "GBps": round(tot / ((acc_ms + cmp_ms) * 1e-3) / 1e9, 1),
+                             "frac_hbm": round(tot / ((acc_ms + cmp_ms) * 1e-3) / 1e9 / hbm, 4),
+                             "note": "rs_tree_accept_compact: the walk (bytes = visited rows x V x dtype) with the "
+                                     "KV commit fused into each sample's tail"}
+        kernels["compact"] = {"fused_into": "accept", "bytes": int(cmp_bytes), "moves": moves}
     if lm is not None:
         lm_flops = 2.0 * b["NT"] * cfg.V * lm[1]
         kernels.pop("accept")

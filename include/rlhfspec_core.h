@@ -264,6 +264,24 @@ rs_status rs_kv_compact(void* const* k_layers_host, void* const* v_layers_host, 
                         const int32_t* accepted_len, const int32_t* path, int32_t B,
                         int32_t* new_len, int32_t* moves, void* stream);
 
+/* rs_tree_accept_compact — rs_tree_accept_ex followed by rs_kv_compact in ONE launch (a3 + a4,
+ * P:76-80 then P:303): the cluster that walks sample b's tree commits its path's K/V as soon as
+ * its walk ends (the other samples are still walking), so no second launch or pass over the
+ * path. Every output (accepted_len, path, bonus_token, status_flags, new_len, moves and the K/V
+ * bytes) is identical to the two calls in sequence; arguments as in rs_tree_accept_ex and
+ * rs_kv_compact (num_pages is not needed). L <= 256 (else RS_ERR_INVALID_ARG: use the two
+ * calls); head_dim % 8 != 0 -> RS_ERR_UNSUPPORTED. The K/V pointers are read at launch (they are
+ * kernel parameters, so a captured CUDA graph keeps the layer list it was captured with). */
+rs_status rs_tree_accept_compact(int32_t mode, const void* logits, int32_t logits_dtype, const void* draft_probs,
+                                 int32_t draft_dtype, const int32_t* parent, const int32_t* token,
+                                 const int32_t* tree_off, const int64_t* gid, int32_t B, int32_t V,
+                                 float temperature, uint64_t seed, uint64_t step, int32_t* accepted_len,
+                                 int32_t* path, int32_t* bonus_token, int32_t* status_flags, void* ws,
+                                 size_t ws_bytes, void* const* k_layers_host, void* const* v_layers_host,
+                                 int32_t L, int32_t Hkv, int32_t head_dim, int32_t page_size,
+                                 const int32_t* block_table, int32_t max_pages, const int32_t* prefix_len,
+                                 int32_t* new_len, int32_t* moves, void* stream);
+
 /* ===================================================================================== a0
  * Workload-aware drafting-strategy selection: n = argmax al(n)/t_sd(n) (Eq. 2)
  * by layer-level priority-queue search with early stop (Eq. 3). Host only. */

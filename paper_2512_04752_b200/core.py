@@ -22,6 +22,7 @@ GREEDY, SAMPLE_DELTA, SAMPLE_MSS = 0, 1, 2
 DTYPE_BF16, DTYPE_F32 = 0, 1
 FLAG_MALFORMED, FLAG_NONFINITE = 1, 2
 MAX_TREE = 64
+COMPACT_MAX_LAYERS = 256   # rs_tree_accept_compact: layers one launch commits
 
 _P = ctypes.c_void_p
 _i32, _i64, _u64, _f32, _f64, _sz = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float,
@@ -58,6 +59,8 @@ _sig("rs_tree_accept_ex", _i32, _i32, _P, _i32, _P, _i32, _P, _P, _P, _P, _i32, 
 _sig("rs_philox4x32_10", _i32, _P, _i64, _P, _P, _P)
 _sig("rs_exp_spec", _i32, _P, _i64, _P, _P)
 _sig("rs_kv_compact", _i32, _P, _P, _i32, _i64, _i32, _i32, _i32, _P, _i32, _P, _P, _P, _i32, _P, _P, _P)
+_sig("rs_tree_accept_compact", _i32, _i32, _P, _i32, _P, _i32, _P, _P, _P, _P, _i32, _i32, _f32, _u64, _u64,
+     _P, _P, _P, _P, _P, _sz, _P, _P, _i32, _i32, _i32, _i32, _P, _i32, _P, _P, _P, _P)
 
 
 class RSError(RuntimeError):
@@ -256,6 +259,37 @@ def tree_accept(mode, logits, parent, token, tree_off, gid, draft_probs=None, te
                                   _ptr(path), _ptr(bonus), _ptr(flags), _ptr(ws) if need else None,
                                   ws.numel() if need else 0, _stream(stream)), "rs_tree_accept_ex")
     return acc, path, bonus, flags
+
+
+def tree_accept_compact(mode, logits, parent, token, tree_off, gid, k_layers, v_layers, block_table, prefix_len,
+                        draft_probs=None, temperature=1.0, seed=0, step=0, out=None, new_len=None, moves=None,
+                        stream=None, ws=None, layer_ptrs=None):
+    """rs_tree_accept_ex + rs_kv_compact in one launch (the sample's cluster commits its path's
+    K/V when its walk ends). layer_ptrs: optional pre-built (k, v) ctypes pointer arrays."""
+    NT, V = logits.shape
+    B = tree_off.numel() - 1
+    need = accept_workspace_bytes(mode, B, V)
+    if ws is None and need:
+        ws = torch.empty(need, dtype=torch.uint8, device=logits.device)
+    dt = DTYPE_BF16 if logits.dtype == torch.bfloat16 else DTYPE_F32
+    dev = logits.device
+    if out is None:
+        out = (torch.empty(B, dtype=torch.int32, device=dev), torch.empty((B, MAX_TREE), dtype=torch.int32, device=dev),
+               torch.empty(B, dtype=torch.int32, device=dev), torch.empty(B, dtype=torch.int32, device=dev))
+    if new_len is None:
+        new_len = torch.empty(B, dtype=torch.int32, device=dev)
+    acc, path, bonus, flags = out
+    qdt = DTYPE_BF16 if (draft_probs is not None and draft_probs.dtype == torch.bfloat16) else DTYPE_F32
+    L = len(k_layers)
+    _, Hkv, ps, d = k_layers[0].shape
+    kp, vp = layer_ptrs if layer_ptrs is not None else (_layer_ptrs(k_layers), _layer_ptrs(v_layers))
+    _check(_lib.rs_tree_accept_compact(int(mode), _ptr(logits), dt, _ptr(draft_probs), qdt, _ptr(parent), _ptr(token),
+                                       _ptr(tree_off), _ptr(gid), B, V, float(temperature), int(seed), int(step),
+                                       _ptr(acc), _ptr(path), _ptr(bonus), _ptr(flags), _ptr(ws) if need else None,
+                                       ws.numel() if need else 0, kp, vp, L, Hkv, d, ps, _ptr(block_table),
+                                       block_table.shape[1], _ptr(prefix_len), _ptr(new_len), _ptr(moves),
+                                       _stream(stream)), "rs_tree_accept_compact")
+    return acc, path, bonus, flags, new_len, moves
 
 
 def philox4x32_10(ctr: torch.Tensor, key, stream=None):

@@ -21,6 +21,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "compact_tail.cuh"
 #include "sampling.cuh"
 #include "sm100_ptx.cuh"
 
@@ -139,7 +140,12 @@ __device__ __forceinline__ void for_slice(const RowView& lv, const RowView& qv, 
 
 struct Smem {
     unsigned long long red[kWarps][2];
+    unsigned long long redn[kWarps][3];   // allreduce_n's per-warp partials
     unsigned long long xch[2][kMaxCluster > 2 ? 4 : 4];   // cluster exchange slots (double-buffered)
+    // push exchange (allreduce_n, draw_bonus): CTA r stores its partials into slot [phase][r] of
+    // EVERY CTA before the cluster barrier, so after it all reads are local (no DSMEM round trip,
+    // and no CTA touches another's shared memory after its last barrier)
+    unsigned long long xp[2][16][3];
     unsigned long long tile_sum[kMaxTiles];
     unsigned long long scan[kWarps];
     int parent[RS_MAX_TREE];
@@ -150,6 +156,7 @@ struct Smem {
     int bcast_i;
     unsigned long long bcast_u;
     int bonus_v;
+    int path_s[RS_MAX_TREE];   // the accepted path (every CTA; the fused KV commit reads it)
 };
 
 // Orderable 32-bit key of a float (larger float -> larger key).
@@ -167,50 +174,63 @@ __device__ __forceinline__ unsigned long long op_apply(int op, unsigned long lon
     return op == OP_MAX ? (a > b ? a : b) : op == OP_SUM ? a + b : (a | b);
 }
 
-// Block + cluster all-reduce of two u64 values (ops op0, op1); identical result in every thread
-// of every CTA of the cluster. `phase` alternates the exchange slot (see cluster_sync_all).
-__device__ __forceinline__ void allreduce2(unsigned long long& v0, int op0, unsigned long long& v1, int op1, Smem& sm,
-                                           int& phase) {
+// Block + cluster all-reduce of N u64 values (ops op[k]); identical result in every thread of
+// every CTA of the cluster. Warps reduce by shuffles, lane 0 parks the warp's values; every warp
+// then reduces the kWarps partials (lane w reads warp w's) by shuffles; with a cluster, warp 0's
+// lane c pushes the CTA's values into CTA c's slot [phase][my rank], one cluster barrier, and every
+// warp reduces the cs slots of its own shared memory. `phase` alternates the slots: CTA A writes
+// B's slot [p] again only after the next barrier, which B passes only after reading [p].
+template <int N>
+__device__ __forceinline__ void allreduce_n(unsigned long long (&v)[N], const int (&op)[N], Smem& sm, int& phase) {
+    static_assert(N >= 1 && N <= 3, "allreduce_n: 1..3 values");
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        v0 = op_apply(op0, v0, __shfl_xor_sync(0xffffffffu, v0, o));
-        v1 = op_apply(op1, v1, __shfl_xor_sync(0xffffffffu, v1, o));
+    for (int o = 16; o; o >>= 1)
+#pragma unroll
+        for (int k = 0; k < N; ++k) v[k] = op_apply(op[k], v[k], __shfl_xor_sync(0xffffffffu, v[k], o));
+    __syncwarp();
+    __syncthreads();   // every read of sm.red by the previous reduction is done
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) sm.redn[w][k] = v[k];
     }
     __syncwarp();
     __syncthreads();
-    if (lane == 0) { sm.red[w][0] = v0; sm.red[w][1] = v1; }
-    __syncwarp();
-    __syncthreads();
-    unsigned long long a = sm.red[0][0], b = sm.red[0][1];
-    for (int k = 1; k < kWarps; ++k) { a = op_apply(op0, a, sm.red[k][0]); b = op_apply(op1, b, sm.red[k][1]); }
+    unsigned long long a[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) a[k] = lane < kWarps ? sm.redn[lane][k] : 0ull;   // 0: identity of MAX/SUM/OR
+#pragma unroll
+    for (int o = 16; o; o >>= 1)
+#pragma unroll
+        for (int k = 0; k < N; ++k) a[k] = op_apply(op[k], a[k], __shfl_xor_sync(0xffffffffu, a[k], o));
     const uint32_t cs = cluster_size();
     if (cs > 1) {
-        if (threadIdx.x == 0) { sm.xch[phase][0] = a; sm.xch[phase][1] = b; }
-        cluster_sync_all();
-        // lane c of warp 0 fetches CTA c's pair (all remote loads in flight at once), then a
-        // shuffle reduction; the result is broadcast through shared memory
-        // (a st.async push into peers' slots + transaction-count mbarrier measured no faster)
-        if (w == 0) {
-            const uint32_t c = (uint32_t)lane;
-            unsigned long long ra = 0, rb = 0;   // identity of MAX (unsigned), SUM and OR
-            if (c < cs) { ra = ld_dsmem_u64(&sm.xch[phase][0], c); rb = ld_dsmem_u64(&sm.xch[phase][1], c); }
+        if (w == 0 && (uint32_t)lane < cs) {
+            const uint32_t me = cluster_rank();
 #pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                ra = op_apply(op0, ra, __shfl_xor_sync(0xffffffffu, ra, o));
-                rb = op_apply(op1, rb, __shfl_xor_sync(0xffffffffu, rb, o));
-            }
-            if (lane == 0) { sm.red[0][0] = ra; sm.red[0][1] = rb; }
+            for (int k = 0; k < N; ++k) st_dsmem_u64(&sm.xp[phase][me][k], (uint32_t)lane, a[k]);
         }
-        __syncwarp();   // (reconverge the warp before the aligned CTA barrier)
         __syncwarp();
-    __syncthreads();
-        a = sm.red[0][0];
-        b = sm.red[0][1];
+        cluster_sync_all();
+#pragma unroll
+        for (int k = 0; k < N; ++k) a[k] = (uint32_t)lane < cs ? sm.xp[phase][lane][k] : 0ull;
+#pragma unroll
+        for (int o = 16; o; o >>= 1)
+#pragma unroll
+            for (int k = 0; k < N; ++k) a[k] = op_apply(op[k], a[k], __shfl_xor_sync(0xffffffffu, a[k], o));
         phase ^= 1;
     }
-    v0 = a;
-    v1 = b;
+#pragma unroll
+    for (int k = 0; k < N; ++k) v[k] = a[k];
+}
+
+__device__ __forceinline__ void allreduce2(unsigned long long& v0, int op0, unsigned long long& v1, int op1, Smem& sm,
+                                           int& phase) {
+    unsigned long long v[2] = {v0, v1};
+    const int op[2] = {op0, op1};
+    allreduce_n<2>(v, op, sm, phase);
+    v0 = v[0];
+    v1 = v[1];
 }
 
 // 128-bit max all-reduce (hi/lo lexicographic).
@@ -299,10 +319,11 @@ __device__ __forceinline__ int draw_bonus(Smem& sm, int& phase, uint64_t t, int 
     unsigned long long slice_total = 0;
     for (int k = 0; k < ntiles; ++k) slice_total += sm.tile_sum[k];
     unsigned long long before = 0;
-    if (cs > 1) {
-        if (tid == 0) sm.xch[phase][0] = slice_total;
+    if (cs > 1) {   // push exchange (see allreduce_n): every CTA learns every slice total locally
+        if (tid < (int)cs) st_dsmem_u64(&sm.xp[phase][crank][0], (uint32_t)tid, slice_total);
+        __syncwarp();
         cluster_sync_all();
-        for (uint32_t r = 0; r < crank; ++r) before += ld_dsmem_u64(&sm.xch[phase][0], r);
+        for (uint32_t r = 0; r < crank; ++r) before += sm.xp[phase][r][0];
         phase ^= 1;
     }
     owner = slice_total > 0 && before <= t && t < before + slice_total;
@@ -354,17 +375,30 @@ __device__ __forceinline__ int draw_bonus(Smem& sm, int& phase, uint64_t t, int 
     return sm.bonus_v;
 }
 
+// The fused KV commit (rs_tree_accept_compact): once the walk is over, the CTAs of the sample's
+// cluster split its compaction lanes (rs::compact_sample; the leader writes new_len and moves).
+// The inverse-CDF tile sums are dead by then: their storage holds the move list.
+template <typename CA>
+__device__ __forceinline__ void fused_commit(const CA& ca, int b, int a, Smem& sm) {
+    static_assert(sizeof(rs::CompactSmem) <= sizeof(sm.tile_sum), "move list must fit the tile sums");
+    __syncwarp();
+    __syncthreads();   // sm.path_s complete; every read of the tile sums done
+    rs::compact_sample(ca, b, a, [&](int k) { return sm.path_s[k]; }, (int)cluster_rank(), (int)cluster_size(),
+                       cluster_rank() == 0, *reinterpret_cast<rs::CompactSmem*>(sm.tile_sum));
+}
+
 // MODE is a template parameter so the greedy walk compiles without the 128-bit sampling
 // machinery (register budget: 4 CTAs/SM greedy, 2 CTAs/SM sampling); DT (the logits dtype)
 // too, so a bf16 vector occupies 4 registers, not 8.
-template <int MODE, int DT>
+template <int MODE, int DT, typename CA>
 __global__ void __launch_bounds__(kThreads, MODE == RS_ACCEPT_GREEDY ? 4 : 2)
 tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype_rt, const float* __restrict__ draft,
                    const int32_t* __restrict__ parent, const int32_t* __restrict__ token,
                    const int32_t* __restrict__ tree_off, const int64_t* __restrict__ gid, int V, float inv_tau,
                    uint64_t seed, uint64_t step, int32_t* __restrict__ acc_out, int32_t* __restrict__ path_out,
                    int32_t* __restrict__ bonus_out, int32_t* __restrict__ flags_out, bool logits_vec_ok,
-                   bool draft_vec_ok, uint32_t* __restrict__ wbuf, int prefetch_children) {
+                   bool draft_vec_ok, uint32_t* __restrict__ wbuf, int prefetch_children,
+                   const __grid_constant__ CA ca) {
     (void)mode_rt;
     (void)dtype_rt;
     constexpr int dtype = DT;
@@ -392,6 +426,7 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype_rt, c
     }
     if (__syncthreads_or(bad_node)) {
         if (leader && tid == 0) { acc_out[b] = 0; bonus_out[b] = -1; flags_out[b] = RS_FLAG_MALFORMED; }
+        if constexpr (CA::kOn) fused_commit(ca, b, 0, sm);   // accepted_len 0: new_len only
         return;   // uniform across the cluster: no cluster barrier is reached
     }
     const int64_t g = gid[b];
@@ -401,6 +436,7 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype_rt, c
     int c = 0, a = 0, bonus = -1, flags = 0;
     bool bonus_mine = leader;   // which CTA writes the bonus
     if (leader && tid == 0) pth[0] = 0;
+    if (tid == 0) sm.path_s[0] = 0;
     __syncwarp();
     __syncthreads();
 
@@ -742,6 +778,7 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype_rt, c
         c = next;
         ++a;
         if (leader && tid == 0) pth[a] = c;
+        if (tid == 0) sm.path_s[a] = c;
         __syncwarp();   // (reconverge the warp before the aligned CTA barrier)
         __syncwarp();
     __syncthreads();
@@ -759,8 +796,11 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype_rt, c
             bonus_out[b] = bonus;
         }
     }
-    // keep every CTA's shared memory alive until all remote reads of the cluster are done
-    if (cs > 1) cluster_sync_all();
+    if constexpr (CA::kOn) fused_commit(ca, b, a, sm);
+    // keep every CTA's shared memory alive until all remote reads of the cluster are done (DELTA's
+    // 128-bit reductions and child tests read peers after their barriers; the greedy walk only
+    // uses push exchanges, whose last barrier already orders every access)
+    if (MODE != RS_ACCEPT_GREEDY && cs > 1) cluster_sync_all();
 }
 
 // ============================================================================ MSS, row in smem
@@ -784,6 +824,10 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype_rt, c
 // no barrier is needed between a node's tests and the next row's loads. The bonus is the
 // inverse CDF of the current weights (draw_bonus).
 constexpr int kMssThreads = kThreads;   // == kTileVecs: one vector per thread per tile row
+#ifndef RS_MSS_LUNROLL
+#define RS_MSS_LUNROLL 2
+#endif
+constexpr int kMssLUnroll = RS_MSS_LUNROLL;   // pass L: row vectors in flight per thread (a slice in one round)
 
 struct MssSmem {
     unsigned long long childw[RS_MAX_TREE];   // current w of child x's token (owner CTA only)
@@ -792,49 +836,9 @@ struct MssSmem {
 
 // Block + cluster all-reduce of three u64 values (ops op[0..2]); same result in every thread.
 __device__ __forceinline__ void allreduce3(unsigned long long v[3], const int op[3], Smem& sm, int& phase) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-    for (int o = 16; o; o >>= 1)
-#pragma unroll
-        for (int k = 0; k < 3; ++k) v[k] = op_apply(op[k], v[k], __shfl_xor_sync(0xffffffffu, v[k], o));
-    __syncwarp();
-    __syncthreads();
-    if (lane == 0) { sm.red[w][0] = v[0]; sm.red[w][1] = v[1]; sm.scan[w] = v[2]; }
-    __syncwarp();
-    __syncthreads();
-    unsigned long long a[3] = {sm.red[0][0], sm.red[0][1], sm.scan[0]};
-    for (int k = 1; k < kWarps; ++k) {
-        a[0] = op_apply(op[0], a[0], sm.red[k][0]);
-        a[1] = op_apply(op[1], a[1], sm.red[k][1]);
-        a[2] = op_apply(op[2], a[2], sm.scan[k]);
-    }
-    const uint32_t cs = cluster_size();
-    if (cs > 1) {
-        if (threadIdx.x == 0) { sm.xch[phase][0] = a[0]; sm.xch[phase][1] = a[1]; sm.xch[phase][2] = a[2]; }
-        cluster_sync_all();
-        if (w == 0) {
-            const uint32_t c = (uint32_t)lane;
-            unsigned long long r[3] = {0, 0, 0};
-            if (c < cs) {
-#pragma unroll
-                for (int k = 0; k < 3; ++k) r[k] = ld_dsmem_u64(&sm.xch[phase][k], c);
-            }
-#pragma unroll
-            for (int o = 16; o; o >>= 1)
-#pragma unroll
-                for (int k = 0; k < 3; ++k) r[k] = op_apply(op[k], r[k], __shfl_xor_sync(0xffffffffu, r[k], o));
-            if (lane == 0) { sm.red[0][0] = r[0]; sm.red[0][1] = r[1]; sm.scan[0] = r[2]; }
-        }
-        __syncwarp();   // (reconverge the warp before the aligned CTA barrier)
-        __syncwarp();
-    __syncthreads();
-        a[0] = sm.red[0][0];
-        a[1] = sm.red[0][1];
-        a[2] = sm.scan[0];
-        phase ^= 1;
-    }
-    __syncwarp();
-    __syncthreads();   // sm.red / sm.scan are reused by the next reduction
+    unsigned long long a[3] = {v[0], v[1], v[2]};
+    const int o[3] = {op[0], op[1], op[2]};
+    allreduce_n<3>(a, o, sm, phase);
     v[0] = a[0];
     v[1] = a[1];
     v[2] = a[2];
@@ -912,14 +916,14 @@ __device__ __forceinline__ uint32_t r96_shr32(const R96& r, int t) {
 #ifndef RS_MSS_MINB_BF16
 #define RS_MSS_MINB_BF16 4
 #endif
-template <int DT, int DQ>   // DT: logits dtype, DQ: draft-probability dtype (bf16 values are exact fp32)
+template <int DT, int DQ, typename CA>   // DT: logits dtype, DQ: draft-probability dtype (bf16 values are exact fp32)
 __global__ void __launch_bounds__(kMssThreads, DQ == RS_DTYPE_BF16 ? RS_MSS_MINB_BF16 : 3)
 mss_accept_kernel(const void* __restrict__ logits, const void* __restrict__ draft,
                   const int32_t* __restrict__ parent, const int32_t* __restrict__ token,
                   const int32_t* __restrict__ tree_off, const int64_t* __restrict__ gid, int V, float inv_tau,
                   uint64_t seed, uint64_t step, int32_t* __restrict__ acc_out, int32_t* __restrict__ path_out,
                   int32_t* __restrict__ bonus_out, int32_t* __restrict__ flags_out, bool logits_vec_ok,
-                  bool draft_vec_ok) {
+                  bool draft_vec_ok, const __grid_constant__ CA ca) {
     __shared__ Smem sm;
     __shared__ MssSmem ms;
     extern __shared__ __align__(16) uint4 mss_dyn[];
@@ -943,6 +947,7 @@ mss_accept_kernel(const void* __restrict__ logits, const void* __restrict__ draf
     }
     if (__syncthreads_or(bad_node)) {
         if (leader && tid == 0) { acc_out[b] = 0; bonus_out[b] = -1; flags_out[b] = RS_FLAG_MALFORMED; }
+        if constexpr (CA::kOn) fused_commit(ca, b, 0, sm);   // accepted_len 0: new_len only
         return;
     }
     const int64_t g = gid[b];
@@ -958,6 +963,7 @@ mss_accept_kernel(const void* __restrict__ logits, const void* __restrict__ draf
     int c = 0, a = 0, bonus = -1, flags = 0;
     bool bonus_mine = leader;
     if (leader && tid == 0) pth[0] = 0;
+    if (tid == 0) sm.path_s[0] = 0;
     __syncthreads();
     // owner CTA: publish the current (w, qw) of the children x > after of node c (tid < T)
     auto publish = [&](int after, bool resid_state) {
@@ -985,15 +991,15 @@ mss_accept_kernel(const void* __restrict__ logits, const void* __restrict__ draf
             float fmx = -INFINITY;
             uint32_t amag = 0, qbad = 0;
             unsigned long long zq = 0;
-            for (int i0 = vbeg + tid; i0 < vend; i0 += 2 * kMssThreads) {
-                Raw8 x[2], q[2];
+            for (int i0 = vbeg + tid; i0 < vend; i0 += kMssLUnroll * kMssThreads) {
+                Raw8 x[kMssLUnroll], q[kMssLUnroll];
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
+                for (int u = 0; u < kMssLUnroll; ++u) {
                     const int i = i0 + u * kMssThreads;
                     if (i < vend) { x[u] = load_raw(lv, i); q[u] = load_raw(qv, i); }
                 }
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
+                for (int u = 0; u < kMssLUnroll; ++u) {
                     const int i = i0 + u * kMssThreads;
                     if (i >= vend) continue;
                     const bool full = (i + 1) * 8 <= V;
@@ -1099,7 +1105,7 @@ mss_accept_kernel(const void* __restrict__ logits, const void* __restrict__ draf
                 uint32_t en[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j)   // w = trunc(exp_spec((l - m) * inv_tau) * 2^32)
-                    en[j] = f2w(rs::exp_spec(__fmul_rn(__fsub_rn(__uint_as_float(lw[j]), m), inv_tau)));
+                    en[j] = rs::exp_spec_w32(__fmul_rn(__fsub_rn(__uint_as_float(lw[j]), m), inv_tau));
                 s8 = wsum8(en);
                 wp[0] = make_uint4(en[0], en[1], en[2], en[3]);
                 wp[1] = make_uint4(en[4], en[5], en[6], en[7]);
@@ -1239,6 +1245,7 @@ mss_accept_kernel(const void* __restrict__ logits, const void* __restrict__ draf
         c = next;
         ++a;
         if (leader && tid == 0) pth[a] = c;
+        if (tid == 0) sm.path_s[a] = c;
         __syncthreads();
     }
     if (tid == 0) {
@@ -1249,7 +1256,10 @@ mss_accept_kernel(const void* __restrict__ logits, const void* __restrict__ draf
         }
         if (!(flags & RS_FLAG_NONFINITE) && bonus_mine) bonus_out[b] = bonus;
     }
-    if (cs > 1) cluster_sync_all();
+    if constexpr (CA::kOn) fused_commit(ca, b, a, sm);
+    // no final cluster barrier: every DSMEM access (pushes, the child tests' reads of published
+    // weights) is followed in every CTA by at least one cluster barrier (the next pass's reduction or
+    // the bonus draw's exchange), so no CTA touches a peer's shared memory after the peer exits
 }
 
 __global__ void philox_kernel(const uint4* ctr, int64_t n, uint2 key, uint4* out) {
@@ -1277,12 +1287,13 @@ static size_t mss_smem_bytes(int nvec, int cs, bool qbf) {
 
 // MSS launch: cluster size = 16 (non-portable) when the device can co-schedule it, else 8, and
 // never more CTAs than give every CTA >= 256 vectors; dynamic shared memory = per * 64 bytes.
-static rs_status launch_mss(bool bf, bool qbf, const void* logits, const void* draft, const int32_t* parent,
+template <typename CA>
+static rs_status launch_mss(const CA& ca, bool bf, bool qbf, const void* logits, const void* draft, const int32_t* parent,
                             const int32_t* token, const int32_t* tree_off, const int64_t* gid, int B, int V,
                             float inv_tau, uint64_t seed, uint64_t step, int32_t* acc, int32_t* path, int32_t* bonus,
                             int32_t* flags, bool lvec, bool dvec, cudaStream_t st) {
-    auto kern = bf ? (qbf ? mss_accept_kernel<RS_DTYPE_BF16, RS_DTYPE_BF16> : mss_accept_kernel<RS_DTYPE_BF16, RS_DTYPE_F32>)
-                   : (qbf ? mss_accept_kernel<RS_DTYPE_F32, RS_DTYPE_BF16> : mss_accept_kernel<RS_DTYPE_F32, RS_DTYPE_F32>);
+    auto kern = bf ? (qbf ? mss_accept_kernel<RS_DTYPE_BF16, RS_DTYPE_BF16, CA> : mss_accept_kernel<RS_DTYPE_BF16, RS_DTYPE_F32, CA>)
+                   : (qbf ? mss_accept_kernel<RS_DTYPE_F32, RS_DTYPE_BF16, CA> : mss_accept_kernel<RS_DTYPE_F32, RS_DTYPE_F32, CA>);
     const int nvec = (V + 7) / 8;
     static int max_cs = 0;            // 16 if a 16-CTA cluster of this kernel can be resident, else 8
     static size_t attr_smem[4] = {0, 0, 0, 0};
@@ -1342,7 +1353,7 @@ static rs_status launch_mss(bool bf, bool qbf, const void* logits, const void* d
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     RS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, logits, draft, parent, token, tree_off, gid, V, inv_tau, seed, step,
-                                     acc, path, bonus, flags, lvec, dvec));
+                                     acc, path, bonus, flags, lvec, dvec, ca));
     return RS_OK;
 }
 
@@ -1366,14 +1377,13 @@ extern "C" rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t lo
                              stream);
 }
 
-extern "C" rs_status rs_tree_accept_ex(int32_t mode, const void* logits, int32_t logits_dtype,
-                                       const void* draft_probs, int32_t draft_dtype, const int32_t* parent,
-                                       const int32_t* token, const int32_t* tree_off,
-                                       const int64_t* gid, int32_t B, int32_t V, float temperature,
-                                       uint64_t seed, uint64_t step, int32_t* accepted_len,
-                                       int32_t* path, int32_t* bonus_token, int32_t* status_flags,
-                                       void* ws, size_t ws_bytes, void* stream) {
-    rs::bind_device(logits);
+template <typename CA>
+static rs_status accept_launch(const CA& ca, int32_t mode, const void* logits, int32_t logits_dtype,
+                               const void* draft_probs, int32_t draft_dtype, const int32_t* parent,
+                               const int32_t* token, const int32_t* tree_off, const int64_t* gid, int32_t B,
+                               int32_t V, float temperature, uint64_t seed, uint64_t step, int32_t* accepted_len,
+                               int32_t* path, int32_t* bonus_token, int32_t* status_flags, void* ws, size_t ws_bytes,
+                               void* stream) {
     RS_REQUIRE(mode == RS_ACCEPT_GREEDY || mode == RS_ACCEPT_SAMPLE_DELTA ||
                    mode == RS_ACCEPT_SAMPLE_MSS,
                RS_ERR_INVALID_ARG, "rs_tree_accept: bad mode %d", mode);
@@ -1421,21 +1431,71 @@ extern "C" rs_status rs_tree_accept_ex(int32_t mode, const void* logits, int32_t
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const bool bf = logits_dtype == RS_DTYPE_BF16;
-    if (mode == RS_ACCEPT_SAMPLE_MSS) return launch_mss(bf, draft_dtype == RS_DTYPE_BF16, logits, draft_probs, parent, token, tree_off, gid, B, V,
+    if (mode == RS_ACCEPT_SAMPLE_MSS) return launch_mss(ca, bf, draft_dtype == RS_DTYPE_BF16, logits, draft_probs, parent, token, tree_off, gid, B, V,
                                                         inv_tau, seed, step, accepted_len, path, bonus_token,
                                                         status_flags, lvec, dvec, cfg.stream);
     auto kern = mode == RS_ACCEPT_GREEDY
-                    ? (bf ? tree_accept_kernel<RS_ACCEPT_GREEDY, RS_DTYPE_BF16> : tree_accept_kernel<RS_ACCEPT_GREEDY, RS_DTYPE_F32>)
-                : mode == RS_ACCEPT_SAMPLE_DELTA
-                    ? (bf ? tree_accept_kernel<RS_ACCEPT_SAMPLE_DELTA, RS_DTYPE_BF16>
-                          : tree_accept_kernel<RS_ACCEPT_SAMPLE_DELTA, RS_DTYPE_F32>)
-                    : (bf ? tree_accept_kernel<RS_ACCEPT_SAMPLE_MSS, RS_DTYPE_BF16>
-                          : tree_accept_kernel<RS_ACCEPT_SAMPLE_MSS, RS_DTYPE_F32>);
+                    ? (bf ? tree_accept_kernel<RS_ACCEPT_GREEDY, RS_DTYPE_BF16, CA>
+                          : tree_accept_kernel<RS_ACCEPT_GREEDY, RS_DTYPE_F32, CA>)
+                    : (bf ? tree_accept_kernel<RS_ACCEPT_SAMPLE_DELTA, RS_DTYPE_BF16, CA>
+                          : tree_accept_kernel<RS_ACCEPT_SAMPLE_DELTA, RS_DTYPE_F32, CA>);
     RS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, (int)mode, logits, (int)logits_dtype, static_cast<const float*>(draft_probs), parent, token,
                                      tree_off, gid, (int)V, inv_tau, seed, step, accepted_len, path, bonus_token,
-                                     status_flags, lvec, dvec, static_cast<uint32_t*>(need ? ws : nullptr), pf));
+                                     status_flags, lvec, dvec, static_cast<uint32_t*>(need ? ws : nullptr), pf, ca));
     return RS_OK;
 }
+
+extern "C" rs_status rs_tree_accept_ex(int32_t mode, const void* logits, int32_t logits_dtype,
+                                       const void* draft_probs, int32_t draft_dtype, const int32_t* parent,
+                                       const int32_t* token, const int32_t* tree_off,
+                                       const int64_t* gid, int32_t B, int32_t V, float temperature,
+                                       uint64_t seed, uint64_t step, int32_t* accepted_len,
+                                       int32_t* path, int32_t* bonus_token, int32_t* status_flags,
+                                       void* ws, size_t ws_bytes, void* stream) {
+    rs::bind_device(logits);
+    return accept_launch(rs::NoCompact{}, mode, logits, logits_dtype, draft_probs, draft_dtype, parent, token, tree_off,
+                         gid, B, V, temperature, seed, step, accepted_len, path, bonus_token, status_flags, ws,
+                         ws_bytes, stream);
+}
+
+extern "C" rs_status rs_tree_accept_compact(int32_t mode, const void* logits, int32_t logits_dtype,
+                                            const void* draft_probs, int32_t draft_dtype, const int32_t* parent,
+                                            const int32_t* token, const int32_t* tree_off, const int64_t* gid,
+                                            int32_t B, int32_t V, float temperature, uint64_t seed, uint64_t step,
+                                            int32_t* accepted_len, int32_t* path, int32_t* bonus_token,
+                                            int32_t* status_flags, void* ws, size_t ws_bytes,
+                                            void* const* k_layers_host, void* const* v_layers_host, int32_t L,
+                                            int32_t Hkv, int32_t head_dim, int32_t page_size,
+                                            const int32_t* block_table, int32_t max_pages, const int32_t* prefix_len,
+                                            int32_t* new_len, int32_t* moves, void* stream) {
+    rs::bind_device(logits);
+    RS_REQUIRE(L >= 0 && L <= rs::kCompactMaxLayers && Hkv > 0 && page_size > 0 && max_pages >= 0,
+               RS_ERR_INVALID_ARG, "rs_tree_accept_compact: bad KV sizes (L=%d, at most %d layers)", L,
+               rs::kCompactMaxLayers);
+    RS_REQUIRE(head_dim > 0 && head_dim % 8 == 0, RS_ERR_UNSUPPORTED, "rs_tree_accept_compact: head_dim %% 8 != 0");
+    if (B == 0) return RS_OK;
+    RS_REQUIRE((L == 0 || (k_layers_host && v_layers_host)) && block_table && prefix_len && new_len,
+               RS_ERR_INVALID_ARG, "rs_tree_accept_compact: null pointer");
+    rs::CompactArgs A;
+    for (int i = 0; i < L; ++i) {
+        RS_REQUIRE(k_layers_host[i] && v_layers_host[i], RS_ERR_INVALID_ARG,
+                   "rs_tree_accept_compact: null layer pointer");
+        A.k[i] = k_layers_host[i];
+        A.v[i] = v_layers_host[i];
+    }
+    A.nl = L;
+    A.Hkv = Hkv;
+    A.d = head_dim;
+    A.ps = page_size;
+    A.max_pages = max_pages;
+    A.block_table = block_table;
+    A.prefix_len = prefix_len;
+    A.new_len = new_len;
+    A.moves = moves;
+    return accept_launch(A, mode, logits, logits_dtype, draft_probs, draft_dtype, parent, token, tree_off, gid, B, V,
+                         temperature, seed, step, accepted_len, path, bonus_token, status_flags, ws, ws_bytes, stream);
+}
+
 
 extern "C" rs_status rs_philox4x32_10(const uint32_t* ctr, int64_t n, const uint32_t* key_host,
                                       uint32_t* out, void* stream) {

@@ -32,13 +32,22 @@ __device__ __forceinline__ uint32_t uniform_word(uint64_t seed, uint64_t step, i
     return philox4x32_10(c, k).x;
 }
 
-// exp_spec(x) for x <= 0 (0 for x < -32 or NaN). Sequence of single RN fp32 operations.
-__device__ __forceinline__ float exp_spec(float x) {
-    if (!(x >= -32.0f)) return 0.0f;
+// exp_spec(x) for x <= 0 (0 for x < -32 or NaN). Sequence of single RN fp32 operations
+// (DESIGN.md "exp_spec"). Branch-free, so the compiler can interleave the independent chains of
+// a vector's elements: the polynomial is evaluated for every x and the x < -32 / NaN lanes are
+// selected to 0 at the end (their intermediate values are discarded, no trap). n = rint(v) is
+// taken as fl(v + 1.5*2^23) - 1.5*2^23: for |v| < 2^22 the sum lies in [2^23, 2^24), where the
+// floats are the integers, so its round-to-nearest-even IS rint(v) (1.5*2^23 is even) and the
+// subtraction is exact; the integer n is then the sum's low mantissa bits (no FRND / F2I).
+// Returns y (the polynomial part) and n with exp_spec(x) = y * 2^n for x in [-32, 0].
+__device__ __forceinline__ float exp_spec_parts(float x, int& ni) {
     const float LOG2E = 1.44269502735137939453125f;
     const float C1 = 0.693359375f;
     const float C2 = -2.12194440e-4f;
-    float n = rintf(__fmul_rn(x, LOG2E));
+    const float SHIFT = 12582912.0f;   // 1.5 * 2^23
+    const float t = __fadd_rn(__fmul_rn(x, LOG2E), SHIFT);
+    const float n = __fsub_rn(t, SHIFT);
+    ni = __float_as_int(t) - 0x4B400000;
     float r = __fsub_rn(x, __fmul_rn(n, C1));
     r = __fsub_rn(r, __fmul_rn(n, C2));
     float p = 1.9875691500e-4f;
@@ -49,10 +58,25 @@ __device__ __forceinline__ float exp_spec(float x) {
     p = __fadd_rn(__fmul_rn(p, r), 5.0000001201e-1f);
     float y = __fmul_rn(p, __fmul_rn(r, r));
     y = __fadd_rn(y, r);
-    y = __fadd_rn(y, 1.0f);
+    return __fadd_rn(y, 1.0f);
+}
+
+__device__ __forceinline__ float exp_spec(float x) {
+    int ni;
+    const float y = exp_spec_parts(x, ni);
     // y * 2^n, n in [-47, 0]: the power of two is a normal float, the product is exact.
-    int ni = __float2int_rn(n);
-    return __fmul_rn(y, __int_as_float((127 + ni) << 23));
+    const float e = __fmul_rn(y, __int_as_float((127 + ni) << 23));
+    return (x >= -32.0f) ? e : 0.0f;
+}
+
+// trunc(exp_spec(x) * 2^32) ENCODED as u32 (2^32 -> 0xFFFFFFFF, the f2w code of the MSS kernel).
+// exp_spec(x) * 2^32 = (y * 2^n) * 2^32 = y * 2^(n+32) exactly (both scalings are exact: y * 2^n
+// is a normal float for n >= -47), so one multiply; cvt.rzi.u32 saturates 2^32 to 0xFFFFFFFF.
+__device__ __forceinline__ uint32_t exp_spec_w32(float x) {
+    int ni;
+    const float y = exp_spec_parts(x, ni);
+    const uint32_t w = __float2uint_rz(__fmul_rn(y, __int_as_float((127 + 32 + ni) << 23)));
+    return (x >= -32.0f) ? w : 0u;
 }
 
 // Target weight: trunc(exp_spec((l - m) * inv_tau) * 2^32).

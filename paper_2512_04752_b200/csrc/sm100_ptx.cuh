@@ -101,6 +101,14 @@ __device__ __forceinline__ unsigned long long ld_dsmem_u64(const void* local, ui
     return v;
 }
 
+// Store a u64 at the same shared-memory offset in CTA `rank` of the cluster (weak store: made
+// visible to that CTA by a following barrier.cluster.arrive.release / wait.acquire pair).
+__device__ __forceinline__ void st_dsmem_u64(void* local, uint32_t rank, unsigned long long v) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
+    asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(remote), "l"(v) : "memory");
+}
+
 // Map a local shared-memory address to the same offset in CTA `rank` of the cluster.
 __device__ __forceinline__ uint32_t mapa_rank(const void* local, uint32_t rank) {
     uint32_t remote;

@@ -1,6 +1,9 @@
 """One batched verification step through the C ABI (SURVEY.md §3 call stack (1)):
 
-    rs_tree_build_mask -> rs_tree_verify_attention_layers (L layers) -> rs_tree_accept -> rs_kv_compact
+    rs_tree_build_mask -> rs_tree_verify_attention_layers (L layers) -> rs_tree_accept_compact
+
+(rs_tree_accept_compact = rs_tree_accept + rs_kv_compact in one launch; `fused_commit=False`
+issues the two calls separately.)
 
 With `lm_head=(hidden, weight)` (f2, greedy only) acceptance starts from the nodes' final hidden
 states instead of materialised logits: rs_lm_head_argmax -> rs_tree_accept_greedy_tokens.
@@ -17,7 +20,7 @@ from . import core
 
 class VerifyStep:
     def __init__(self, batch: dict, mode: int = core.GREEDY, temperature: float = 1.0, num_ctas: int = 0,
-                 with_lse: bool = False, lm_head=None):
+                 with_lse: bool = False, lm_head=None, fused_commit: bool = True):
         b = batch
         dev = b["q"].device
         self.b = b
@@ -48,6 +51,10 @@ class VerifyStep:
         if self.hidden is not None:
             assert mode == core.GREEDY, "the fused LM head feeds greedy acceptance only"
         self.draft = b.get("draft_probs") if mode == core.SAMPLE_MSS else None
+        # acceptance and the KV commit in one launch (not for the f2 token path, nor for more
+        # layers than one launch's parameter block holds)
+        self.fused_commit = bool(fused_commit) and self.hidden is None and self.L <= core.COMPACT_MAX_LAYERS
+        self.layer_ptrs = (core._layer_ptrs(self.k_layers), core._layer_ptrs(self.v_layers))
         NT = self.q.shape[1]
         self.mask = torch.empty(NT, dtype=torch.int64, device=dev)
         self.depth = torch.empty(NT, dtype=torch.int32, device=dev)
@@ -99,6 +106,13 @@ class VerifyStep:
                         self.ps, new_len=self.new_len, stream=stream)
 
     def accept_compact_step(self, seed, step, stream=None):
+        if self.fused_commit:
+            core.tree_accept_compact(self.mode, self.logits, self.parent, self.token, self.tree_off, self.gid,
+                                     self.k_layers, self.v_layers, self.block_table, self.prefix_len,
+                                     draft_probs=self.draft, temperature=self.temperature, seed=seed, step=step,
+                                     out=(self.acc, self.path, self.bonus, self.flags), new_len=self.new_len,
+                                     stream=stream, ws=self.accept_ws, layer_ptrs=self.layer_ptrs)
+            return
         self.accept_step(seed, step, stream)
         self.compact_step(stream)
 
@@ -135,7 +149,8 @@ class VerifyStep:
 
     def capture_parts(self, seed=0, step=0):
         """Four CUDA graphs (mask | L x attention | accept | compact) so a caller can time each
-        part with events between replays."""
+        part with events between replays. With the fused commit the third graph is accept +
+        compact (one launch) and the fourth is None."""
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
@@ -143,12 +158,18 @@ class VerifyStep:
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
         parts = []
-        for fn in (lambda st: self.mask_step(st), lambda st: self.attention_step(st),
-                   lambda st: self.accept_step(seed, step, st), lambda st: self.compact_step(st)):
+        fns = [lambda st: self.mask_step(st), lambda st: self.attention_step(st)]
+        if self.fused_commit:
+            fns.append(lambda st: self.accept_compact_step(seed, step, st))
+        else:
+            fns += [lambda st: self.accept_step(seed, step, st), lambda st: self.compact_step(st)]
+        for fn in fns:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 fn(torch.cuda.current_stream())
             parts.append(g)
+        if self.fused_commit:
+            parts.append(None)
         self.parts = parts
         return parts
 
