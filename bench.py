@@ -478,6 +478,20 @@ def main():
     return run_ours(args, world, rank, local)
 
 
+def _pack_draft_rows(b, dev):
+    """MSS draft rows of the nodes WITH children only, plus the node -> row map (Z29:
+    a leaf's draft row is never read, so it is neither stored nor uploaded)."""
+    par, off = np.asarray(b["parent"]), np.asarray(b["tree_off"])
+    has = np.zeros(len(par), bool)
+    for s_ in range(len(off) - 1):
+        has[par[off[s_] + 1:off[s_ + 1]] + off[s_]] = True
+    idx = np.nonzero(has)[0]
+    row = np.full(len(par), -1, np.int32)
+    row[idx] = np.arange(len(idx), dtype=np.int32)
+    dq = b["draft_probs"].index_select(0, torch.as_tensor(idx, device=b["draft_probs"].device)).contiguous()
+    return dq, torch.as_tensor(row, device=dev), has
+
+
 def run_ours(args, world, rank, local):
     from paper_2512_04752_b200 import core
     from paper_2512_04752_b200.step import VerifyStep
@@ -507,6 +521,9 @@ def run_ours(args, world, rank, local):
     if n_buf is not None and n_buf < cfg.L:
         b["L_logical"] = cfg.L
     mode = {"greedy": core.GREEDY, "delta": core.SAMPLE_DELTA, "mss": core.SAMPLE_MSS}[cfg.mode]
+    has_kids = None
+    if mode == core.SAMPLE_MSS and b.get("draft_probs") is not None:
+        b["draft_probs"], b["draft_row"], has_kids = _pack_draft_rows(b, dev)
     lm_in = None
     if lm is not None:
         lm_in = make_lm_head_inputs(b, Dm=lm[1], seed=7 + 1000 * rank, device=dev, gen_device=dev)
@@ -610,7 +627,12 @@ def run_ours(args, world, rank, local):
     moves = int(sum(int(np.sum(path_np[i, 1:acc_np[i] + 1] != np.arange(1, acc_np[i] + 1))) for i in range(b["B"])))
     esz = 2 if lm is not None or b["logits"].dtype == torch.bfloat16 else 4
     qsz = (b["draft_probs"].element_size() if mode == core.SAMPLE_MSS else 0)
-    acc_bytes = tokens_per_step * cfg.V * (esz + qsz)   # visited rows (logits + MSS draft row)
+    # visited rows: logits, plus (MSS) the draft row of every visited node that has children
+    q_rows = 0
+    if has_kids is not None:
+        off_np = np.asarray(b["tree_off"])
+        q_rows = int(sum(int(has_kids[off_np[i] + path_np[i, :acc_np[i] + 1]].sum()) for i in range(b["B"])))
+    acc_bytes = tokens_per_step * cfg.V * esz + q_rows * cfg.V * qsz
     cmp_bytes = 2 * moves * step.L * 4 * cfg.Hkv * cfg.d
     kernels = {
         "attention": {"ms_per_step": round(attn_ms, 4), "launches": step.L, "bytes": by * step.L,
@@ -929,6 +951,8 @@ def run_e2e(step, b, n_steps, tokens_per_step, world, dev, barrier, mode, temper
         b2["logits"] = torch.empty_like(step.logits)
     if step.draft is not None:
         b2["draft_probs"] = torch.empty_like(step.draft)
+    if step.draft_row is not None:
+        b2["draft_row"] = torch.empty_like(step.draft_row)   # per-step metadata: its own buffer
     step2 = VerifyStep(b2, mode=mode, temperature=temperature,
                        lm_head=(b2["hidden"], step.lm_w) if lm else None)
     steps = [step, step2]
@@ -936,7 +960,8 @@ def run_e2e(step, b, n_steps, tokens_per_step, world, dev, barrier, mode, temper
     ins = [[s.q] * q_reps + [s.hidden if lm else s.logits] for s in steps]
     h_q = torch.empty(step.q.shape, dtype=step.q.dtype, pin_memory=True).copy_(step.q)
     h_ins = [h_q] * q_reps + [torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t) for t in ins[0][q_reps:]]
-    metas = [[s.parent, s.token, s.tree_off, s.prefix_len, s.block_table, s.gid] for s in steps]
+    metas = [[s.parent, s.token, s.tree_off, s.prefix_len, s.block_table, s.gid] +
+             ([s.draft_row] if s.draft_row is not None else []) for s in steps]
     h_meta = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t) for t in metas[0]]
     h_draft = None
     if step.draft is not None:

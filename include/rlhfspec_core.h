@@ -208,7 +208,8 @@ rs_status rs_tree_verify_attention_layers(
  *   mode        RS_ACCEPT_GREEDY | RS_ACCEPT_SAMPLE_DELTA | RS_ACCEPT_SAMPLE_MSS
  *   logits      device [NT, V], RS_DTYPE_BF16 or RS_DTYPE_F32 (target LLM row per node)
  *   draft_probs device fp32 [NT, V]: row c = the draft distribution the children of c were
- *               drawn from (MSS only; must be NULL otherwise)
+ *               drawn from (MSS only; must be NULL otherwise); read only for nodes that have
+ *               children (Z29)
  *   parent, token device int32 [NT]; tree_off device int32 [B+1]; gid device int64 [B]
  *               (global sample ids; the RNG is keyed by gid, so results do not depend on
  *               which GPU/slot holds the sample)
@@ -219,8 +220,9 @@ rs_status rs_tree_verify_attention_layers(
  *   status_flags device int32 [B]  out: RS_FLAG_* bits. RS_FLAG_MALFORMED (accepted_len 0,
  *               bonus -1): T_b outside [1, 64], parent[0] != -1, parent[i] outside [0, i), or a
  *               draft node (i >= 1) whose token is outside [0, V) (e.g. rs_tree_select's -1 pad).
- *               RS_FLAG_NONFINITE: a visited row holds NaN/Inf logits, or (MSS) its draft row
- *               holds a value outside [0, 1] or NaN (walk stops there, bonus -1).
+ *               RS_FLAG_NONFINITE: a visited row holds NaN/Inf logits, or (MSS) the draft row of
+ *               a visited node with children holds a value outside [0, 1] or NaN (walk stops
+ *               there, bonus -1).
  *   ws, ws_bytes: device workspace >= rs_tree_accept_workspace_bytes(mode, B, V) bytes, 16-byte
  *               aligned (MSS keeps each sample's residual weights there; 0 bytes otherwise:
  *               NULL allowed); too small -> RS_ERR_WORKSPACE. */
@@ -271,9 +273,18 @@ rs_status rs_kv_compact(void* const* k_layers_host, void* const* v_layers_host, 
  * bytes) is identical to the two calls in sequence; arguments as in rs_tree_accept_ex and
  * rs_kv_compact (num_pages is not needed). L <= 256 (else RS_ERR_INVALID_ARG: use the two
  * calls); head_dim % 8 != 0 -> RS_ERR_UNSUPPORTED. The K/V pointers are read at launch (they are
- * kernel parameters, so a captured CUDA graph keeps the layer list it was captured with). */
+ * kernel parameters, so a captured CUDA graph keeps the layer list it was captured with).
+ *   draft_row  MSS only (else must be NULL): device int32 [NT] or NULL. NULL: node i's draft
+ *              distribution is row i of draft_probs ([NT, V], as in rs_tree_accept_ex). Else
+ *              draft_probs is [R, V] holding only the rows that are used, and draft_row[i] is the
+ *              row of node i (-1 for a node without children). Either way the draft row of a node
+ *              WITHOUT children is never read (Z29: nothing was drawn from it; a visited
+ *              leaf's bonus comes from the target weights), so a caller uploads only the rows of
+ *              nodes with children; a node with children whose draft_row is negative sets
+ *              RS_FLAG_MALFORMED (accepted_len 0, bonus -1). */
 rs_status rs_tree_accept_compact(int32_t mode, const void* logits, int32_t logits_dtype, const void* draft_probs,
-                                 int32_t draft_dtype, const int32_t* parent, const int32_t* token,
+                                 int32_t draft_dtype, const int32_t* draft_row, const int32_t* parent,
+                                 const int32_t* token,
                                  const int32_t* tree_off, const int64_t* gid, int32_t B, int32_t V,
                                  float temperature, uint64_t seed, uint64_t step, int32_t* accepted_len,
                                  int32_t* path, int32_t* bonus_token, int32_t* status_flags, void* ws,

@@ -46,6 +46,9 @@ def _load():
         _lib.oracle_tree_accept.argtypes = [ctypes.c_int, P, ctypes.c_int, P, P, P, P, P,
                                             ctypes.c_int, ctypes.c_int, ctypes.c_float,
                                             ctypes.c_uint64, ctypes.c_uint64, P, P, P, P]
+        _lib.oracle_tree_accept_rows.argtypes = [ctypes.c_int, P, ctypes.c_int, P, P, P, P, P, P,
+                                                 ctypes.c_int, ctypes.c_int, ctypes.c_float,
+                                                 ctypes.c_uint64, ctypes.c_uint64, P, P, P, P]
     return _lib
 
 
@@ -88,9 +91,11 @@ def row_weights(logits_row, inv_tau=1.0):
 
 
 def tree_accept(mode, logits, parent, token, tree_off, gid, V, draft_probs=None,
-                temperature=1.0, seed=0, step=0):
+                temperature=1.0, seed=0, step=0, draft_row=None):
     """logits: [NT, V] as np.uint16 (bf16 bits) or np.float32. Returns
-    (accepted_len[B], path[B,64], bonus[B], flags[B])."""
+    (accepted_len[B], path[B,64], bonus[B], flags[B]). MSS: draft_probs [R, V]; draft_row
+    (optional, int32 [NT]) = the row of node i's draft distribution (None: row i); only nodes
+    with children are read (reading Z29)."""
     lg = np.ascontiguousarray(logits)
     is_bf16 = 1 if lg.dtype == np.uint16 else 0
     if not is_bf16:
@@ -107,8 +112,10 @@ def tree_accept(mode, logits, parent, token, tree_off, gid, V, draft_probs=None,
     path = np.zeros((B, MAX_TREE), dtype=np.int32)
     bonus = np.zeros(B, dtype=np.int32)
     flags = np.zeros(B, dtype=np.int32)
-    _load().oracle_tree_accept(int(mode), _ptr(lg), is_bf16, _ptr(dp) if dp is not None else None,
-                               _ptr(par), _ptr(tok), _ptr(off), _ptr(g), B, int(V),
-                               ctypes.c_float(temperature), ctypes.c_uint64(seed),
-                               ctypes.c_uint64(step), _ptr(acc), _ptr(path), _ptr(bonus), _ptr(flags))
+    dr = None if draft_row is None else np.ascontiguousarray(draft_row, dtype=np.int32)
+    _load().oracle_tree_accept_rows(int(mode), _ptr(lg), is_bf16, _ptr(dp) if dp is not None else None,
+                                    _ptr(dr) if dr is not None else None,
+                                    _ptr(par), _ptr(tok), _ptr(off), _ptr(g), B, int(V),
+                                    ctypes.c_float(temperature), ctypes.c_uint64(seed),
+                                    ctypes.c_uint64(step), _ptr(acc), _ptr(path), _ptr(bonus), _ptr(flags))
     return acc, path, bonus, flags

@@ -16,7 +16,9 @@
  *                 min(1, p(x)/1) (draft q = one-hot); on rejection p <- norm(p with p(x)=0);
  *                 bonus ~ residual p.
  *   SAMPLE_MSS    children drawn i.i.d. from q_c (draft_probs row c): accept w.p.
- *                 min(1, p(x)/q(x)); on rejection p <- norm(max(p - q, 0)).
+ *                 min(1, p(x)/q(x)); on rejection p <- norm(max(p - q, 0)). q_c is read only
+ *                 for a node that HAS children (reading Z29: a node without children has no
+ *                 distribution its children were drawn from; its draft row is never used).
  * Arithmetic: distributions are unsigned integer weights
  *   w_v = trunc(exp_spec((l_v - max l) * inv_tau) * 2^32), all sums/compares in integers,
  *   uniforms are word 0 of Philox4x32-10(counter=(trial, node, lo32(step), lo32(gid)),
@@ -162,11 +164,13 @@ static int greedy_argmax(const void* logits, int is_bf16, int64_t row, int V, in
     return best;
 }
 
-int oracle_tree_accept(int mode, const void* logits, int logits_is_bf16, const float* draft_probs,
-                       const int32_t* parent, const int32_t* token, const int32_t* tree_off,
-                       const int64_t* gid, int B, int V, float temperature, uint64_t seed,
-                       uint64_t step, int32_t* accepted_len, int32_t* path, int32_t* bonus,
-                       int32_t* flags) {
+/* draft_row (MSS, may be NULL = identity): row of draft_probs holding node i's q (global node
+ * index i); a node with children whose draft_row is negative makes the tree malformed. */
+int oracle_tree_accept_rows(int mode, const void* logits, int logits_is_bf16, const float* draft_probs,
+                            const int32_t* draft_row, const int32_t* parent, const int32_t* token,
+                            const int32_t* tree_off, const int64_t* gid, int B, int V, float temperature,
+                            uint64_t seed, uint64_t step, int32_t* accepted_len, int32_t* path, int32_t* bonus,
+                            int32_t* flags) {
     float inv_tau = 1.0f / temperature;
     uint64_t* w = (uint64_t*)malloc(sizeof(uint64_t) * V);
     uint64_t* w_saved = (uint64_t*)malloc(sizeof(uint64_t) * V);
@@ -185,6 +189,9 @@ int oracle_tree_accept(int mode, const void* logits, int logits_is_bf16, const f
         int ok = (T >= 1 && T <= MAX_TREE && parent[off] == -1);
         for (int i = 1; ok && i < T; ++i)
             ok = (parent[off + i] >= 0 && parent[off + i] < i && token[off + i] >= 0 && token[off + i] < V);
+        /* MSS with a row map: every node with children needs a draft row */
+        for (int i = 1; ok && mode == MODE_MSS && draft_row && i < T; ++i)
+            ok = draft_row[off + parent[off + i]] >= 0;
         if (!ok) { flags[b] = FLAG_MALFORMED; continue; }
 
         int c = 0, a = 0;
@@ -209,16 +216,17 @@ int oracle_tree_accept(int mode, const void* logits, int logits_is_bf16, const f
                     break;
                 }
                 uint64_t Zq = 0;
-                if (mode == MODE_MSS) {
+                if (mode == MODE_MSS && nch > 0) {   /* reading Z29: leaves' rows are not read */
+                    const int64_t qrow = draft_row ? draft_row[off + c] : row;
                     /* the draft row must be a probability vector: every q_v in [0, 1] (reading
                      * Z15 extended: otherwise the sample is flagged like a non-finite row) */
                     int okq = 1;
                     for (int v = 0; v < V && okq; ++v) {
-                        float qv = draft_probs[row * (int64_t)V + v];
+                        float qv = draft_probs[qrow * (int64_t)V + v];
                         okq = (qv >= 0.0f && qv <= 1.0f);
                     }
                     if (!okq) { flags[b] |= FLAG_NONFINITE; break; }
-                    Zq = draft_weights(draft_probs, row, V, qw);
+                    Zq = draft_weights(draft_probs, qrow, V, qw);
                 }
                 for (int k = 0; k < nch; ++k) {
                     int x = ch[k];
@@ -271,6 +279,15 @@ int oracle_tree_accept(int mode, const void* logits, int logits_is_bf16, const f
     }
     free(w); free(w_saved); free(qw); free(r);
     return 0;
+}
+
+int oracle_tree_accept(int mode, const void* logits, int logits_is_bf16, const float* draft_probs,
+                       const int32_t* parent, const int32_t* token, const int32_t* tree_off,
+                       const int64_t* gid, int B, int V, float temperature, uint64_t seed,
+                       uint64_t step, int32_t* accepted_len, int32_t* path, int32_t* bonus,
+                       int32_t* flags) {
+    return oracle_tree_accept_rows(mode, logits, logits_is_bf16, draft_probs, NULL, parent, token, tree_off, gid,
+                                   B, V, temperature, seed, step, accepted_len, path, bonus, flags);
 }
 
 /* Elementwise exp_spec over an array (for pin tests that sweep many inputs). */

@@ -59,7 +59,7 @@ _sig("rs_tree_accept_ex", _i32, _i32, _P, _i32, _P, _i32, _P, _P, _P, _P, _i32, 
 _sig("rs_philox4x32_10", _i32, _P, _i64, _P, _P, _P)
 _sig("rs_exp_spec", _i32, _P, _i64, _P, _P)
 _sig("rs_kv_compact", _i32, _P, _P, _i32, _i64, _i32, _i32, _i32, _P, _i32, _P, _P, _P, _i32, _P, _P, _P)
-_sig("rs_tree_accept_compact", _i32, _i32, _P, _i32, _P, _i32, _P, _P, _P, _P, _i32, _i32, _f32, _u64, _u64,
+_sig("rs_tree_accept_compact", _i32, _i32, _P, _i32, _P, _i32, _P, _P, _P, _P, _P, _i32, _i32, _f32, _u64, _u64,
      _P, _P, _P, _P, _P, _sz, _P, _P, _i32, _i32, _i32, _i32, _P, _i32, _P, _P, _P, _P)
 
 
@@ -263,9 +263,10 @@ def tree_accept(mode, logits, parent, token, tree_off, gid, draft_probs=None, te
 
 def tree_accept_compact(mode, logits, parent, token, tree_off, gid, k_layers, v_layers, block_table, prefix_len,
                         draft_probs=None, temperature=1.0, seed=0, step=0, out=None, new_len=None, moves=None,
-                        stream=None, ws=None, layer_ptrs=None):
+                        stream=None, ws=None, layer_ptrs=None, draft_row=None):
     """rs_tree_accept_ex + rs_kv_compact in one launch (the sample's cluster commits its path's
-    K/V when its walk ends). layer_ptrs: optional pre-built (k, v) ctypes pointer arrays."""
+    K/V when its walk ends). layer_ptrs: optional pre-built (k, v) ctypes pointer arrays.
+    draft_row (MSS): optional int32 [NT] row of draft_probs per node (-1: no children)."""
     NT, V = logits.shape
     B = tree_off.numel() - 1
     need = accept_workspace_bytes(mode, B, V)
@@ -283,7 +284,8 @@ def tree_accept_compact(mode, logits, parent, token, tree_off, gid, k_layers, v_
     L = len(k_layers)
     _, Hkv, ps, d = k_layers[0].shape
     kp, vp = layer_ptrs if layer_ptrs is not None else (_layer_ptrs(k_layers), _layer_ptrs(v_layers))
-    _check(_lib.rs_tree_accept_compact(int(mode), _ptr(logits), dt, _ptr(draft_probs), qdt, _ptr(parent), _ptr(token),
+    _check(_lib.rs_tree_accept_compact(int(mode), _ptr(logits), dt, _ptr(draft_probs), qdt, _ptr(draft_row),
+                                       _ptr(parent), _ptr(token),
                                        _ptr(tree_off), _ptr(gid), B, V, float(temperature), int(seed), int(step),
                                        _ptr(acc), _ptr(path), _ptr(bonus), _ptr(flags), _ptr(ws) if need else None,
                                        ws.numel() if need else 0, kp, vp, L, Hkv, d, ps, _ptr(block_table),

@@ -19,6 +19,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "compact_tail.cuh"
@@ -157,6 +158,8 @@ struct Smem {
     unsigned long long bcast_u;
     int bonus_v;
     int path_s[RS_MAX_TREE];   // the accepted path (every CTA; the fused KV commit reads it)
+    unsigned long long kids;   // MSS: bit i = node i has children (its draft row is read, Z29)
+    int qrow[RS_MAX_TREE];     // MSS: row of node i's draft distribution (draft_row, or off + i)
 };
 
 // Orderable 32-bit key of a float (larger float -> larger key).
@@ -919,7 +922,7 @@ __device__ __forceinline__ uint32_t r96_shr32(const R96& r, int t) {
 template <int DT, int DQ, typename CA>   // DT: logits dtype, DQ: draft-probability dtype (bf16 values are exact fp32)
 __global__ void __launch_bounds__(kMssThreads, DQ == RS_DTYPE_BF16 ? RS_MSS_MINB_BF16 : 3)
 mss_accept_kernel(const void* __restrict__ logits, const void* __restrict__ draft,
-                  const int32_t* __restrict__ parent, const int32_t* __restrict__ token,
+                  const int32_t* __restrict__ draft_row, const int32_t* __restrict__ parent, const int32_t* __restrict__ token,
                   const int32_t* __restrict__ tree_off, const int64_t* __restrict__ gid, int V, float inv_tau,
                   uint64_t seed, uint64_t step, int32_t* __restrict__ acc_out, int32_t* __restrict__ path_out,
                   int32_t* __restrict__ bonus_out, int32_t* __restrict__ flags_out, bool logits_vec_ok,
@@ -938,13 +941,20 @@ mss_accept_kernel(const void* __restrict__ logits, const void* __restrict__ draf
     int phase = 0;
     if (leader && tid < RS_MAX_TREE) pth[tid] = -1;
     bool bad_node = !(T >= 1 && T <= RS_MAX_TREE);
+    if (tid == 0) sm.kids = 0ull;
+    __syncthreads();
     if (!bad_node && tid < T) {
         const int pp = parent[off + tid];
         const int tk = token[off + tid];
         sm.parent[tid] = pp;
         sm.token[tid] = tk;
         bad_node = tid == 0 ? pp != -1 : !(pp >= 0 && pp < tid && tk >= 0 && tk < V);
+        if (!bad_node && tid > 0) atomicOr(&sm.kids, 1ull << pp);
+        sm.qrow[tid] = draft_row ? draft_row[off + tid] : off + tid;
     }
+    __syncthreads();
+    // with a row map, every node with children needs its draft row (else the tree is malformed)
+    if (draft_row && !bad_node && tid < T && ((sm.kids >> tid) & 1ull) && draft_row[off + tid] < 0) bad_node = true;
     if (__syncthreads_or(bad_node)) {
         if (leader && tid == 0) { acc_out[b] = 0; bonus_out[b] = -1; flags_out[b] = RS_FLAG_MALFORMED; }
         if constexpr (CA::kOn) fused_commit(ca, b, 0, sm);   // accepted_len 0: new_len only
@@ -982,7 +992,10 @@ mss_accept_kernel(const void* __restrict__ logits, const void* __restrict__ draf
     };
     for (;;) {
         const RowView lv{logits, (int64_t)(off + c), V, DT, logits_vec_ok};
-        const RowView qv{draft, (int64_t)(off + c), V, DQ, draft_vec_ok};
+        // reading Z29: the draft row is read only for a node with children (a leaf's q is unused:
+        // no child tests, no residual; its bonus is drawn from the target weights alone)
+        const bool with_q = (sm.kids >> c) & 1ull;   // (read here: no register held across the walk)
+        const RowView qv{draft, (int64_t)sm.qrow[c], V, DQ, draft_vec_ok};   // (the row from shared memory)
         // ---- pass L: the row from HBM into shared memory; max, validity, Zq
         // (bf16 logits stay packed: the first 16 bytes of the vector's w words hold the 8 raw
         // values until pass E expands them)
@@ -996,46 +1009,51 @@ mss_accept_kernel(const void* __restrict__ logits, const void* __restrict__ draf
 #pragma unroll
                 for (int u = 0; u < kMssLUnroll; ++u) {
                     const int i = i0 + u * kMssThreads;
-                    if (i < vend) { x[u] = load_raw(lv, i); q[u] = load_raw(qv, i); }
+                    if (i < vend) {
+                        x[u] = load_raw(lv, i);
+                        q[u] = with_q ? load_raw(qv, i) : Raw8{make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < kMssLUnroll; ++u) {
                     const int i = i0 + u * kMssThreads;
                     if (i >= vend) continue;
                     const bool full = (i + 1) * 8 <= V;
-                    uint32_t qb[8];
-                    if (DQ == RS_DTYPE_BF16) {   // bf16 -> the fp32 bit pattern of the same value
-                        const uint32_t h4[4] = {q[u].a.x, q[u].a.y, q[u].a.z, q[u].a.w};
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) { qb[2 * k] = h4[k] << 16; qb[2 * k + 1] = h4[k] & 0xFFFF0000u; }
-                    } else {
-                        qb[0] = q[u].a.x; qb[1] = q[u].a.y; qb[2] = q[u].a.z; qb[3] = q[u].a.w;
-                        qb[4] = q[u].b.x; qb[5] = q[u].b.y; qb[6] = q[u].b.z; qb[7] = q[u].b.w;
-                    }
-                    uint32_t qe[8], qu[8];
-                    if (full) {
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) qu[j] = qb[j];
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) qu[j] = i * 8 + j < V ? qb[j] : 0u;
-                    }
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        // a probability: bits <= 1.0f, or -0
-                        qbad |= (qu[j] > 0x3F800000u && qu[j] != 0x80000000u) ? 1u : 0u;
-                        qe[j] = f2w(__uint_as_float(qu[j]));
-                    }
-                    zq += wsum8(qe);
                     uint4* wp = reinterpret_cast<uint4*>(wsl + (size_t)(i - vbeg) * 8);
-                    if (DQ == RS_DTYPE_BF16) {   // the raw values back (padding lanes zero)
-                        *reinterpret_cast<uint4*>(qsl16 + (size_t)(i - vbeg) * 8) =
-                            make_uint4((qu[0] >> 16) | (qu[1] & 0xFFFF0000u), (qu[2] >> 16) | (qu[3] & 0xFFFF0000u),
-                                       (qu[4] >> 16) | (qu[5] & 0xFFFF0000u), (qu[6] >> 16) | (qu[7] & 0xFFFF0000u));
-                    } else {
-                        uint4* qp = reinterpret_cast<uint4*>(qsl + (size_t)(i - vbeg) * 8);
-                        qp[0] = make_uint4(qe[0], qe[1], qe[2], qe[3]);
-                        qp[1] = make_uint4(qe[4], qe[5], qe[6], qe[7]);
+                    {   // the draft row (zeros at a leaf: its row is not read, Z29)
+                        uint32_t qb[8];
+                        if (DQ == RS_DTYPE_BF16) {   // bf16 -> the fp32 bit pattern of the same value
+                            const uint32_t h4[4] = {q[u].a.x, q[u].a.y, q[u].a.z, q[u].a.w};
+    #pragma unroll
+                            for (int k = 0; k < 4; ++k) { qb[2 * k] = h4[k] << 16; qb[2 * k + 1] = h4[k] & 0xFFFF0000u; }
+                        } else {
+                            qb[0] = q[u].a.x; qb[1] = q[u].a.y; qb[2] = q[u].a.z; qb[3] = q[u].a.w;
+                            qb[4] = q[u].b.x; qb[5] = q[u].b.y; qb[6] = q[u].b.z; qb[7] = q[u].b.w;
+                        }
+                        uint32_t qe[8], qu[8];
+                        if (full) {
+    #pragma unroll
+                            for (int j = 0; j < 8; ++j) qu[j] = qb[j];
+                        } else {
+    #pragma unroll
+                            for (int j = 0; j < 8; ++j) qu[j] = i * 8 + j < V ? qb[j] : 0u;
+                        }
+    #pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            // a probability: bits <= 1.0f, or -0
+                            qbad |= (qu[j] > 0x3F800000u && qu[j] != 0x80000000u) ? 1u : 0u;
+                            qe[j] = f2w(__uint_as_float(qu[j]));
+                        }
+                        zq += wsum8(qe);
+                        if (DQ == RS_DTYPE_BF16) {   // the raw values back (padding lanes zero)
+                            *reinterpret_cast<uint4*>(qsl16 + (size_t)(i - vbeg) * 8) =
+                                make_uint4((qu[0] >> 16) | (qu[1] & 0xFFFF0000u), (qu[2] >> 16) | (qu[3] & 0xFFFF0000u),
+                                           (qu[4] >> 16) | (qu[5] & 0xFFFF0000u), (qu[6] >> 16) | (qu[7] & 0xFFFF0000u));
+                        } else {
+                            uint4* qp = reinterpret_cast<uint4*>(qsl + (size_t)(i - vbeg) * 8);
+                            qp[0] = make_uint4(qe[0], qe[1], qe[2], qe[3]);
+                            qp[1] = make_uint4(qe[4], qe[5], qe[6], qe[7]);
+                        }
                     }
                     if (DT == RS_DTYPE_BF16) {
                         uint32_t w4[4] = {x[u].a.x, x[u].a.y, x[u].a.z, x[u].a.w};
@@ -1288,7 +1306,8 @@ static size_t mss_smem_bytes(int nvec, int cs, bool qbf) {
 // MSS launch: cluster size = 16 (non-portable) when the device can co-schedule it, else 8, and
 // never more CTAs than give every CTA >= 256 vectors; dynamic shared memory = per * 64 bytes.
 template <typename CA>
-static rs_status launch_mss(const CA& ca, bool bf, bool qbf, const void* logits, const void* draft, const int32_t* parent,
+static rs_status launch_mss(const CA& ca, bool bf, bool qbf, const void* logits, const void* draft,
+                            const int32_t* draft_row, const int32_t* parent,
                             const int32_t* token, const int32_t* tree_off, const int64_t* gid, int B, int V,
                             float inv_tau, uint64_t seed, uint64_t step, int32_t* acc, int32_t* path, int32_t* bonus,
                             int32_t* flags, bool lvec, bool dvec, cudaStream_t st) {
@@ -1352,7 +1371,8 @@ static rs_status launch_mss(const CA& ca, bool bf, bool qbf, const void* logits,
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    RS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, logits, draft, parent, token, tree_off, gid, V, inv_tau, seed, step,
+    RS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, logits, draft, draft_row, parent, token, tree_off, gid, V, inv_tau,
+                                     seed, step,
                                      acc, path, bonus, flags, lvec, dvec, ca));
     return RS_OK;
 }
@@ -1379,7 +1399,8 @@ extern "C" rs_status rs_tree_accept(int32_t mode, const void* logits, int32_t lo
 
 template <typename CA>
 static rs_status accept_launch(const CA& ca, int32_t mode, const void* logits, int32_t logits_dtype,
-                               const void* draft_probs, int32_t draft_dtype, const int32_t* parent,
+                               const void* draft_probs, int32_t draft_dtype, const int32_t* draft_row,
+                               const int32_t* parent,
                                const int32_t* token, const int32_t* tree_off, const int64_t* gid, int32_t B,
                                int32_t V, float temperature, uint64_t seed, uint64_t step, int32_t* accepted_len,
                                int32_t* path, int32_t* bonus_token, int32_t* status_flags, void* ws, size_t ws_bytes,
@@ -1394,6 +1415,8 @@ static rs_status accept_launch(const CA& ca, int32_t mode, const void* logits, i
     RS_REQUIRE(B >= 0 && V >= 1, RS_ERR_INVALID_ARG, "rs_tree_accept: B=%d V=%d", B, V);
     RS_REQUIRE((mode == RS_ACCEPT_SAMPLE_MSS) == (draft_probs != nullptr), RS_ERR_INVALID_ARG,
                "rs_tree_accept: draft_probs must be given for MSS only");
+    RS_REQUIRE(mode == RS_ACCEPT_SAMPLE_MSS || draft_row == nullptr, RS_ERR_INVALID_ARG,
+               "rs_tree_accept: draft_row is an MSS argument");
     RS_REQUIRE(mode == RS_ACCEPT_GREEDY || temperature > 0.0f, RS_ERR_INVALID_ARG,
                "rs_tree_accept: temperature must be > 0");
     if (B == 0) return RS_OK;
@@ -1431,7 +1454,8 @@ static rs_status accept_launch(const CA& ca, int32_t mode, const void* logits, i
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const bool bf = logits_dtype == RS_DTYPE_BF16;
-    if (mode == RS_ACCEPT_SAMPLE_MSS) return launch_mss(ca, bf, draft_dtype == RS_DTYPE_BF16, logits, draft_probs, parent, token, tree_off, gid, B, V,
+    if (mode == RS_ACCEPT_SAMPLE_MSS) return launch_mss(ca, bf, draft_dtype == RS_DTYPE_BF16, logits, draft_probs,
+                                                        draft_row, parent, token, tree_off, gid, B, V,
                                                         inv_tau, seed, step, accepted_len, path, bonus_token,
                                                         status_flags, lvec, dvec, cfg.stream);
     auto kern = mode == RS_ACCEPT_GREEDY
@@ -1453,13 +1477,14 @@ extern "C" rs_status rs_tree_accept_ex(int32_t mode, const void* logits, int32_t
                                        int32_t* path, int32_t* bonus_token, int32_t* status_flags,
                                        void* ws, size_t ws_bytes, void* stream) {
     rs::bind_device(logits);
-    return accept_launch(rs::NoCompact{}, mode, logits, logits_dtype, draft_probs, draft_dtype, parent, token, tree_off,
-                         gid, B, V, temperature, seed, step, accepted_len, path, bonus_token, status_flags, ws,
-                         ws_bytes, stream);
+    return accept_launch(rs::NoCompact{}, mode, logits, logits_dtype, draft_probs, draft_dtype, nullptr, parent,
+                         token, tree_off, gid, B, V, temperature, seed, step, accepted_len, path, bonus_token,
+                         status_flags, ws, ws_bytes, stream);
 }
 
 extern "C" rs_status rs_tree_accept_compact(int32_t mode, const void* logits, int32_t logits_dtype,
-                                            const void* draft_probs, int32_t draft_dtype, const int32_t* parent,
+                                            const void* draft_probs, int32_t draft_dtype,
+                                            const int32_t* draft_row, const int32_t* parent,
                                             const int32_t* token, const int32_t* tree_off, const int64_t* gid,
                                             int32_t B, int32_t V, float temperature, uint64_t seed, uint64_t step,
                                             int32_t* accepted_len, int32_t* path, int32_t* bonus_token,
@@ -1492,8 +1517,9 @@ extern "C" rs_status rs_tree_accept_compact(int32_t mode, const void* logits, in
     A.prefix_len = prefix_len;
     A.new_len = new_len;
     A.moves = moves;
-    return accept_launch(A, mode, logits, logits_dtype, draft_probs, draft_dtype, parent, token, tree_off, gid, B, V,
-                         temperature, seed, step, accepted_len, path, bonus_token, status_flags, ws, ws_bytes, stream);
+    return accept_launch(A, mode, logits, logits_dtype, draft_probs, draft_dtype, draft_row, parent, token, tree_off,
+                         gid, B, V, temperature, seed, step, accepted_len, path, bonus_token, status_flags, ws,
+                         ws_bytes, stream);
 }
 
 

@@ -64,6 +64,13 @@ constexpr bool kStageOut = RS_ATTN_STAGE != 0;   // epilogue output through smem
 constexpr int kQBufs = RS_ATTN_QBUFS;   // Q tile buffers (RM 2/3; RM = 1 uses the two halves of one tile)
 static_assert(kQBufs == 2, "the Q producer / S issuer handshake assumes two Q buffers (1 deadlocks)");
 constexpr int kPF = 0;          // L2 prefetch distance in KV blocks (0 = off; measured: no gain)
+#ifndef RS_ATTN_WARM
+#define RS_ATTN_WARM 0
+#endif
+// Launch-time L2 warm-up: with early prefix streaming, each producer prefetches the prefix blocks
+// [0, kWarm) of its CTA's first item into L2 before its ring wait, i.e. while the preceding
+// layer's slowest CTAs still stream (PDL), so the first blocks of the launch come from L2.
+constexpr int kWarm = RS_ATTN_WARM;
 constexpr int kThreads = 384;    // 12 warps (RM 2/3)
 // RM = 1 (every tile R = 16): 16 warps; warps 12-15 are an epilogue warpgroup, and consecutive
 // items alternate between the two 16-lane halves of each TMEM sub-partition, so item i's O is
@@ -426,6 +433,17 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             WorkItem wn = wnx >= 0 ? load_item(p.items, wnx) : wi;
             const int q0_at = min(wi.blk_end - wi.blk_begin, C::KS) - 1;   // first Q after the first K ring fill
             int pg_cur = page_chunk(wi, 0);
+            // launch-time warm-up (kWarm, early prefix only: prefix blocks, before the wait)
+            if (kWarm > 0 && p.early_prefix) {
+                const int nw = min(min(kWarm, 32), wi.blk_end - wi.blk_begin);
+                for (int k = 0; k < nw; ++k) {
+                    const int page = __shfl_sync(0xffffffffu, pg_cur, k);
+                    if ((wi.blk_begin + k + 1) * kBlockN <= wi.P && elect_one())
+#pragma unroll
+                        for (int bx = 0; bx < C::kBoxes; ++bx) tma_prefetch_2d(tm, bx * 64, (page * p.Hkv + wi.kvh) * kBlockN);
+                    __syncwarp();
+                }
+            }
             // warm L2 with the first blocks of this CTA
             for (int k = 0; k < pf && k < wi.blk_end - wi.blk_begin; ++k) {
                 const int page = __shfl_sync(0xffffffffu, pg_cur, k & 31);

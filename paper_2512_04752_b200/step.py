@@ -55,6 +55,11 @@ class VerifyStep:
         # layers than one launch's parameter block holds)
         self.fused_commit = bool(fused_commit) and self.hidden is None and self.L <= core.COMPACT_MAX_LAYERS
         self.layer_ptrs = (core._layer_ptrs(self.k_layers), core._layer_ptrs(self.v_layers))
+        # MSS: optional row map (draft rows only for nodes with children, Z29)
+        self.draft_row = b.get("draft_row") if mode == core.SAMPLE_MSS else None
+        if self.draft_row is not None:
+            self.draft_row = t32(self.draft_row)
+            assert self.fused_commit, "a draft row map needs the fused acceptance call"
         NT = self.q.shape[1]
         self.mask = torch.empty(NT, dtype=torch.int64, device=dev)
         self.depth = torch.empty(NT, dtype=torch.int32, device=dev)
@@ -111,7 +116,8 @@ class VerifyStep:
                                      self.k_layers, self.v_layers, self.block_table, self.prefix_len,
                                      draft_probs=self.draft, temperature=self.temperature, seed=seed, step=step,
                                      out=(self.acc, self.path, self.bonus, self.flags), new_len=self.new_len,
-                                     stream=stream, ws=self.accept_ws, layer_ptrs=self.layer_ptrs)
+                                     stream=stream, ws=self.accept_ws, layer_ptrs=self.layer_ptrs,
+                                     draft_row=self.draft_row)
             return
         self.accept_step(seed, step, stream)
         self.compact_step(stream)

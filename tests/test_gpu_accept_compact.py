@@ -149,7 +149,7 @@ def test_fused_equals_two_calls_and_layers_edge(cuda_lib):
     nl0 = torch.empty(b["B"], dtype=torch.int32, device="cuda")
     keep = {k: _dev(b[k]) for k in ("parent", "token", "tree_off", "gid", "block_table", "prefix_len")}
     core._check(core._lib.rs_tree_accept_compact(
-        core.GREEDY, core._ptr(b["logits"]), core.DTYPE_BF16, None, core.DTYPE_F32, core._ptr(keep["parent"]),
+        core.GREEDY, core._ptr(b["logits"]), core.DTYPE_BF16, None, core.DTYPE_F32, None, core._ptr(keep["parent"]),
         core._ptr(keep["token"]), core._ptr(keep["tree_off"]), core._ptr(keep["gid"]), b["B"], b["V"], 1.0,
         0, 0, core._ptr(acc), core._ptr(path), core._ptr(bonus), core._ptr(flags), None, 0, None, None, 0, b["Hkv"],
         b["d"], b["page_size"], core._ptr(keep["block_table"]), b["max_pages"], core._ptr(keep["prefix_len"]),
@@ -181,3 +181,75 @@ def test_fused_full_config3s_mss_bit_exact(cuda_lib):
     acc, _ = _check(core, b, b["logits"], core.SAMPLE_MSS, OAcc.MSS, draft=draft, temperature=1.0, seed=11, step=0,
                     samples=samples)
     assert acc.sum() > 0
+
+
+def _packed_rows(b, draft):
+    """Rows of the nodes with children + the node -> row map (-1: no children), Z29."""
+    par, off = np.asarray(b["parent"]), np.asarray(b["tree_off"])
+    has = np.zeros(len(par), bool)
+    for s in range(len(off) - 1):
+        has[par[off[s] + 1:off[s + 1]] + off[s]] = True
+    idx = np.nonzero(has)[0]
+    row = np.full(len(par), -1, np.int32)
+    row[idx] = np.arange(len(idx), dtype=np.int32)
+    return draft[torch.as_tensor(idx, device=draft.device)].contiguous(), row, has
+
+
+def _fused_rows(core, b, logits, draft, row, seed=5, step=2):
+    L = b["k_cache"].shape[0]
+    ks = [b["k_cache"][l] for l in range(L)]
+    vs = [b["v_cache"][l] for l in range(L)]
+    moves = torch.empty((b["B"], 64, 2), dtype=torch.int32, device="cuda")
+    r = core.tree_accept_compact(core.SAMPLE_MSS, logits.cuda(), _dev(b["parent"]), _dev(b["token"]),
+                                 _dev(b["tree_off"]), _dev(b["gid"]), ks, vs, _dev(b["block_table"]),
+                                 _dev(b["prefix_len"]), draft_probs=draft.cuda(), temperature=1.0, seed=seed,
+                                 step=step, moves=moves, draft_row=None if row is None else _dev(row))
+    torch.cuda.synchronize()
+    return [x.cpu().numpy() for x in r]
+
+
+@pytest.mark.parametrize("draft_dtype", ["f32", "bf16"])
+def test_fused_mss_draft_row_map_bit_exact(cuda_lib, draft_dtype):
+    """MSS through the row map (draft rows of the nodes with children only) vs the oracle with the
+    same map, bit for bit; one sample whose internal node has no row is MALFORMED; and garbage in
+    the rows of leaves (full layout, identity map) changes nothing (Z29: never read)."""
+    core = cuda_lib
+    b = _small("mss", 25, V=4000, draft_dtype=draft_dtype, L=2)
+    draft = b["draft_probs"] if draft_dtype == "f32" else b["draft_probs"].to(torch.bfloat16)
+    dq, row, has = _packed_rows(b, draft)
+    off = b["tree_off"]
+    victim = next(s for s in range(2, b["B"]) if off[s + 1] - off[s] > 2 and has[off[s] + 1])
+    row[off[victim] + 1] = -1                      # an internal node without a row
+    o = OAcc.tree_accept(OAcc.MSS, tensor_bf16_bits(b["logits"].cpu()), b["parent"], b["token"], off, b["gid"],
+                         b["V"], draft_probs=dq.float().cpu().numpy(), temperature=1.0, seed=5, step=2, draft_row=row)
+    g = _fused_rows(core, b, b["logits"], dq, row)
+    for x, y in zip(g[:4], o):
+        np.testing.assert_array_equal(x, y)
+    assert o[3][victim] == OAcc.FLAG_MALFORMED and g[0].sum() > 0
+    # leaves' rows hold garbage in the full layout: identical to clean rows
+    dg = draft.clone()
+    leaves = torch.as_tensor(np.nonzero(~has)[0], device=dg.device)
+    dg[leaves] = float("nan")
+    ref = OAcc.tree_accept(OAcc.MSS, tensor_bf16_bits(b["logits"].cpu()), b["parent"], b["token"], off, b["gid"],
+                           b["V"], draft_probs=draft.float().cpu().numpy(), temperature=1.0, seed=5, step=2)
+    g2 = _fused_rows(core, b, b["logits"], dg, None)
+    for x, y in zip(g2[:4], ref):
+        np.testing.assert_array_equal(x, y)
+    assert not (g2[3] & core.FLAG_NONFINITE).any()
+
+
+def test_fused_full_config3s_packed_rows(cuda_lib):
+    """configs[2] as bench.py runs it: draft rows of the nodes with children only (half the rows
+    of an S(n) tree), fused launch over 2 layers of KV; the oracle (same map) walks every sample."""
+    core = cuda_lib
+    from tests.test_gpu_parity import _c3s_batch
+    b = _c3s_batch(layers=2)
+    dq, row, has = _packed_rows(b, b["draft_probs"])
+    assert 0.3 < has.mean() < 0.8
+    o = OAcc.tree_accept(OAcc.MSS, tensor_bf16_bits(b["logits"].cpu()), b["parent"], b["token"], b["tree_off"],
+                         b["gid"], b["V"], draft_probs=dq.float().cpu().numpy(), temperature=1.0, seed=11, step=0,
+                         draft_row=row)
+    g = _fused_rows(core, b, b["logits"], dq, row, seed=11, step=0)
+    for x, y in zip(g[:4], o):
+        np.testing.assert_array_equal(x, y)
+    assert g[0].sum() > 0

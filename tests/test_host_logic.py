@@ -186,3 +186,23 @@ def test_sampling_kernels_have_no_fused_multiply_add():
     assert len(funcs) >= 6
     for f in funcs:
         assert "FFMA" not in f, f.split("\n")[0]
+
+
+def test_accept_compact_argument_validation(core):
+    """rs_tree_accept_compact rejects bad KV arguments before touching the device (CPU-only)."""
+    import ctypes
+    L = core._lib
+    P = ctypes.c_void_p
+
+    def call(B=3, L_=2, Hkv=8, d=128, ps=64, bt=P(16), pl=P(16), nl=P(16), kl=None, vl=None):
+        k = (P * 2)(16, 16) if kl is None else kl
+        v = (P * 2)(16, 16) if vl is None else vl
+        return L.rs_tree_accept_compact(core.GREEDY, P(16), core.DTYPE_BF16, None, core.DTYPE_F32, None, P(16), P(16),
+                                        P(16), P(16), B, 1000, 1.0, 0, 0, P(16), P(16), P(16), P(16), None, 0,
+                                        k, v, L_, Hkv, d, ps, bt, 4, pl, nl, None, None)
+    assert call(B=0) == 0                    # no samples: no-op
+    assert call(L_=257) == 1                 # more layers than one launch's parameter block holds
+    assert call(Hkv=0) == 1
+    assert call(d=12) == 8                   # head_dim % 8 != 0: RS_ERR_UNSUPPORTED
+    assert call(bt=None) == 1 and call(pl=None) == 1 and call(nl=None) == 1
+    assert call(kl=(P * 2)(16, None)) == 1   # a null layer pointer

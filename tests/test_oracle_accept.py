@@ -379,3 +379,59 @@ def test_mss_draft_row_must_be_probabilities():
         acc, path, bonus, flags = A.tree_accept(A.MSS, bf16_bits(l2), [-1, 0, 1], [0, 2, 3], [0, 3], [0], V,
                                                 draft_probs=qb)
         assert flags[0] == 0 and acc[0] == 1
+
+
+def test_mss_leaf_draft_row_is_not_read():
+    """Reading Z29 (children are drawn from q_c): the draft row of a node WITHOUT children
+    is not a distribution anything was drawn from, so a visited leaf's row is never read — a
+    NaN / out-of-range row there changes nothing, while the same row on a node with children
+    flags the sample (test_mss_draft_row_must_be_probabilities)."""
+    V = 8
+    l = np.zeros((2, V), np.float32)
+    l[0, 2] = 30.0                                     # child token 2 is (almost) certain at the root
+    l[1, 6] = 3.0                                      # the leaf's target row (bonus drawn from it)
+    q = softmax64(np.zeros((2, V))).astype(np.float32)
+    q[0, :] = 0.0
+    q[0, 2] = 1.0
+    ref = A.tree_accept(A.MSS, bf16_bits(l), [-1, 0], [0, 2], [0, 2], [5], V, draft_probs=q, seed=1, step=2)
+    assert ref[3][0] == 0 and ref[0][0] == 1 and list(ref[1][0, :2]) == [0, 1]
+    for bad in (1.5, -0.25, np.nan):
+        qb = q.copy()
+        qb[1, :] = bad                                 # the leaf's row: garbage
+        got = A.tree_accept(A.MSS, bf16_bits(l), [-1, 0], [0, 2], [0, 2], [5], V, draft_probs=qb, seed=1, step=2)
+        for x, y in zip(got, ref):
+            np.testing.assert_array_equal(x, y)
+
+
+def test_mss_draft_row_map():
+    """draft_row (row of node i's q, -1 = none) is a pure relayout: the rows of the nodes with
+    children packed into a smaller array give the results of the full [NT, V] array; a node with
+    children but no row makes its tree malformed (other samples unaffected)."""
+    V, n = 32, 40
+    rng = np.random.default_rng(13)
+    par = np.tile(np.array([-1, 0, 0, 1, 1, 2], np.int32), n)   # internal: 0, 1, 2; leaves: 3, 4, 5
+    q = rng.dirichlet(np.ones(V) * 0.3, size=6 * n).astype(np.float32)
+    tok = np.zeros(6 * n, np.int32)
+    for i in range(6 * n):
+        if par[i] >= 0:
+            pr = q[(i // 6) * 6 + par[i]].astype(np.float64)
+            tok[i] = rng.choice(V, p=pr / pr.sum())
+    lg = (np.log(q + 1e-12) + rng.standard_normal((6 * n, V))).astype(np.float32)
+    off = (np.arange(n + 1) * 6).astype(np.int32)
+    gid = np.arange(n) * 3 + 7
+    full = A.tree_accept(A.MSS, lg, par, tok, off, gid, V, draft_probs=q, seed=4, step=1)
+    internal = np.array([i for i in range(6 * n) if (i % 6) in (0, 1, 2)])
+    row = np.full(6 * n, -1, np.int32)
+    row[internal] = np.arange(len(internal))
+    qc = q[internal].copy()
+    packed = A.tree_accept(A.MSS, lg, par, tok, off, gid, V, draft_probs=qc, seed=4, step=1, draft_row=row)
+    for x, y in zip(packed, full):
+        np.testing.assert_array_equal(x, y)
+    assert full[0].sum() > 0 and (full[3] == 0).all()
+    row2 = row.copy()
+    row2[6 * 3 + 1] = -1                               # sample 3: node 1 has children but no row
+    bad = A.tree_accept(A.MSS, lg, par, tok, off, gid, V, draft_probs=qc, seed=4, step=1, draft_row=row2)
+    assert bad[3][3] == A.FLAG_MALFORMED and bad[0][3] == 0 and bad[2][3] == -1
+    keep = np.arange(n) != 3
+    for x, y in zip(bad, full):
+        np.testing.assert_array_equal(x[keep], y[keep])

@@ -1,0 +1,10 @@
+#!/bin/bash
+TAG=${1:-r2b_rows2}; OUT=gpurun_out/$TAG; mkdir -p $OUT
+timeout 900 python -m pytest tests/test_gpu_accept_compact.py tests/test_gpu_parity.py -m gpu -x -q --timeout 400 -k "fused or exp_spec or mss or accept or compact or delta or greedy" > $OUT/pytest.log 2>&1; echo "exit $?" >> $OUT/pytest.log
+tail -3 $OUT/pytest.log
+V=paper_2512_04752_b200/_variants
+for r in 1 2; do
+echo "cur $(timeout 200 python tools/mss_bench.py 30 2>>$OUT/err.log)" >> $OUT/mss.txt
+echo "pre $(RS_CORE_LIB=$V/pre/librlhfspec_core.so timeout 200 python tools/mss_bench.py 30 2>>$OUT/err.log)" >> $OUT/mss.txt
+done
+cut -c1-100 $OUT/mss.txt
