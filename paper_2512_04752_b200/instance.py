@@ -5,8 +5,8 @@ Per step:
     host: live samples -> page reservations for the tree slots, block tables, lengths, the
           tree tokens of this step, the attention schedule (rs_attn_plan_create)
     device: one H2D of the packed metadata, rs_tree_build_mask, rs_tree_verify_attention_layers
-          (L LLM layers), rs_tree_accept, rs_kv_compact (LLM layers + the SSM layer), one D2H
-          of (accepted_len, new_len)
+          (L LLM layers), rs_tree_accept_compact (acceptance + the commit of the LLM layers and the
+          SSM layer in one launch), one D2H of (accepted_len, new_len)
     host: lengths advance by a_b + 1; a sample whose response is complete leaves and its pages
           return to the pool (the long tail of P:95-101 shrinks the batch).
 Every `cooldown` steps the instances rebalance (realloc.Rebalancer: all-gathered loads,
@@ -97,6 +97,7 @@ class GenerationInstance:
         self.out = torch.empty((L, NTmax, Hq, d), dtype=torch.bfloat16, device=self.dev)
         self._ptrs = (core.ptr_array([self.q[l] for l in range(L)]), core.ptr_array(self.k_llm),
                       core.ptr_array(self.v_llm), core.ptr_array([self.out[l] for l in range(L)]))
+        self._kv_ptrs = (core._layer_ptrs(self.k_llm + self.k_ssm), core._layer_ptrs(self.v_llm + self.v_ssm))
         # packed per-step metadata: prefix_len [B] | tree_off [B+1] | parent [NT] | token [NT] |
         # block_table [B, max_pages]; one pinned host buffer, one H2D copy
         cap = self.max_batch * (2 + 2 * T + max_pages) + 1
@@ -228,11 +229,11 @@ class GenerationInstance:
                                               self.Hq, self.d, 1.0 / math.sqrt(self.d), oa, self.ws, stream=st)
             if timing:
                 self._ev[1].record(st)
-            core.tree_accept(core.GREEDY, self.logits[:NT], par, tok, to, self.gid_d[:B], seed=seed,
-                             step=self.step_no, out=(self.acc[:B], self.path[:B], self.bonus[:B], self.aflags[:B]),
-                             stream=st)
-            core.kv_compact(self.k_llm + self.k_ssm, self.v_llm + self.v_ssm, bt, pl, self.acc[:B], self.path[:B],
-                            PAGE, new_len=self.res_d[B:2 * B], stream=st)
+            # acceptance + the KV commit of the LLM and SSM layers in one launch
+            core.tree_accept_compact(core.GREEDY, self.logits[:NT], par, tok, to, self.gid_d[:B],
+                                     self.k_llm + self.k_ssm, self.v_llm + self.v_ssm, bt, pl, seed=seed,
+                                     step=self.step_no, out=(self.acc[:B], self.path[:B], self.bonus[:B], self.aflags[:B]),
+                                     new_len=self.res_d[B:2 * B], stream=st, layer_ptrs=self._kv_ptrs)
             self.res_d[:B].copy_(self.acc[:B])
             self.res_h[:2 * B].copy_(self.res_d[:2 * B], non_blocking=True)
         self._tok_next = self._tokens(self.max_batch)   # next step's tree tokens while the GPU works
