@@ -450,7 +450,8 @@ def main():
     ap.add_argument("--config", default="c3s",
                     help="default c3s = BASELINE configs[2] (the largest single-GPU config) as the method runs it")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=20,
+                    help="pipelined end-to-end steps (the first upload and the last step's kernels are not overlapped)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-n", type=int, default=None,
                     help="c3s: every tree = S(n) for this n under the prior F (profiling runs: the calibrated "
