@@ -406,6 +406,10 @@ rs_status rs_knee_threshold(const double* counts, const double* tput, int32_t n,
  * (arrays of capacity G). Every instance appears in at most one transfer. */
 rs_status rs_plan_reallocation(const int32_t* loads, int32_t G, int32_t threshold, int32_t* src,
                                int32_t* dst, int32_t* count, int32_t* n_transfers);
+/* The reallocation trigger: *trigger = 1 iff steps_since_last >= cooldown and some
+ * instance's load is below threshold while another's is above it (loads: host int32 [G]). */
+rs_status rs_realloc_should_trigger(const int32_t* loads, int32_t G, int32_t threshold, int32_t steps_since_last,
+                                    int32_t cooldown, int32_t* trigger);
 /* Samples to move: shortest sequence first, then lowest average accepted tokens, then gid. */
 rs_status rs_choose_samples(const int64_t* gid, const int32_t* seq_len, const double* avg_accepted,
                             int32_t n, int32_t k, int64_t* chosen);

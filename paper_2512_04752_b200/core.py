@@ -408,6 +408,7 @@ def cost_model_fit(n_seq, n_draft, t_sec, cost):
 _sig("rs_knee_threshold", _i32, _P, _P, _i32, _f64, ctypes.POINTER(_i32))
 _sig("rs_plan_reallocation", _i32, _P, _i32, _i32, _P, _P, _P, ctypes.POINTER(_i32))
 _sig("rs_choose_samples", _i32, _P, _P, _P, _i32, _i32, _P)
+_sig("rs_realloc_should_trigger", _i32, _P, _i32, _i32, _i32, _i32, ctypes.POINTER(_i32))
 
 
 _sig("rs_acceptance_fit", _i32, _P, _P, _i64, _i32, _P, _P, ctypes.POINTER(_i32))
@@ -441,6 +442,14 @@ def knee_threshold(counts, tput, frac=0.1) -> int:
     thr = _i32()
     _check(_lib.rs_knee_threshold(_ptr(c), _ptr(t), len(c), float(frac), ctypes.byref(thr)), "rs_knee_threshold")
     return thr.value
+
+
+def realloc_should_trigger(loads, threshold, steps_since_last, cooldown):
+    ld = _host_i32(loads)
+    t = _i32()
+    _check(_lib.rs_realloc_should_trigger(_ptr(ld), len(ld), int(threshold), int(steps_since_last), int(cooldown),
+                                          ctypes.byref(t)), "rs_realloc_should_trigger")
+    return bool(t.value)
 
 
 def plan_reallocation(loads, threshold):

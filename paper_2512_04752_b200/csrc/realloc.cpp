@@ -70,3 +70,19 @@ extern "C" rs_status rs_choose_samples(const int64_t* gid, const int32_t* seq_le
     for (int i = 0; i < k; ++i) chosen[i] = gid[idx[i]];
     return RS_OK;
 }
+
+// the decision is taken every `cooldown` steps and a reallocation is triggered only if the
+// inefficiency is present: some instance is below the threshold (it could take samples without
+// losing throughput) while another is above it (reading Z13).
+extern "C" rs_status rs_realloc_should_trigger(const int32_t* loads, int32_t G, int32_t thr, int32_t steps_since_last,
+                                               int32_t cooldown, int32_t* trigger) {
+    RS_REQUIRE(loads && trigger && G >= 0 && thr >= 0 && cooldown >= 0, RS_ERR_INVALID_ARG,
+               "rs_realloc_should_trigger: bad args");
+    bool below = false, above = false;
+    for (int i = 0; i < G; ++i) {
+        below = below || loads[i] < thr;
+        above = above || loads[i] > thr;
+    }
+    *trigger = (steps_since_last >= cooldown && below && above) ? 1 : 0;
+    return RS_OK;
+}

@@ -59,9 +59,8 @@ class Rebalancer:
         return [int(x.item()) for x in out]
 
     def should_trigger(self, loads) -> bool:
-        thr = self.threshold
-        return (self.steps_since >= self.cooldown and any(x < thr for x in loads)
-                and any(x > thr for x in loads))
+        """P:300 trigger (rs_realloc_should_trigger, host C++)."""
+        return core.realloc_should_trigger(loads, self.threshold, self.steps_since, self.cooldown)
 
     def plan(self, local_load: int, force: bool = False) -> list[Transfer]:
         """Collective: identical plan on every rank (empty when not triggered)."""

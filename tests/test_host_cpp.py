@@ -116,6 +116,21 @@ def test_plan_reallocation_and_choose_samples_match_oracle(core):
         assert core.choose_samples(gid, sl, aa, k) == ref
 
 
+def test_realloc_trigger_matches_oracle(core):
+    """rs_realloc_should_trigger equals oracle.realloc.should_trigger on fuzzed fleets,
+    including the cooldown boundary and fleets with nobody on one side of the threshold."""
+    from oracle import realloc as OR
+    rng = np.random.default_rng(17)
+    for _ in range(400):
+        G = int(rng.integers(1, 9))
+        loads = rng.integers(0, 40, size=G).tolist()
+        thr = int(rng.integers(0, 40))
+        since, cd = int(rng.integers(0, 70)), int(rng.integers(0, 64))
+        assert core.realloc_should_trigger(loads, thr, since, cd) == OR.should_trigger(loads, thr, since, cd)
+    assert core.realloc_should_trigger([24, 1], 6, 32, 32) and not core.realloc_should_trigger([24, 1], 6, 31, 32)
+    assert not core.realloc_should_trigger([6, 6], 6, 100, 32) and not core.realloc_should_trigger([], 6, 100, 32)
+
+
 def test_page_pool_all_or_nothing(core):
     pool = core.PagePool(10)
     a = pool.alloc(4)
