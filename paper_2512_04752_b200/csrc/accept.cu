@@ -56,6 +56,20 @@ constexpr int kGreedyInflight = RS_ACC_INFLIGHT;   // 16-byte loads in flight pe
 #define RS_ACC_PF 0         // greedy: L2 prefetch of the children's rows
 #endif
 
+#ifdef RS_ACC_TRACE
+// profiling variant only (-DRS_ACC_TRACE): globaltimer stamps of the greedy walk per sample
+// [0] kernel start, [1..5] start of rows 1..5, [6] walk end, [7] commit end
+__device__ unsigned long long g_acc_trace[4096][8];
+__device__ __forceinline__ unsigned long long acc_gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define ACC_TRACE(b, k) do { if (cluster_rank() == 0 && threadIdx.x == 0 && (b) < 4096) g_acc_trace[b][k] = acc_gtime(); } while (0)
+#else
+#define ACC_TRACE(b, k) do { } while (0)
+#endif
+
 struct RowView {
     const void* base;
     int64_t row;
@@ -416,6 +430,7 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype_rt, c
     const int T = tree_off[b + 1] - off;
     int32_t* pth = path_out + (int64_t)b * RS_MAX_TREE;
     int phase = 0;
+    ACC_TRACE(b, 0);
     if (leader && tid < RS_MAX_TREE) pth[tid] = -1;
     // tree check in parallel: node i needs parent[i] in [0, i) (root: -1) and, for a draft
     // node (i >= 1), a vocabulary token 0 <= token[i] < V (sampling modes index rows by it)
@@ -444,6 +459,7 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype_rt, c
     __syncthreads();
 
     for (;;) {
+        if (a >= 1 && a <= 5) ACC_TRACE(b, a);
         const RowView lv{logits, (int64_t)(off + c), V, dtype, logits_vec_ok};
         const RowView qv{draft, (int64_t)(off + c), V, RS_DTYPE_F32, draft_vec_ok};
         int next = -1;
@@ -799,7 +815,9 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype_rt, c
             bonus_out[b] = bonus;
         }
     }
+    ACC_TRACE(b, 6);
     if constexpr (CA::kOn) fused_commit(ca, b, a, sm);
+    ACC_TRACE(b, 7);
     // keep every CTA's shared memory alive until all remote reads of the cluster are done (DELTA's
     // 128-bit reductions and child tests read peers after their barriers; the greedy walk only
     // uses push exchanges, whose last barrier already orders every access)
@@ -1543,3 +1561,9 @@ extern "C" rs_status rs_exp_spec(const float* x, int64_t n, float* y, void* stre
     RS_LAUNCH_CHECK();
     return RS_OK;
 }
+
+#ifdef RS_ACC_TRACE
+extern "C" int rs_debug_acc_trace(unsigned long long* host, int n_samples) {
+    return (int)cudaMemcpyFromSymbol(host, g_acc_trace, sizeof(unsigned long long) * 8 * (size_t)n_samples);
+}
+#endif
