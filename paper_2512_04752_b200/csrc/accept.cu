@@ -1336,6 +1336,9 @@ static rs_status launch_mss(const CA& ca, bool bf, bool qbf, const void* logits,
     static size_t attr_smem[4] = {0, 0, 0, 0};
     int cs = 1;
     while (cs < 16 && nvec / (cs * 2) >= kMssThreads) cs *= 2;
+#ifdef RS_MSS_CS
+    cs = cs > RS_MSS_CS ? RS_MSS_CS : cs;   // (profiling variant: smaller clusters)
+#endif
     const size_t smem = mss_smem_bytes(nvec, cs, qbf);
     size_t& cur = attr_smem[(bf ? 0 : 1) + (qbf ? 2 : 0)];
     if (cur < smem) {
