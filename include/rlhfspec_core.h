@@ -84,6 +84,13 @@ rs_status rs_tree_build_mask(const int32_t* parent, const int32_t* tree_off, int
  *   max_logit    device fp32 [rows] out (the fp32 maximum), or NULL
  *   ws, ws_bytes device workspace >= rs_lm_head_argmax_workspace_bytes(rows), 8-byte aligned
  * Launches a memset, the GEMM kernel and a finalize kernel on `stream`. */
+/* rs_lm_head_logits — the same GEMM for the sampling modes (SAMPLE_DELTA / SAMPLE_MSS need
+ * whole rows): logits[r, v] = bf16_RN( sum_k hidden[r,k] * weight[v,k] ), fp32 accumulation on the
+ * tensor cores, the bf16 tile written by the epilogue (the input of rs_tree_accept_compact).
+ *   hidden, weight as above; logits device bf16 [rows, V] out, 16-byte aligned; V % 8 == 0.
+ * Errors: Dm not a positive multiple of 64, V % 8 != 0 or misaligned pointers -> RS_ERR_INVALID_ARG. */
+rs_status rs_lm_head_logits(const void* hidden, const void* weight, int32_t rows, int32_t V, int32_t Dm,
+                            void* logits, void* stream);
 size_t rs_lm_head_argmax_workspace_bytes(int32_t rows);
 rs_status rs_lm_head_argmax(const void* hidden, const void* weight, int32_t rows, int32_t V, int32_t Dm,
                             int32_t* argmax_token, float* max_logit, void* ws, size_t ws_bytes,

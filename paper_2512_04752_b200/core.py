@@ -617,6 +617,20 @@ def lm_head_argmax_workspace_bytes(rows) -> int:
     return int(_lib.rs_lm_head_argmax_workspace_bytes(int(rows)))
 
 
+_sig("rs_lm_head_logits", _i32, _P, _P, _i32, _i32, _i32, _P, _P)
+
+
+def lm_head_logits(hidden, weight, out=None, stream=None):
+    """bf16 logits [rows, V] of the LM head (f2 for the sampling modes): rs_lm_head_logits."""
+    rows, Dm = hidden.shape
+    V = weight.shape[0]
+    if out is None:
+        out = torch.empty((rows, V), dtype=torch.bfloat16, device=hidden.device)
+    _check(_lib.rs_lm_head_logits(_ptr(hidden), _ptr(weight), rows, V, Dm, _ptr(out), _stream(stream)),
+           "rs_lm_head_logits")
+    return out
+
+
 def lm_head_argmax(hidden, weight, out=None, max_logit=True, ws=None, stream=None):
     """Per-row arg-max of hidden @ weight^T (bf16 in, fp32 accumulate), computed in the GEMM
     epilogue; returns (argmax_token int32 [rows], max_logit fp32 [rows] or None)."""

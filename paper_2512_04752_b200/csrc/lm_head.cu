@@ -52,9 +52,13 @@ __device__ __forceinline__ unsigned long long argmax_key(float x, int v) {
     return ((unsigned long long)b << 32) | (unsigned long long)(~(uint32_t)v);
 }
 
+// kLogits: the epilogue writes the bf16 logits tile instead (the LM head feeding the sampling
+// modes, which need whole rows: rs_lm_head_logits).
+template <bool kLogits>
 __global__ void __launch_bounds__(kThreads, 1)
 lm_head_argmax_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW,
-                      int rows, int V, int Dm, unsigned long long* __restrict__ keys) {
+                      int rows, int V, int Dm, unsigned long long* __restrict__ keys,
+                      __nv_bfloat16* __restrict__ logits) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     Bars* bars = reinterpret_cast<Bars*>(smem + kStages * kStageBytes);
@@ -137,6 +141,43 @@ lm_head_argmax_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_cons
             const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + a * kBN;
             const int v0 = n * kBN;
             const bool full_tile = v0 + kBN <= V;
+            if constexpr (kLogits) {
+                // one accumulator row per thread: 64 columns per round out of TMEM, rounded to
+                // bf16 (RN) and stored as 8 x 16-byte vectors (V % 8 == 0: rows stay aligned)
+                const int row = m * kBM + q * 32 + lane;
+                __nv_bfloat16* dst = logits + (size_t)row * V + v0;
+#pragma unroll 1
+                for (int c = 0; c < kBN; c += 64) {
+                    uint32_t r0[32], r1[32];
+                    tmem_ld32(base + c, r0);
+                    tmem_ld32(base + c + 32, r1);
+                    tmem_wait_ld();
+                    if (row < rows) {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const uint32_t* rr = h ? r1 : r0;
+#pragma unroll
+                            for (int j8 = 0; j8 < 32; j8 += 8) {
+                                const int v = c + 32 * h + j8;
+                                if (full_tile || v0 + v + 8 <= V) {
+                                    uint32_t pk[4];
+#pragma unroll
+                                    for (int e = 0; e < 4; ++e) {
+                                        const __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(rr[j8 + 2 * e]),
+                                                                                        __uint_as_float(rr[j8 + 2 * e + 1]));
+                                        pk[e] = *reinterpret_cast<const uint32_t*>(&b2);
+                                    }
+                                    *reinterpret_cast<uint4*>(dst + v) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                                }
+                            }
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->acc_empty[a]);
+                continue;
+            }
             float best = -INFINITY;
             int bi = -1;
             uint32_t amag = 0;   // max |x| bits of the row's valid columns: >= 0x7F800000 <=> Inf / NaN
@@ -322,13 +363,13 @@ extern "C" rs_status rs_lm_head_argmax(const void* hidden, const void* weight, i
     RS_CUDA_CHECK(cudaMemsetAsync(keys, 0, need, st));
     static bool attr = false;
     if (!attr) {
-        RS_CUDA_CHECK(cudaFuncSetAttribute(lm_head_argmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        RS_CUDA_CHECK(cudaFuncSetAttribute(lm_head_argmax_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            kSmemBytes));
         attr = true;
     }
     const int ntiles = ((rows + kBM - 1) / kBM) * ((V + kBN - 1) / kBN);
     const int grid = std::min(ntiles, num_sms());
-    lm_head_argmax_kernel<<<grid, kThreads, kSmemBytes, st>>>(tmH, tmW, rows, V, Dm, keys);
+    lm_head_argmax_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(tmH, tmW, rows, V, Dm, keys, nullptr);
     RS_LAUNCH_CHECK();
     lm_head_finalize_kernel<<<(rows + 255) / 256, 256, 0, st>>>(keys, rows, argmax_token, max_logit);
     RS_LAUNCH_CHECK();
@@ -347,6 +388,49 @@ extern "C" rs_status rs_tree_accept_greedy_tokens(const int32_t* argmax_token, c
     const int wpb = 4;
     greedy_walk_kernel<<<(B + wpb - 1) / wpb, 32 * wpb, 0, rs::as_stream(stream)>>>(
         argmax_token, parent, token, tree_off, B, accepted_len, path, bonus_token, status_flags);
+    RS_LAUNCH_CHECK();
+    return RS_OK;
+}
+
+extern "C" rs_status rs_lm_head_logits(const void* hidden, const void* weight, int32_t rows, int32_t V, int32_t Dm,
+                                       void* logits, void* stream) {
+    rs::bind_device(hidden);
+    RS_REQUIRE(rows >= 0 && V >= 8 && V % 8 == 0 && Dm >= kBK && Dm % kBK == 0, RS_ERR_INVALID_ARG,
+               "rs_lm_head_logits: rows=%d V=%d Dm=%d (V a multiple of 8, Dm a positive multiple of 64)", rows, V,
+               Dm);
+    if (rows == 0) return RS_OK;
+    RS_REQUIRE(hidden && weight && logits, RS_ERR_INVALID_ARG, "rs_lm_head_logits: null pointer");
+    RS_REQUIRE((reinterpret_cast<uintptr_t>(hidden) & 15) == 0 && (reinterpret_cast<uintptr_t>(weight) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(logits) & 15) == 0,
+               RS_ERR_INVALID_ARG, "rs_lm_head_logits: hidden/weight/logits must be 16-byte aligned");
+    PFN_encodeTiled enc = encode_fn();
+    RS_REQUIRE(enc, RS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    CUtensorMap tmH, tmW;
+    const void* src[2] = {hidden, weight};
+    CUtensorMap* tm[2] = {&tmH, &tmW};
+    const cuuint64_t nrow[2] = {(cuuint64_t)rows, (cuuint64_t)V};
+    const cuuint32_t brow[2] = {kBM, kBN};
+    for (int i = 0; i < 2; ++i) {
+        cuuint64_t dims[2] = {(cuuint64_t)Dm, nrow[i]};
+        cuuint64_t strides[1] = {(cuuint64_t)Dm * 2};
+        cuuint32_t box[2] = {kBK, brow[i]};
+        cuuint32_t es[2] = {1, 1};
+        CUresult r = enc(tm[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(src[i]), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        RS_REQUIRE(r == CUDA_SUCCESS, RS_ERR_CUDA, "rs_lm_head_logits: tensor map %d failed (%d)", i, (int)r);
+    }
+    cudaStream_t st = rs::as_stream(stream);
+    static bool attr = false;
+    if (!attr) {
+        RS_CUDA_CHECK(cudaFuncSetAttribute(lm_head_argmax_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kSmemBytes));
+        attr = true;
+    }
+    const int ntiles = ((rows + kBM - 1) / kBM) * ((V + kBN - 1) / kBN);
+    const int grid = std::min(ntiles, num_sms());
+    lm_head_argmax_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(tmH, tmW, rows, V, Dm, nullptr,
+                                                                    static_cast<__nv_bfloat16*>(logits));
     RS_LAUNCH_CHECK();
     return RS_OK;
 }

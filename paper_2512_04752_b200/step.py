@@ -5,8 +5,9 @@
 (rs_tree_accept_compact = rs_tree_accept + rs_kv_compact in one launch; `fused_commit=False`
 issues the two calls separately.)
 
-With `lm_head=(hidden, weight)` (f2, greedy only) acceptance starts from the nodes' final hidden
-states instead of materialised logits: rs_lm_head_argmax -> rs_tree_accept_greedy_tokens.
+With `lm_head=(hidden, weight)` (f2) acceptance starts from the nodes' final hidden states:
+greedy: rs_lm_head_argmax -> rs_tree_accept_greedy_tokens (the logits are never written);
+sampling: rs_lm_head_logits (the bf16 logits from the GEMM epilogue) -> rs_tree_accept_compact.
 
 Pure orchestration: buffers are torch tensors, every computation is a library call; arguments
 are marshalled once so a step costs four ctypes calls. The device part can be captured into a
@@ -48,12 +49,12 @@ class VerifyStep:
         self.v_layers = [b["v_cache"][i] for i in self.layer_buf]
         self.logits = b.get("logits")
         self.hidden, self.lm_w = lm_head if lm_head is not None else (None, None)
-        if self.hidden is not None:
-            assert mode == core.GREEDY, "the fused LM head feeds greedy acceptance only"
         self.draft = b.get("draft_probs") if mode == core.SAMPLE_MSS else None
         # acceptance and the KV commit in one launch (not for the f2 token path, nor for more
         # layers than one launch's parameter block holds)
-        self.fused_commit = bool(fused_commit) and self.hidden is None and self.L <= core.COMPACT_MAX_LAYERS
+        self.lm_sampling = self.hidden is not None and mode != core.GREEDY
+        self.fused_commit = (bool(fused_commit) and (self.hidden is None or self.lm_sampling)
+                             and self.L <= core.COMPACT_MAX_LAYERS)
         self.layer_ptrs = (core._layer_ptrs(self.k_layers), core._layer_ptrs(self.v_layers))
         # MSS: optional row map (draft rows only for nodes with children, Z29)
         self.draft_row = b.get("draft_row") if mode == core.SAMPLE_MSS else None
@@ -80,7 +81,9 @@ class VerifyStep:
         self.flags = torch.empty(self.B, dtype=torch.int32, device=dev)
         self.new_len = torch.empty(self.B, dtype=torch.int32, device=dev)
         nws = core.accept_workspace_bytes(mode, self.B, b["V"]) if self.hidden is None else 0
-        if self.hidden is not None:
+        if self.lm_sampling:   # the LM head's logits (written by its epilogue every step)
+            self.logits = torch.empty((NT, self.lm_w.shape[0]), dtype=torch.bfloat16, device=dev)
+        elif self.hidden is not None:
             self.amax = torch.empty(NT, dtype=torch.int32, device=dev)
             self.lm_ws = torch.empty(max(core.lm_head_argmax_workspace_bytes(NT), 8), dtype=torch.uint8, device=dev)
         self.accept_ws = torch.empty(max(nws, 16), dtype=torch.uint8, device=dev)   # MSS residual weights
@@ -96,8 +99,13 @@ class VerifyStep:
     def attention_step(self, stream=None):
         self.attn_call(stream)
 
+    def lm_head_step(self, stream=None):
+        if self.lm_sampling:
+            core.lm_head_logits(self.hidden, self.lm_w, out=self.logits, stream=stream)
+
     def accept_step(self, seed, step, stream=None):
-        if self.hidden is not None:
+        self.lm_head_step(stream)
+        if self.hidden is not None and not self.lm_sampling:
             core.lm_head_argmax(self.hidden, self.lm_w, out=(self.amax, None), ws=self.lm_ws, stream=stream)
             core.tree_accept_greedy_tokens(self.amax, self.parent, self.token, self.tree_off,
                                            out=(self.acc, self.path, self.bonus, self.flags), stream=stream)
@@ -112,6 +120,7 @@ class VerifyStep:
 
     def accept_compact_step(self, seed, step, stream=None):
         if self.fused_commit:
+            self.lm_head_step(stream)
             core.tree_accept_compact(self.mode, self.logits, self.parent, self.token, self.tree_off, self.gid,
                                      self.k_layers, self.v_layers, self.block_table, self.prefix_len,
                                      draft_probs=self.draft, temperature=self.temperature, seed=seed, step=step,

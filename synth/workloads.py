@@ -25,7 +25,7 @@ import torch
 __all__ = [
     "VerifyConfig", "CONFIGS", "TINY_PARENT", "random_tree_parents", "draw_prefix_lengths",
     "make_verify_batch", "make_candidate_tree", "lmsys_response_lengths", "planted_targets",
-    "make_lm_head_inputs",
+    "make_lm_head_inputs", "make_lm_head_sampling_inputs",
 ]
 
 # Tiny config tree: paths [0,1,3,6], [0,1,4,7], [0,2,5].
@@ -337,3 +337,52 @@ def make_lm_head_inputs(batch: dict, Dm: int, seed: int = 7, device="cpu", gen_d
     t = torch.from_numpy(tgt).to(w.device)
     h = plant * w[t].float() + noise * torch.randn((NT, Dm), generator=gen, device=gen_device).to(w.device)
     return dict(hidden=h.to(torch.bfloat16), weight=w, planted=tgt, Dm=Dm)
+
+
+def make_lm_head_sampling_inputs(batch: dict, Dm: int, seed: int = 7, device="cpu", gen_device: Optional[str] = None,
+                                 hidden_sd: float = 0.05, draft_noise: float = 1.0,
+                                 draft_dtype: Optional[str] = None) -> dict:
+    """f2 for the sampling modes: final hidden states [NT, Dm] ~ N(0, hidden_sd) and an LM-head
+    weight [V, Dm] ~ N(0, 1) (bf16), so the target logits H W^T have sd ~ hidden_sd * sqrt(Dm)
+    (3.2 at Dm = 4096, the spread of the default recipe's log q + N(0, 1)); the draft
+    distribution of node c is q_c = softmax(target logits of c + draft_noise * N(0, 1)) (the
+    reverse of the default recipe: the draft is a noisy target) and the children of c are drawn
+    i.i.d. from q_c. Returns hidden, weight, draft_probs [NT, V] and the node tokens (root tokens
+    kept). The target logits here are the generator's own fp32 GEMM, an input property only."""
+    cfg = batch["cfg"]
+    gen_device = gen_device or device
+    gen = torch.Generator(device=gen_device)
+    gen.manual_seed(seed + 991)
+    V, NT = batch["V"], batch["NT"]
+    w = torch.empty((V, Dm), dtype=torch.bfloat16, device=device)
+    step = 8192
+    for v0 in range(0, V, step):
+        v1 = min(V, v0 + step)
+        w[v0:v1].copy_(torch.randn((v1 - v0, Dm), generator=gen, device=gen_device).to(torch.bfloat16))
+    h = (hidden_sd * torch.randn((NT, Dm), generator=gen, device=gen_device)).to(torch.bfloat16).to(device)
+    ddt = draft_dtype or cfg.draft_dtype
+    q = torch.empty((NT, V), dtype=torch.bfloat16 if ddt == "bf16" else torch.float32, device=device)
+    tok = np.array(batch["token"], dtype=np.int32, copy=True)
+    par, off = np.asarray(batch["parent"]), np.asarray(batch["tree_off"])
+    rows_per = 256
+    wf = w.float()
+    for r0 in range(0, NT, rows_per):   # bounded fp32 temporaries
+        r1 = min(NT, r0 + rows_per)
+        lg = h[r0:r1].float() @ wf.T
+        z = lg + draft_noise * torch.randn(lg.shape, generator=gen, device=gen_device).to(lg.device)
+        q[r0:r1].copy_(torch.softmax(z, dim=-1).to(q.dtype))
+    # children of c drawn i.i.d. from q_c (as the drafted tokens are), one multinomial per parent row
+    kids_of = {}
+    for s_ in range(batch["B"]):
+        o = int(off[s_])
+        for i in range(1, int(off[s_ + 1]) - o):
+            kids_of.setdefault(o + int(par[o + i]), []).append(o + i)
+    if kids_of:
+        prow = torch.as_tensor(sorted(kids_of), device=q.device)
+        pq = q.index_select(0, prow).float()
+        nk = max(len(v) for v in kids_of.values())
+        draws = torch.multinomial(pq.to(gen_device), nk, replacement=True, generator=gen).cpu().numpy()
+        for j, c in enumerate(sorted(kids_of)):
+            for k, x in enumerate(kids_of[c]):
+                tok[x] = int(draws[j, k])
+    return dict(hidden=h, weight=w, draft_probs=q, token=tok, Dm=Dm)

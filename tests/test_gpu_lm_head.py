@@ -233,3 +233,75 @@ def test_lm_head_argmax_all_negative_ragged_tail(cuda_lib):
     assert np.all(t == 997)
     assert np.all(mx.cpu().numpy() < 0)
     _check_rows(t, mx.cpu().numpy(), Hd.double().cpu().numpy(), Wd, min_exact=1.0)
+
+
+# ------------------------------------------------------------------ f2 for the sampling modes
+def _check_logits(lg_gpu, H, W, rows):
+    """bf16 logits of `rows` vs the fp64 definition: |gpu - ref| <= tol_r + 2^-8 (|ref| + tol_r)
+    (fp32 accumulation bound tol_r as above, then one bf16 round-to-nearest: 2^-8 relative)."""
+    ref, tol = _reference(H[rows], W)
+    g = lg_gpu[rows].float().cpu().numpy().astype(np.float64)
+    bound = tol[:, None] + 2.0 ** -8 * (np.abs(ref) + tol[:, None])
+    assert np.all(np.abs(g - ref) <= bound), float(np.max(np.abs(g - ref) - bound))
+
+
+@pytest.mark.parametrize("rows,V,Dm", [(200, 1000, 256), (5, 104, 64), (128, 256, 128), (129, 264, 192),
+                                       (300, 4104, 512)])
+def test_lm_head_logits_random(cuda_lib, rows, V, Dm):
+    rng = np.random.default_rng(rows * 11 + V)
+    H = _dev_bf16(rng.standard_normal((rows, Dm)))
+    W = _dev_bf16(rng.standard_normal((V, Dm)))
+    lg = cuda_lib.lm_head_logits(H, W)
+    torch.cuda.synchronize()
+    _check_logits(lg, H.double().cpu().numpy(), W, np.arange(rows))
+
+
+def test_lm_head_logits_full_size_sampled(cuda_lib):
+    """c3s-sized LM head (2304 nodes x 128256 x 4096) through the epilogue-writing GEMM; 48
+    sampled rows (every row tile, first / last) checked element by element."""
+    rng = np.random.default_rng(3)
+    rows, V, Dm = 2304, 128256, 4096
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(5)
+    H = (0.05 * torch.randn((rows, Dm), generator=gen, device="cuda")).to(torch.bfloat16)
+    W = torch.randn((V, Dm), generator=gen, device="cuda").to(torch.bfloat16)
+    lg = cuda_lib.lm_head_logits(H, W)
+    torch.cuda.synchronize()
+    sel = np.unique(np.concatenate([[0, rows - 1], np.arange(0, rows, 128), rng.integers(0, rows, 30)]))
+    _check_logits(lg, H.double().cpu().numpy(), W, sel)
+
+
+def test_verify_step_mss_with_lm_head(cuda_lib):
+    """The sampling f2 step (rs_lm_head_logits -> rs_tree_accept_compact, MSS with the draft-row
+    map): the GEMM's logits are within the bound of the definition, and the acceptance on them is
+    the oracle's, bit for bit, on the same (downloaded) logits."""
+    core = cuda_lib
+    from oracle import accept as OAcc
+    from paper_2512_04752_b200.step import VerifyStep
+    from synth import VerifyConfig, make_lm_head_sampling_inputs, make_verify_batch
+    from tests.helpers import tensor_bf16_bits
+    cfg = VerifyConfig("lmss", B=24, Hq=8, Hkv=2, d=128, V=4104, L=2, prefix=("lognormal", 100, 0.8, 1, 300),
+                       tree=("range", 2, 40), mode="mss", draft_dtype="bf16", seed=31)
+    b = make_verify_batch(cfg, device="cuda", gen_device="cuda", with_logits=False)
+    li = make_lm_head_sampling_inputs(b, Dm=256, device="cuda", gen_device="cuda", hidden_sd=0.2)
+    b["token"] = li["token"]
+    par, off = np.asarray(b["parent"]), np.asarray(b["tree_off"])
+    has = np.zeros(len(par), bool)
+    for s in range(b["B"]):
+        has[par[off[s] + 1:off[s + 1]] + off[s]] = True
+    idx = np.nonzero(has)[0]
+    row = np.full(len(par), -1, np.int32)
+    row[idx] = np.arange(len(idx))
+    dq = li["draft_probs"][torch.as_tensor(idx, device="cuda")].contiguous()
+    b["draft_probs"], b["draft_row"] = dq, row
+    st = VerifyStep(b, mode=core.SAMPLE_MSS, lm_head=(li["hidden"], li["weight"]))
+    res = st.run(seed=9, step=4)
+    torch.cuda.synchronize()
+    _check_logits(st.logits, li["hidden"].double().cpu().numpy(), li["weight"], np.arange(b["NT"]))
+    o = OAcc.tree_accept(OAcc.MSS, tensor_bf16_bits(st.logits.cpu()), b["parent"], b["token"], off, b["gid"],
+                         b["V"], draft_probs=dq.float().cpu().numpy(), seed=9, step=4, draft_row=row)
+    np.testing.assert_array_equal(res["accepted_len"], o[0])
+    np.testing.assert_array_equal(res["path"], o[1])
+    np.testing.assert_array_equal(res["bonus"], o[2])
+    np.testing.assert_array_equal(res["flags"], o[3])
+    assert res["accepted_len"].sum() > 0
