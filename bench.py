@@ -456,6 +456,8 @@ def main():
     ap.add_argument("--force-n", type=int, default=None,
                     help="c3s: every tree = S(n) for this n under the prior F (profiling runs: the calibrated "
                          "shapes without the calibration launches)")
+    ap.add_argument("--no-lm-variant", action="store_true",
+                    help="sampling configs: skip the f2 variant (the LM head in the step) reported beside the line")
     ap.add_argument("--no-calibrate", action="store_true",
                     help="c3s: keep the prior F / t_sd instead of profiling + rs_calibrate at startup")
     ap.add_argument("--realloc", default="on", choices=["on", "off"], help="c4: sample reallocation")
@@ -699,6 +701,9 @@ def run_ours(args, world, rank, local):
 
     # ---------------- end-to-end through the public API with host buffers ----------------
     e2e = run_e2e(step, b, args.e2e_steps, tokens_per_step, world, dev, barrier, mode, cfg.temperature)
+    lm_variant = None
+    if mode == core.SAMPLE_MSS and lm is None and not args.no_lm_variant:
+        lm_variant = run_lm_sampling_variant(args, cfg, b, dev, barrier, world, stream)
 
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -728,6 +733,8 @@ def run_ours(args, world, rank, local):
         "roofline": roof,
         "kernels": kernels,
     }
+    if lm_variant is not None:
+        line["lm_head_variant"] = lm_variant
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = run_cpu_baseline(cfg, b, parents=None if strat is None else strat.parents)
     if rank == 0:
@@ -928,6 +935,77 @@ def run_c4(args, world, rank, local):
         comm.destroy()
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def run_lm_sampling_variant(args, cfg, b, dev, barrier, world, stream, Dm=4096):
+    """f2 for the sampling configs, reported beside the line (the
+    hidden-state path is the realistic end-to-end): the same batch (trees, prefixes, KV, Q) with
+    the LM head in the step — rs_lm_head_logits (tcgen05 GEMM, bf16 logits from its epilogue)
+    then rs_tree_accept_compact — on synthetic final hidden states whose draft rows are noisy
+    targets (synth.make_lm_head_sampling_inputs); end to end it uploads hidden states instead
+    of logits. Device-timed like the main line (events between graph parts), then e2e."""
+    from paper_2512_04752_b200 import core
+    from paper_2512_04752_b200.step import VerifyStep
+    from synth import make_lm_head_sampling_inputs
+    li = make_lm_head_sampling_inputs(b, Dm=Dm, seed=17, device=dev, gen_device=dev)
+    bl = dict(b)
+    bl["token"] = li["token"]
+    bl["draft_probs"] = li["draft_probs"]
+    bl.pop("logits", None)
+    bl["draft_probs"], bl["draft_row"], _ = _pack_draft_rows(bl, dev)
+    del li["draft_probs"]
+    st = VerifyStep(bl, mode=core.SAMPLE_MSS, temperature=cfg.temperature, lm_head=(li["hidden"], li["weight"]))
+    K = min(args.steps, 20)
+    for w in range(args.warmup):
+        st.device_step(seed=7, step=w)
+    barrier()
+    res = st.results()
+    tps = int(np.sum(res["accepted_len"]) + b["B"])
+    g_mask, g_attn, g_acc, _ = st.capture_parts(seed=11, step=0)
+    g_lm = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_lm):
+        st.lm_head_step(torch.cuda.current_stream())
+    for w in range(args.warmup):
+        g_mask.replay(); g_attn.replay(); g_acc.replay()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    s0.record(stream)
+    for k in range(K):
+        g_mask.replay()
+        ev[k][0].record(stream)
+        g_attn.replay()
+        ev[k][1].record(stream)
+        g_acc.replay()
+        ev[k][2].record(stream)
+    s1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = s0.elapsed_time(s1)
+    if world > 1:
+        ms = _allreduce(ms, "max")
+    acc_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / K
+    # the LM head alone (its share of the accept part), 10 replays
+    l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g_lm.replay()
+    l0.record(stream)
+    for _ in range(10):
+        g_lm.replay()
+    l1.record(stream)
+    torch.cuda.synchronize()
+    lm_ms = l0.elapsed_time(l1) / 10
+    flops = 2.0 * int(b["NT"]) * int(b["V"]) * Dm
+    _, tc_burst, _, _ = _peaks()
+    e2e = run_e2e(st, bl, args.e2e_steps, tps, world, dev, barrier, core.SAMPLE_MSS, cfg.temperature)
+    return {"workload": "the line's batch with the LM head in the step (f2): final hidden states [NT, %d] -> "
+                        "rs_lm_head_logits -> MSS acceptance + commit; draft = noisy target (synthetic)" % Dm,
+            "value": round(tps * world * K / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms / K, 4),
+            "steps": K, "tokens_per_step": tps,
+            "accept_part_ms": round(acc_ms, 4),
+            "lm_head": {"ms_alone": round(lm_ms, 4), "flops": flops, "TFLOPs": round(flops / (lm_ms * 1e-3) / 1e12, 1),
+                        "frac_burst_bf16": round(flops / (lm_ms * 1e-3) / 1e12 / tc_burst, 4),
+                        "logits_bytes_written": int(b["NT"]) * int(b["V"]) * 2},
+            "e2e": e2e}
 
 
 def run_e2e(step, b, n_steps, tokens_per_step, world, dev, barrier, mode, temperature):
