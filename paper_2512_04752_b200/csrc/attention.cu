@@ -485,13 +485,13 @@ static rs_status launch_attn(const rs_attn_plan* pl, const void* q, const void* 
     const int rm = pl->rmodes == 1 ? 1 : (pl->rmodes == 2 ? 2 : (pl->rmodes == 4 ? 4 : 3));
     auto kern = rm == 1 ? tree_attn_kernel<D, 1>
                         : (rm == 2 ? tree_attn_kernel<D, 2> : (rm == 4 ? tree_attn_kernel<D, 4> : tree_attn_kernel<D, 3>));
-    const int smem_bytes = rm == 1 ? Cfg<D, 1>::kSmemBytes : Cfg<D, 2>::kSmemBytes;
+    const int smem_bytes = rm == 1 ? Cfg<D, 1>::kSmemBytes : (rm == 4 ? Cfg<D, 4>::kSmemBytes : Cfg<D, 2>::kSmemBytes);
     static bool attr_set[2][5] = {};
     if (!attr_set[D == 128][rm]) {
         RS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
         attr_set[D == 128][rm] = true;
     }
-    const int threads = rm == 1 ? KT<1>::kThreads : KT<2>::kThreads;
+    const int threads = rm == 1 ? KT<1>::kThreads : (rm == 4 ? KT<4>::kThreads : KT<2>::kThreads);
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3((unsigned)pl->n_ctas);
     lc.blockDim = dim3((unsigned)threads);

@@ -75,7 +75,18 @@ constexpr int kThreads = 384;    // 12 warps (RM 2/3)
 // RM = 1 (every tile R = 16): 16 warps; warps 12-15 are an epilogue warpgroup, and consecutive
 // items alternate between the two 16-lane halves of each TMEM sub-partition, so item i's O is
 // normalised and stored while item i+1 already accumulates.
-template <int RM> struct KT { static constexpr bool kEW = (RM == 1); static constexpr int kThreads = kEW ? 512 : 384; };
+#ifndef RS_ATTN_DU_SPLIT
+#define RS_ATTN_DU_SPLIT 0
+#endif
+// RM = 4 ("dual"): two warps per query row, each owning half of the 64 keys of a block (and half
+// of the O columns in the epilogue): 8 softmax warps per tile, 20 warps in all
+constexpr bool kDuSplit = RS_ATTN_DU_SPLIT != 0;
+template <int RM> struct KT {
+    static constexpr bool kEW = (RM == 1);
+    static constexpr bool kCS = (RM == 4) && kDuSplit;
+    static constexpr int kThreads = kEW ? 512 : (kCS ? 640 : 384);
+    static constexpr int kSmWarps = kCS ? 8 : 4;   // softmax warps per warpgroup (tile)
+};
 // RM = 1: an item's 64 rows are half the TMEM lanes (16 per sub-partition), so its S and PV MMAs
 // are issued with M = 64 at the item's lane half (tcgen05 M = 64 layout: A row m <-> lane
 // (m % 16) + 32 (m / 16), + 16 for the odd half) instead of M = 128 over both items' halves: half
@@ -130,7 +141,12 @@ struct Cfg {
     static constexpr int kOffV = kOffK + KS * kKVBytes;
     static constexpr int kOffStage = kOffV + VS * kKVBytes;   // epilogue staging [2][128 rows][128 B]
     static constexpr int kOffBar = kOffStage + (kStageOut ? 2 * kM * 128 : 0);
-    static constexpr int kSmemBytes = kOffBar + 512 + 1024;  // + barriers + alignment slack
+    // column-split dual softmax: per (tile, slot, key half, row) a partial row max (two slots, by
+    // the warpgroup's block parity), and per (tile, half, row) the partial row sum at the end
+    static constexpr int kBarBytes = 1024;                    // the mbarrier block (struct Bars)
+    static constexpr int kOffXch = kOffBar + kBarBytes;
+    static constexpr int kXchBytes = KT<RM>::kCS ? (2 * 2 * 2 * kM + 2 * 2 * kM) * 4 : 0;
+    static constexpr int kSmemBytes = kOffXch + kXchBytes + 1024;  // + exchange + alignment slack
     // TMEM columns: O0 [0,D) O1 [D,2D) | S0 S1 (64 fp32 each) | P0 P1 (32 bf16x2 each) | m,l x2
     static constexpr int kTmemCols = 512;
     static constexpr int kColS = 2 * D;
@@ -278,6 +294,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     Bars* bars = reinterpret_cast<Bars*>(smem + C::kOffBar);
+    static_assert(sizeof(Bars) <= C::kBarBytes, "barrier block overlaps the exchange region");
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int item_begin = p.cta_off[blockIdx.x];
@@ -325,11 +342,11 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         for (int i = 0; i < C::VS; ++i) { mbar_init(&bars->v_full[i], 1); mbar_init(&bars->v_empty[i], 1); }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bars->s_full[i], 1);
-            mbar_init(&bars->s_free[i], 4);
-            mbar_init(&bars->p_full[i], 4);
+            mbar_init(&bars->s_free[i], KT<RM>::kSmWarps);
+            mbar_init(&bars->p_full[i], KT<RM>::kSmWarps);
             mbar_init(&bars->pv_done[i], 1);
         }
-        mbar_init(&bars->o_free, 8);
+        mbar_init(&bars->o_free, 2 * KT<RM>::kSmWarps);
         for (int i = 0; i < kRing; ++i) {
             mbar_init(&bars->item_full[i], 1);
             mbar_init(&bars->item_empty[i], KT<RM>::kThreads / 32 - 1);   // every warp but warp 0
@@ -992,12 +1009,15 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         }
     } else if (warp >= 4) {
         // ============================ softmax + epilogue ============================
-        const int grp = (warp - 4) >> 2;         // warpgroup: handles blocks with (J & 1) == grp
+        constexpr bool CS = KT<RM>::kCS;
+        const int grp = CS ? (warp - 4) >> 3 : (warp - 4) >> 2;   // warpgroup: handles blocks with (J & 1) == grp
+        const int hh = CS ? ((warp - 4) >> 2) & 1 : 0;             // CS: key / O-column half of this warp
         const int wq = warp & 3;                 // TMEM sub-partition of this warp
         const int r = wq * 32 + lane;            // UMMA row / TMEM lane of this thread
         const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
         const uint32_t o_mine = tmem + lane_base + grp * D;
         uint32_t J = 0;
+        uint32_t bcnt = 0;   // CS: blocks this warpgroup has done (the max-exchange slot parity)
         int it = 0;
         int w = seq_read(0);
         WorkItem wi = w >= 0 ? load_item(p.items, w) : WorkItem{};
@@ -1038,7 +1058,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 const int kbase = (wi.blk_begin + (DU ? (j >> 1) : j)) * kBlockN;
                 mbar_wait(&bars->s_full[grp], (Jj >> 1) & 1);
                 tc_fence_after();
-                if (wq == 0 && lane == 0) TRACE(Jj, 3);
+                if (wq == 0 && lane == 0 && hh == 0) TRACE(Jj, 3);
                 // P buffer / O of this warpgroup were last used by its previous block (Jj - 2);
                 // waited for only right before they are touched (rescale / P store)
                 bool pv_waited = Jj < 2;
@@ -1126,6 +1146,90 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                     } else {
                         wait_prev_pv();
                     }
+                } else {
+                if constexpr (CS) {
+                // ---- column split (dual items): this warp owns keys [32 hh, 32 hh + 32) of the
+                // block and O columns [D/2 hh, D/2 hh + D/2); the row max is combined with the
+                // partner warp (same rows, other half) through shared memory and a 64-thread barrier
+                uint32_t sr[32];
+                if (warp_active) {
+                    tmem_ld32(tmem + lane_base + C::kColS + grp * kBlockN + 32 * hh, sr);
+                    tmem_wait_ld();
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->s_free[grp]);
+                float* xm = reinterpret_cast<float*>(smem + C::kOffXch) + (grp * 2 + (int)(bcnt & 1)) * 2 * kM;
+                float mxh = -INFINITY;
+                if (warp_active) {
+                    float mx8[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) mx8[k] = -INFINITY;
+                    if (kbase + kBlockN <= P) {
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sr[c]));
+                    } else {
+                        const int dlt = P - kbase;
+                        uint64_t vb = dlt >= 64 ? ~0ull : (dlt <= 0 ? 0ull : ((1ull << dlt) - 1ull));
+                        if (dlt >= 0 && dlt < 64) vb |= mask << dlt;
+                        else if (dlt < 0 && dlt > -64) vb |= mask >> (-dlt);
+                        const uint32_t vh = (uint32_t)(vb >> (32 * hh));
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) {
+                            sr[c] = ((vh >> c) & 1u) ? sr[c] : 0xFF800000u;   // -inf
+                            mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sr[c]));
+                        }
+                    }
+                    mxh = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+                    xm[hh * kM + r] = mxh;
+                }
+                named_bar_sync(8 + grp * 4 + wq, 64);
+                if (warp_active) {
+                    const float m_blk = fmaxf(mxh, xm[(hh ^ 1) * kM + r]) * p.scale_log2;
+                    bool need_o = false;
+                    float alpha = 1.0f;
+                    if (m_blk > m_run + 8.0f) {          // lazy rescale (both halves decide alike)
+                        alpha = ex2(m_run - m_blk);
+                        need_o = had && row_valid && (m_run != -INFINITY);
+                        l_run *= alpha;
+                        m_run = m_blk;
+                    }
+                    if (__any_sync(0xffffffffu, need_o)) {
+                        wait_prev_pv();
+                        const float f = need_o ? alpha : 1.0f;
+#pragma unroll 1
+                        for (int c0 = 0; c0 < D / 2; c0 += 32) {
+                            uint32_t o[32];
+                            tmem_ld32(o_mine + (D / 2) * hh + c0, o);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
+                            tmem_st32(o_mine + (D / 2) * hh + c0, o);
+                        }
+                    }
+                    const float mo = (m_run == -INFINITY) ? 0.0f : m_run;
+                    float ls8[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) ls8[k] = 0.0f;
+                    uint32_t pk16[16];
+#pragma unroll
+                    for (int c = 0; c < 32; c += 2) {
+                        const float e0 = ex2_mix<kEmu>(fmaf(__uint_as_float(sr[c]), p.scale_log2, -mo), c);
+                        const float e1 = ex2_mix<kEmu>(fmaf(__uint_as_float(sr[c + 1]), p.scale_log2, -mo), c + 1);
+                        pk16[c >> 1] = pack_bf16(e0, e1);
+                        ls8[(c >> 1) & 7] += e0 + e1;
+                    }
+                    l_run += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
+                    if (wq == 0 && lane == 0 && hh == 0) TRACE(Jj, 6);   // (profiling: softmax math done)
+                    wait_prev_pv();
+                    if (wq == 0 && lane == 0 && hh == 0) TRACE(Jj, 7);   // (profiling: P buffer free)
+                    tmem_st16(tmem + lane_base + C::kColP + grp * (kBlockN / 2) + 16 * hh, pk16);
+                    tmem_wait_st();
+                } else {
+                    wait_prev_pv();
+                }
+                ++bcnt;
                 } else {
                 // sr: raw S bits -> masked S -> packed bf16 P in sr[0..31]
                 uint32_t sr[64];
@@ -1222,19 +1326,22 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                     }
                     l_run += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
 #endif
+                    if (RM == 4 && wq == 0 && lane == 0) TRACE(Jj, 6);   // (profiling: softmax math done)
                     wait_prev_pv();
+                    if (RM == 4 && wq == 0 && lane == 0) TRACE(Jj, 7);   // (profiling: P buffer free)
                     tmem_st32(tmem + lane_base + C::kColP + grp * (kBlockN / 2),
                               reinterpret_cast<const uint32_t(&)[32]>(sr[0]));
                     tmem_wait_st();
                 } else {
                     wait_prev_pv();
                 }
+                }   // !CS
                 }   // !hs
                 // (V rows past the sample's end are zeroed by the PV issuer before the first MMA
                 // that reads the tile — dual: tile 0's, which it issues before tile 1's)
                 tc_fence_before();
                 __syncwarp();
-                if (wq == 0 && lane == 0) TRACE(Jj, 4);
+                if (wq == 0 && lane == 0 && hh == 0) TRACE(Jj, 4);
                 if (lane == 0) mbar_arrive(&bars->p_full[grp]);
                 had = true;
                 Jlast = Jj;
@@ -1250,13 +1357,21 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 }
                 const bool direct = wi.part < 0;
                 const int part = direct ? -1 : wi.part + grp * wi.pad;   // tile 1's parts follow tile 0's
+                if constexpr (CS) {   // the row sum: both halves' partial sums
+                    float* xl = reinterpret_cast<float*>(smem + C::kOffXch) + 2 * 2 * 2 * kM + grp * 2 * kM;
+                    xl[hh * kM + r] = l_run;
+                    named_bar_sync(8 + grp * 4 + wq, 64);
+                    l_run += xl[(hh ^ 1) * kM + r];
+                    named_bar_sync(8 + grp * 4 + wq, 64);   // (xl is rewritten at the next item end)
+                }
+                constexpr int kEpiCols = CS ? D / 2 : D;   // O columns of this warp
                 if (warp_active) {
                     const float invL = (had && l_run > 0.0f) ? 1.0f / l_run : 0.0f;
                     const int h = wi.kvh * p.g + (grow % p.g);
                     __nv_bfloat16* orow = p.out + ((int64_t)(off + node) * p.Hq + h) * D;
                     float* prow = direct ? nullptr : p.part_o + ((int64_t)part * kM + rr) * D;
 #pragma unroll 1
-                    for (int cc = 0; cc < ((p.dbg & 1) ? 0 : D); cc += kDuEpi) {
+                    for (int cc = kEpiCols * hh; cc < ((p.dbg & 1) ? 0 : kEpiCols * (hh + 1)); cc += kDuEpi) {
                         uint32_t a[kDuEpi];                  // kDuEpi columns in flight per TMEM wait
 #pragma unroll
                         for (int q = 0; q < kDuEpi / 16; ++q)
@@ -1282,7 +1397,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                             }
                         }
                     }
-                    if (row_valid) {
+                    if (row_valid && hh == 0) {
                         const float lse2 = (had && l_run > 0.0f) ? m_run + __log2f(l_run) : -INFINITY;
                         if (direct) {
                             if (p.lse) p.lse[(int64_t)(off + node) * p.Hq + h] = lse2 * 0.6931471805599453f;
@@ -1298,15 +1413,15 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                     // this tile's split-KV unit (wi.unit + grp): the warpgroup that completes its
                     // last part merges all parts
                     __threadfence();
-                    named_bar_sync(5 + grp, 128);
-                    if (wq == 0 && lane == 0) {
+                    named_bar_sync(5 + grp, 32 * KT<RM>::kSmWarps);
+                    if (wq == 0 && lane == 0 && hh == 0) {
                         const int unit = wi.unit + grp;
                         const int old = atomicAdd(&p.unit_counter[unit], 1);
                         const int last = (old == p.units[unit].n_parts - 1) ? 1 : 0;
                         if (last) p.unit_counter[unit] = 0;      // ready for the next launch
                         bars->merge_flags[grp] = last;
                     }
-                    named_bar_sync(5 + grp, 128);
+                    named_bar_sync(5 + grp, 32 * KT<RM>::kSmWarps);
                     if (bars->merge_flags[grp] && row_valid && warp_active) {
                         __threadfence();
                         const SplitUnit u = p.units[wi.unit + grp];
@@ -1322,7 +1437,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                         const int h = wi.kvh * p.g + (grow % p.g);
                         __nv_bfloat16* orow = p.out + ((int64_t)(off + node) * p.Hq + h) * D;
 #pragma unroll 1
-                        for (int c0 = 0; c0 < D; c0 += 8) {
+                        for (int c0 = kEpiCols * hh; c0 < kEpiCols * (hh + 1); c0 += 8) {
                             float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
                             for (int q = 0; q < u.n_parts; ++q) {
                                 const float lq = __ldcg(p.part_lse + (int64_t)(u.part_base + q) * kM + rr);
@@ -1340,7 +1455,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                             o.w = pack_bf16(acc[6], acc[7]);
                             *reinterpret_cast<uint4*>(orow + c0) = o;
                         }
-                        if (p.lse) p.lse[(int64_t)(off + node) * p.Hq + h] = (M + __log2f(wsum)) * 0.6931471805599453f;
+                        if (p.lse && hh == 0) p.lse[(int64_t)(off + node) * p.Hq + h] = (M + __log2f(wsum)) * 0.6931471805599453f;
                     }
                 }
                 J += nv;
