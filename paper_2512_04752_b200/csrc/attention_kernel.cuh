@@ -1221,9 +1221,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                         ls8[(c >> 1) & 7] += e0 + e1;
                     }
                     l_run += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
-                    if (wq == 0 && lane == 0 && hh == 0) TRACE(Jj, 6);   // (profiling: softmax math done)
                     wait_prev_pv();
-                    if (wq == 0 && lane == 0 && hh == 0) TRACE(Jj, 7);   // (profiling: P buffer free)
                     tmem_st16(tmem + lane_base + C::kColP + grp * (kBlockN / 2) + 16 * hh, pk16);
                     tmem_wait_st();
                 } else {
@@ -1326,9 +1324,7 @@ tree_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                     }
                     l_run += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
 #endif
-                    if (RM == 4 && wq == 0 && lane == 0) TRACE(Jj, 6);   // (profiling: softmax math done)
                     wait_prev_pv();
-                    if (RM == 4 && wq == 0 && lane == 0) TRACE(Jj, 7);   // (profiling: P buffer free)
                     tmem_st32(tmem + lane_base + C::kColP + grp * (kBlockN / 2),
                               reinterpret_cast<const uint32_t(&)[32]>(sr[0]));
                     tmem_wait_st();
