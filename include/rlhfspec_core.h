@@ -284,7 +284,8 @@ rs_status rs_kv_compact(void* const* k_layers_host, void* const* v_layers_host, 
  *   draft_row  MSS only (else must be NULL): device int32 [NT] or NULL. NULL: node i's draft
  *              distribution is row i of draft_probs ([NT, V], as in rs_tree_accept_ex). Else
  *              draft_probs is [R, V] holding only the rows that are used, and draft_row[i] is the
- *              row of node i (-1 for a node without children). Either way the draft row of a node
+ *              row of node i (-1 for a node without children; a non-negative entry must index a
+ *              row of draft_probs: the caller's guarantee, not checked). Either way the draft row of a node
  *              WITHOUT children is never read (Z29: nothing was drawn from it; a visited
  *              leaf's bonus comes from the target weights), so a caller uploads only the rows of
  *              nodes with children; a node with children whose draft_row is negative sets

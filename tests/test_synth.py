@@ -32,3 +32,27 @@ def test_sampling_batch_children_drawn_from_q():
     b = make_verify_batch(cfg)
     assert b["draft_probs"].shape == (b["NT"], 50)
     np.testing.assert_allclose(b["draft_probs"].sum(-1).numpy(), 1.0, rtol=1e-5)
+
+
+def test_lm_head_sampling_inputs_shapes_and_draws():
+    """synth.make_lm_head_sampling_inputs: seeded (same seed -> same tensors), draft rows are
+    probability vectors, every child's token lies in the support of its parent's q, root tokens
+    are kept."""
+    import torch
+    from synth import VerifyConfig, make_lm_head_sampling_inputs, make_verify_batch
+    cfg = VerifyConfig("ls", B=3, Hq=2, Hkv=1, d=64, V=48, L=1, prefix=("fixed", 5), tree=("range", 2, 9),
+                       mode="mss", seed=2)
+    b = make_verify_batch(cfg, device="cpu", with_logits=False)
+    a = make_lm_head_sampling_inputs(b, Dm=64, seed=3)
+    c = make_lm_head_sampling_inputs(b, Dm=64, seed=3)
+    assert a["hidden"].shape == (b["NT"], 64) and a["weight"].shape == (48, 64)
+    assert torch.equal(a["hidden"], c["hidden"]) and torch.equal(a["draft_probs"], c["draft_probs"])
+    assert np.array_equal(a["token"], c["token"])
+    q = a["draft_probs"].float()
+    assert torch.all(q >= 0) and torch.allclose(q.sum(-1), torch.ones(b["NT"]), atol=1e-5)
+    par, off = b["parent"], b["tree_off"]
+    for s in range(b["B"]):
+        o = off[s]
+        assert a["token"][o] == b["token"][o]
+        for i in range(1, off[s + 1] - o):
+            assert 0 <= a["token"][o + i] < 48 and q[o + par[o + i], a["token"][o + i]] > 0
