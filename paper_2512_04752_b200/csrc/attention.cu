@@ -28,6 +28,10 @@
 
 using namespace attn;
 
+#ifndef RS_ATTN_R16_MAX
+#define RS_ATTN_R16_MAX 64   // units with T*g above this use 32-row tiles (else 16-row, several per unit as a gang)
+#endif
+
 // Profiling hook state (rs_attn_set_trace).
 static unsigned long long* g_trace_buf = nullptr;
 static size_t g_trace_bytes = 0;
@@ -137,7 +141,7 @@ extern "C" rs_status rs_attn_plan_create(const int32_t* prefix_len_host, const i
             return (T < 1 || T > RS_MAX_TREE) ? RS_ERR_MALFORMED_TREE : RS_ERR_UNSUPPORTED;
         }
         const int nblk = (P + T + kBlockN - 1) / kBlockN;
-        const int R = (T * g <= 64) ? 16 : 32;         // rows per TMEM sub-partition
+        const int R = (T * g <= RS_ATTN_R16_MAX) ? 16 : 32;   // rows per TMEM sub-partition
         const int M = (T * g + 4 * R - 1) / (4 * R);   // query tiles per (sample, kv head)
         for (int kvh = 0; kvh < Hkv; ++kvh) gus.push_back({b, kvh, M, nblk, R, P, tree_off_host[b], T});
         pl->rmodes |= (R == 16) ? 1 : 2;
