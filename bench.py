@@ -667,7 +667,8 @@ def run_ours(args, world, rank, local):
             "peak_kind": "burst (one ~1 ms launch per step)",
             "bound": "tensor", "logits_bytes_not_written": int(b["NT"]) * cfg.V * 2,
             "note": "f2: rs_lm_head_argmax (tcgen05 GEMM [NT x Dm] x [V x Dm]^T, arg-max in the epilogue) "
-                    "+ finalize + rs_tree_accept_greedy_tokens walk"}
+                    "+ finalize + " + ("rs_tree_accept_greedy_tokens_compact (the walk with the KV commit)"
+                                      if step.fused_commit else "rs_tree_accept_greedy_tokens walk")}
 
     # ---------------- f3: GPU verification-tree construction (timed alone, outside the step) ----------------
     if strat is not None:

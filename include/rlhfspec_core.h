@@ -106,6 +106,19 @@ rs_status rs_tree_accept_greedy_tokens(const int32_t* argmax_token, const int32_
                                        const int32_t* token, const int32_t* tree_off, int32_t B,
                                        int32_t* accepted_len, int32_t* path, int32_t* bonus_token,
                                        int32_t* status_flags, void* stream);
+/* rs_tree_accept_greedy_tokens followed by rs_kv_compact in ONE launch (the f2 walk with the
+ * KV commit, as rs_tree_accept_compact is for logits): a CTA per (sample, pair of layers) walks
+ * the sample's tree on the per-node arg-max tokens and commits its layers' share of the path.
+ * Outputs identical to the two calls in sequence; KV arguments as rs_kv_compact (L <= 256, else
+ * RS_ERR_INVALID_ARG; head_dim % 8 != 0 -> RS_ERR_UNSUPPORTED). */
+rs_status rs_tree_accept_greedy_tokens_compact(const int32_t* argmax_token, const int32_t* parent,
+                                               const int32_t* token, const int32_t* tree_off, int32_t B,
+                                               int32_t* accepted_len, int32_t* path, int32_t* bonus_token,
+                                               int32_t* status_flags, void* const* k_layers_host,
+                                               void* const* v_layers_host, int32_t L, int32_t Hkv,
+                                               int32_t head_dim, int32_t page_size, const int32_t* block_table,
+                                               int32_t max_pages, const int32_t* prefix_len, int32_t* new_len,
+                                               int32_t* moves, void* stream);
 
 /* ===================================================================================== f3
  * rs_tree_select — the verification trees of a batch, built on the GPU from the draft's

@@ -649,6 +649,32 @@ def lm_head_argmax(hidden, weight, out=None, max_logit=True, ws=None, stream=Non
     return tok, mx
 
 
+_sig("rs_tree_accept_greedy_tokens_compact", _i32, _P, _P, _P, _P, _i32, _P, _P, _P, _P, _P, _P, _i32, _i32,
+     _i32, _i32, _P, _i32, _P, _P, _P, _P)
+
+
+def tree_accept_greedy_tokens_compact(argmax_token, parent, token, tree_off, k_layers, v_layers, block_table,
+                                      prefix_len, out=None, new_len=None, moves=None, stream=None, layer_ptrs=None):
+    """The f2 walk on per-node arg-max tokens with the KV commit in one launch."""
+    B = tree_off.numel() - 1
+    dev = argmax_token.device
+    if out is None:
+        out = (torch.empty(B, dtype=torch.int32, device=dev), torch.empty((B, MAX_TREE), dtype=torch.int32, device=dev),
+               torch.empty(B, dtype=torch.int32, device=dev), torch.empty(B, dtype=torch.int32, device=dev))
+    if new_len is None:
+        new_len = torch.empty(B, dtype=torch.int32, device=dev)
+    acc, path, bonus, flags = out
+    L = len(k_layers)
+    _, Hkv, ps, d = k_layers[0].shape
+    kp, vp = layer_ptrs if layer_ptrs is not None else (_layer_ptrs(k_layers), _layer_ptrs(v_layers))
+    _check(_lib.rs_tree_accept_greedy_tokens_compact(_ptr(argmax_token), _ptr(parent), _ptr(token), _ptr(tree_off), B,
+                                                     _ptr(acc), _ptr(path), _ptr(bonus), _ptr(flags), kp, vp, L, Hkv,
+                                                     d, ps, _ptr(block_table), block_table.shape[1], _ptr(prefix_len),
+                                                     _ptr(new_len), _ptr(moves), _stream(stream)),
+           "rs_tree_accept_greedy_tokens_compact")
+    return acc, path, bonus, flags, new_len, moves
+
+
 def tree_accept_greedy_tokens(argmax_token, parent, token, tree_off, out=None, stream=None):
     B = tree_off.numel() - 1
     dev = parent.device

@@ -25,6 +25,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "compact_tail.cuh"
 #include "sm100_ptx.cuh"
 
 namespace {
@@ -250,13 +251,15 @@ __global__ void lm_head_finalize_kernel(const unsigned long long* __restrict__ k
 
 // One warp per sample: validate the tree, then walk (c-2). At the current node c the lanes
 // test nodes x > c for (parent == c, token == argmax[c]); the lowest such x wins (ballot).
-__global__ void greedy_walk_kernel(const int32_t* __restrict__ amax, const int32_t* __restrict__ parent,
-                                   const int32_t* __restrict__ token, const int32_t* __restrict__ tree_off,
-                                   int B, int32_t* __restrict__ acc, int32_t* __restrict__ path,
-                                   int32_t* __restrict__ bonus, int32_t* __restrict__ flags) {
-    const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+// write: this warp writes the outputs; path_s (optional, shared memory): the path for a fused
+// commit. Returns the accepted length (all lanes).
+__device__ __forceinline__ int greedy_walk_warp(const int32_t* __restrict__ amax, const int32_t* __restrict__ parent,
+                                                const int32_t* __restrict__ token,
+                                                const int32_t* __restrict__ tree_off, int b, bool write,
+                                                int32_t* __restrict__ acc, int32_t* __restrict__ path,
+                                                int32_t* __restrict__ bonus, int32_t* __restrict__ flags,
+                                                int* path_s) {
     const int lane = threadIdx.x & 31;
-    if (b >= B) return;
     const int s = tree_off[b], T = tree_off[b + 1] - s;
     int32_t* pb = path + (size_t)b * RS_MAX_TREE;
     bool ok = T >= 1 && T <= RS_MAX_TREE;
@@ -271,8 +274,11 @@ __global__ void greedy_walk_kernel(const int32_t* __restrict__ amax, const int32
     const int t0 = (ok && lane < T) ? token[s + lane] : 0;
     const int t1 = (ok && lane + 32 < T) ? token[s + lane + 32] : 0;
     int c = 0, n = 0, fl = ok ? 0 : RS_FLAG_MALFORMED;
-    pb[lane] = -1;
-    pb[lane + 32] = -1;
+    if (write) {
+        pb[lane] = -1;
+        pb[lane + 32] = -1;
+    }
+    if (path_s && lane == 0) path_s[0] = 0;
     __syncwarp();
     if (ok) {
         for (;;) {
@@ -284,15 +290,48 @@ __global__ void greedy_walk_kernel(const int32_t* __restrict__ amax, const int32
             if (nx < 0) break;
             c = nx;
             ++n;
-            if (lane == 0) pb[n] = c;
+            if (write && lane == 0) pb[n] = c;
+            if (path_s && lane == 0) path_s[n] = c;
         }
     }
-    if (lane == 0) {
+    if (write && lane == 0) {
         pb[0] = 0;
         acc[b] = ok ? n : 0;
         bonus[b] = (ok && !(fl & RS_FLAG_NONFINITE)) ? amax[s + c] : -1;
         flags[b] = fl;
     }
+    return ok ? n : 0;
+}
+
+__global__ void greedy_walk_kernel(const int32_t* __restrict__ amax, const int32_t* __restrict__ parent,
+                                   const int32_t* __restrict__ token, const int32_t* __restrict__ tree_off,
+                                   int B, int32_t* __restrict__ acc, int32_t* __restrict__ path,
+                                   int32_t* __restrict__ bonus, int32_t* __restrict__ flags) {
+    const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (b >= B) return;
+    greedy_walk_warp(amax, parent, token, tree_off, b, true, acc, path, bonus, flags, nullptr);
+}
+
+// The walk fused with the KV commit (rs_tree_accept_greedy_tokens_compact): a CTA per (sample,
+// group of layers) as kv_compact_kernel; its warp 0 walks the sample's tree (cheap: a ballot per
+// node over the per-node arg-max tokens), group 0 writes the walk's outputs, and every CTA then
+// commits the path for its layer group (rs::compact_sample).
+__global__ void __launch_bounds__(256)
+greedy_walk_compact_kernel(const __grid_constant__ rs::CompactArgs A, const int32_t* __restrict__ amax,
+                           const int32_t* __restrict__ parent, const int32_t* __restrict__ token,
+                           const int32_t* __restrict__ tree_off, int32_t* __restrict__ acc,
+                           int32_t* __restrict__ path, int32_t* __restrict__ bonus, int32_t* __restrict__ flags) {
+    __shared__ rs::CompactSmem cm;
+    __shared__ int path_s[RS_MAX_TREE];
+    __shared__ int a_s;
+    const int b = blockIdx.x;
+    if (threadIdx.x < 32) {
+        const int a = greedy_walk_warp(amax, parent, token, tree_off, b, blockIdx.y == 0, acc, path, bonus, flags,
+                                       path_s);
+        if (threadIdx.x == 0) a_s = a;
+    }
+    __syncthreads();
+    rs::compact_sample(A, b, a_s, [&](int k) { return path_s[k]; }, blockIdx.y, gridDim.y, blockIdx.y == 0, cm);
 }
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -431,6 +470,44 @@ extern "C" rs_status rs_lm_head_logits(const void* hidden, const void* weight, i
     const int grid = std::min(ntiles, num_sms());
     lm_head_argmax_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(tmH, tmW, rows, V, Dm, nullptr,
                                                                     static_cast<__nv_bfloat16*>(logits));
+    RS_LAUNCH_CHECK();
+    return RS_OK;
+}
+
+extern "C" rs_status rs_tree_accept_greedy_tokens_compact(
+    const int32_t* argmax_token, const int32_t* parent, const int32_t* token, const int32_t* tree_off, int32_t B,
+    int32_t* accepted_len, int32_t* path, int32_t* bonus_token, int32_t* status_flags, void* const* k_layers_host,
+    void* const* v_layers_host, int32_t L, int32_t Hkv, int32_t head_dim, int32_t page_size, const int32_t* block_table,
+    int32_t max_pages, const int32_t* prefix_len, int32_t* new_len, int32_t* moves, void* stream) {
+    rs::bind_device(argmax_token);
+    RS_REQUIRE(B >= 0 && L >= 0 && L <= rs::kCompactMaxLayers && Hkv > 0 && page_size > 0 && max_pages >= 0,
+               RS_ERR_INVALID_ARG, "rs_tree_accept_greedy_tokens_compact: bad sizes (L=%d, at most %d layers)", L,
+               rs::kCompactMaxLayers);
+    RS_REQUIRE(head_dim > 0 && head_dim % 8 == 0, RS_ERR_UNSUPPORTED,
+               "rs_tree_accept_greedy_tokens_compact: head_dim %% 8 != 0");
+    if (B == 0) return RS_OK;
+    RS_REQUIRE(argmax_token && parent && token && tree_off && accepted_len && path && bonus_token && status_flags &&
+                   block_table && prefix_len && new_len && (L == 0 || (k_layers_host && v_layers_host)),
+               RS_ERR_INVALID_ARG, "rs_tree_accept_greedy_tokens_compact: null pointer");
+    rs::CompactArgs A;
+    for (int i = 0; i < L; ++i) {
+        RS_REQUIRE(k_layers_host[i] && v_layers_host[i], RS_ERR_INVALID_ARG,
+                   "rs_tree_accept_greedy_tokens_compact: null layer pointer");
+        A.k[i] = k_layers_host[i];
+        A.v[i] = v_layers_host[i];
+    }
+    A.nl = L;
+    A.Hkv = Hkv;
+    A.d = head_dim;
+    A.ps = page_size;
+    A.max_pages = max_pages;
+    A.block_table = block_table;
+    A.prefix_len = prefix_len;
+    A.new_len = new_len;
+    A.moves = moves;
+    const int groups = L > 0 ? (L + 1) / 2 : 1;   // two layers per CTA, as rs_kv_compact
+    greedy_walk_compact_kernel<<<dim3((unsigned)B, (unsigned)groups), 256, 0, rs::as_stream(stream)>>>(
+        A, argmax_token, parent, token, tree_off, accepted_len, path, bonus_token, status_flags);
     RS_LAUNCH_CHECK();
     return RS_OK;
 }

@@ -53,8 +53,7 @@ class VerifyStep:
         # acceptance and the KV commit in one launch (not for the f2 token path, nor for more
         # layers than one launch's parameter block holds)
         self.lm_sampling = self.hidden is not None and mode != core.GREEDY
-        self.fused_commit = (bool(fused_commit) and (self.hidden is None or self.lm_sampling)
-                             and self.L <= core.COMPACT_MAX_LAYERS)
+        self.fused_commit = bool(fused_commit) and self.L <= core.COMPACT_MAX_LAYERS
         self.layer_ptrs = (core._layer_ptrs(self.k_layers), core._layer_ptrs(self.v_layers))
         # MSS: optional row map (draft rows only for nodes with children, Z29)
         self.draft_row = b.get("draft_row") if mode == core.SAMPLE_MSS else None
@@ -119,6 +118,14 @@ class VerifyStep:
                         self.ps, new_len=self.new_len, stream=stream)
 
     def accept_compact_step(self, seed, step, stream=None):
+        if self.fused_commit and self.hidden is not None and not self.lm_sampling:
+            # f2 greedy: the arg-max GEMM, then the walk with the KV commit in one launch
+            core.lm_head_argmax(self.hidden, self.lm_w, out=(self.amax, None), ws=self.lm_ws, stream=stream)
+            core.tree_accept_greedy_tokens_compact(self.amax, self.parent, self.token, self.tree_off, self.k_layers,
+                                                   self.v_layers, self.block_table, self.prefix_len,
+                                                   out=(self.acc, self.path, self.bonus, self.flags),
+                                                   new_len=self.new_len, stream=stream, layer_ptrs=self.layer_ptrs)
+            return
         if self.fused_commit:
             self.lm_head_step(stream)
             core.tree_accept_compact(self.mode, self.logits, self.parent, self.token, self.tree_off, self.gid,

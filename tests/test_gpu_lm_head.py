@@ -305,3 +305,42 @@ def test_verify_step_mss_with_lm_head(cuda_lib):
     np.testing.assert_array_equal(res["bonus"], o[2])
     np.testing.assert_array_equal(res["flags"], o[3])
     assert res["accepted_len"].sum() > 0
+
+
+def test_fused_walk_commit_equals_two_calls(cuda_lib):
+    """rs_tree_accept_greedy_tokens_compact == rs_tree_accept_greedy_tokens then rs_kv_compact:
+    outputs, new_len, moves and every K/V byte, on ragged trees with planted arg-max tokens, a
+    malformed tree and a -1 (non-finite row) token mid-walk."""
+    core = cuda_lib
+    from synth import VerifyConfig, make_verify_batch, planted_targets
+    cfg = VerifyConfig("wc", B=20, Hq=4, Hkv=2, d=128, V=500, L=3, prefix=("lognormal", 90, 0.7, 1, 300),
+                       tree=("range", 1, 64), mode="greedy", seed=12)
+    b = make_verify_batch(cfg, device="cuda", gen_device="cpu", with_logits=False)
+    rng = np.random.default_rng(4)
+    amax = planted_targets(rng, b["parent"], b["tree_off"], b["token"], cfg.V, 0.9).astype(np.int32)
+    par = b["parent"].copy()
+    to = b["tree_off"]
+    if to[3] - to[2] > 2:
+        par[to[2] + 2] = 2                      # sample 2 malformed
+    amax[to[5] + 1:to[6]] = -1                  # sample 5: no arg-max below the root
+    d = lambda x: torch.as_tensor(np.ascontiguousarray(x)).cuda()   # noqa: E731
+    L = cfg.L
+    kc0, vc0 = b["k_cache"].clone(), b["v_cache"].clone()
+    a1 = core.tree_accept_greedy_tokens(d(amax), d(par), d(b["token"]), d(to))
+    mv1 = torch.empty((b["B"], 64, 2), dtype=torch.int32, device="cuda")
+    nl1, _ = core.kv_compact([b["k_cache"][l] for l in range(L)], [b["v_cache"][l] for l in range(L)],
+                             d(b["block_table"]), d(b["prefix_len"]), a1[0], a1[1], moves=mv1)
+    k1, v1 = b["k_cache"].clone(), b["v_cache"].clone()
+    b["k_cache"].copy_(kc0)
+    b["v_cache"].copy_(vc0)
+    mv2 = torch.empty((b["B"], 64, 2), dtype=torch.int32, device="cuda")
+    a2 = core.tree_accept_greedy_tokens_compact(d(amax), d(par), d(b["token"]), d(to),
+                                                [b["k_cache"][l] for l in range(L)], [b["v_cache"][l] for l in range(L)],
+                                                d(b["block_table"]), d(b["prefix_len"]), moves=mv2)
+    torch.cuda.synchronize()
+    for x, y in zip(a1, a2[:4]):
+        assert torch.equal(x, y)
+    assert torch.equal(nl1, a2[4]) and torch.equal(mv1, mv2)
+    assert torch.equal(b["k_cache"], k1) and torch.equal(b["v_cache"], v1)
+    f = a2[3].cpu().numpy()
+    assert f[2] == core.FLAG_MALFORMED and (f[5] & core.FLAG_NONFINITE) and a2[0].sum() > 0
