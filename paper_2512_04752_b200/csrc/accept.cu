@@ -846,7 +846,7 @@ tree_accept_kernel(int mode_rt, const void* __restrict__ logits, int dtype_rt, c
 // inverse CDF of the current weights (draw_bonus).
 constexpr int kMssThreads = kThreads;   // == kTileVecs: one vector per thread per tile row
 #ifndef RS_MSS_LUNROLL
-#define RS_MSS_LUNROLL 2
+#define RS_MSS_LUNROLL 1
 #endif
 constexpr int kMssLUnroll = RS_MSS_LUNROLL;   // pass L: row vectors in flight per thread (a slice in one round)
 
