@@ -339,7 +339,8 @@ void rs_selector_destroy(rs_selector* sel);
 /* cand_parent host int32 [N] (per sample, -1 = child of the committed root, parent < index),
  * cand_o host double [N] draft probabilities o(v) in (0,1], cand_off host int32 [B+1],
  * prefix_len host int32 [B]. selected: host int32 [B, n_max] candidate ids in selection order
- * (the first n of each row form S_b(n)), -1 padded, or NULL. */
+ * (the first n of each row form S_b(n)) up to out->n_stop — the search runs step-major over the
+ * batch and stops with the objective's early stop (Eq. 3) — then -1, or NULL. */
 rs_status rs_select_strategy(rs_selector* sel, const int32_t* cand_parent, const double* cand_o,
                              const int32_t* cand_off, const int32_t* prefix_len, int32_t B,
                              int32_t n_min, int32_t n_max, int32_t patience, rs_strategy* out,

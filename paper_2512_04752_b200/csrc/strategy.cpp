@@ -92,9 +92,9 @@ extern "C" void rs_selector_destroy(rs_selector* sel) { delete sel; }
 namespace {
 // Reused per-thread buffers of the selector (no allocation per call once warm).
 struct SelScratch {
-    std::vector<double> dl, w, ow;   // per candidate: dl, w; per (sample, step): w of the popped node
-    std::vector<int> dep, cnt, byd, ord, odep, olen;
-    std::vector<PQItem> heap;
+    std::vector<double> w, ow;            // per candidate (flat over the batch): w; per (sample, step): popped w
+    std::vector<int> dep, byd, cnt, cnt_off, ord, odep, lo, maxd, hsz;
+    std::vector<PQItem> heap;             // per sample a heap slice of its candidate count
 };
 thread_local SelScratch tls;
 }  // namespace
@@ -107,82 +107,93 @@ extern "C" rs_status rs_select_strategy(rs_selector* sel, const int32_t* cand_pa
                "rs_select_strategy: need 1 <= n_min <= n_max, patience >= 1");
     RS_REQUIRE(B >= 1, RS_ERR_EMPTY_TREE, "rs_select_strategy: empty batch");
     SelScratch& S = tls;
+    const int NT = cand_off[B] - cand_off[0];
     S.ord.assign((size_t)B * n_max, -1);   // per sample: the popped candidates in order (S(n) = first n)
     S.ow.resize((size_t)B * n_max);
     S.odep.resize((size_t)B * n_max);
-    S.olen.assign(B, 0);
-    int feasible = n_max;
+    S.w.resize(NT > 0 ? NT : 1);
+    S.dep.resize(NT > 0 ? NT : 1);
+    S.byd.resize(NT > 0 ? NT : 1);
+    S.heap.resize(NT > 0 ? NT : 1);
+    S.cnt_off.assign(B + 1, 0);
+    S.lo.assign(B, 0);
+    S.maxd.assign(B, 0);
+    S.hsz.assign(B, 0);
+    S.cnt.clear();
+    // per sample: dl, depth, w = F(dl), nodes grouped by depth (layer m is one contiguous range)
     for (int b = 0; b < B; ++b) {
         const int o0 = cand_off[b], N = cand_off[b + 1] - cand_off[b];
         RS_REQUIRE(N >= 0, RS_ERR_INVALID_ARG, "rs_select_strategy: cand_off not non-decreasing at %d", b);
-        S.dl.resize(N);
-        S.dep.resize(N);
-        S.w.resize(N);
+        const int base = o0 - cand_off[0];
+        double* dl = S.w.data() + base;   // dl first, then replaced by w in place
+        int* dep = S.dep.data() + base;
         bool has_root_child = false;
         int max_dep = 0;
         for (int i = 0; i < N; ++i) {
             const int pa = cand_parent[o0 + i];
             RS_REQUIRE(pa < i, RS_ERR_MALFORMED_TREE, "rs_select_strategy: sample %d node %d parent %d", b, i, pa);
-            S.dl[i] = cand_o[o0 + i] * (pa < 0 ? 1.0 : S.dl[pa]);
-            S.dep[i] = pa < 0 ? 0 : S.dep[pa] + 1;
-            max_dep = std::max(max_dep, S.dep[i]);
+            dl[i] = cand_o[o0 + i] * (pa < 0 ? 1.0 : dl[pa]);
+            dep[i] = pa < 0 ? 0 : dep[pa] + 1;
+            max_dep = std::max(max_dep, dep[i]);
             has_root_child |= pa < 0;
         }
         RS_REQUIRE(N > 0 && has_root_child, RS_ERR_EMPTY_TREE, "rs_select_strategy: sample %d has no candidates", b);
-        for (int i = 0; i < N; ++i) S.w[i] = acceptance_fit(sel, S.dl[i]);
-        // nodes grouped by depth (ascending id inside a layer): layer m is one contiguous range
-        S.cnt.assign(max_dep + 2, 0);
-        for (int i = 0; i < N; ++i) ++S.cnt[S.dep[i] + 1];
-        for (int d = 0; d <= max_dep; ++d) S.cnt[d + 1] += S.cnt[d];
-        S.byd.resize(N);
-        for (int i = 0; i < N; ++i) S.byd[S.cnt[S.dep[i]]++] = i;   // cnt[d] ends at the start of d + 1
-        // layer-level search: at step m push layer m (depth m-1), pop u_max
-        S.heap.clear();
-        int* ord = S.ord.data() + (size_t)b * n_max;
-        int len = 0, lo = 0;
-        for (int m = 1; m <= n_max; ++m) {
-            if (m - 1 <= max_dep) {
-                const int hi = S.cnt[m - 1];
-                for (int k = lo; k < hi; ++k) {
-                    const int i = S.byd[k];
-                    S.heap.push_back({S.w[i], S.dep[i], i});
-                    std::push_heap(S.heap.begin(), S.heap.end());
-                }
-                lo = hi;
-            }
-            if (S.heap.empty()) break;
-            std::pop_heap(S.heap.begin(), S.heap.end());
-            const PQItem top = S.heap.back();
-            S.heap.pop_back();
-            ord[len] = top.id;
-            S.ow[(size_t)b * n_max + len] = top.w;
-            S.odep[(size_t)b * n_max + len] = top.depth;
-            ++len;
-        }
-        S.olen[b] = len;
-        feasible = std::min<int>(feasible, len);
+        for (int i = 0; i < N; ++i) dl[i] = acceptance_fit(sel, dl[i]);
+        S.maxd[b] = max_dep;
+        S.cnt_off[b] = (int)S.cnt.size();
+        S.cnt.resize(S.cnt.size() + max_dep + 2, 0);
+        int* cnt = S.cnt.data() + S.cnt_off[b];
+        for (int i = 0; i < N; ++i) ++cnt[dep[i] + 1];
+        for (int d = 0; d <= max_dep; ++d) cnt[d + 1] += cnt[d];
+        int* byd = S.byd.data() + base;
+        for (int i = 0; i < N; ++i) byd[cnt[dep[i]]++] = i;   // cnt[d] ends at the start of d + 1
     }
-    RS_REQUIRE(feasible >= n_min, RS_ERR_INSUFFICIENT_NODES,
-               "rs_select_strategy: only %d candidate steps (n_min %d)", feasible, n_min);
+    // layer-level search, step-major over the batch so the early stop of Eq. 3 also
+    // stops the search: at step m every sample pushes its layer m (depth m-1) and pops its u_max;
+    // al(m) adds the popped weights (Z20: one n for the batch). A sample whose heap runs dry ends
+    // the feasible range (S(n) must exist for every sample).
     long long n_seq = 0;
     for (int b = 0; b < B; ++b) n_seq += prefix_len[b];
-    // profile + early-stopped argmax (Eq. 2, Eq. 3)
     double al = 0.0, best_obj = -INFINITY, prev = 0.0;
-    int best_n = -1, dec = 0, n_stop = 0, best_hit = 0;
+    int best_n = -1, dec = 0, n_stop = 0, best_hit = 0, feasible = n_max;
     double best_al = 0.0, best_t = 0.0;
     bool have_prev = false;
-    for (int n = 1; n <= feasible; ++n) {
+    for (int m = 1; m <= n_max; ++m) {
         double add = 0.0;
-        for (int b = 0; b < B; ++b) add += S.ow[(size_t)b * n_max + n - 1];
+        bool dry = false;
+        for (int b = 0; b < B && !dry; ++b) {
+            const int base = cand_off[b] - cand_off[0];
+            PQItem* hp = S.heap.data() + base;
+            int& hs = S.hsz[b];
+            if (m - 1 <= S.maxd[b]) {
+                const int* cnt = S.cnt.data() + S.cnt_off[b];
+                const int* byd = S.byd.data() + base;
+                const int hi = cnt[m - 1];
+                for (int k = S.lo[b]; k < hi; ++k) {
+                    const int i = byd[k];
+                    hp[hs++] = {S.w[base + i], S.dep[base + i], i};
+                    std::push_heap(hp, hp + hs);
+                }
+                S.lo[b] = hi;
+            }
+            if (hs == 0) { dry = true; break; }
+            std::pop_heap(hp, hp + hs);
+            const PQItem top = hp[--hs];
+            S.ord[(size_t)b * n_max + m - 1] = top.id;
+            S.ow[(size_t)b * n_max + m - 1] = top.w;
+            S.odep[(size_t)b * n_max + m - 1] = top.depth;
+        }
+        if (dry) { feasible = m - 1; break; }
+        for (int b = 0; b < B; ++b) add += S.ow[(size_t)b * n_max + m - 1];   // (the reference's summation order)
         al += add;
         bool hit = false;
-        const double t = t_sd(sel, n_seq, (long long)B * (n + 1), &hit);
-        n_stop = n;
-        if (n < n_min) continue;
+        const double t = t_sd(sel, n_seq, (long long)B * (m + 1), &hit);
+        n_stop = m;
+        if (m < n_min) continue;
         const double obj = al / t;
         if (obj > best_obj) {
             best_obj = obj;
-            best_n = n;
+            best_n = m;
             best_al = al;
             best_t = t;
             best_hit = hit ? 1 : 0;
@@ -193,6 +204,11 @@ extern "C" rs_status rs_select_strategy(rs_selector* sel, const int32_t* cand_pa
         have_prev = true;
         if (dec >= patience) break;
     }
+    RS_REQUIRE(feasible >= n_min && best_n >= 1, RS_ERR_INSUFFICIENT_NODES,
+               "rs_select_strategy: only %d candidate steps (n_min %d)", feasible, n_min);
+    // selection rows are defined up to n_stop (the search stopped there); -1 after
+    for (int b = 0; b < B; ++b)
+        for (int k = n_stop; k < n_max; ++k) S.ord[(size_t)b * n_max + k] = -1;
     int depth = 0, width = 0;
     int per_layer[RS_MAX_TREE + 2];
     for (int b = 0; b < B; ++b) {

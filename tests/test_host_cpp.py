@@ -46,12 +46,14 @@ def test_select_strategy_matches_oracle(core, seed):
         assert got[k] == ref[k], k
     for k in ("al", "t_sd", "objective"):
         assert got[k] == ref[k], k          # same expression, same order: bit-identical
-    # the selection order per sample equals the oracle's layer search
+    # the selection order per sample equals the oracle's layer search up to the early stop (the
+    # search stops with Eq. 3: rows hold S(n_stop), -1 after)
+    ns = got["n_stop"]
     for b, (p, o) in enumerate(trees):
         w = np.array([OS.acceptance_fit(KX, KY, x) for x in OS.draft_logits(p, o)])
         order = OS.layer_search_order(p, w, n_max)
         row = got["selected"][b]
-        assert list(row[:len(order)]) == order and np.all(row[len(order):] == -1)
+        assert list(row[:ns]) == order[:ns] and np.all(row[ns:] == -1)
 
 
 def test_selector_bucket_cache_hits(core):
