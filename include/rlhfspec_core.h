@@ -244,8 +244,9 @@ rs_status rs_tree_verify_attention_layers(
  *               a visited node with children holds a value outside [0, 1] or NaN (walk stops
  *               there, bonus -1).
  *   ws, ws_bytes: device workspace >= rs_tree_accept_workspace_bytes(mode, B, V) bytes, 16-byte
- *               aligned (MSS keeps each sample's residual weights there; 0 bytes otherwise:
- *               NULL allowed); too small -> RS_ERR_WORKSPACE. */
+ *               aligned; currently 0 bytes for every mode (MSS keeps the visited row and its
+ *               residual in the cluster's shared memory), so NULL is allowed; too small ->
+ *               RS_ERR_WORKSPACE. */
 size_t rs_tree_accept_workspace_bytes(int32_t mode, int32_t B, int32_t V);
 /* As rs_tree_accept with the draft probabilities' dtype given: draft_dtype RS_DTYPE_F32 or
  * RS_DTYPE_BF16 (a bf16 value is used as the fp32 number it denotes, so the arithmetic of
