@@ -10,7 +10,7 @@ greedy: rs_lm_head_argmax -> rs_tree_accept_greedy_tokens (the logits are never 
 sampling: rs_lm_head_logits (the bf16 logits from the GEMM epilogue) -> rs_tree_accept_compact.
 
 Pure orchestration: buffers are torch tensors, every computation is a library call; arguments
-are marshalled once so a step costs four ctypes calls. The device part can be captured into a
+are marshalled once so a step costs three ctypes calls. The device part can be captured into a
 CUDA graph (one launch per step)."""
 from __future__ import annotations
 
@@ -85,7 +85,7 @@ class VerifyStep:
         elif self.hidden is not None:
             self.amax = torch.empty(NT, dtype=torch.int32, device=dev)
             self.lm_ws = torch.empty(max(core.lm_head_argmax_workspace_bytes(NT), 8), dtype=torch.uint8, device=dev)
-        self.accept_ws = torch.empty(max(nws, 16), dtype=torch.uint8, device=dev)   # MSS residual weights
+        self.accept_ws = torch.empty(max(nws, 16), dtype=torch.uint8, device=dev)   # (0 bytes needed today)
         self.attn_call = core.AttentionLayersCall(
             self.plan, [self.q[i] for i in self.layer_buf], self.k_layers, self.v_layers, self.block_table,
             self.prefix_len, self.tree_off, self.mask, self.sm_scale, self.ws,
